@@ -1,0 +1,240 @@
+/*
+ * lsg.h -- C ABI of the B200-native lip-sync hot path (liblsg.so).
+ *
+ * Drop-in boundary for the per-segment lip-sync stage of the lipstream
+ * reference (arXiv 2512.18318).  Every entry point replaces one reference
+ * interface; the interface it replaces is cited next to it (paths relative
+ * to /root/reference/proj/core/).  Plain pointers and sizes only -- no C++,
+ * no torch types.  The C++ drop-in classes in include/lsg/lipstream_b200.hpp
+ * wrap this ABI behind the reference's own class/function signatures.
+ *
+ * Conventions
+ *  - Every function returns an lsg_status.  LSG_EINVAL / LSG_ELOGIC /
+ *    LSG_ERUNTIME correspond to the reference's std::invalid_argument /
+ *    std::logic_error / std::runtime_error (segmenter.cpp:11-38, mel.cpp:27-36,
+ *    visual_mocks.cpp:43-46); LSG_ECUDA is a device failure.  The message of
+ *    the last failure on the calling thread is lsg_last_error().
+ *  - Handles own every device workspace, sized at create time; the compute
+ *    calls do not allocate.  A handle is externally synchronised (one host
+ *    thread at a time), like one reference Segmenter per stream
+ *    (SPEC.md:258-259).
+ *  - Pointers marked [dev] are device pointers on the context's device,
+ *    [host] are host pointers (pinned memory makes the copies async), and
+ *    [any] are resolved with cudaPointerGetAttributes.
+ *  - All device work is issued on the context's stream; calls that return
+ *    results to host memory synchronise that stream.
+ *  - There is no CPU fallback: with no usable sm_100 device, lsg_ctx_create
+ *    fails with LSG_ECUDA.
+ */
+#ifndef LSG_H
+#define LSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int lsg_status;
+#define LSG_OK 0
+#define LSG_EINVAL 1   /* std::invalid_argument in the reference */
+#define LSG_ELOGIC 2   /* std::logic_error */
+#define LSG_ERUNTIME 3 /* std::runtime_error */
+#define LSG_ECUDA 4    /* CUDA error, unsupported device */
+
+#define LSG_ABI_VERSION 1
+
+/* ------------------------------------------------------------------ core */
+int32_t lsg_abi_version(void);
+const char* lsg_last_error(void);
+lsg_status lsg_device_count(int32_t* n);
+
+typedef struct lsg_ctx_s* lsg_ctx;
+/* One context per GPU: device, a non-blocking stream, event pool. */
+lsg_status lsg_ctx_create(int32_t device, lsg_ctx* out);
+lsg_status lsg_ctx_destroy(lsg_ctx ctx);
+/* Replace the context stream with a caller-owned cudaStream_t (NULL = own). */
+lsg_status lsg_ctx_set_stream(lsg_ctx ctx, void* cuda_stream);
+lsg_status lsg_ctx_get_stream(lsg_ctx ctx, void** cuda_stream);
+lsg_status lsg_ctx_sync(lsg_ctx ctx);
+/* Kernel launches issued through this context since creation (telemetry). */
+lsg_status lsg_ctx_launch_count(lsg_ctx ctx, int64_t* n);
+/* Device / pinned-host memory helpers for callers without a CUDA runtime. */
+lsg_status lsg_dev_alloc(lsg_ctx ctx, size_t bytes, void** out);
+lsg_status lsg_dev_free(lsg_ctx ctx, void* p);
+lsg_status lsg_host_alloc(size_t bytes, void** out);
+lsg_status lsg_host_free(void* p);
+lsg_status lsg_copy(lsg_ctx ctx, void* dst, const void* src, size_t bytes); /* async, [any]->[any] */
+
+/* ------------------------------------------------------------- segmenter
+ * Replaces lipstream::Segmenter (segmenter.hpp:76-111) and VadTracker
+ * (vad.hpp:30-47) for many streams at once.  Each stream is an independent
+ * reference Segmenter: same chunk discipline, same cuts, same metrics. */
+typedef struct {
+  int32_t mode;                /* 0 Baseline, 1 Semantic        (segmenter.hpp:43-50) */
+  int32_t peak_mode;           /* 0 Decay, 1 MaxHold, 2 Absolute (vad.hpp:13-17)      */
+  double peak_half_life_ms;    /* 10000                          (vad.hpp:21)         */
+  double speech_threshold_db;  /* -40                            (vad.hpp:22)         */
+  int64_t frame_ms;            /* 20                             (vad.hpp:23)         */
+  int64_t min_silence_ms;      /* 500                            (segmenter.hpp:54)   */
+  int64_t min_segment_ms;      /* 1500                           (segmenter.hpp:55)   */
+  int64_t max_segment_ms;      /* 10000                          (segmenter.hpp:56)   */
+  int32_t sample_rate;         /* 16000                          (segmenter.hpp:57)   */
+  int32_t flags_only;          /* 1: run the VAD only and keep per-frame speech flags
+                                  for a host state machine (BoundaryScorer path,
+                                  segmenter.cpp:84-90); 0: full device state machine */
+} lsg_seg_cfg;
+
+typedef struct {
+  int64_t begin, end;          /* ms, RawSegment::begin/end (segmenter.hpp:13-21) */
+  double confidence;
+  int32_t cause;               /* 0 Pause, 1 Forced, 2 Eos (segmenter.hpp:11)      */
+  int32_t stream;
+  int64_t sample_off;          /* first sample of RawSegment::audio in the stream  */
+  int64_t sample_len;          /* == RawSegment::audio.samples.size()              */
+} lsg_cut;
+
+typedef struct {               /* SegmenterMetrics (segmenter.hpp:60-68) */
+  int64_t frames, speech_frames, cuts_pause, cuts_forced, cuts_eos, scorer_calls;
+  double scorer_cost_ms;
+} lsg_seg_metrics;
+
+typedef struct lsg_seg_s* lsg_seg;
+lsg_status lsg_seg_cfg_default(lsg_seg_cfg* cfg);
+/* Segmenter::Segmenter (segmenter.cpp:9-23): EINVAL on the same configs.
+ * max_push_samples bounds the samples of one stream in one push call. */
+lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams,
+                          int64_t max_push_samples, lsg_seg* out);
+lsg_status lsg_seg_destroy(lsg_seg h);
+/* Segmenter::push for n_chunks streams at once (segmenter.cpp:25-49); a
+ * stream appears at most once per call.  pcm[i] is [any] unless
+ * pcm_on_device, then [dev].  ELOGIC after finish, EINVAL on a rate
+ * mismatch or a non-contiguous chunk -- checked for every chunk before any
+ * device work, so a failing call changes no stream. */
+lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams,
+                        const int16_t* const* pcm, const int64_t* n_samples,
+                        const int64_t* start_ms, int32_t sample_rate, int32_t pcm_on_device);
+/* Segmenter::finish (segmenter.cpp:120-145) for the listed streams. */
+lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams);
+/* Drains the cuts a stream emitted since the last call, in order.  Returns
+ * the count in *n_out even when it exceeds cap (nothing is drained then). */
+lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t cap,
+                             int64_t* n_out);
+/* All streams at once: cuts of every stream appended in stream order. */
+lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* n_out);
+lsg_status lsg_seg_get_metrics(lsg_seg h, int32_t stream, lsg_seg_metrics* out);
+/* flags_only mode: per-frame speech decisions of the frames the stream
+ * consumed in the last push (VadTracker::FrameResult::speech, vad.hpp:34-37). */
+lsg_status lsg_seg_take_flags(lsg_seg h, int32_t stream, uint8_t* speech, int64_t cap,
+                              int64_t* n_out);
+
+/* ------------------------------------------------------------------- mel
+ * Replaces compute_mel / mel_frame_count (mel.hpp:33-39, mel.cpp:40-127). */
+typedef struct {               /* MelConfig (mel.hpp:12-19) */
+  int32_t sample_rate, fft_size, hop, n_mels;
+  double fmin, fmax;
+} lsg_mel_cfg;
+
+typedef struct lsg_mel_s* lsg_mel;
+lsg_status lsg_mel_cfg_default(lsg_mel_cfg* cfg);
+/* mel_frame_count (mel.cpp:40-44); EINVAL on a bad config (mel.cpp:27-37). */
+lsg_status lsg_mel_frames(int64_t n_samples, const lsg_mel_cfg* cfg, int64_t* frames);
+/* Builds window, filterbank (host fp64, exactly mel.cpp:83-110) and FFT
+ * tables once.  max_frames bounds one compute call. */
+lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frames, lsg_mel* out);
+lsg_status lsg_mel_destroy(lsg_mel h);
+/* compute_mel of one buffer: pcm [any] (n samples) -> out [any]
+ * [frames][n_mels] f32, row major like MelSpectrogram::data. */
+lsg_status lsg_mel_compute(lsg_mel h, const int16_t* pcm, int64_t n, float* out,
+                           int64_t* frames);
+/* Many segments of device-resident PCM in one launch: segment i reads
+ * n_samples[i] samples at pcm_base + pcm_off[i] and writes its frames at row
+ * out_row[i] of out_base.  Offsets/lengths are [host]; pcm_base, out_base [dev]. */
+lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_base,
+                                 const int64_t* pcm_off, const int64_t* n_samples,
+                                 float* out_base, const int64_t* out_row);
+
+/* ------------------------------------------------------------- generator
+ * The lip-sync stage.  The reference only has the cost model mock_lipsync
+ * (visual_mocks.hpp:17-43, visual_mocks.cpp:24-51); this is the Wav2Lip
+ * generator forward it stands for, in bf16 on
+ * tcgen05 tensor cores. */
+#define LSG_PREC_BF16 0
+#define LSG_OUT_F32_NCHW 0      /* [B][3][96][96] f32 in [0,1] */
+#define LSG_OUT_U8_NHWC 1       /* [B][96][96][3] u8, round(255*x) */
+
+typedef struct lsg_gen_s* lsg_gen;
+/* Number of floats in the weight blob (BN folded; layer order and per-layer
+ * layout documented in DESIGN.md §Generator and lsg_gen_layer_info). */
+lsg_status lsg_gen_param_count(int64_t* n);
+/* Per-layer shape table: 12 ints per layer {kind(0 conv,1 convT), cin, cout,
+ * kh, kw, sh, sw, ph, pw, oph, opw, residual}; *n_layers on return. */
+lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap_layers, int32_t* n_layers);
+lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights /*[host]*/, int64_t n_floats,
+                          int32_t precision, int32_t max_batch, lsg_gen* out);
+lsg_status lsg_gen_destroy(lsg_gen h);
+/* Forward of B frames, all inputs [dev]:
+ *   mel_rows  [rows][80] f32 log-mel rows (lsg_mel output)
+ *   chunk_row [B] first row of each frame's 16-row mel window
+ *   target    [B][96][96][3] u8 face crops (lower half masked on device)
+ *   refs      [R][96][96][3] u8 reference crops, ref_index [B] into them
+ *   out       see out_format.  B <= max_batch. */
+lsg_status lsg_gen_forward(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
+                           const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
+                           void* out, int32_t out_format, int32_t B);
+/* mock_lipsync's input contract (visual_mocks.cpp:40-51): EINVAL when
+ * n_frames < 2 or |audio_span - frame_span| > 150 ms. */
+lsg_status lsg_lipsync_validate(int64_t audio_span_ms, int64_t frame_span_ms, int64_t n_frames);
+
+/* -------------------------------------------------------------- pipeline
+ * Replaces the per-clip driver run_pipeline_input (runner.cpp:239-351) for
+ * the GPU stages: segment -> mel per segment -> gather frames -> generator,
+ * for many streams.  Streams are independent; a multi-GPU job gives each
+ * rank its own context and shard of streams (no collective). */
+typedef struct {
+  int32_t n_streams;
+  int32_t max_stream_ms;       /* longest stream accepted                      */
+  double fps;                  /* video frame rate (frames at llround(i*1000/fps)) */
+  int64_t gather_margin_ms;    /* 50 (runner.cpp:30, orchestrator.cpp:90-91)   */
+  int32_t max_batch;           /* generator batch (<= lsg_gen max_batch)       */
+  int32_t out_format;          /* LSG_OUT_*                                    */
+} lsg_pipe_cfg;
+
+typedef struct {
+  int32_t stream, segment;     /* segment index within the stream            */
+  int64_t frame_index;         /* video frame index                          */
+  int64_t ts_ms;
+  int32_t mel_row;             /* chunk start row within the segment mel    */
+  int32_t pad;
+} lsg_frame_rec;
+
+typedef struct {
+  int64_t segments, mel_frames, frames_rendered, unique_frames;
+  double ms_segment, ms_mel, ms_generator, ms_total; /* device time per stage */
+} lsg_pipe_stats;
+
+typedef struct lsg_pipe_s* lsg_pipe;
+lsg_status lsg_pipe_create(lsg_ctx ctx, const lsg_pipe_cfg* cfg, const lsg_seg_cfg* seg,
+                           const lsg_mel_cfg* mel, lsg_gen gen, lsg_pipe* out);
+lsg_status lsg_pipe_destroy(lsg_pipe h);
+/* One pass over all streams.  [host] inputs: pcm[s] (n_samples[s]),
+ * video[s] [n_video[s]][96][96][3] u8 face crops, refs [n_streams][96][96][3].
+ * Outputs [host]: recs [cap] and frames [cap] in out_format; *n_out frames. */
+lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_samples,
+                        const uint8_t* const* video, const int64_t* n_video, const uint8_t* refs,
+                        lsg_frame_rec* recs, void* frames, int64_t cap, int64_t* n_out,
+                        lsg_pipe_stats* stats);
+
+/* ------------------------------------------------------- synthetic input
+ * render_pattern (synth.cpp:46-65) for workload generation: tone bursts on
+ * a silence floor, phase restarting per burst.  Host-only. */
+lsg_status lsg_synth_pattern(int64_t lead_silence_ms, int32_t n_bursts, const int64_t* speech_ms,
+                             const int64_t* pause_ms, double tone_hz, double amplitude,
+                             int64_t total_ms, int32_t sample_rate, int16_t* out, int64_t cap,
+                             int64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSG_H */

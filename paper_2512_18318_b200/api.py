@@ -1,0 +1,467 @@
+"""Host-side mirror of the reference operator API over the C ABI.
+
+Same names, argument meaning and error behaviour as lipstream's
+``Segmenter`` (segmenter.hpp:76-111), ``VadConfig`` (vad.hpp:19-24),
+``compute_mel`` / ``mel_frame_count`` (mel.hpp:33-39) and the lip-sync stage
+(visual_mocks.hpp:17-43), so parity tests read like the reference's own
+tests.  All compute runs in liblsg.so on the GPU; this module only moves
+buffers and keeps the per-stream bookkeeping a RawSegment needs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import (Cut, InvalidArgument, LogicError, MelCfg, SegCfg, SegMetrics, lib)
+
+
+class SegmenterMode(enum.IntEnum):
+    Baseline = 0
+    Semantic = 1
+
+
+class PeakMode(enum.IntEnum):
+    Decay = 0
+    MaxHold = 1
+    Absolute = 2
+
+
+class CutCause(enum.IntEnum):
+    Pause = 0
+    Forced = 1
+    Eos = 2
+
+
+@dataclass
+class AudioBuffer:
+    """include/lipstream/audio.hpp:12-20."""
+    samples: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int16))
+    sample_rate: int = 16000
+    start: int = 0
+
+    def duration_ms(self) -> int:
+        return int(round(1000.0 * len(self.samples) / self.sample_rate))
+
+    def empty(self) -> bool:
+        return len(self.samples) == 0
+
+
+@dataclass
+class VadConfig:
+    peak_mode: PeakMode = PeakMode.Decay
+    peak_half_life_ms: float = 10000.0
+    speech_threshold_db: float = -40.0
+    frame_ms: int = 20
+
+
+@dataclass
+class SegmenterConfig:
+    mode: SegmenterMode = SegmenterMode.Semantic
+    vad: VadConfig = field(default_factory=VadConfig)
+    min_silence_ms: int = 500
+    min_segment_ms: int = 1500
+    max_segment_ms: int = 10000
+    sample_rate: int = 16000
+
+    def to_c(self, flags_only: bool = False) -> SegCfg:
+        return SegCfg(int(self.mode), int(self.vad.peak_mode), float(self.vad.peak_half_life_ms),
+                      float(self.vad.speech_threshold_db), int(self.vad.frame_ms), int(self.min_silence_ms),
+                      int(self.min_segment_ms), int(self.max_segment_ms), int(self.sample_rate),
+                      1 if flags_only else 0)
+
+
+@dataclass
+class RawSegment:
+    begin: int = 0
+    end: int = 0
+    audio: AudioBuffer = field(default_factory=AudioBuffer)
+    confidence: float = 1.0
+    cause: CutCause = CutCause.Eos
+
+    def duration_ms(self) -> int:
+        return self.end - self.begin
+
+
+@dataclass
+class BoundaryContext:
+    pause_start: int
+    silence_run_ms: int
+    segment_span_ms: int
+
+
+@dataclass
+class BoundaryDecision:
+    cut: bool = True
+    confidence: float = 1.0
+    cost_ms: float = 0.0
+
+
+@dataclass
+class SegmenterMetrics:
+    frames: int = 0
+    speech_frames: int = 0
+    cuts_pause: int = 0
+    cuts_forced: int = 0
+    cuts_eos: int = 0
+    scorer_calls: int = 0
+    scorer_cost_ms: float = 0.0
+
+
+class Context:
+    """One GPU: device + stream (lsg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = lib()
+        h = C.c_void_p()
+        self.lib.call("lsg_ctx_create", device, C.byref(h))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        self.lib.call("lsg_ctx_sync", self.h)
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        self.lib.call("lsg_ctx_launch_count", self.h, C.byref(n))
+        return n.value
+
+    def stream_ptr(self) -> int:
+        p = C.c_void_p()
+        self.lib.call("lsg_ctx_get_stream", self.h, C.byref(p))
+        return p.value or 0
+
+    def set_stream(self, ptr: int | None):
+        self.lib.call("lsg_ctx_set_stream", self.h, C.c_void_p(ptr or 0))
+
+
+_DEFAULT_CTX: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _DEFAULT_CTX:
+        _DEFAULT_CTX[device] = Context(device)
+    return _DEFAULT_CTX[device]
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+class MultiStreamSegmenter:
+    """n independent reference Segmenters on one GPU (lsg_seg)."""
+
+    def __init__(self, cfg: SegmenterConfig, n_streams: int, max_push_samples: int, ctx: Context | None = None,
+                 flags_only: bool = False):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.cfg = cfg
+        self.n = n_streams
+        h = C.c_void_p()
+        c = cfg.to_c(flags_only)
+        self.lib.call("lsg_seg_create", self.ctx.h, C.byref(c), n_streams, max_push_samples, C.byref(h))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_seg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def push(self, streams, chunks, starts, sample_rate=None, on_device=False):
+        """chunks: list of int16 numpy arrays (host) or raw device pointers + lengths."""
+        n = len(streams)
+        ids = (C.c_int32 * max(n, 1))(*streams)
+        if on_device:
+            ptrs = (C.c_void_p * max(n, 1))(*[p for p, _ in chunks])
+            lens = (C.c_int64 * max(n, 1))(*[ln for _, ln in chunks])
+            keep = None
+        else:
+            keep = [np.ascontiguousarray(c, np.int16) for c in chunks]
+            ptrs = (C.c_void_p * max(n, 1))(*[k.ctypes.data for k in keep])
+            lens = (C.c_int64 * max(n, 1))(*[len(k) for k in keep])
+        st = (C.c_int64 * max(n, 1))(*starts)
+        rate = self.cfg.sample_rate if sample_rate is None else sample_rate
+        self.lib.call("lsg_seg_push", self.h, n, ids, ptrs, lens, st, rate, 1 if on_device else 0)
+        del keep
+
+    def finish(self, streams):
+        n = len(streams)
+        ids = (C.c_int32 * max(n, 1))(*streams)
+        self.lib.call("lsg_seg_finish", self.h, n, ids)
+
+    def take_cuts(self, stream: int) -> list[Cut]:
+        n = C.c_int64()
+        self.lib.call("lsg_seg_take_cuts", self.h, stream, None, 0, C.byref(n))
+        buf = (Cut * max(n.value, 1))()
+        self.lib.call("lsg_seg_take_cuts", self.h, stream, buf, n.value, C.byref(n))
+        return [buf[i] for i in range(n.value)]
+
+    def take_all_cuts(self) -> list[Cut]:
+        n = C.c_int64()
+        self.lib.call("lsg_seg_take_all_cuts", self.h, None, 0, C.byref(n))
+        buf = (Cut * max(n.value, 1))()
+        self.lib.call("lsg_seg_take_all_cuts", self.h, buf, n.value, C.byref(n))
+        return [buf[i] for i in range(n.value)]
+
+    def take_flags(self, stream: int) -> np.ndarray:
+        n = C.c_int64()
+        self.lib.call("lsg_seg_take_flags", self.h, stream, None, 0, C.byref(n))
+        out = np.zeros(max(n.value, 1), np.uint8)
+        self.lib.call("lsg_seg_take_flags", self.h, stream, _ptr(out), n.value, C.byref(n))
+        return out[: n.value]
+
+    def metrics(self, stream: int) -> SegmenterMetrics:
+        m = SegMetrics()
+        self.lib.call("lsg_seg_get_metrics", self.h, stream, C.byref(m))
+        return SegmenterMetrics(m.frames, m.speech_frames, m.cuts_pause, m.cuts_forced, m.cuts_eos,
+                                m.scorer_calls, m.scorer_cost_ms)
+
+
+class Segmenter:
+    """Drop-in for lipstream::Segmenter (segmenter.hpp:76-111).
+
+    VAD, frame decisions and (without a scorer) the whole state machine run
+    on the GPU.  With a BoundaryScorer the device returns per-frame speech
+    flags and the state machine runs here, so scorer calls happen once per
+    qualifying pause, in order, exactly as segmenter.cpp:84-90."""
+
+    def __init__(self, cfg: SegmenterConfig | None = None, scorer=None, ctx: Context | None = None,
+                 max_push_samples: int = 1 << 22):
+        self.cfg = cfg or SegmenterConfig()
+        self.scorer = scorer
+        self._dev = MultiStreamSegmenter(self.cfg, 1, max_push_samples, ctx, flags_only=scorer is not None)
+        self._rate = self.cfg.sample_rate
+        self._pending = np.zeros(0, np.int16)  # samples of the open segment (host copy for RawSegment.audio)
+        self._stage = 0
+        self._finished = False
+        self._metrics = SegmenterMetrics()
+        # host state machine (scorer path only)
+        self._fs = self.cfg.sample_rate * self.cfg.vad.frame_ms // 1000
+        self._sm = dict(base=0, seg_start=0, consumed=0, speech_seen=False, silence_run=0, cand_open=False,
+                        cand_cut=False, conf=1.0, pause_start=0, emitted=0)
+        self._started = False
+
+    def push(self, chunk: AudioBuffer) -> list[RawSegment]:
+        samples = np.ascontiguousarray(chunk.samples, np.int16)
+        # discipline checks happen in the C ABI (LogicError / InvalidArgument)
+        self._dev.push([0], [samples], [int(chunk.start)], sample_rate=chunk.sample_rate)
+        if len(samples) == 0:
+            return []
+        self._pending = np.concatenate([self._pending, samples])
+        if not self._started:
+            self._started = True
+            self._sm["base"] = self._sm["seg_start"] = int(chunk.start)
+        if self.scorer is None:
+            return self._materialise(self._dev.take_cuts(0))
+        return self._host_machine(self._dev.take_flags(0))
+
+    def finish(self) -> list[RawSegment]:
+        self._dev.finish([0])
+        self._finished = True
+        if self.scorer is None:
+            return self._materialise(self._dev.take_cuts(0))
+        # finish() (segmenter.cpp:120-145) on the host state
+        sm = self._sm
+        fs = self._fs
+        stage = sm["emitted"] + len(self._pending) - sm["consumed"] * fs  # samples never framed
+        tail_ms = stage * 1000 // self._rate
+        if not sm["speech_seen"] or len(self._pending) == 0:
+            self._pending = self._pending[:0]
+            return []
+        end = sm["base"] + sm["consumed"] * self.cfg.vad.frame_ms + tail_ms
+        seg = RawSegment(sm["seg_start"], end, AudioBuffer(self._pending.copy(), self._rate, sm["seg_start"]),
+                         1.0, CutCause.Eos)
+        self._pending = self._pending[:0]
+        self._metrics.cuts_eos += 1
+        return [seg]
+
+    def metrics(self) -> SegmenterMetrics:
+        if self.scorer is None:
+            return self._dev.metrics(0)
+        m = self._dev.metrics(0)
+        self._metrics.frames = m.frames
+        self._metrics.speech_frames = m.speech_frames
+        return self._metrics
+
+    # -- helpers -------------------------------------------------------
+    def _materialise(self, cuts) -> list[RawSegment]:
+        out = []
+        for c in cuts:
+            k = int(c.sample_len)
+            audio = AudioBuffer(self._pending[:k].copy(), self._rate, int(c.begin))
+            self._pending = self._pending[k:]
+            out.append(RawSegment(int(c.begin), int(c.end), audio, float(c.confidence), CutCause(c.cause)))
+        return out
+
+    def _emit(self, out, cut_ms, conf, cause):
+        sm = self._sm
+        split = (cut_ms - sm["seg_start"]) * self._rate // 1000
+        audio = AudioBuffer(self._pending[:split].copy(), self._rate, sm["seg_start"])
+        self._pending = self._pending[split:]
+        out.append(RawSegment(sm["seg_start"], cut_ms, audio, conf, cause))
+        sm["emitted"] += split
+        sm["seg_start"] = cut_ms
+        sm["speech_seen"] = False
+
+    def _host_machine(self, flags) -> list[RawSegment]:
+        """process_frame (segmenter.cpp:51-99) over device VAD decisions."""
+        cfg, sm, out = self.cfg, self._sm, []
+        fm = cfg.vad.frame_ms
+        for sp in flags:
+            f0 = sm["base"] + sm["consumed"] * fm
+            f1 = f0 + fm
+            if sp:
+                if sm["speech_seen"] and sm["silence_run"] >= cfg.min_silence_ms and sm["cand_open"] and sm["cand_cut"]:
+                    self._emit(out, sm["pause_start"] + sm["silence_run"] // 2, sm["conf"], CutCause.Pause)
+                    self._metrics.cuts_pause += 1
+                sm["silence_run"] = 0
+                sm["cand_open"] = False
+                sm["cand_cut"] = False
+                sm["speech_seen"] = True
+            else:
+                if sm["silence_run"] == 0:
+                    sm["pause_start"] = f0
+                sm["silence_run"] += fm
+                if not sm["cand_open"] and sm["silence_run"] >= cfg.min_silence_ms and sm["speech_seen"]:
+                    sm["cand_open"] = True
+                    sm["cand_cut"] = True
+                    sm["conf"] = 1.0
+                    if cfg.mode == SegmenterMode.Semantic:
+                        if sm["pause_start"] - sm["seg_start"] < cfg.min_segment_ms:
+                            sm["cand_cut"] = False
+                        elif self.scorer is not None:
+                            d = self.scorer(BoundaryContext(sm["pause_start"], sm["silence_run"],
+                                                            sm["pause_start"] - sm["seg_start"]))
+                            self._metrics.scorer_calls += 1
+                            self._metrics.scorer_cost_ms += d.cost_ms
+                            sm["cand_cut"] = bool(d.cut)
+                            sm["conf"] = float(d.confidence)
+            if cfg.mode == SegmenterMode.Semantic and sm["speech_seen"] and f1 - sm["seg_start"] >= cfg.max_segment_ms:
+                self._emit(out, f1, 1.0, CutCause.Forced)
+                self._metrics.cuts_forced += 1
+            sm["consumed"] += 1
+        return out
+
+
+# --------------------------------------------------------------------- mel
+@dataclass(frozen=True)
+class MelConfig:
+    """include/lipstream/mel.hpp:12-19."""
+    sample_rate: int = 16000
+    fft_size: int = 1024
+    hop: int = 256
+    n_mels: int = 80
+    fmin: float = 0.0
+    fmax: float = 8000.0
+
+    def to_c(self) -> MelCfg:
+        return MelCfg(self.sample_rate, self.fft_size, self.hop, self.n_mels, self.fmin, self.fmax)
+
+
+@dataclass
+class MelSpectrogram:
+    n_frames: int = 0
+    n_mels: int = 0
+    data: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.float32))  # [frame][mel]
+
+    def at(self, frame: int, mel: int) -> float:
+        return float(self.data[frame, mel])
+
+
+def mel_frame_count(n_samples: int, cfg: MelConfig = MelConfig()) -> int:
+    c = cfg.to_c()
+    f = C.c_int64()
+    lib().call("lsg_mel_frames", n_samples, C.byref(c), C.byref(f))
+    return f.value
+
+
+class MelExtractor:
+    """A reusable lsg_mel handle (tables built once)."""
+
+    def __init__(self, cfg: MelConfig = MelConfig(), max_frames: int = 1 << 16, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self.cfg = cfg
+        c = cfg.to_c()
+        h = C.c_void_p()
+        self.lib.call("lsg_mel_create", self.ctx.h, C.byref(c), max_frames, C.byref(h))
+        self.h = h
+        self.max_frames = max_frames
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_mel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __call__(self, audio: AudioBuffer) -> MelSpectrogram:
+        pcm = np.ascontiguousarray(audio.samples, np.int16)
+        F = mel_frame_count(len(pcm), self.cfg)
+        out = np.zeros((max(F, 1), self.cfg.n_mels), np.float32)
+        f = C.c_int64()
+        self.lib.call("lsg_mel_compute", self.h, _ptr(pcm), len(pcm), _ptr(out), C.byref(f))
+        return MelSpectrogram(f.value, self.cfg.n_mels, out[: f.value])
+
+    def batch_device(self, pcm_dev: int, offsets, lengths, out_dev: int, out_rows):
+        n = len(offsets)
+        o = (C.c_int64 * max(n, 1))(*offsets)
+        ln = (C.c_int64 * max(n, 1))(*lengths)
+        r = (C.c_int64 * max(n, 1))(*out_rows)
+        self.lib.call("lsg_mel_compute_batch", self.h, n, C.c_void_p(pcm_dev), o, ln, C.c_void_p(out_dev), r)
+
+
+_MEL_CACHE: dict = {}
+
+
+def compute_mel(audio: AudioBuffer, cfg: MelConfig = MelConfig()) -> MelSpectrogram:
+    """Drop-in for compute_mel (mel.hpp:39)."""
+    F = mel_frame_count(len(audio.samples), cfg)  # validates like mel.cpp:27-37
+    key = cfg
+    ext = _MEL_CACHE.get(key)
+    if ext is None or ext.max_frames < F:
+        ext = MelExtractor(cfg, max(F, 1 << 12))
+        _MEL_CACHE[key] = ext
+    return ext(audio)
+
+
+def synth_pattern(lead_silence_ms: int, bursts, tone_hz: float, amplitude: float, total_ms: int,
+                  sample_rate: int = 16000) -> np.ndarray:
+    """render_pattern restated in liblsg (workload generation)."""
+    n = C.c_int64()
+    sp = (C.c_int64 * len(bursts))(*[b[0] for b in bursts])
+    pa = (C.c_int64 * len(bursts))(*[b[1] for b in bursts])
+    cap = total_ms * sample_rate // 1000
+    out = np.zeros(max(cap, 1), np.int16)
+    lib().call("lsg_synth_pattern", lead_silence_ms, len(bursts), sp, pa, tone_hz, amplitude, total_ms, sample_rate,
+               _ptr(out), cap, C.byref(n))
+    return out[: n.value]
+
+
+__all__ = ["AudioBuffer", "BoundaryContext", "BoundaryDecision", "Context", "CutCause", "InvalidArgument",
+           "LogicError", "MelConfig", "MelExtractor", "MelSpectrogram", "MultiStreamSegmenter", "PeakMode",
+           "RawSegment", "Segmenter", "SegmenterConfig", "SegmenterMetrics", "SegmenterMode", "VadConfig",
+           "compute_mel", "default_context", "mel_frame_count", "synth_pattern"]

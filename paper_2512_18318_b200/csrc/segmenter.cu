@@ -1,0 +1,901 @@
+// segmenter.cu -- energy/silence segmenter on sm_100a (include/lsg.h "segmenter").
+//
+// Replaces lipstream::VadTracker::update (vad.cpp:26-53) and the Segmenter
+// state machine (segmenter.cpp:25-145) for many streams per launch.
+//
+//   K1 seg_frame_stats  HBM-streaming pass: per 20 ms frame, sum of squares
+//                       (int64, exact like the reference's double sum of
+//                       integer squares) and max|s|; 16-byte vector loads,
+//                       warp-shuffle reductions.  2 B/sample read, 16 B/frame
+//                       written (2.5% of the input).
+//   K2 seg_scan         one CTA per stream: the decaying-peak recurrence
+//                       (sequential by definition, one DMUL+DMAX per frame),
+//                       per-frame dB decisions in parallel (ballot-packed),
+//                       then the integer-millisecond state machine, which
+//                       fast-forwards over runs of frames that cannot raise
+//                       an event and steps event frames exactly like
+//                       process_frame (segmenter.cpp:51-99).
+//   K3 seg_carry        keeps each stream's sub-frame tail (stage_,
+//                       segmenter.cpp:40-48) on the device.
+//   K4 seg_collect      compacts cuts/flags/state into mapped pinned memory,
+//                       so a push costs one stream synchronisation.
+//
+// Bit-exactness: sqrt, division and the peak multiply are
+// IEEE round-to-nearest on both sides (__dsqrt_rn/__ddiv_rn/__dmul_rn, no
+// FMA contraction); the decay factor exp2(-frame/half_life) is computed on
+// the host by the same libm call as vad.cpp:37.  log10 is the only libm
+// function on the device: frames whose fast log10 lands within 1e-9 dB of
+// the threshold are re-decided with a double-double log10 (error ~1e-30),
+// i.e. with the correctly rounded value, which agrees with glibc's log10 on
+// every decision tested (tests/test_segmenter_gpu.py exact-threshold frames).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "lsg_common.cuh"
+
+namespace lsg {
+namespace seg {
+
+struct Params {
+  int32_t mode, peak_mode;
+  double decay;  // exp2(-frame_ms / half_life), host libm
+  double thr;
+  int64_t frame_ms, min_sil, min_seg, max_seg;
+  int32_t rate, fs;
+  int32_t flags_only, cut_cap;
+  int32_t flag_words;  // per stream, per push
+};
+
+struct alignas(16) DevState {
+  double peak;
+  int64_t base, seg_start, pause_start, silence_run, consumed, emitted;
+  double cand_conf;
+  int32_t speech_seen, cand_open, cand_cut, carry_len;
+  int32_t n_cuts, overflow, n_flag_frames, pad;
+  int64_t m_frames, m_speech, m_pause, m_forced, m_eos;
+};
+
+struct alignas(16) Chunk {
+  const int16_t* pcm;  // device
+  int64_t n;
+  int64_t frame_off;   // into the push-global stats array
+  int64_t start_ms;
+  int64_t total_after; // samples pushed to the stream including this chunk
+  int32_t nframes;
+  int32_t stream;
+  int32_t carry_len;
+  int32_t first;
+};
+
+struct alignas(16) FrameStat {
+  long long sumsq;
+  int32_t fmax;
+  int32_t pad;
+};
+
+// ---------------------------------------------------------------- K1 -----
+constexpr int K1_WARPS = 8;
+constexpr int K1_FPW = 2;  // frames per warp per block
+
+__device__ __forceinline__ void acc8(int4 v, long long& ss, int& mx) {
+  const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int lo = (int)(int16_t)(w[k] & 0xffff);
+    int hi = w[k] >> 16;
+    ss += (long long)(lo * lo) + (long long)(hi * hi);
+    mx = max(mx, max(abs(lo), abs(hi)));
+  }
+}
+
+__global__ void __launch_bounds__(K1_WARPS * 32)
+seg_frame_stats(const Chunk* __restrict__ chunks, const int16_t* __restrict__ carry, int fs,
+                FrameStat* __restrict__ out) {
+  const Chunk c = chunks[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t f0 = ((int64_t)blockIdx.x * K1_WARPS + warp) * K1_FPW;
+  if (f0 >= c.nframes) return;
+  const bool vec = c.carry_len == 0 && (fs & 7) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(c.pcm) & 15) == 0);
+  long long ss[K1_FPW];
+  int mx[K1_FPW];
+#pragma unroll
+  for (int j = 0; j < K1_FPW; ++j) { ss[j] = 0; mx[j] = 0; }
+  if (vec) {
+    const int nv = fs >> 3;  // int4 per frame
+    // issue every load of the warp's frames before reducing (memory-level parallelism)
+#pragma unroll
+    for (int j = 0; j < K1_FPW; ++j) {
+      const int64_t f = f0 + j;
+      if (f >= c.nframes) break;
+      const int4* p = reinterpret_cast<const int4*>(c.pcm + f * fs);
+      for (int q = lane; q < nv; q += 32) acc8(__ldg(p + q), ss[j], mx[j]);
+    }
+  } else {
+    const int16_t* cs = carry + (int64_t)c.stream * fs;
+    for (int j = 0; j < K1_FPW; ++j) {
+      const int64_t f = f0 + j;
+      if (f >= c.nframes) break;
+      for (int q = lane; q < fs; q += 32) {
+        const int64_t idx = f * fs + q;  // index into carry ++ chunk
+        int v = idx < c.carry_len ? cs[idx] : c.pcm[idx - c.carry_len];
+        ss[j] += (long long)(v * v);
+        mx[j] = max(mx[j], abs(v));
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < K1_FPW; ++j) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ss[j] += __shfl_xor_sync(0xffffffffu, ss[j], o);
+      mx[j] = max(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+    }
+  }
+  if (lane < K1_FPW) {
+    const int64_t f = f0 + lane;
+    long long s = ss[0];
+    int m = mx[0];
+#pragma unroll
+    for (int j = 1; j < K1_FPW; ++j)
+      if (lane == j) { s = ss[j]; m = mx[j]; }
+    if (f < c.nframes) {
+      FrameStat r;
+      r.sumsq = s;
+      r.fmax = m;
+      r.pad = 0;
+      out[c.frame_off + f] = r;
+    }
+  }
+}
+
+// ------------------------------------------------------ exact log10 ------
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ dd quick_two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double e = __dsub_rn(b, __dsub_rn(s, a));
+  return {s, e};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  dd t = two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return quick_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  double p = __dmul_rn(a.hi, b.hi);
+  double e = __fma_rn(a.hi, b.hi, -p);
+  e = __fma_rn(a.hi, b.lo, e);
+  e = __fma_rn(a.lo, b.hi, e);
+  return quick_two_sum(p, e);
+}
+__device__ __forceinline__ dd dd_div(dd a, dd b) {
+  double q1 = __ddiv_rn(a.hi, b.hi);
+  dd r = dd_add(a, dd_mul({-q1, 0.0}, b));
+  double q2 = __ddiv_rn(r.hi, b.hi);
+  r = dd_add(r, dd_mul({-q2, 0.0}, b));
+  double q3 = __ddiv_rn(r.hi, b.hi);
+  dd q = quick_two_sum(q1, q2);
+  return dd_add(q, {q3, 0.0});
+}
+
+// log10(x) in double-double, rounded once to double.  x = m 2^e with
+// m in [sqrt(1/2), sqrt(2)); ln m = 2 atanh((m-1)/(m+1)) by its series.
+__device__ double log10_dd(double x) {
+  int e;
+  double m = frexp(x, &e);  // m in [0.5, 1)
+  if (m < 0.70710678118654752440) {
+    m *= 2.0;
+    e -= 1;
+  }
+  dd num = two_sum(m, -1.0);
+  dd den = two_sum(m, 1.0);
+  dd s = dd_div(num, den);
+  dd s2 = dd_mul(s, s);
+  dd term = s;
+  dd sum = s;
+  for (int k = 3; k < 80; k += 2) {
+    term = dd_mul(term, s2);
+    dd t = dd_div(term, {(double)k, 0.0});
+    sum = dd_add(sum, t);
+    if (fabs(t.hi) < 1e-40) break;
+  }
+  const dd ln2 = {6.93147180559945286227e-01, 2.31904681384629955842e-17};
+  const dd inv_ln10 = {4.34294481903251816668e-01, 1.09872180683456050377e-17};
+  dd lnm = dd_add(sum, sum);
+  dd ln = dd_add(dd_mul(ln2, {(double)e, 0.0}), lnm);
+  dd r = dd_mul(ln, inv_ln10);
+  return __dadd_rn(r.hi, r.lo);
+}
+
+// VadTracker::update's decision (vad.cpp:47-52) from exact frame stats.
+__device__ __forceinline__ bool vad_decide(long long sumsq, double peak, int n, double thr) {
+  double rms = __dsqrt_rn(__ddiv_rn((double)sumsq, (double)n));
+  double db = -120.0;
+  if (rms > 0.0 && peak > 0.0) {
+    double x = __ddiv_rn(rms, peak);
+    double d = __dmul_rn(20.0, log10(x));
+    if (fabs(d - thr) < 1e-9 * fmax(1.0, fabs(thr))) d = __dmul_rn(20.0, log10_dd(x));
+    db = d > -120.0 ? d : -120.0;
+  }
+  return db > thr;
+}
+
+// ---------------------------------------------------------------- K2 -----
+constexpr int K2_THREADS = 256;
+constexpr int K2_TILE = 2048;
+
+struct Machine {
+  int64_t base, seg_start, pause_start, silence_run, consumed, emitted;
+  double conf;
+  int speech_seen, cand_open, cand_cut;
+  int64_t n_pause, n_forced;
+  int n_cuts, overflow;
+};
+
+__device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) {  // ceil(a/b), b > 0
+  return a >= 0 ? (a + b - 1) / b : -((-a) / b);
+}
+
+// emit_cut (segmenter.cpp:101-118)
+__device__ __forceinline__ void emit(Machine& M, const Params& P, lsg_cut* cuts, int stream,
+                                     int64_t cut_ms, double conf, int cause) {
+  const int64_t split = (cut_ms - M.seg_start) * P.rate / 1000;
+  if (M.n_cuts < P.cut_cap) {
+    lsg_cut c;
+    c.begin = M.seg_start;
+    c.end = cut_ms;
+    c.confidence = conf;
+    c.cause = cause;
+    c.stream = stream;
+    c.sample_off = M.emitted;
+    c.sample_len = split;
+    cuts[M.n_cuts] = c;
+    M.n_cuts++;
+  } else {
+    M.overflow = 1;
+  }
+  M.emitted += split;
+  M.seg_start = cut_ms;
+  M.speech_seen = 0;
+}
+
+// process_frame (segmenter.cpp:51-99), device state machine (no scorer).
+__device__ __forceinline__ void step(Machine& M, const Params& P, lsg_cut* cuts, int stream,
+                                     bool speech) {
+  const int64_t f0 = M.base + M.consumed * P.frame_ms;
+  const int64_t f1 = f0 + P.frame_ms;
+  if (speech) {
+    if (M.speech_seen && M.silence_run >= P.min_sil && M.cand_open && M.cand_cut) {
+      emit(M, P, cuts, stream, M.pause_start + M.silence_run / 2, M.conf, 0);
+      M.n_pause++;
+    }
+    M.silence_run = 0;
+    M.cand_open = 0;
+    M.cand_cut = 0;
+    M.speech_seen = 1;
+  } else {
+    if (M.silence_run == 0) M.pause_start = f0;
+    M.silence_run += P.frame_ms;
+    if (!M.cand_open && M.silence_run >= P.min_sil && M.speech_seen) {
+      M.cand_open = 1;
+      M.cand_cut = 1;
+      M.conf = 1.0;
+      if (P.mode == 1 && M.pause_start - M.seg_start < P.min_seg) M.cand_cut = 0;
+    }
+  }
+  if (P.mode == 1 && M.speech_seen && f1 - M.seg_start >= P.max_seg) {
+    emit(M, P, cuts, stream, f1, 1.0, 1);
+    M.n_forced++;
+  }
+  M.consumed++;
+}
+
+__device__ __forceinline__ int get_bit(const uint32_t* bits, int i) { return (bits[i >> 5] >> (i & 31)) & 1; }
+
+// first index >= i in [i, n) whose bit differs from b, or n
+__device__ __forceinline__ int run_end(const uint32_t* bits, int i, int n, int b) {
+  int wi = i >> 5;
+  uint32_t w = (b ? ~bits[wi] : bits[wi]) & (0xffffffffu << (i & 31));
+  const int nw = (n + 31) >> 5;
+  while (!w) {
+    if (++wi >= nw) return n;
+    w = b ? ~bits[wi] : bits[wi];
+  }
+  int p = (wi << 5) + __ffs(w) - 1;
+  return p < n ? p : n;
+}
+
+// The state machine over n decided frames, skipping event-free runs.
+__device__ void run_machine(Machine& M, const Params& P, lsg_cut* cuts, int stream,
+                            const uint32_t* bits, int n) {
+  int i = 0;
+  while (i < n) {
+    const int b = get_bit(bits, i);
+    const int e = run_end(bits, i, n, b);
+    if (b && M.silence_run == 0 && !M.cand_open && !M.cand_cut && M.speech_seen) {
+      // steady speech: only the forced split can fire (segmenter.cpp:94-98)
+      if (P.mode == 1) {
+        int64_t k = cdiv(P.max_seg + M.seg_start - M.base, P.frame_ms) - M.consumed - 1;
+        if (k < 0) k = 0;
+        if (i + k < e) {
+          M.consumed += k;
+          i += (int)k;
+          step(M, P, cuts, stream, true);
+          ++i;
+          continue;
+        }
+      }
+      M.consumed += e - i;
+      i = e;
+      continue;
+    }
+    if (!b && M.silence_run > 0) {
+      // steady silence: candidate opening and forced split are the only events
+      int64_t k = INT64_MAX;
+      if (!M.cand_open && M.speech_seen) {
+        int64_t kc = cdiv(P.min_sil - M.silence_run, P.frame_ms) - 1;
+        k = kc < 0 ? 0 : kc;
+      }
+      if (P.mode == 1 && M.speech_seen) {
+        int64_t kf = cdiv(P.max_seg + M.seg_start - M.base, P.frame_ms) - M.consumed - 1;
+        if (kf < 0) kf = 0;
+        k = kf < k ? kf : k;
+      }
+      if (k < (int64_t)(e - i)) {
+        M.silence_run += k * P.frame_ms;
+        M.consumed += k;
+        i += (int)k;
+        step(M, P, cuts, stream, false);
+        ++i;
+        continue;
+      }
+      M.silence_run += (int64_t)(e - i) * P.frame_ms;
+      M.consumed += e - i;
+      i = e;
+      continue;
+    }
+    step(M, P, cuts, stream, b != 0);
+    ++i;
+  }
+}
+
+__global__ void __launch_bounds__(K2_THREADS)
+seg_scan(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, DevState* st,
+         lsg_cut* __restrict__ cuts_all, uint32_t* __restrict__ flags_all, Params P) {
+  __shared__ double s_peak[K2_TILE];
+  __shared__ uint32_t s_bits[K2_TILE / 32];
+  __shared__ int s_speech;
+  const Chunk c = chunks[blockIdx.x];
+  DevState* S = st + c.stream;
+  lsg_cut* cuts = cuts_all + (int64_t)c.stream * P.cut_cap;
+  uint32_t* flags = flags_all + (int64_t)c.stream * P.flag_words;
+  const int tid = threadIdx.x;
+
+  Machine M;
+  double peak;
+  if (tid == 0) {
+    if (c.first) {
+      S->base = c.start_ms;
+      S->seg_start = c.start_ms;
+    }
+    M.base = S->base;
+    M.seg_start = S->seg_start;
+    M.pause_start = S->pause_start;
+    M.silence_run = S->silence_run;
+    M.consumed = S->consumed;
+    M.emitted = S->emitted;
+    M.conf = S->cand_conf;
+    M.speech_seen = S->speech_seen;
+    M.cand_open = S->cand_open;
+    M.cand_cut = S->cand_cut;
+    M.n_pause = 0;
+    M.n_forced = 0;
+    M.n_cuts = 0;
+    M.overflow = S->overflow;
+    peak = S->peak;
+    s_speech = 0;
+  }
+  const FrameStat* fst = stats + c.frame_off;
+  for (int t0 = 0; t0 < c.nframes; t0 += K2_TILE) {
+    const int n = min(K2_TILE, c.nframes - t0);
+    // phase A: decaying peak (vad.cpp:35-45), sequential
+    for (int i = tid; i < n; i += K2_THREADS) s_peak[i] = (double)fst[t0 + i].fmax;
+    __syncthreads();
+    if (tid == 0) {
+      if (P.peak_mode == 0) {
+        for (int i = 0; i < n; ++i) {
+          peak = __dmul_rn(peak, P.decay);
+          const double fm = s_peak[i];
+          peak = fm > peak ? fm : peak;
+          s_peak[i] = peak;
+        }
+      } else if (P.peak_mode == 1) {
+        for (int i = 0; i < n; ++i) {
+          const double fm = s_peak[i];
+          peak = fm > peak ? fm : peak;
+          s_peak[i] = peak;
+        }
+      } else {
+        for (int i = 0; i < n; ++i) s_peak[i] = peak;
+      }
+    }
+    __syncthreads();
+    // phase B: per-frame decisions in parallel, ballot-packed
+    int my_speech = 0;
+    for (int i0 = 0; i0 < n; i0 += K2_THREADS) {
+      const int i = i0 + tid;
+      bool sp = false;
+      if (i < n) sp = vad_decide(fst[t0 + i].sumsq, s_peak[i], P.fs, P.thr);
+      const unsigned bal = __ballot_sync(0xffffffffu, sp);
+      if ((tid & 31) == 0 && i < n) s_bits[i >> 5] = bal;
+      my_speech += sp;
+    }
+    atomicAdd(&s_speech, my_speech);
+    __syncthreads();
+    // phase C: state machine or flag export
+    if (P.flags_only) {
+      const int nw = (n + 31) >> 5;
+      for (int w = tid; w < nw; w += K2_THREADS) flags[(t0 >> 5) + w] = s_bits[w];
+    } else if (tid == 0) {
+      run_machine(M, P, cuts, c.stream, s_bits, n);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (P.flags_only) M.consumed += c.nframes;
+    S->peak = peak;
+    S->seg_start = M.seg_start;
+    S->pause_start = M.pause_start;
+    S->silence_run = M.silence_run;
+    S->consumed = M.consumed;
+    S->emitted = M.emitted;
+    S->cand_conf = M.conf;
+    S->speech_seen = M.speech_seen;
+    S->cand_open = M.cand_open;
+    S->cand_cut = M.cand_cut;
+    S->n_cuts = M.n_cuts;
+    S->overflow = M.overflow;
+    S->n_flag_frames = c.nframes;
+    S->m_frames += c.nframes;
+    S->m_speech += s_speech;
+    S->m_pause += M.n_pause;
+    S->m_forced += M.n_forced;
+  }
+}
+
+// ---------------------------------------------------------------- K3 -----
+// New stage_ after the push: the last (carry_len + n) % fs samples.
+__global__ void seg_carry(const Chunk* __restrict__ chunks, int16_t* carry, DevState* st, int fs) {
+  const Chunk c = chunks[blockIdx.x];
+  int16_t* cs = carry + (int64_t)c.stream * fs;
+  const int64_t total = c.carry_len + c.n;
+  const int r = (int)(total % fs);
+  if (c.nframes == 0) {
+    for (int64_t i = threadIdx.x; i < c.n; i += blockDim.x) cs[c.carry_len + i] = c.pcm[i];
+  } else {
+    for (int i = threadIdx.x; i < r; i += blockDim.x) cs[i] = c.pcm[c.n - r + i];
+  }
+  if (threadIdx.x == 0) st[c.stream].carry_len = r;
+}
+
+// ---------------------------------------------------------------- K4 -----
+// finish() (segmenter.cpp:120-145): EOS flush of the open segment.
+__global__ void seg_finish(const int32_t* __restrict__ streams, const int64_t* __restrict__ totals,
+                           int n, DevState* st, lsg_cut* cuts_all, Params P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = streams[i];
+  DevState* S = st + s;
+  S->n_cuts = 0;
+  S->n_flag_frames = 0;
+  const int64_t tail_ms = (int64_t)S->carry_len * 1000 / P.rate;
+  const int64_t pending = totals[i] - S->emitted;
+  if (!S->speech_seen || pending == 0) return;
+  lsg_cut c;
+  c.begin = S->seg_start;
+  c.end = S->base + S->consumed * P.frame_ms + tail_ms;
+  c.confidence = 1.0;
+  c.cause = 2;
+  c.stream = s;
+  c.sample_off = S->emitted;
+  c.sample_len = pending;
+  cuts_all[(int64_t)s * P.cut_cap] = c;
+  S->n_cuts = 1;
+  S->emitted += pending;
+  S->m_eos += 1;
+}
+
+// Compacts the touched streams' cuts + state (+flags) into mapped host memory.
+__global__ void seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
+                            const lsg_cut* __restrict__ cuts_all, const uint32_t* __restrict__ flags_all,
+                            Params P, DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts,
+                            uint32_t* h_flags, int cut_cap_total) {
+  __shared__ int s_off[1025];
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < n; ++i) {
+      s_off[i] = acc;
+      acc += st[streams[i]].n_cuts;
+    }
+    s_off[n] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) h_offsets[i] = s_off[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) h_state[i] = st[streams[i]];
+  for (int i = 0; i < n; ++i) {
+    const int s = streams[i];
+    const int k = st[s].n_cuts;
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+      if (s_off[i] + j < cut_cap_total) h_cuts[s_off[i] + j] = cuts_all[(int64_t)s * P.cut_cap + j];
+    if (P.flags_only) {
+      const int nw = (st[s].n_flag_frames + 31) >> 5;
+      for (int j = threadIdx.x; j < nw; j += blockDim.x)
+        h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
+    }
+  }
+}
+
+}  // namespace seg
+}  // namespace lsg
+
+using namespace lsg;
+using namespace lsg::seg;
+
+struct StreamHost {
+  bool finished = false;
+  int64_t base = 0;
+  int64_t consumed = 0;   // frames
+  int64_t stage_len = 0;  // samples
+  int64_t total = 0;      // samples pushed
+  std::vector<lsg_cut> cuts;
+  std::vector<uint8_t> flags;
+  lsg_seg_metrics metrics{};
+};
+
+constexpr int kMaxCollect = 1024;  // streams per push call handled by one collect launch
+
+struct lsg_seg_s {
+  Ctx* ctx = nullptr;
+  Params P{};
+  int32_t n_streams = 0;
+  int64_t max_push = 0;
+  int64_t max_frames_push = 0;
+  std::vector<StreamHost> hs;
+  DevBuf<DevState> st;
+  DevBuf<int16_t> carry;
+  DevBuf<lsg_cut> cuts;
+  DevBuf<uint32_t> flags;
+  DevBuf<FrameStat> stats;
+  DevBuf<Chunk> chunks_dev;
+  DevBuf<int16_t> staging;
+  DevBuf<int32_t> streams_dev;
+  DevBuf<int64_t> totals_dev;
+  PinnedBuf<Chunk> chunks_host;
+  PinnedBuf<int32_t> streams_host;
+  PinnedBuf<int64_t> totals_host;
+  // mapped (zero-copy) result area
+  DevState* h_state = nullptr;
+  int32_t* h_off = nullptr;
+  lsg_cut* h_cuts = nullptr;
+  uint32_t* h_flags = nullptr;
+  int64_t h_cut_cap = 0;
+  ~lsg_seg_s() {
+    if (h_state) cudaFreeHost(h_state);
+    if (h_off) cudaFreeHost(h_off);
+    if (h_cuts) cudaFreeHost(h_cuts);
+    if (h_flags) cudaFreeHost(h_flags);
+  }
+};
+
+static void validate_cfg(const lsg_seg_cfg* c) {
+  // member init order: VadTracker(cfg.vad) runs before the Segmenter body
+  // checks (segmenter.cpp:9-10, vad.cpp:13-19)
+  if (c->peak_half_life_ms <= 0) invalid("vad: non-positive half life");
+  if (c->frame_ms <= 0) invalid("vad: non-positive frame");
+  if (c->sample_rate <= 0 || c->sample_rate % 1000 != 0)
+    invalid("segmenter: rate must be a multiple of 1 kHz");
+  if (c->min_silence_ms <= 0) invalid("segmenter: non-positive min silence");
+  if (c->mode == 1) {
+    if (c->min_segment_ms < 0 || c->max_segment_ms <= 0) invalid("segmenter: bad segment bounds");
+    if (c->max_segment_ms <= c->min_segment_ms) invalid("segmenter: max segment under min");
+  }
+  if (c->mode != 0 && c->mode != 1) invalid("segmenter: unknown mode");
+  if (c->peak_mode < 0 || c->peak_mode > 2) invalid("vad: unknown peak mode");
+}
+
+// Runs collect for the listed streams, synchronises, and distributes results.
+static void collect(lsg_seg h, int n, bool finishing) {
+  Ctx* ctx = h->ctx;
+  seg_collect<<<1, 256, 0, ctx->stream>>>(h->streams_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
+                                          h->h_state, h->h_off, h->h_cuts, h->h_flags,
+                                          (int)h->h_cut_cap);
+  LSG_LAUNCHED(ctx);
+  ctx->sync();
+  for (int i = 0; i < n; ++i) {
+    const int s = h->streams_host.p[i];
+    StreamHost& S = h->hs[s];
+    const DevState& D = h->h_state[i];
+    if (D.overflow) fail(LSG_ERUNTIME, "segmenter: cut buffer overflow");
+    const int a = h->h_off[i], b = h->h_off[i + 1];
+    for (int k = a; k < b; ++k) S.cuts.push_back(h->h_cuts[k]);
+    S.metrics.frames = D.m_frames;
+    S.metrics.speech_frames = D.m_speech;
+    S.metrics.cuts_pause = D.m_pause;
+    S.metrics.cuts_forced = D.m_forced;
+    S.metrics.cuts_eos = D.m_eos;
+    if (h->P.flags_only && !finishing) {
+      S.flags.resize((size_t)D.n_flag_frames);
+      const uint32_t* w = h->h_flags + (int64_t)i * h->P.flag_words;
+      for (int f = 0; f < D.n_flag_frames; ++f) S.flags[f] = (w[f >> 5] >> (f & 31)) & 1;
+    }
+  }
+}
+
+extern "C" {
+
+lsg_status lsg_seg_cfg_default(lsg_seg_cfg* c) {
+  return guard([&] {
+    c->mode = 1;
+    c->peak_mode = 0;
+    c->peak_half_life_ms = 10000.0;
+    c->speech_threshold_db = -40.0;
+    c->frame_ms = 20;
+    c->min_silence_ms = 500;
+    c->min_segment_ms = 1500;
+    c->max_segment_ms = 10000;
+    c->sample_rate = 16000;
+    c->flags_only = 0;
+  });
+}
+
+lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams,
+                          int64_t max_push_samples, lsg_seg* out) {
+  return guard([&] {
+    *out = nullptr;
+    validate_cfg(cfg);
+    if (n_streams <= 0 || n_streams > kMaxCollect) invalid("lsg_seg_create: n_streams out of range");
+    if (max_push_samples <= 0) invalid("lsg_seg_create: max_push_samples must be positive");
+    DeviceGuard g(ctx);
+    auto h = new lsg_seg_s();
+    try {
+      h->ctx = ctx;
+      Params& P = h->P;
+      P.mode = cfg->mode;
+      P.peak_mode = cfg->peak_mode;
+      P.decay = std::exp2(-double(cfg->frame_ms) / cfg->peak_half_life_ms);  // vad.cpp:37
+      P.thr = cfg->speech_threshold_db;
+      P.frame_ms = cfg->frame_ms;
+      P.min_sil = cfg->min_silence_ms;
+      P.min_seg = cfg->min_segment_ms;
+      P.max_seg = cfg->max_segment_ms;
+      P.rate = cfg->sample_rate;
+      const int64_t fs = int64_t(cfg->sample_rate) * cfg->frame_ms / 1000;
+      if (fs > (1 << 24)) invalid("segmenter: frame too long");
+      P.fs = (int32_t)fs;
+      P.flags_only = cfg->flags_only ? 1 : 0;
+      h->n_streams = n_streams;
+      h->max_push = max_push_samples;
+      h->max_frames_push = (max_push_samples + fs) / fs + 1;
+      P.cut_cap = (int32_t)std::min<int64_t>(2 * h->max_frames_push + 2, INT32_MAX);  // <= 2 cuts/frame
+      P.flag_words = (int32_t)((h->max_frames_push + 31) / 32);
+      h->hs.resize(n_streams);
+      h->st.alloc(n_streams);
+      LSG_CUDA(cudaMemsetAsync(h->st.p, 0, h->st.bytes(), ctx->stream));
+      if (cfg->peak_mode == 2) {
+        std::vector<DevState> init(n_streams);
+        std::memset(init.data(), 0, init.size() * sizeof(DevState));
+        for (auto& d : init) d.peak = 32767.0;  // vad.cpp:22-24
+        LSG_CUDA(cudaMemcpy(h->st.p, init.data(), h->st.bytes(), cudaMemcpyHostToDevice));
+      }
+      for (auto& d : h->hs) d = StreamHost{};
+      h->carry.alloc((size_t)n_streams * fs);
+      h->cuts.alloc((size_t)n_streams * P.cut_cap);
+      h->flags.alloc((size_t)n_streams * P.flag_words);
+      h->stats.alloc((size_t)n_streams * h->max_frames_push);
+      h->chunks_dev.alloc(n_streams);
+      h->staging.alloc((size_t)n_streams * max_push_samples + 64);
+      h->streams_dev.alloc(n_streams);
+      h->totals_dev.alloc(n_streams);
+      h->chunks_host.alloc(n_streams);
+      h->streams_host.alloc(n_streams);
+      h->totals_host.alloc(n_streams);
+      h->h_cut_cap = (int64_t)n_streams * P.cut_cap;
+      LSG_CUDA(cudaHostAlloc(&h->h_state, sizeof(DevState) * n_streams, cudaHostAllocMapped));
+      LSG_CUDA(cudaHostAlloc(&h->h_off, sizeof(int32_t) * (n_streams + 1), cudaHostAllocMapped));
+      LSG_CUDA(cudaHostAlloc(&h->h_cuts, sizeof(lsg_cut) * h->h_cut_cap, cudaHostAllocMapped));
+      LSG_CUDA(cudaHostAlloc(&h->h_flags, sizeof(uint32_t) * (size_t)n_streams * P.flag_words,
+                             cudaHostAllocMapped));
+      ctx->sync();
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+lsg_status lsg_seg_destroy(lsg_seg h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard g(h->ctx);
+    h->ctx->sync();
+    delete h;
+  });
+}
+
+lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, const int16_t* const* pcm,
+                        const int64_t* n_samples, const int64_t* start_ms, int32_t sample_rate,
+                        int32_t pcm_on_device) {
+  return guard([&] {
+    Ctx* ctx = h->ctx;
+    const Params& P = h->P;
+    if (n_chunks < 0 || n_chunks > h->n_streams) invalid("lsg_seg_push: bad chunk count");
+    // pass 1: the reference's discipline checks (segmenter.cpp:26-38), all
+    // chunks before any state changes
+    std::vector<char> seen(h->n_streams, 0);
+    for (int i = 0; i < n_chunks; ++i) {
+      const int s = streams[i];
+      if (s < 0 || s >= h->n_streams) invalid("lsg_seg_push: stream id out of range");
+      if (seen[s]) invalid("lsg_seg_push: stream listed twice in one push");
+      seen[s] = 1;
+      const StreamHost& S = h->hs[s];
+      if (S.finished) logic("segmenter: push after finish");
+      if (sample_rate != P.rate) invalid("segmenter: sample rate mismatch");
+      if (n_samples[i] < 0 || n_samples[i] > h->max_push) invalid("lsg_seg_push: chunk longer than max_push_samples");
+      if (n_samples[i] == 0) continue;
+      const int64_t staged_ms = S.consumed * P.frame_ms + S.stage_len * 1000 / P.rate;
+      const bool first = S.consumed == 0 && S.stage_len == 0;
+      if (!first && std::llabs(start_ms[i] - (S.base + staged_ms)) > 1)
+        invalid("segmenter: non-contiguous chunk");
+    }
+    DeviceGuard g(ctx);
+    // pass 2: stage + describe chunks
+    int nc = 0;
+    int64_t frame_total = 0, max_frames = 0, stage_off = 0;
+    for (int i = 0; i < n_chunks; ++i) {
+      if (n_samples[i] == 0) continue;
+      const int s = streams[i];
+      StreamHost& S = h->hs[s];
+      Chunk& c = h->chunks_host.p[nc];
+      const bool first = S.consumed == 0 && S.stage_len == 0;
+      const int16_t* src = pcm[i];
+      if (!pcm_on_device && !is_device_ptr(src)) {
+        int16_t* dst = h->staging.p + stage_off;
+        LSG_CUDA(cudaMemcpyAsync(dst, src, n_samples[i] * 2, cudaMemcpyHostToDevice, ctx->stream));
+        src = dst;
+        stage_off += (n_samples[i] + 63) & ~int64_t(63);  // keep 128 B alignment
+      }
+      c.pcm = src;
+      c.n = n_samples[i];
+      c.frame_off = frame_total;
+      c.start_ms = start_ms[i];
+      c.stream = s;
+      c.carry_len = (int32_t)S.stage_len;
+      c.first = first ? 1 : 0;
+      const int64_t tot = S.stage_len + n_samples[i];
+      c.nframes = (int32_t)(tot / P.fs);
+      c.total_after = S.total + n_samples[i];
+      frame_total += c.nframes;
+      max_frames = std::max<int64_t>(max_frames, c.nframes);
+      h->streams_host.p[nc] = s;
+      // host mirror
+      if (first) S.base = start_ms[i];
+      S.consumed += c.nframes;
+      S.stage_len = tot % P.fs;
+      S.total += n_samples[i];
+      ++nc;
+    }
+    for (int i = 0; i < n_chunks; ++i) {
+      StreamHost& S = h->hs[streams[i]];
+      S.flags.clear();
+    }
+    if (nc == 0) return;
+    LSG_CUDA(cudaMemcpyAsync(h->chunks_dev.p, h->chunks_host.p, sizeof(Chunk) * nc, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    LSG_CUDA(cudaMemcpyAsync(h->streams_dev.p, h->streams_host.p, sizeof(int32_t) * nc,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    if (max_frames > 0) {
+      dim3 grid((unsigned)ceil_div(max_frames, K1_WARPS * K1_FPW), (unsigned)nc);
+      seg_frame_stats<<<grid, K1_WARPS * 32, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, P.fs,
+                                                               h->stats.p);
+      LSG_LAUNCHED(ctx);
+    }
+    seg_scan<<<nc, K2_THREADS, 0, ctx->stream>>>(h->chunks_dev.p, h->stats.p, h->st.p, h->cuts.p,
+                                                 h->flags.p, P);
+    LSG_LAUNCHED(ctx);
+    seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
+    LSG_LAUNCHED(ctx);
+    collect(h, nc, false);
+  });
+}
+
+lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
+  return guard([&] {
+    Ctx* ctx = h->ctx;
+    if (n < 0 || n > h->n_streams) invalid("lsg_seg_finish: bad stream count");
+    std::vector<char> seen(h->n_streams, 0);
+    for (int i = 0; i < n; ++i) {
+      const int s = streams[i];
+      if (s < 0 || s >= h->n_streams) invalid("lsg_seg_finish: stream id out of range");
+      if (seen[s]) invalid("lsg_seg_finish: stream listed twice");
+      seen[s] = 1;
+      if (h->hs[s].finished) logic("segmenter: finish twice");
+    }
+    if (n == 0) return;
+    DeviceGuard g(ctx);
+    for (int i = 0; i < n; ++i) {
+      h->streams_host.p[i] = streams[i];
+      h->totals_host.p[i] = h->hs[streams[i]].total;
+      h->hs[streams[i]].finished = true;
+      h->hs[streams[i]].stage_len = 0;
+    }
+    LSG_CUDA(cudaMemcpyAsync(h->streams_dev.p, h->streams_host.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    LSG_CUDA(cudaMemcpyAsync(h->totals_dev.p, h->totals_host.p, sizeof(int64_t) * n, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    seg_finish<<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(h->streams_dev.p, h->totals_dev.p, n,
+                                                                    h->st.p, h->cuts.p, h->P);
+    LSG_LAUNCHED(ctx);
+    collect(h, n, true);
+  });
+}
+
+lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_take_cuts: stream id out of range");
+    auto& v = h->hs[stream].cuts;
+    *n_out = (int64_t)v.size();
+    if ((int64_t)v.size() > cap) return;
+    if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(lsg_cut));
+    v.clear();
+  });
+}
+
+lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    int64_t tot = 0;
+    for (auto& s : h->hs) tot += (int64_t)s.cuts.size();
+    *n_out = tot;
+    if (tot > cap) return;
+    int64_t k = 0;
+    for (auto& s : h->hs) {
+      if (!s.cuts.empty()) std::memcpy(out + k, s.cuts.data(), s.cuts.size() * sizeof(lsg_cut));
+      k += (int64_t)s.cuts.size();
+      s.cuts.clear();
+    }
+  });
+}
+
+lsg_status lsg_seg_get_metrics(lsg_seg h, int32_t stream, lsg_seg_metrics* out) {
+  return guard([&] {
+    if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_get_metrics: stream id out of range");
+    *out = h->hs[stream].metrics;
+  });
+}
+
+lsg_status lsg_seg_take_flags(lsg_seg h, int32_t stream, uint8_t* speech, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_take_flags: stream id out of range");
+    if (!h->P.flags_only) logic("lsg_seg_take_flags: handle was not created with flags_only");
+    auto& v = h->hs[stream].flags;
+    *n_out = (int64_t)v.size();
+    if ((int64_t)v.size() > cap) return;
+    if (!v.empty()) std::memcpy(speech, v.data(), v.size());
+    v.clear();
+  });
+}
+
+}  // extern "C"
