@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark: lip-sync frames/sec of the full GPU hot path (BASELINE.json
+metric; config 5 "full queue-decoupled pipeline (segmenter->mel->generator)",
+unpaced).
+
+One step = lsg_pipe_run over this rank's streams: segment every stream,
+log-mel every segment, gather each segment's 25 fps face crops with the
++-50 ms margin, render every gathered frame with the Wav2Lip generator.
+  value  frames/s with inputs resident in HBM (device pointers in, rendered
+         frames left on the device), device time with CUDA events;
+  e2e    the same call with pinned HOST inputs and the rendered u8 frames
+         copied back to host inside the timed region.
+Multi-GPU: one process per GPU, streams sharded (weak scaling: the per-GPU
+stream count is fixed), no data-path collective; the step time is the max
+over ranks (NCCL all-reduce of the timing only).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M64 = (1 << 64) - 1
+FLOPS_PER_FRAME = 7.933968384e9  # generator.flops_per_frame(), SURVEY §0.6
+
+
+def splitmix64(st):
+    st[0] = (st[0] + 0x9E3779B97F4A7C15) & M64
+    z = st[0]
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def stream_pattern(seed: int):
+    """random_scenario-style pattern (scenario.cpp:110-170): lead 0-600 ms,
+    150-400 Hz, 1-4 bursts of 600-2000 ms speech / 520-960 ms pause; every
+    8th stream gets a 12 s burst to exercise forced splits."""
+    st = [seed * 0x9E3779B97F4A7C15 & M64]
+
+    def pick(lo, hi, step):
+        return lo + step * (splitmix64(st) % ((hi - lo) // step + 1))
+    lead = pick(0, 600, 20)
+    hz = float(pick(150, 400, 1))
+    bursts = [(pick(600, 2000, 20), pick(520, 960, 40)) for _ in range(pick(1, 4, 1))]
+    if seed % 8 == 7:
+        bursts = [(12000, 700)] + bursts
+    return lead, bursts, hz, 0.2 + 0.1 * (seed % 5)
+
+
+def make_workload(rank: int, n_streams: int, seconds: int, fps: float, api, generator):
+    """Host inputs of one rank: PCM, per-frame face crops, reference crops."""
+    pcm, video, refs = [], [], []
+    for i in range(n_streams):
+        sid = rank * n_streams + i
+        lead, bursts, hz, amp = stream_pattern(sid + 1)
+        pcm.append(api.synth_pattern(lead, bursts, hz, amp, seconds * 1000))
+        ref = generator.synthetic_face(10_000 + sid)
+        refs.append(ref)
+        n_video = int(np.ceil(seconds * fps / 1000.0 * 1000.0))
+        rng = np.random.default_rng(sid)
+        sh = rng.integers(-3, 4, (n_video, 2))
+        v = np.empty((n_video, 96, 96, 3), np.uint8)
+        # seeded +-3 px wobble of the reference crop (mock_face_detect, visual_mocks.cpp:10-22)
+        for f in range(n_video):
+            v[f] = np.roll(ref, (int(sh[f, 0]), int(sh[f, 1])), axis=(0, 1))
+        video.append(v)
+    return pcm, video, np.stack(refs)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+def cpu_reference_step(n_streams: int, seconds: int, gen_frames: int, threads: int):
+    """The reference's CPU path on a bounded sample: the reference's own
+    Segmenter + compute_mel (oracle/_ref, compiled from /root/reference's
+    sources) on `n_streams` x `seconds` streams, one stream per thread, and
+    the fp32 CPU restatement of the generator (oracle/generator_ref.py; the
+    reference only has a cost model) on `gen_frames` frames with all host
+    threads.  Returns (frames/s, details)."""
+    import concurrent.futures as cf
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Reference
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("generator_ref", os.path.join(ROOT, "oracle", "generator_ref.py"))
+    gref = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gref)
+    from paper_2512_18318_b200 import api, generator
+    ref = Reference()
+    streams = []
+    for i in range(n_streams):
+        lead, bursts, hz, amp = stream_pattern(i + 1)
+        streams.append(api.synth_pattern(lead, bursts, hz, amp, seconds * 1000))
+
+    def segmel(pcm):
+        cuts, _, _ = ref.segment(pcm)
+        nfr = 0
+        for c in cuts:
+            seg = pcm[c["sample_off"]:c["sample_off"] + c["sample_len"]]
+            ref.compute_mel(seg)
+            # frames the stage would render: 25 fps over [begin-50, end+50]
+            lo, hi = c["begin"] - 50, c["end"] + 50
+            nfr += sum(1 for f in range(int(seconds * 25) + 1) if lo <= 40 * f <= hi and 40 * f < seconds * 1000)
+        return nfr
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        frames = sum(ex.map(segmel, streams))
+    t_segmel = time.perf_counter() - t0
+    torch.set_num_threads(threads)
+    w = generator.synthetic_weights(0)
+    rng = np.random.default_rng(0)
+    mel = rng.normal(-5.0, 2.5, (gen_frames, 1, 80, 16)).astype(np.float32)
+    faces = np.stack([generator.face_input(generator.synthetic_face(i), generator.synthetic_face(i + 1))
+                      for i in range(gen_frames)])
+    gref.forward(w, mel[:1], faces[:1])  # warm
+    t0 = time.perf_counter()
+    gref.forward(w, mel, faces)
+    t_gen = (time.perf_counter() - t0) / gen_frames
+    total = t_segmel + frames * t_gen
+    return frames / total, {"t_segmel_s": t_segmel, "gen_s_per_frame": t_gen, "frames": frames}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=32, help="streams per GPU")
+    ap.add_argument("--seconds", type=int, default=30, help="seconds of audio/video per stream")
+    ap.add_argument("--batch", type=int, default=512, help="generator frames per launch sequence")
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    fps = 25.0
+    cfg_desc = {"workload": f"config5-unpaced: {args.streams} streams/GPU x {args.seconds} s 16 kHz synthetic speech "
+                            f"+ 25 fps 96x96 face crops; segmenter -> 80-bin log-mel -> Wav2Lip generator",
+                "streams_per_gpu": args.streams, "seconds_per_stream": args.seconds, "fps": fps,
+                "generator_batch": args.batch, "parallelism": f"streams sharded over {args.gpus} GPU(s), no collective",
+                "l2": "inputs (PCM + face crops) and activations are larger than the 126 MB L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        vals = []
+        for _ in range(max(args.warmup, 0) and 1):
+            pass
+        for _ in range(args.steps):
+            v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
+            vals.append(v)
+        value = float(np.median(vals))
+        sample = (f"reference Segmenter+compute_mel (oracle/_ref, /root/reference sources) on {min(threads, 8)} x 10 s "
+                  f"streams, one per thread, + fp32 CPU generator restatement (oracle/generator_ref.py) on 8 frames, "
+                  f"extrapolated per frame")
+        print(json.dumps({"impl": "reference", "metric": "lip-sync frames/sec (96x96)", "value": value,
+                          "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "higher_is_better": True, "dtype": "f64 (seg/mel) + f32 (generator)", "data": "synthetic",
+                          "config": cfg_desc,
+                          "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
+                                           "sample": sample},
+                          "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    torch.cuda.set_device(local)
+    from paper_2512_18318_b200 import api, generator
+    from paper_2512_18318_b200.pipeline import CROP, Pipeline, PipelineConfig
+
+    ctx = api.Context(local)
+    torch_stream = torch.cuda.Stream(device=local)
+    ctx.set_stream(torch_stream.cuda_stream)
+    prec = 1 if args.precision == "fp16" else 0
+    weights = generator.synthetic_weights(0)
+    eng = generator.LipsyncEngine(weights, max_batch=args.batch, ctx=ctx, precision=prec)
+    pipe = Pipeline(PipelineConfig(args.streams, args.seconds * 1000, fps, 50, args.batch, True), eng, ctx=ctx)
+
+    pcm, video, refs = make_workload(rank, args.streams, args.seconds, fps, api, generator)
+    # pinned host copies (e2e leg) and device-resident copies (value leg)
+    lib = ctx.lib
+    import ctypes as C
+
+    def pinned(nbytes):
+        p = C.c_void_p()
+        lib.call("lsg_host_alloc", nbytes, C.byref(p))
+        return p.value
+    h_pcm = [pinned(p.nbytes) for p in pcm]
+    h_vid = [pinned(v.nbytes) for v in video]
+    h_refs = pinned(refs.nbytes)
+    for ptr, arr in list(zip(h_pcm, pcm)) + list(zip(h_vid, video)) + [(h_refs, refs)]:
+        C.memmove(ptr, arr.ctypes.data, arr.nbytes)
+    d_pcm = [torch.from_numpy(p).to(f"cuda:{local}") for p in pcm]
+    d_vid = [torch.from_numpy(v).to(f"cuda:{local}") for v in video]
+    d_refs = torch.from_numpy(refs).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    n_samples = [len(p) for p in pcm]
+    n_video = [len(v) for v in video]
+    max_frames = sum(n_video) * 2 + 64
+    h_out = pinned(max_frames * CROP)
+
+    def step_device():
+        return pipe.run_ptrs([t.data_ptr() for t in d_pcm], n_samples, [t.data_ptr() for t in d_vid], n_video,
+                             d_refs.data_ptr(), 0, 0, None)
+
+    def step_e2e():
+        return pipe.run_ptrs(h_pcm, n_samples, h_vid, n_video, h_refs, h_out, max_frames, None)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3)):
+        n_frames, st = step_device()
+    # ---------------------------------------------------------- value leg
+    launches0 = ctx.launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with Clocks(local) as clk:
+        ev0.record(torch_stream)
+        stats = []
+        for _ in range(args.steps):
+            n_frames, st = step_device()
+            stats.append(st)
+        ev1.record(torch_stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launches() - launches0
+    ms_dev = ev0.elapsed_time(ev1) / args.steps
+    ms_dev = max_over_ranks(ms_dev)
+    total_frames = n_frames * world
+    value = total_frames / (ms_dev / 1000.0)
+    # ------------------------------------------------------------ e2e leg
+    for _ in range(2):
+        step_e2e()
+    barrier()
+    ev0.record(torch_stream)
+    for _ in range(args.steps):
+        n_e2e, _ = step_e2e()
+    ev1.record(torch_stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    e2e = n_e2e * world / (ms_e2e / 1000.0)
+    h2d = sum(p.nbytes for p in pcm) + sum(v.nbytes for v in video) + refs.nbytes
+    d2h = n_e2e * CROP
+    # -------------------------------------------- generator kernel roofline
+    B = args.batch
+    gen_ms = measure_generator(eng, torch, torch_stream, local, B, reps=10)
+    peaks = measured_peaks()
+    achieved = FLOPS_PER_FRAME * B / (gen_ms / 1000.0) / 1e12
+    peak = peaks.get("bf16_tflops", 1590.0)
+    gen_b128_ms = measure_generator(eng, torch, torch_stream, local, 128, reps=10) if B >= 128 else None
+    clocks = clk.summary()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    med = {k: float(np.median([s[k] for s in stats])) for k in stats[0]}
+    out = {
+        "metric": "lip-sync frames/sec (96x96), full segmenter->mel->generator path",
+        "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_dev, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f16" if prec else "bf16", "data": "synthetic (seeded speech patterns, synthetic face crops, "
+                                                    "BN-calibrated random weights)",
+        "config": cfg_desc,
+        "frames_per_step": total_frames, "unique_frames_per_step": int(med["unique_frames"]) * world,
+        "stage_ms_median": {"segment": med["ms_segment"], "mel": med["ms_mel"], "generator": med["ms_generator"],
+                            "segments": med["segments"], "mel_frames": med["mel_frames"]},
+        "e2e": {"value": e2e, "unit": "frames/s", "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "tensor", "kernel": f"generator forward (51 tcgen05 conv launches, batch {B})",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense fp16 == bf16 rate)",
+                     "ms_per_launch_sequence": gen_ms, "flops_per_frame": FLOPS_PER_FRAME, "traffic": None},
+        "generator_b128": ({"ms": gen_b128_ms, "frames_per_s": 128 / (gen_b128_ms / 1000.0),
+                            "tflops": FLOPS_PER_FRAME * 128 / (gen_b128_ms / 1000.0) / 1e12}
+                           if gen_b128_ms else None),
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
+        out["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
+                               "sample": f"reference Segmenter+compute_mel (oracle/_ref) on {min(threads, 8)} x 10 s "
+                                         f"streams + fp32 CPU generator restatement on 8 frames, per-frame "
+                                         f"extrapolation; {det}"}
+    print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def measure_generator(eng, torch, stream, local, B, reps=10):
+    """Average device time of one generator forward (B frames), CUDA events
+    on the launching stream, device-resident inputs."""
+    from paper_2512_18318_b200 import generator
+    dev = f"cuda:{local}"
+    rng = np.random.default_rng(1)
+    rows = torch.from_numpy(rng.normal(-5, 2.5, (B + 16, 80)).astype(np.float32)).to(dev)
+    chunk = torch.from_numpy(rng.integers(0, B, B).astype(np.int32)).to(dev)
+    face = generator.synthetic_face(1)
+    target = torch.from_numpy(np.stack([face] * B)).to(dev)
+    refs = torch.from_numpy(face[None]).to(dev)
+    ridx = torch.zeros(B, dtype=torch.int32, device=dev)
+    out = torch.empty(B, 96, 96, 3, dtype=torch.uint8, device=dev)
+    args = [rows.data_ptr(), chunk.data_ptr(), target.data_ptr(), refs.data_ptr(), ridx.data_ptr(), out.data_ptr(), 1, B]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        eng.forward_device(*args)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        eng.forward_device(*args)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+if __name__ == "__main__":
+    main()

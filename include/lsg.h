@@ -107,6 +107,9 @@ lsg_status lsg_seg_cfg_default(lsg_seg_cfg* cfg);
 lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams,
                           int64_t max_push_samples, lsg_seg* out);
 lsg_status lsg_seg_destroy(lsg_seg h);
+/* Returns every stream to its freshly constructed state without
+ * reallocating (VadTracker::reset, vad.cpp:20-24, for the whole handle). */
+lsg_status lsg_seg_reset(lsg_seg h);
 /* Segmenter::push for n_chunks streams at once (segmenter.cpp:25-49); a
  * stream appears at most once per call.  pcm[i] is [any] unless
  * pcm_on_device, then [dev].  ELOGIC after finish, EINVAL on a rate
@@ -160,9 +163,11 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
  * (visual_mocks.hpp:17-43, visual_mocks.cpp:24-51); this is the Wav2Lip
  * generator forward it stands for, in bf16 on
  * tcgen05 tensor cores. */
-#define LSG_PREC_BF16 0
+#define LSG_PREC_BF16 0         /* bf16 weights/activations, f32 accumulate */
+#define LSG_PREC_FP16 1         /* fp16 weights/activations, f32 accumulate (same tcgen05 rate) */
 #define LSG_OUT_F32_NCHW 0      /* [B][3][96][96] f32 in [0,1] */
 #define LSG_OUT_U8_NHWC 1       /* [B][96][96][3] u8, round(255*x) */
+#define LSG_OUT_F32_LOGITS 2    /* [B][3][96][96] f32 pre-sigmoid (parity checks) */
 
 typedef struct lsg_gen_s* lsg_gen;
 /* Number of floats in the weight blob (BN folded; layer order and per-layer

@@ -89,6 +89,7 @@ _SIGS = {
     "lsg_seg_cfg_default": [C.POINTER(SegCfg)],
     "lsg_seg_create": [P, C.POINTER(SegCfg), I32, I64, PP],
     "lsg_seg_destroy": [P],
+    "lsg_seg_reset": [P],
     "lsg_seg_push": [P, I32, PI32, PP, PI64, PI64, I32, I32],
     "lsg_seg_finish": [P, I32, PI32],
     "lsg_seg_take_cuts": [P, I32, C.POINTER(Cut), I64, PI64],

@@ -1,7 +1,553 @@
-// generator.cu -- Wav2Lip generator forward (placeholder until the tcgen05 path lands).
+// generator.cu -- Wav2Lip generator forward on sm_100a tensor cores
+// (include/lsg.h "generator").
+//
+// The reference renders with a cost model only (mock_lipsync,
+// visual_mocks.cpp:40-51; profiles wav2lip_fp32 / wav2lip_trt_fp16 at
+// visual_mocks.cpp:24-26); this is the network those profiles stand for,
+// restated from the public Wav2Lip topology: audio
+// encoder on the [80 x 16] mel window, face encoder on [target(masked) ||
+// reference], decoder of transposed convs with skip concatenation, 1x1 +
+// sigmoid output.  BatchNorm is folded into the weights on the host.
+//
+// Every layer is one launch of conv_tc, an implicit-GEMM convolution:
+//   M = output pixels (batch folded in), N = Cout, K = taps x Cin (NHWC, K
+//   ordered tap-major so a 64-wide K block is one tap when Cin >= 64).
+//   * producer warps 0-3 gather the im2col rows of A straight from the NHWC
+//     activation with 16-byte cp.async (zero-fill for padding/halo) into a
+//     128-byte-swizzled K-major tile;
+//   * the packed weight tile B is one bulk async copy (TMA engine) per stage;
+//   * warp 8 issues tcgen05.mma (M=128, N=BN, K=16) into a TMEM accumulator;
+//   * warps 4-7 drain TMEM with tcgen05.ld and run the fused epilogue:
+//     folded-BN bias, residual add, ReLU, bf16 store into a channel slice of
+//     the destination (skip concatenation is free: encoder features are
+//     written straight into the decoder's concat buffers), or, for the last
+//     layer, the 1x1 32->3 conv + sigmoid of the output block.
+//   * stride-2 transposed convs run as 4 phase GEMMs (1/2/2/4 taps) in one
+//     launch (grid.z = phase), so no zero-insertion work is done.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "gen_internal.h"
 #include "lsg_common.cuh"
+#include "tc.cuh"
+
+namespace lsg {
+namespace gen {
+
+enum { CONV = 0, CONVT = 1 };
+
+struct LayerSpec {
+  const char* name;
+  int kind, cin, cout, kh, kw, sh, sw, ph, pw, oph, opw, res;
+};
+
+// Layer order = weight blob order.  conv weights are
+// [cout][cin][kh][kw], convT weights [cin][cout][kh][kw], each followed by
+// bias[cout]; BN already folded.
+static const LayerSpec kLayers[] = {
+    // face encoder (7 blocks)
+    {"fe0", CONV, 6, 16, 7, 7, 1, 1, 3, 3, 0, 0, 0},
+    {"fe1.0", CONV, 16, 32, 3, 3, 2, 2, 1, 1, 0, 0, 0},
+    {"fe1.1", CONV, 32, 32, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe1.2", CONV, 32, 32, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe2.0", CONV, 32, 64, 3, 3, 2, 2, 1, 1, 0, 0, 0},
+    {"fe2.1", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe2.2", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe2.3", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe3.0", CONV, 64, 128, 3, 3, 2, 2, 1, 1, 0, 0, 0},
+    {"fe3.1", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe3.2", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe4.0", CONV, 128, 256, 3, 3, 2, 2, 1, 1, 0, 0, 0},
+    {"fe4.1", CONV, 256, 256, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe4.2", CONV, 256, 256, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe5.0", CONV, 256, 512, 3, 3, 2, 2, 1, 1, 0, 0, 0},
+    {"fe5.1", CONV, 512, 512, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fe6.0", CONV, 512, 512, 3, 3, 1, 1, 0, 0, 0, 0, 0},
+    {"fe6.1", CONV, 512, 512, 1, 1, 1, 1, 0, 0, 0, 0, 0},
+    // audio encoder
+    {"ae0", CONV, 1, 32, 3, 3, 1, 1, 1, 1, 0, 0, 0},
+    {"ae1", CONV, 32, 32, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae2", CONV, 32, 32, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae3", CONV, 32, 64, 3, 3, 3, 1, 1, 1, 0, 0, 0},
+    {"ae4", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae5", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae6", CONV, 64, 128, 3, 3, 3, 3, 1, 1, 0, 0, 0},
+    {"ae7", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae8", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae9", CONV, 128, 256, 3, 3, 3, 2, 1, 1, 0, 0, 0},
+    {"ae10", CONV, 256, 256, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"ae11", CONV, 256, 512, 3, 3, 1, 1, 0, 0, 0, 0, 0},
+    {"ae12", CONV, 512, 512, 1, 1, 1, 1, 0, 0, 0, 0, 0},
+    // decoder
+    {"fd0", CONV, 512, 512, 1, 1, 1, 1, 0, 0, 0, 0, 0},
+    {"fd1.0", CONVT, 1024, 512, 3, 3, 1, 1, 0, 0, 0, 0, 0},
+    {"fd1.1", CONV, 512, 512, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd2.0", CONVT, 1024, 512, 3, 3, 2, 2, 1, 1, 1, 1, 0},
+    {"fd2.1", CONV, 512, 512, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd2.2", CONV, 512, 512, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd3.0", CONVT, 768, 384, 3, 3, 2, 2, 1, 1, 1, 1, 0},
+    {"fd3.1", CONV, 384, 384, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd3.2", CONV, 384, 384, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd4.0", CONVT, 512, 256, 3, 3, 2, 2, 1, 1, 1, 1, 0},
+    {"fd4.1", CONV, 256, 256, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd4.2", CONV, 256, 256, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd5.0", CONVT, 320, 128, 3, 3, 2, 2, 1, 1, 1, 1, 0},
+    {"fd5.1", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd5.2", CONV, 128, 128, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd6.0", CONVT, 160, 64, 3, 3, 2, 2, 1, 1, 1, 1, 0},
+    {"fd6.1", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    {"fd6.2", CONV, 64, 64, 3, 3, 1, 1, 1, 1, 0, 0, 1},
+    // output block: conv 80->32 (+BN, ReLU), conv 1x1 32->3 (bias), sigmoid
+    {"out0", CONV, 80, 32, 3, 3, 1, 1, 1, 1, 0, 0, 0},
+    {"out1", CONV, 32, 3, 1, 1, 1, 1, 0, 0, 0, 0, 0},
+};
+constexpr int kNumLayers = sizeof(kLayers) / sizeof(kLayers[0]);
+static_assert(kNumLayers == 51, "Wav2Lip has 51 conv layers");
+
+constexpr int BM = 128;        // UMMA M (TMEM lanes)
+constexpr int BK = 64;         // bf16 per 128-byte swizzle row
+constexpr int MAX_TAPS = 49;
+constexpr int NUM_THREADS = 288;  // 4 producer warps, 4 epilogue warps, 1 MMA warp
+
+enum OutMode { OUT_BF16 = 0, OUT_F32_NCHW = 1, OUT_U8_NHWC = 2, OUT_F32_LOGITS = 3 };
+
+struct Phase {
+  const uint16_t* w;       // packed [ntiles][kblocks][BN][64], 128 B swizzled rows
+  int ntaps, kblocks, K;
+  int oy, ox;              // output offset of this phase
+  int GH, GW;              // GEMM pixel grid of this phase (per image)
+  int M;                   // B * GH * GW
+  signed char dy[MAX_TAPS], dx[MAX_TAPS];
+};
+
+// Activations/weights are 16-bit storage (bf16 or fp16, chosen per engine).
+struct ConvParams {
+  const uint16_t* in;
+  int H, W, in_pitch, in_coff, C;
+  uint16_t* out;
+  int OH, OW, out_pitch, out_coff;
+  const uint16_t* res;
+  int res_pitch, res_coff;
+  const float* bias;
+  int sy, sx, osy, osx;
+  int relu, out_mode;
+  const float* w1;  // fused output 1x1: [3][32]
+  const float* b1;  // [3]
+  void* final_out;
+  Phase ph[4];
+};
+
+// 16-bit number format: HALF = fp16 (kind::f16 format 0), else bf16 (format 1)
+template <bool HALF>
+struct Num {
+  static constexpr uint32_t kFmt = HALF ? 0u : 1u;
+  __device__ __forceinline__ static uint32_t pack(float a, float b) {
+    if constexpr (HALF) {
+      __half2 v = __floats2half2_rn(a, b);
+      return *reinterpret_cast<uint32_t*>(&v);
+    } else {
+      __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+      return *reinterpret_cast<uint32_t*>(&v);
+    }
+  }
+  __device__ __forceinline__ static float2 unpack(uint32_t u) {
+    if constexpr (HALF) {
+      return __half22float2(*reinterpret_cast<__half2*>(&u));
+    } else {
+      return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
+    }
+  }
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (100 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int KTAB_MAX = 1152;  // K/8 granules (fd1.0: 9 x 1024 / 8)
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + KTAB_MAX * 4 + 256;
+};
+
+template <int BN, bool FUSED_OUT, bool HALF>
+__global__ void __launch_bounds__(NUM_THREADS, 2) conv_tc(const __grid_constant__ ConvParams p) {
+  using CF = Cfg<BN>;
+  using NF = Num<HALF>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * CF::A_BYTES;
+  int* ktab = reinterpret_cast<int*>(sB + S * CF::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ktab + CF::KTAB_MAX);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Phase& P = p.ph[blockIdx.z];
+  const int m0 = blockIdx.x * BM;
+  if (m0 >= P.M) return;  // phases have different M; uniform per CTA
+  const int n0 = blockIdx.y * BN;
+
+  // K-granule table: (dy, dx, channel) per 8-wide K granule
+  for (int gi = threadIdx.x; gi < P.kblocks * 8; gi += NUM_THREADS) {
+    const int k = gi * 8;
+    int e = -1;  // K padding: zero-filled granule
+    if (k < P.K) {
+      const int tap = k / p.C, c = k - tap * p.C;
+      e = (((int)P.dy[tap] + 64) << 24) | (((int)P.dx[tap] + 64) << 16) | c;
+    }
+    ktab[gi] = e;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 128);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tmem_full, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 8) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int KB = P.kblocks;
+
+  if (warp < 4) {
+    // ------------------------------------------------ producers (A gather)
+    const int t = threadIdx.x;
+    const int g = t & 7, r0 = t >> 3;
+    int iy0[8], ix0[8];
+    const uint16_t* rb[8];
+    const int HW = P.GH * P.GW;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = m0 + r0 + 16 * i;
+      if (m < P.M) {
+        const int n = m / HW, rem = m - n * HW;
+        const int gy = rem / P.GW, gx = rem - gy * P.GW;
+        iy0[i] = gy * p.sy;
+        ix0[i] = gx * p.sx;
+        rb[i] = p.in + (size_t)n * p.H * p.W * p.in_pitch + p.in_coff;
+      } else {
+        iy0[i] = -100000;
+        ix0[i] = -100000;
+        rb[i] = p.in;
+      }
+    }
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    const uint32_t swz = (uint32_t)((g ^ (r0 & 7)) << 4);
+    const uint16_t* wbase = P.w + (size_t)blockIdx.y * KB * BN * BK;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % S;
+      const uint32_t ph = (kb / S) & 1;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      if (t == 0) {
+        tc::mbar_expect_tx(&full[s], CF::B_BYTES);
+        tc::bulk_g2s(sB0 + s * CF::B_BYTES, wbase + (size_t)kb * BN * BK, CF::B_BYTES, &full[s]);
+      }
+      const int e = ktab[kb * 8 + g];
+      const bool kv = e >= 0;
+      const int dy = ((e >> 24) & 0xff) - 64, dx = ((e >> 16) & 0xff) - 64, c = e & 0xffff;
+      const uint32_t dst0 = sA0 + s * CF::A_BYTES + r0 * 128 + swz;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int iy = iy0[i] + dy, ix = ix0[i] + dx;
+        const bool ok = kv && (unsigned)iy < (unsigned)p.H && (unsigned)ix < (unsigned)p.W;
+        const uint16_t* src = ok ? rb[i] + ((size_t)iy * p.W + ix) * p.in_pitch + c : p.in;
+        tc::cp_async16(dst0 + i * 16 * 128, src, ok ? 16u : 0u);
+      }
+      tc::cp_async_commit();
+      if (kb >= 1) {
+        tc::cp_async_wait<1>();
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&full[(kb - 1) % S]);
+      }
+    }
+    tc::cp_async_wait<0>();
+    tc::fence_proxy_async();
+    if (KB >= 1) tc::mbar_arrive(&full[(KB - 1) % S]);
+  } else if (warp == 8) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % S;
+        tc::mbar_wait(&full[s], (kb / S) & 1);
+        tc::tc_fence_after();
+        const uint64_t a = tc::sdesc_sw128(sA0 + s * CF::A_BYTES);
+        const uint64_t b = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          tc::mma_f16(tmem, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 4-7)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int m = m0 + r;
+    tc::mbar_wait(tmem_full, 0);
+    tc::tc_fence_after();
+    const bool valid = m < P.M;
+    int n = 0, oy = 0, ox = 0;
+    if (valid) {
+      const int HW = P.GH * P.GW;
+      n = m / HW;
+      const int rem = m - n * HW;
+      const int gy = rem / P.GW, gx = rem - gy * P.GW;
+      oy = gy * p.osy + P.oy;
+      ox = gx * p.osx + P.ox;
+    }
+    const size_t pix = ((size_t)n * p.OH + oy) * p.OW + ox;
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+    if constexpr (!FUSED_OUT) {
+      uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + n0;
+      const uint16_t* rrow = p.res ? p.res + pix * p.res_pitch + p.res_coff + n0 : nullptr;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(tbase + c0, v);
+        tc::tmem_ld_wait();
+        if (valid) {
+          float f[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + __ldg(p.bias + n0 + c0 + j);
+          if (rrow) {
+            const uint4 a = *reinterpret_cast<const uint4*>(rrow + c0);
+            const uint4 b = *reinterpret_cast<const uint4*>(rrow + c0 + 8);
+            const uint32_t ra[4] = {a.x, a.y, a.z, a.w};
+            const uint32_t rbv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 x = NF::unpack(ra[j]);
+              const float2 y = NF::unpack(rbv[j]);
+              f[2 * j] += x.x;
+              f[2 * j + 1] += x.y;
+              f[8 + 2 * j] += y.x;
+              f[8 + 2 * j + 1] += y.y;
+            }
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
+          }
+          uint4 o0, o1;
+          o0.x = NF::pack(f[0], f[1]);
+          o0.y = NF::pack(f[2], f[3]);
+          o0.z = NF::pack(f[4], f[5]);
+          o0.w = NF::pack(f[6], f[7]);
+          o1.x = NF::pack(f[8], f[9]);
+          o1.y = NF::pack(f[10], f[11]);
+          o1.z = NF::pack(f[12], f[13]);
+          o1.w = NF::pack(f[14], f[15]);
+          *reinterpret_cast<uint4*>(orow + c0) = o0;
+          *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
+        }
+      }
+    } else {
+      // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid
+      float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tc::tmem_ld16(tbase + c0, v);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float a = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+#pragma unroll
+          for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), a, o[o3]);
+        }
+      }
+      if (valid) {
+        const int HWo = p.OH * p.OW;
+        const size_t pp = (size_t)oy * p.OW + ox;
+        if (p.out_mode == OUT_F32_LOGITS) {
+          float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+          for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
+        } else if (p.out_mode == OUT_F32_NCHW) {
+          float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+          for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
+        } else {
+          uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
+#pragma unroll
+          for (int o3 = 0; o3 < 3; ++o3) {
+            const float s = 1.f / (1.f + __expf(-o[o3]));
+            out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
+          }
+        }
+      }
+    }
+    tc::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
+  }
+}
+
+// ------------------------------------------------------------ input prep
+// faces: [B][96][96][3] u8 target (rows >= 48 masked), refs [R][96][96][3]
+// -> [B][96][96][8] bf16 = (target/255 masked, ref/255, 0, 0)
+template <bool HALF>
+__global__ void prep_faces(const uint8_t* __restrict__ target, const int64_t* __restrict__ target_idx,
+                           const uint8_t* __restrict__ refs, const int32_t* __restrict__ ref_index,
+                           uint16_t* __restrict__ out, int B) {
+  using NF = Num<HALF>;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel
+  const int64_t total = (int64_t)B * 96 * 96;
+  if (i >= total) return;
+  const int b = (int)(i / (96 * 96));
+  const int pix = (int)(i - (int64_t)b * 96 * 96);
+  const int y = pix / 96;
+  const int64_t tf = target_idx ? __ldg(target_idx + b) : b;
+  const uint8_t* t = target + (tf * 96 * 96 + pix) * 3;
+  const uint8_t* r = refs + ((int64_t)__ldg(ref_index + b) * 96 * 96 + pix) * 3;
+  const float k = 1.f / 255.f;
+  const bool mask = y >= 48;
+  uint4 o;
+  o.x = NF::pack(mask ? 0.f : t[0] * k, mask ? 0.f : t[1] * k);
+  o.y = NF::pack(mask ? 0.f : t[2] * k, r[0] * k);
+  o.z = NF::pack(r[1] * k, r[2] * k);
+  o.w = 0;
+  reinterpret_cast<uint4*>(out)[i] = o;
+}
+
+// mel rows [rows][80] f32, chunk_row [B] -> [B][80][16][8] bf16, chunk[h][w] = rows[r0 + w][h]
+template <bool HALF>
+__global__ void prep_mel(const float* __restrict__ rows, const int32_t* __restrict__ chunk_row,
+                         uint16_t* __restrict__ out, int B) {
+  using NF = Num<HALF>;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, h, w)
+  const int64_t total = (int64_t)B * 80 * 16;
+  if (i >= total) return;
+  const int b = (int)(i / (80 * 16));
+  const int hw = (int)(i - (int64_t)b * 80 * 16);
+  const int h = hw / 16, w = hw - h * 16;
+  const float v = __ldg(rows + ((int64_t)__ldg(chunk_row + b) + w) * 80 + h);
+  uint4 o;
+  o.x = NF::pack(v, 0.f);
+  o.y = 0;
+  o.z = 0;
+  o.w = 0;
+  reinterpret_cast<uint4*>(out)[i] = o;
+}
+
+}  // namespace gen
+}  // namespace lsg
 
 using namespace lsg;
+using namespace lsg::gen;
+
+namespace {
+
+struct View {
+  uint16_t* p = nullptr;
+  int H = 0, W = 0, pitch = 0, coff = 0, C = 0;
+};
+
+struct LayerRun {
+  int layer;
+  int bn;
+  int nphases;
+  int ntiles;
+  bool fused;
+  ConvParams p;
+  int GH[4], GW[4];  // per phase, per image
+};
+
+int pick_bn(int cout) {
+  if (cout <= 256) return cout;
+  if (cout == 384) return 192;
+  return 256;
+}
+
+uint16_t f2bf(float f) {  // round to nearest even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffff) > 0x7f800000) return 0x7fc0;
+  u += 0x7fff + ((u >> 16) & 1);
+  return (uint16_t)(u >> 16);
+}
+
+uint16_t f2h(float f) {  // round to nearest even (host)
+  __half h = __float2half_rn(f);
+  uint16_t u;
+  std::memcpy(&u, &h, 2);
+  return u;
+}
+
+}  // namespace
+
+struct lsg_gen_s {
+  Ctx* ctx = nullptr;
+  int max_batch = 0;
+  bool half = false;  // LSG_PREC_FP16
+  DevBuf<uint16_t> wpack;
+  DevBuf<float> bias;
+  DevBuf<float> w1b1;
+  DevBuf<uint16_t> act;  // all activation buffers
+  View x_face, x_mel, cat[7], S0, S1, A0, A1;
+  std::vector<LayerRun> plan;
+};
+
+static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
+
+template <int BN, bool F, bool H>
+static void launch_conv(const LayerRun& r, int B, cudaStream_t st) {
+  ConvParams p = r.p;
+  int mt = 0;
+  for (int z = 0; z < r.nphases; ++z) {
+    p.ph[z].M = B * r.GH[z] * r.GW[z];
+    mt = std::max(mt, (int)ceil_div(p.ph[z].M, BM));
+  }
+  dim3 grid(mt, r.ntiles, r.nphases);
+  conv_tc<BN, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
+}
+
+template <int BN, bool F>
+static void set_smem_attr() {
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+}
+
+template <bool H>
+static void dispatch_t(const LayerRun& r, int B, cudaStream_t st) {
+  if (r.fused) return launch_conv<32, true, H>(r, B, st);
+  switch (r.bn) {
+    case 16: return launch_conv<16, false, H>(r, B, st);
+    case 32: return launch_conv<32, false, H>(r, B, st);
+    case 64: return launch_conv<64, false, H>(r, B, st);
+    case 128: return launch_conv<128, false, H>(r, B, st);
+    case 192: return launch_conv<192, false, H>(r, B, st);
+    case 256: return launch_conv<256, false, H>(r, B, st);
+  }
+  fail(LSG_ERUNTIME, "generator: no kernel for this tile width");
+}
+
+static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
+  if (h->half) dispatch_t<true>(r, B, st);
+  else dispatch_t<false>(r, B, st);
+}
 
 extern "C" {
 
@@ -12,13 +558,428 @@ lsg_status lsg_lipsync_validate(int64_t audio_span_ms, int64_t frame_span_ms, in
   });
 }
 
-lsg_status lsg_gen_param_count(int64_t*) { return guard([] { fail(LSG_ERUNTIME, "generator not built"); }); }
-lsg_status lsg_gen_layer_info(int32_t*, int32_t, int32_t*) { return guard([] { fail(LSG_ERUNTIME, "generator not built"); }); }
-lsg_status lsg_gen_create(lsg_ctx, const float*, int64_t, int32_t, int32_t, lsg_gen*) { return guard([] { fail(LSG_ERUNTIME, "generator not built"); }); }
-lsg_status lsg_gen_destroy(lsg_gen) { return LSG_OK; }
-lsg_status lsg_gen_forward(lsg_gen, const float*, const int32_t*, const uint8_t*, const uint8_t*, const int32_t*, void*, int32_t, int32_t) { return guard([] { fail(LSG_ERUNTIME, "generator not built"); }); }
-lsg_status lsg_pipe_create(lsg_ctx, const lsg_pipe_cfg*, const lsg_seg_cfg*, const lsg_mel_cfg*, lsg_gen, lsg_pipe*) { return guard([] { fail(LSG_ERUNTIME, "pipeline not built"); }); }
-lsg_status lsg_pipe_destroy(lsg_pipe) { return LSG_OK; }
-lsg_status lsg_pipe_run(lsg_pipe, const int16_t* const*, const int64_t*, const uint8_t* const*, const int64_t*, const uint8_t*, lsg_frame_rec*, void*, int64_t, int64_t*, lsg_pipe_stats*) { return guard([] { fail(LSG_ERUNTIME, "pipeline not built"); }); }
-
+lsg_status lsg_gen_param_count(int64_t* n) {
+  return guard([&] {
+    int64_t t = 0;
+    for (const auto& L : kLayers) t += layer_params(L);
+    *n = t;
+  });
 }
+
+lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap, int32_t* n_layers) {
+  return guard([&] {
+    *n_layers = kNumLayers;
+    for (int i = 0; i < kNumLayers && i < cap; ++i) {
+      const auto& L = kLayers[i];
+      const int32_t v[12] = {L.kind, L.cin, L.cout, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.oph, L.opw, L.res};
+      std::memcpy(info + 12 * i, v, sizeof(v));
+    }
+  });
+}
+
+lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, int32_t precision, int32_t max_batch,
+                          lsg_gen* out) {
+  return guard([&] {
+    *out = nullptr;
+    int64_t want = 0;
+    lsg_gen_param_count(&want);
+    if (n_floats != want) invalid("lsg_gen_create: weight blob has " + std::to_string(n_floats) + " floats, expected " +
+                                  std::to_string(want));
+    if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16) invalid("lsg_gen_create: unsupported precision");
+    if (max_batch <= 0 || max_batch > 4096) invalid("lsg_gen_create: max_batch out of range");
+    DeviceGuard g(ctx);
+    auto h = new lsg_gen_s();
+    try {
+      h->ctx = ctx;
+      h->max_batch = max_batch;
+      h->half = precision == LSG_PREC_FP16;
+      const int B = max_batch;
+      // ---------------- activation buffers (bf16 NHWC)
+      struct Req { View* v; int H, W, C; };
+      const int cat_hw[7] = {1, 3, 6, 12, 24, 48, 96};
+      const int cat_c[7] = {1024, 1024, 768, 512, 320, 160, 80};
+      std::vector<Req> reqs;
+      reqs.push_back({&h->x_face, 96, 96, 8});
+      reqs.push_back({&h->x_mel, 80, 16, 8});
+      for (int l = 0; l < 7; ++l) reqs.push_back({&h->cat[l], cat_hw[l], cat_hw[l], cat_c[l]});
+      reqs.push_back({&h->S0, 96, 96, 64});
+      reqs.push_back({&h->S1, 96, 96, 64});
+      reqs.push_back({&h->A0, 80, 16, 32});
+      reqs.push_back({&h->A1, 80, 16, 32});
+      size_t tot = 0;
+      for (auto& r : reqs) tot += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
+      h->act.alloc(tot);
+      LSG_CUDA(cudaMemset(h->act.p, 0, h->act.bytes()));
+      size_t off = 0;
+      for (auto& r : reqs) {
+        *r.v = View{h->act.p + off, r.H, r.W, r.C, 0, r.C};
+        off += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
+      }
+      // ---------------- weights: pack per layer / phase / N tile / K block
+      std::vector<uint16_t> pack;
+      std::vector<float> bias;
+      std::vector<float> w1b1(3 * 32 + 3);
+      std::vector<int64_t> pack_off(kNumLayers * 4, 0);
+      std::vector<int64_t> bias_off(kNumLayers, 0);
+      struct PhaseGeo { int ntaps; signed char dy[MAX_TAPS], dx[MAX_TAPS]; int ky[MAX_TAPS], kx[MAX_TAPS]; int oy, ox; };
+      std::vector<std::vector<PhaseGeo>> geo(kNumLayers);
+      const float* wp = weights;
+      for (int li = 0; li < kNumLayers; ++li) {
+        const LayerSpec& L = kLayers[li];
+        const float* w = wp;
+        const float* b = wp + (int64_t)L.cin * L.cout * L.kh * L.kw;
+        wp = b + L.cout;
+        if (li == kNumLayers - 1) {  // out1: fused into out0's epilogue
+          for (int o = 0; o < 3; ++o)
+            for (int c = 0; c < 32; ++c) w1b1[o * 32 + c] = w[o * 32 + c];
+          for (int o = 0; o < 3; ++o) w1b1[96 + o] = b[o];
+          continue;
+        }
+        bias_off[li] = (int64_t)bias.size();
+        bias.insert(bias.end(), b, b + L.cout);
+        // phases
+        std::vector<PhaseGeo>& G = geo[li];
+        if (L.kind == CONV) {
+          PhaseGeo pg{};
+          pg.ntaps = 0;
+          for (int ky = 0; ky < L.kh; ++ky)
+            for (int kx = 0; kx < L.kw; ++kx) {
+              pg.dy[pg.ntaps] = (signed char)(ky - L.ph);
+              pg.dx[pg.ntaps] = (signed char)(kx - L.pw);
+              pg.ky[pg.ntaps] = ky;
+              pg.kx[pg.ntaps] = kx;
+              ++pg.ntaps;
+            }
+          pg.oy = pg.ox = 0;
+          G.push_back(pg);
+        } else {
+          // out[o] = sum_{i,k: o = i*s - p + k} in[i] w[k]; phase a of o = g*s + a
+          for (int a = 0; a < L.sh; ++a)
+            for (int bb = 0; bb < L.sw; ++bb) {
+              PhaseGeo pg{};
+              pg.ntaps = 0;
+              for (int ky = 0; ky < L.kh; ++ky) {
+                if (((a + L.ph - ky) % L.sh + L.sh) % L.sh) continue;
+                for (int kx = 0; kx < L.kw; ++kx) {
+                  if (((bb + L.pw - kx) % L.sw + L.sw) % L.sw) continue;
+                  pg.dy[pg.ntaps] = (signed char)((a + L.ph - ky) / L.sh);
+                  pg.dx[pg.ntaps] = (signed char)((bb + L.pw - kx) / L.sw);
+                  pg.ky[pg.ntaps] = ky;
+                  pg.kx[pg.ntaps] = kx;
+                  ++pg.ntaps;
+                }
+              }
+              pg.oy = a;
+              pg.ox = bb;
+              G.push_back(pg);
+            }
+        }
+        const int cin_pad = (L.cin + 7) / 8 * 8;
+        const int bn = (li == kNumLayers - 2) ? 32 : pick_bn(L.cout);
+        const int ntiles = L.cout / bn;
+        for (size_t z = 0; z < G.size(); ++z) {
+          const PhaseGeo& pg = G[z];
+          const int K = pg.ntaps * cin_pad;
+          const int kbs = (int)ceil_div(K, BK);
+          pack_off[li * 4 + z] = (int64_t)pack.size();
+          pack.resize(pack.size() + (size_t)ntiles * kbs * bn * BK, 0);
+          uint16_t* dst = pack.data() + pack_off[li * 4 + z];
+          for (int nt = 0; nt < ntiles; ++nt)
+            for (int kb = 0; kb < kbs; ++kb) {
+              uint16_t* blk = dst + ((size_t)nt * kbs + kb) * bn * BK;
+              for (int r = 0; r < bn; ++r) {
+                const int co = nt * bn + r;
+                for (int j = 0; j < BK; ++j) {
+                  const int k = kb * BK + j;
+                  float v = 0.f;
+                  if (k < K) {
+                    const int t = k / cin_pad, ci = k % cin_pad;
+                    if (ci < L.cin) {
+                      const int ky = pg.ky[t], kx = pg.kx[t];
+                      v = L.kind == CONV ? w[(((int64_t)co * L.cin + ci) * L.kh + ky) * L.kw + kx]
+                                         : w[(((int64_t)ci * L.cout + co) * L.kh + ky) * L.kw + kx];
+                    }
+                  }
+                  // 128-byte swizzle: 16-byte chunk (j/8) of row r lands at chunk (j/8) ^ (r%8)
+                  const int chunk = (j >> 3) ^ (r & 7);
+                  blk[r * BK + chunk * 8 + (j & 7)] = h->half ? f2h(v) : f2bf(v);
+                }
+              }
+            }
+        }
+      }
+      h->wpack.alloc(pack.size());
+      LSG_CUDA(cudaMemcpy(h->wpack.p, pack.data(), pack.size() * 2, cudaMemcpyHostToDevice));
+      h->bias.alloc(bias.size());
+      LSG_CUDA(cudaMemcpy(h->bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+      h->w1b1.alloc(w1b1.size());
+      LSG_CUDA(cudaMemcpy(h->w1b1.p, w1b1.data(), w1b1.size() * 4, cudaMemcpyHostToDevice));
+
+      // ---------------- plan: input/output views per layer
+      auto slice = [](View v, int coff, int C) {
+        View s = v;
+        s.pitch = v.C;
+        s.coff = coff;
+        s.C = C;
+        return s;
+      };
+      auto resize = [](View v, int H, int W, int C) {
+        View s = v;
+        s.H = H;
+        s.W = W;
+        s.C = C;
+        s.pitch = C;
+        s.coff = 0;
+        return s;
+      };
+      // (in, out) views per layer, in layer order
+      std::vector<std::pair<View, View>> io(kNumLayers);
+      View S0 = h->S0, S1 = h->S1, A0 = h->A0, A1 = h->A1;
+      View* cat = h->cat;
+      int li = 0;
+      // face encoder
+      io[li++] = {h->x_face, slice(cat[6], 64, 16)};
+      io[li++] = {slice(cat[6], 64, 16), resize(S0, 48, 48, 32)};
+      io[li++] = {resize(S0, 48, 48, 32), resize(S1, 48, 48, 32)};
+      io[li++] = {resize(S1, 48, 48, 32), slice(cat[5], 128, 32)};
+      io[li++] = {slice(cat[5], 128, 32), resize(S0, 24, 24, 64)};
+      io[li++] = {resize(S0, 24, 24, 64), resize(S1, 24, 24, 64)};
+      io[li++] = {resize(S1, 24, 24, 64), resize(S0, 24, 24, 64)};
+      io[li++] = {resize(S0, 24, 24, 64), slice(cat[4], 256, 64)};
+      io[li++] = {slice(cat[4], 256, 64), resize(S0, 12, 12, 128)};
+      io[li++] = {resize(S0, 12, 12, 128), resize(S1, 12, 12, 128)};
+      io[li++] = {resize(S1, 12, 12, 128), slice(cat[3], 384, 128)};
+      io[li++] = {slice(cat[3], 384, 128), resize(S0, 6, 6, 256)};
+      io[li++] = {resize(S0, 6, 6, 256), resize(S1, 6, 6, 256)};
+      io[li++] = {resize(S1, 6, 6, 256), slice(cat[2], 512, 256)};
+      io[li++] = {slice(cat[2], 512, 256), resize(S0, 3, 3, 512)};
+      io[li++] = {resize(S0, 3, 3, 512), slice(cat[1], 512, 512)};
+      io[li++] = {slice(cat[1], 512, 512), resize(S0, 1, 1, 512)};
+      io[li++] = {resize(S0, 1, 1, 512), slice(cat[0], 512, 512)};
+      // audio encoder
+      io[li++] = {h->x_mel, resize(A0, 80, 16, 32)};
+      io[li++] = {resize(A0, 80, 16, 32), resize(A1, 80, 16, 32)};
+      io[li++] = {resize(A1, 80, 16, 32), resize(A0, 80, 16, 32)};
+      io[li++] = {resize(A0, 80, 16, 32), resize(A1, 27, 16, 64)};
+      io[li++] = {resize(A1, 27, 16, 64), resize(A0, 27, 16, 64)};
+      io[li++] = {resize(A0, 27, 16, 64), resize(A1, 27, 16, 64)};
+      io[li++] = {resize(A1, 27, 16, 64), resize(A0, 9, 6, 128)};
+      io[li++] = {resize(A0, 9, 6, 128), resize(A1, 9, 6, 128)};
+      io[li++] = {resize(A1, 9, 6, 128), resize(A0, 9, 6, 128)};
+      io[li++] = {resize(A0, 9, 6, 128), resize(A1, 3, 3, 256)};
+      io[li++] = {resize(A1, 3, 3, 256), resize(A0, 3, 3, 256)};
+      io[li++] = {resize(A0, 3, 3, 256), resize(A1, 1, 1, 512)};
+      io[li++] = {resize(A1, 1, 1, 512), resize(A0, 1, 1, 512)};
+      // decoder
+      io[li++] = {resize(A0, 1, 1, 512), slice(cat[0], 0, 512)};
+      io[li++] = {cat[0], resize(S0, 3, 3, 512)};
+      io[li++] = {resize(S0, 3, 3, 512), slice(cat[1], 0, 512)};
+      io[li++] = {cat[1], resize(S0, 6, 6, 512)};
+      io[li++] = {resize(S0, 6, 6, 512), resize(S1, 6, 6, 512)};
+      io[li++] = {resize(S1, 6, 6, 512), slice(cat[2], 0, 512)};
+      io[li++] = {cat[2], resize(S0, 12, 12, 384)};
+      io[li++] = {resize(S0, 12, 12, 384), resize(S1, 12, 12, 384)};
+      io[li++] = {resize(S1, 12, 12, 384), slice(cat[3], 0, 384)};
+      io[li++] = {cat[3], resize(S0, 24, 24, 256)};
+      io[li++] = {resize(S0, 24, 24, 256), resize(S1, 24, 24, 256)};
+      io[li++] = {resize(S1, 24, 24, 256), slice(cat[4], 0, 256)};
+      io[li++] = {cat[4], resize(S0, 48, 48, 128)};
+      io[li++] = {resize(S0, 48, 48, 128), resize(S1, 48, 48, 128)};
+      io[li++] = {resize(S1, 48, 48, 128), slice(cat[5], 0, 128)};
+      io[li++] = {cat[5], resize(S0, 96, 96, 64)};
+      io[li++] = {resize(S0, 96, 96, 64), resize(S1, 96, 96, 64)};
+      io[li++] = {resize(S1, 96, 96, 64), slice(cat[6], 0, 64)};
+      io[li++] = {cat[6], View{}};  // out0 (+ out1 fused)
+      if (li != kNumLayers - 1) fail(LSG_ERUNTIME, "generator plan does not cover every layer");
+
+      for (int l = 0; l < kNumLayers - 1; ++l) {
+        const LayerSpec& L = kLayers[l];
+        const View in = io[l].first, ov = io[l].second;
+        const bool fused = (l == kNumLayers - 2);
+        LayerRun r{};
+        r.layer = l;
+        r.fused = fused;
+        r.bn = fused ? 32 : pick_bn(L.cout);
+        r.ntiles = L.cout / r.bn;
+        r.nphases = (int)geo[l].size();
+        ConvParams& p = r.p;
+        p.in = in.p;
+        p.H = in.H;
+        p.W = in.W;
+        p.in_pitch = in.pitch;
+        p.in_coff = in.coff;
+        p.C = (L.cin + 7) / 8 * 8;
+        if (in.C != p.C) fail(LSG_ERUNTIME, std::string("generator plan: channel mismatch at ") + L.name);
+        // output geometry
+        int OH, OW;
+        if (L.kind == CONV) {
+          OH = (in.H + 2 * L.ph - L.kh) / L.sh + 1;
+          OW = (in.W + 2 * L.pw - L.kw) / L.sw + 1;
+        } else {
+          OH = (in.H - 1) * L.sh - 2 * L.ph + L.kh + L.oph;
+          OW = (in.W - 1) * L.sw - 2 * L.pw + L.kw + L.opw;
+        }
+        if (!fused && (ov.H != OH || ov.W != OW || ov.C != L.cout))
+          fail(LSG_ERUNTIME, std::string("generator plan: shape mismatch at ") + L.name);
+        p.out = ov.p;
+        p.OH = OH;
+        p.OW = OW;
+        p.out_pitch = ov.pitch;
+        p.out_coff = ov.coff;
+        p.res = L.res ? in.p : nullptr;
+        p.res_pitch = in.pitch;
+        p.res_coff = in.coff;
+        p.bias = h->bias.p + bias_off[l];
+        p.relu = 1;
+        p.out_mode = OUT_BF16;
+        if (L.kind == CONV) {
+          p.sy = L.sh;
+          p.sx = L.sw;
+          p.osy = p.osx = 1;
+        } else {
+          p.sy = p.sx = 1;
+          p.osy = L.sh;
+          p.osx = L.sw;
+        }
+        if (fused) {
+          p.w1 = h->w1b1.p;
+          p.b1 = h->w1b1.p + 96;
+        }
+        for (int z = 0; z < r.nphases; ++z) {
+          const PhaseGeo& pg = geo[l][z];
+          Phase& P = p.ph[z];
+          P.w = h->wpack.p + pack_off[l * 4 + z];
+          P.ntaps = pg.ntaps;
+          P.K = pg.ntaps * p.C;
+          P.kblocks = (int)ceil_div(P.K, BK);
+          if (P.kblocks * 8 > 1152) fail(LSG_ERUNTIME, "generator: K table overflow");
+          P.oy = pg.oy;
+          P.ox = pg.ox;
+          for (int t = 0; t < pg.ntaps; ++t) {
+            P.dy[t] = pg.dy[t];
+            P.dx[t] = pg.dx[t];
+          }
+          r.GH[z] = L.kind == CONV ? OH : (int)ceil_div(OH - pg.oy, L.sh);
+          r.GW[z] = L.kind == CONV ? OW : (int)ceil_div(OW - pg.ox, L.sw);
+          P.GH = r.GH[z];
+          P.GW = r.GW[z];
+        }
+        h->plan.push_back(r);
+      }
+      set_smem_attr<16, false>();
+      set_smem_attr<32, false>();
+      set_smem_attr<64, false>();
+      set_smem_attr<128, false>();
+      set_smem_attr<192, false>();
+      set_smem_attr<256, false>();
+      set_smem_attr<32, true>();
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+lsg_status lsg_gen_destroy(lsg_gen h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard g(h->ctx);
+    h->ctx->sync();
+    delete h;
+  });
+}
+
+lsg_status lsg_gen_forward(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
+                           const uint8_t* refs, const int32_t* ref_index, void* out, int32_t out_format, int32_t B) {
+  return guard([&] {
+    DeviceGuard g(h->ctx);
+    gen::forward_gather(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, out, out_format, B);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- debug
+// Not part of include/lsg.h: test-only introspection used by
+// tests/test_generator.py to check each layer in isolation.
+template <bool HALF>
+__global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int64_t pixels, float* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= pixels * C) return;
+  const int64_t px = i / C;
+  const int c = (int)(i - px * C);
+  const uint16_t u = src[px * pitch + coff + c];
+  dst[i] = HALF ? __half2float(__ushort_as_half(u)) : __bfloat162float(__ushort_as_bfloat16(u));
+}
+
+extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
+                                        const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
+                                        int32_t B, int32_t stop_layer, int32_t which, float* out_dev,
+                                        int32_t* shape4) {
+  return guard([&] {
+    Ctx* ctx = h->ctx;
+    DeviceGuard g(ctx);
+    cudaStream_t st = ctx->stream;
+    const int64_t n = (int64_t)B * 96 * 96;
+    if (h->half) prep_faces<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target, nullptr, refs, ref_index, h->x_face.p, B);
+    else prep_faces<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target, nullptr, refs, ref_index, h->x_face.p, B);
+    const int64_t m = (int64_t)B * 80 * 16;
+    if (h->half) prep_mel<true><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
+    else prep_mel<false><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
+    if (stop_layer < 0 || stop_layer >= (int)h->plan.size() - 1) invalid("lsgdbg_run_until: bad layer");
+    for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
+    const LayerRun& r = h->plan[stop_layer];
+    const ConvParams& p = r.p;
+    const LayerSpec& L = kLayers[stop_layer];
+    const uint16_t* src = which ? p.out : p.in;
+    const int H = which ? p.OH : p.H, W = which ? p.OW : p.W;
+    const int pitch = which ? p.out_pitch : p.in_pitch, coff = which ? p.out_coff : p.in_coff;
+    const int C = which ? L.cout : p.C;
+    const int64_t pixels = (int64_t)B * H * W;
+    if (h->half) view_to_f32<true><<<(unsigned)ceil_div(pixels * C, 256), 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev);
+    else view_to_f32<false><<<(unsigned)ceil_div(pixels * C, 256), 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev);
+    LSG_CUDA(cudaGetLastError());
+    shape4[0] = B;
+    shape4[1] = H;
+    shape4[2] = W;
+    shape4[3] = C;
+  });
+}
+
+namespace lsg {
+namespace gen {
+
+int32_t max_batch(lsg_gen h) { return h->max_batch; }
+
+void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target_base,
+                    const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, void* out,
+                    int32_t out_format, int32_t B) {
+  if (B <= 0 || B > h->max_batch) invalid("lsg_gen_forward: batch out of range");
+  if (out_format < 0 || out_format > 2) invalid("lsg_gen_forward: unknown output format");
+  Ctx* ctx = h->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = (int64_t)B * 96 * 96;
+  if (h->half)
+    prep_faces<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target_base, target_idx, refs, ref_index, h->x_face.p, B);
+  else
+    prep_faces<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target_base, target_idx, refs, ref_index, h->x_face.p, B);
+  LSG_LAUNCHED(ctx);
+  const int64_t m = (int64_t)B * 80 * 16;
+  if (h->half) prep_mel<true><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
+  else prep_mel<false><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
+  LSG_LAUNCHED(ctx);
+  const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
+                                                  : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
+  for (auto& r : h->plan) {
+    if (r.fused) {
+      r.p.out_mode = mode;
+      r.p.final_out = out;
+    }
+    dispatch(h, r, B, st);
+    LSG_LAUNCHED(ctx);
+  }
+}
+
+}  // namespace gen
+}  // namespace lsg

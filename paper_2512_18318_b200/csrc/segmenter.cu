@@ -727,6 +727,20 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
   });
 }
 
+lsg_status lsg_seg_reset(lsg_seg h) {
+  return guard([&] {
+    Ctx* ctx = h->ctx;
+    DeviceGuard g(ctx);
+    std::vector<DevState> init(h->n_streams);
+    std::memset(init.data(), 0, init.size() * sizeof(DevState));
+    if (h->P.peak_mode == 2)
+      for (auto& d : init) d.peak = 32767.0;  // vad.cpp:22-24
+    LSG_CUDA(cudaMemcpyAsync(h->st.p, init.data(), h->st.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->sync();
+    for (auto& d : h->hs) d = StreamHost{};
+  });
+}
+
 lsg_status lsg_seg_destroy(lsg_seg h) {
   return guard([&] {
     if (!h) return;

@@ -1,0 +1,248 @@
+"""Wav2Lip generator host side: layer table (from liblsg), synthetic
+BN-calibrated weights, synthetic face crops, and the LipsyncEngine wrapper
+over lsg_gen (the GPU forward).
+
+The reference has no generator (mock_lipsync is a cost model,
+visual_mocks.cpp:40-51) and no checkpoint is available offline, so weights
+are synthetic: He-normal convolutions whose BatchNorm running statistics are
+calibrated on a seeded batch (pre-activations ~N(0,1), output logits
+~N(0,1)) and then folded -- random weights otherwise saturate the sigmoid and
+make any precision comparison meaningless.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import lib
+
+CONV, CONVT = 0, 1
+
+
+@dataclass(frozen=True)
+class Layer:
+    kind: int
+    cin: int
+    cout: int
+    kh: int
+    kw: int
+    sh: int
+    sw: int
+    ph: int
+    pw: int
+    oph: int
+    opw: int
+    res: int
+
+    @property
+    def n_params(self) -> int:
+        return self.cin * self.cout * self.kh * self.kw + self.cout
+
+
+def layers() -> list[Layer]:
+    L = lib()
+    info = (C.c_int32 * (12 * 64))()
+    n = C.c_int32()
+    L.call("lsg_gen_layer_info", info, 64, C.byref(n))
+    return [Layer(*[info[12 * i + j] for j in range(12)]) for i in range(n.value)]
+
+
+def param_count() -> int:
+    n = C.c_int64()
+    lib().call("lsg_gen_param_count", C.byref(n))
+    return n.value
+
+
+# face encoder blocks / decoder blocks as [first, last] layer indices
+FACE_BLOCKS = [(0, 0), (1, 3), (4, 7), (8, 10), (11, 13), (14, 15), (16, 17)]
+AUDIO = (18, 30)
+DEC_BLOCKS = [(31, 31), (32, 33), (34, 36), (37, 39), (40, 42), (43, 45), (46, 48)]
+OUT0, OUT1 = 49, 50
+
+
+def layer_shapes() -> list[tuple[int, int, int, int]]:
+    """(H_in, W_in, H_out, W_out) per layer, walking the Wav2Lip graph."""
+    Ls = layers()
+    shapes = [None] * len(Ls)
+
+    def out_hw(L, h, w):
+        if L.kind == CONV:
+            return (h + 2 * L.ph - L.kh) // L.sh + 1, (w + 2 * L.pw - L.kw) // L.sw + 1
+        return (h - 1) * L.sh - 2 * L.ph + L.kh + L.oph, (w - 1) * L.sw - 2 * L.pw + L.kw + L.opw
+
+    def run(a, b, h, w):
+        for i in range(a, b + 1):
+            oh, ow = out_hw(Ls[i], h, w)
+            shapes[i] = (h, w, oh, ow)
+            h, w = oh, ow
+        return h, w
+    h, w = 96, 96
+    for a, b in FACE_BLOCKS:
+        h, w = run(a, b, h, w)
+    h, w = run(AUDIO[0], AUDIO[1], 80, 16)
+    for a, b in DEC_BLOCKS:
+        h, w = run(a, b, h, w)
+    run(OUT0, OUT1, h, w)
+    return shapes
+
+
+def flops_per_frame() -> float:
+    """Algorithmic FLOPs of one forward (2 x MAC; convT counted on its input
+    grid, Hin*Win*Cin*Cout*k*k, i.e. no zero-insertion work)."""
+    tot = 0
+    for L, (hi, wi, ho, wo) in zip(layers(), layer_shapes()):
+        pix = ho * wo if L.kind == CONV else hi * wi
+        tot += 2 * pix * L.cin * L.cout * L.kh * L.kw
+    return float(tot)
+
+
+def synthetic_face(seed: int, size: int = 96) -> np.ndarray:
+    """Smooth synthetic face crop [96,96,3] u8: gradient background, skin
+    ellipse, darker eyes and mouth, seeded colours and mild noise."""
+    rng = np.random.default_rng(seed)
+    y, x = np.mgrid[0:size, 0:size].astype(np.float32) / size
+    bg = rng.uniform(40, 200, 3)
+    img = bg[None, None, :] * (0.6 + 0.4 * y[..., None])
+    skin = rng.uniform([150, 100, 80], [240, 190, 160])
+    face = ((x - 0.5) / 0.36) ** 2 + ((y - 0.52) / 0.45) ** 2 < 1.0
+    img[face] = skin
+    for ex in (0.35, 0.65):
+        eye = ((x - ex) / 0.07) ** 2 + ((y - 0.4) / 0.04) ** 2 < 1.0
+        img[eye] = skin * 0.3
+    mouth = ((x - 0.5) / (0.14 + 0.04 * rng.random())) ** 2 + ((y - 0.72) / 0.05) ** 2 < 1.0
+    img[mouth] = [120, 30, 40]
+    img += rng.normal(0, 4, img.shape)
+    return np.clip(img, 0, 255).astype(np.uint8)
+
+
+def jitter_face(ref: np.ndarray, frame_index: int, seed: int) -> np.ndarray:
+    """Per-frame target: the reference crop shifted by a seeded +-3 px wobble
+    (mock_face_detect's jitter, visual_mocks.cpp:10-22)."""
+    rng = np.random.default_rng((seed * 1000003 + frame_index) & 0xFFFFFFFF)
+    dy, dx = rng.integers(-3, 4, 2)
+    return np.roll(ref, (int(dy), int(dx)), axis=(0, 1))
+
+
+def _forward_calibrate(blob_layers, mel, faces, rng):
+    """fp32 forward that sets each BN layer's statistics from its own
+    pre-activations (batch statistics, gamma=1, beta=0) and folds them."""
+    import torch
+    import torch.nn.functional as F
+    Ls = layers()
+    out = []
+
+    def conv(i, x):
+        L = Ls[i]
+        fan_in = L.cin * L.kh * L.kw / (L.sh * L.sw if L.kind == CONVT else 1)
+        std = np.sqrt(2.0 / fan_in)
+        if L.kind == CONV:
+            w = rng.normal(0, std, (L.cout, L.cin, L.kh, L.kw)).astype(np.float32)
+            y = F.conv2d(x, torch.from_numpy(w), None, (L.sh, L.sw), (L.ph, L.pw))
+        else:
+            w = rng.normal(0, std, (L.cin, L.cout, L.kh, L.kw)).astype(np.float32)
+            y = F.conv_transpose2d(x, torch.from_numpy(w), None, (L.sh, L.sw), (L.ph, L.pw), (L.oph, L.opw))
+        if i == OUT1:
+            mu = y.mean(dim=(0, 2, 3)).numpy()
+            sd = y.std(dim=(0, 2, 3)).numpy() + 1e-6
+            w = w / sd[:, None, None, None]
+            b = (-mu / sd).astype(np.float32)
+            out.append((w.astype(np.float32), b))
+            return (y - torch.from_numpy(mu)[None, :, None, None]) / torch.from_numpy(sd)[None, :, None, None]
+        mu = y.mean(dim=(0, 2, 3))
+        var = y.var(dim=(0, 2, 3), unbiased=False)
+        inv = 1.0 / torch.sqrt(var + 1e-5)
+        shape = (-1, 1, 1, 1) if L.kind == CONV else (1, -1, 1, 1)
+        wf = (torch.from_numpy(w) * inv.reshape(shape)).numpy().astype(np.float32)
+        bf = (-mu * inv).numpy().astype(np.float32)
+        out.append((wf, bf))
+        y = (y - mu[None, :, None, None]) * inv[None, :, None, None]
+        if L.res:
+            y = y + x
+        return torch.relu(y)
+
+    feats = []
+    x = faces
+    for a, b in FACE_BLOCKS:
+        for i in range(a, b + 1):
+            x = conv(i, x)
+        feats.append(x)
+    a_out = mel
+    for i in range(AUDIO[0], AUDIO[1] + 1):
+        a_out = conv(i, a_out)
+    # weights must be appended in layer order: audio layers were generated
+    # after the face layers, matching the blob order (face, audio, decoder)
+    x = a_out
+    for a, b in DEC_BLOCKS:
+        for i in range(a, b + 1):
+            x = conv(i, x)
+        x = torch.cat([x, feats.pop()], dim=1)
+    x = conv(OUT0, x)
+    conv(OUT1, x)
+    return out
+
+
+def synthetic_weights(seed: int = 0, calib: int = 16) -> np.ndarray:
+    """Folded fp32 weight blob in lsg_gen's layer order (deterministic)."""
+    import torch
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    rng = np.random.default_rng(seed)
+    crng = np.random.default_rng(seed + 12345)
+    mel = torch.from_numpy(crng.normal(-5.0, 2.5, (calib, 1, 80, 16)).astype(np.float32))
+    faces = np.stack([face_input(synthetic_face(seed * 100 + i), synthetic_face(seed * 100 + i + 50))
+                      for i in range(calib)])
+    with torch.no_grad():
+        folded = _forward_calibrate(None, mel, torch.from_numpy(faces), rng)
+    blob = np.concatenate([np.concatenate([w.ravel(), b.ravel()]) for w, b in folded]).astype(np.float32)
+    assert blob.size == param_count(), (blob.size, param_count())
+    return blob
+
+
+def face_input(target_u8: np.ndarray, ref_u8: np.ndarray) -> np.ndarray:
+    """[6,96,96] f32 network input: lower half of the target masked, then the
+    reference, /255 (Wav2Lip's preprocessing)."""
+    t = target_u8.astype(np.float32) / 255.0
+    t[48:] = 0.0
+    r = ref_u8.astype(np.float32) / 255.0
+    return np.concatenate([t, r], axis=2).transpose(2, 0, 1).copy()
+
+
+class LipsyncEngine:
+    """The lip-sync stage on the GPU (lsg_gen): replaces mock_lipsync's cost
+    model (visual_mocks.hpp:41-43) with the generator forward."""
+
+    PREC_BF16, PREC_FP16 = 0, 1
+
+    def __init__(self, weights: np.ndarray, max_batch: int = 128, ctx=None, precision: int = 1):
+        from .api import default_context
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        w = np.ascontiguousarray(weights, np.float32)
+        h = C.c_void_p()
+        self.precision = precision
+        self.lib.call("lsg_gen_create", self.ctx.h, C.c_void_p(w.ctypes.data), w.size, precision, max_batch,
+                      C.byref(h))
+        self.h = h
+        self.max_batch = max_batch
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_gen_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward_device(self, mel_rows: int, chunk_row: int, target: int, refs: int, ref_index: int, out: int,
+                       out_format: int, B: int):
+        """All arguments are device pointers (ints)."""
+        self.lib.call("lsg_gen_forward", self.h, C.c_void_p(mel_rows), C.c_void_p(chunk_row), C.c_void_p(target),
+                      C.c_void_p(refs), C.c_void_p(ref_index), C.c_void_p(out), out_format, B)
+
+    @staticmethod
+    def validate(audio_span_ms: int, frame_span_ms: int, n_frames: int):
+        lib().call("lsg_lipsync_validate", audio_span_ms, frame_span_ms, n_frames)

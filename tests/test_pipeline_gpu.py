@@ -1,0 +1,78 @@
+"""Multi-stream pipeline (lsg_pipe): segments equal the reference
+Segmenter's, frame gathering follows the FrameRing window rule
+(frame_ring.cpp:36-55, +-50 ms, orchestrator.cpp:90-91), the frame -> mel
+chunk index rule is exact, and every rendered frame is
+bit-identical to the standalone stages (compute_mel of the segment audio +
+generator forward of that frame)."""
+import numpy as np
+import pytest
+
+from streams import random_scenario_pattern
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pipeline_matches_standalone_stages(reference):
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import api, generator
+    from paper_2512_18318_b200.pipeline import Pipeline, PipelineConfig
+    S, secs, fps = 4, 9, 25.0
+    pcm = [reference.render_pattern(random_scenario_pattern(i + 1), secs * 1000) for i in range(S)]
+    # one stream with a short EOS tail (< 16 mel frames: edge padding)
+    tail = reference.render_pattern(random_scenario_pattern(9), 4000)
+    pcm[3] = np.concatenate([tail, np.zeros(16000 * 1 + 320 * 3, np.int16),
+                             reference.render_pattern(random_scenario_pattern(9), 1600)[:3000]])
+    refs = np.stack([generator.synthetic_face(50 + s) for s in range(S)])
+    nvid = [int(np.ceil(len(p) / 16000 * fps)) for p in pcm]
+    video = [np.stack([generator.jitter_face(refs[s], f, s) for f in range(nvid[s])]) for s in range(S)]
+    w = generator.synthetic_weights(0)
+    ctx = api.Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng = generator.LipsyncEngine(w, max_batch=64, ctx=ctx, precision=1)
+    pipe = Pipeline(PipelineConfig(S, 12000, fps, 50, 64, True), eng, ctx=ctx)
+    recs, frames, st = pipe.run(pcm, video, refs)
+    assert st["frames_rendered"] == len(recs) == len(frames)
+
+    # segments: the reference's own segmenter, stream by stream
+    segs = {}
+    for s in range(S):
+        cuts, _, _ = reference.segment(pcm[s])
+        segs[s] = cuts
+    assert st["segments"] == sum(len(v) for v in segs.values())
+
+    # gathering + chunk rule, then re-render every frame standalone
+    expect = []
+    for s in range(S):
+        for j, c in enumerate(segs[s]):
+            audio = pcm[s][c["sample_off"]:c["sample_off"] + c["sample_len"]]
+            F = 0 if len(audio) < 1024 else 1 + (len(audio) - 1024) // 256
+            mel = api.compute_mel(api.AudioBuffer(audio)).data
+            rows = np.zeros((max(F, 16), 80), np.float32)
+            rows[:F] = mel
+            rows[F:] = mel[-1] if F else np.float32(np.log(1e-10))
+            for f in range(nvid[s]):
+                ts = int(round(f * 1000.0 / fps))
+                if not (c["begin"] - 50 <= ts <= c["end"] + 50):
+                    continue
+                k = min(max((ts - c["begin"]) // 16, 0), max(0, F - 16))
+                expect.append((s, j, f, ts, k, rows[k:k + 16]))
+    assert [(r["stream"], r["segment"], r["frame_index"], r["ts_ms"], r["mel_row"]) for r in recs] == \
+        [e[:5] for e in expect]
+    B = len(expect)
+    mel_rows = np.concatenate([e[5] for e in expect])  # [B*16, 80]
+    chunk = (np.arange(B) * 16).astype(np.int32)
+    target = np.stack([video[e[0]][e[2]] for e in expect])
+    ridx = np.array([e[0] for e in expect], np.int32)
+    out = np.zeros((B, 96, 96, 3), np.uint8)
+    for b0 in range(0, B, 64):
+        b1 = min(B, b0 + 64)
+        d = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in
+             (mel_rows[b0 * 16:b1 * 16], chunk[:b1 - b0], target[b0:b1], refs, ridx[b0:b1])]
+        o = torch.empty(b1 - b0, 96, 96, 3, dtype=torch.uint8, device="cuda")
+        eng.forward_device(*[t.data_ptr() for t in d], o.data_ptr(), 1, b1 - b0)
+        torch.cuda.synchronize()
+        out[b0:b1] = o.cpu().numpy()
+    assert np.array_equal(frames, out)
+    pipe.close()
+    eng.close()
+    ctx.set_stream(None)
