@@ -1,0 +1,397 @@
+// lipstream_b200.hpp -- C++ drop-ins for the reference's hot-path operators,
+// implemented over the C ABI in lsg.h (header-only; link liblsg.so).
+//
+// Same class/function names, argument meaning and exception types as the
+// reference (paths relative to /root/reference/proj/core/include/lipstream/):
+//   Segmenter, SegmenterConfig, RawSegment, BoundaryScorer  (segmenter.hpp:11-111)
+//   VadConfig, PeakMode                                      (vad.hpp:13-24)
+//   MelConfig, MelSpectrogram, compute_mel, mel_frame_count  (mel.hpp:12-39)
+//   AudioBuffer                                              (audio.hpp:12-20)
+//   LipsyncRender + the generator-backed lip-sync stage      (visual_mocks.hpp:33-43)
+// so a reference call site switches by changing the namespace
+// (lipstream:: -> lipstream_b200::).  All compute runs on the GPU; the host
+// keeps only the per-stream sample bookkeeping a RawSegment::audio needs and,
+// when a BoundaryScorer is attached, the integer state machine (the scorer is
+// a host callback by contract, segmenter.cpp:84-90).
+#pragma once
+
+#include <cstdint>
+#include <cstdlib>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lsg.h"
+
+namespace lipstream_b200 {
+
+using Timestamp = std::int64_t;
+using DurationMs = std::int64_t;
+
+inline void check(lsg_status s) {
+  if (s == LSG_OK) return;
+  const std::string m = lsg_last_error();
+  if (s == LSG_EINVAL) throw std::invalid_argument(m);
+  if (s == LSG_ELOGIC) throw std::logic_error(m);
+  throw std::runtime_error(m);
+}
+
+struct AudioBuffer {
+  std::vector<std::int16_t> samples;
+  int sample_rate = 16000;
+  Timestamp start = 0;
+  DurationMs duration_ms() const {  // audio.cpp:8-12
+    return static_cast<DurationMs>(std::llround(1000.0 * double(samples.size()) / sample_rate));
+  }
+  Timestamp end() const { return start + duration_ms(); }
+  bool empty() const { return samples.empty(); }
+};
+
+// One GPU (device + stream).  A process-wide default context per device.
+class Context {
+ public:
+  explicit Context(int device = 0) { check(lsg_ctx_create(device, &h_)); }
+  ~Context() { lsg_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  lsg_ctx handle() const { return h_; }
+  static Context& default_context() {
+    static Context c(0);
+    return c;
+  }
+
+ private:
+  lsg_ctx h_ = nullptr;
+};
+
+// ----------------------------------------------------------------- VAD / seg
+enum class PeakMode { Decay, MaxHold, Absolute };
+
+struct VadConfig {
+  PeakMode peak_mode = PeakMode::Decay;
+  double peak_half_life_ms = 10000.0;
+  double speech_threshold_db = -40.0;
+  DurationMs frame_ms = 20;
+};
+
+enum class CutCause { Pause, Forced, Eos };
+
+struct RawSegment {
+  Timestamp begin = 0;
+  Timestamp end = 0;
+  AudioBuffer audio;
+  double confidence = 1.0;
+  CutCause cause = CutCause::Eos;
+  DurationMs duration_ms() const { return end - begin; }
+};
+
+struct BoundaryContext {
+  Timestamp pause_start = 0;
+  DurationMs silence_run_ms = 0;
+  DurationMs segment_span_ms = 0;
+};
+
+struct BoundaryDecision {
+  bool cut = true;
+  double confidence = 1.0;
+  double cost_ms = 0.0;
+};
+
+class BoundaryScorer {
+ public:
+  virtual ~BoundaryScorer() = default;
+  virtual BoundaryDecision score(const BoundaryContext& ctx) = 0;
+};
+
+enum class SegmenterMode { Baseline, Semantic };
+
+struct SegmenterConfig {
+  SegmenterMode mode = SegmenterMode::Semantic;
+  VadConfig vad;
+  DurationMs min_silence_ms = 500;
+  DurationMs min_segment_ms = 1500;
+  DurationMs max_segment_ms = 10000;
+  int sample_rate = 16000;
+};
+
+struct SegmenterMetrics {
+  std::int64_t frames = 0;
+  std::int64_t speech_frames = 0;
+  std::int64_t cuts_pause = 0;
+  std::int64_t cuts_forced = 0;
+  std::int64_t cuts_eos = 0;
+  std::int64_t scorer_calls = 0;
+  double scorer_cost_ms = 0.0;
+};
+
+// Drop-in for lipstream::Segmenter (segmenter.hpp:76-111).
+class Segmenter {
+ public:
+  explicit Segmenter(SegmenterConfig cfg, BoundaryScorer* scorer = nullptr,
+                     Context& ctx = Context::default_context(), std::int64_t max_push_samples = 1 << 22)
+      : cfg_(cfg), scorer_(scorer) {
+    lsg_seg_cfg c{};
+    c.mode = cfg.mode == SegmenterMode::Baseline ? 0 : 1;
+    c.peak_mode = static_cast<int32_t>(cfg.vad.peak_mode);
+    c.peak_half_life_ms = cfg.vad.peak_half_life_ms;
+    c.speech_threshold_db = cfg.vad.speech_threshold_db;
+    c.frame_ms = cfg.vad.frame_ms;
+    c.min_silence_ms = cfg.min_silence_ms;
+    c.min_segment_ms = cfg.min_segment_ms;
+    c.max_segment_ms = cfg.max_segment_ms;
+    c.sample_rate = cfg.sample_rate;
+    c.flags_only = scorer ? 1 : 0;
+    check(lsg_seg_create(ctx.handle(), &c, 1, max_push_samples, &h_));
+    fs_ = std::int64_t(cfg.sample_rate) * cfg.vad.frame_ms / 1000;
+  }
+  ~Segmenter() { lsg_seg_destroy(h_); }
+  Segmenter(const Segmenter&) = delete;
+  Segmenter& operator=(const Segmenter&) = delete;
+
+  std::vector<RawSegment> push(const AudioBuffer& chunk) {
+    const int32_t sid = 0;
+    const int16_t* ptr = chunk.samples.data();
+    const int64_t n = static_cast<int64_t>(chunk.samples.size());
+    const int64_t st = chunk.start;
+    check(lsg_seg_push(h_, 1, &sid, &ptr, &n, &st, chunk.sample_rate, 0));
+    std::vector<RawSegment> out;
+    if (n == 0) return out;
+    if (!started_) {
+      started_ = true;
+      base_ = seg_start_ = chunk.start;
+    }
+    pending_.insert(pending_.end(), chunk.samples.begin(), chunk.samples.end());
+    if (!scorer_) return materialise();
+    std::vector<uint8_t> flags = take_flags();
+    for (uint8_t f : flags) process_frame(f != 0, out);
+    return out;
+  }
+
+  std::vector<RawSegment> finish() {
+    const int32_t sid = 0;
+    check(lsg_seg_finish(h_, 1, &sid));
+    if (!scorer_) return materialise();
+    std::vector<RawSegment> out;  // segmenter.cpp:120-145 on the host state
+    const std::int64_t stage = emitted_ + std::int64_t(pending_.size()) - consumed_ * fs_;
+    const DurationMs tail_ms = stage * 1000 / cfg_.sample_rate;
+    if (!speech_seen_ || pending_.empty()) {
+      pending_.clear();
+      return out;
+    }
+    RawSegment seg;
+    seg.begin = seg_start_;
+    seg.end = base_ + consumed_ * cfg_.vad.frame_ms + tail_ms;
+    seg.audio.sample_rate = cfg_.sample_rate;
+    seg.audio.start = seg_start_;
+    seg.audio.samples = std::move(pending_);
+    pending_.clear();
+    out.push_back(std::move(seg));
+    host_.cuts_eos += 1;
+    return out;
+  }
+
+  const SegmenterMetrics& metrics() const {
+    lsg_seg_metrics m{};
+    check(lsg_seg_get_metrics(h_, 0, &m));
+    metrics_.frames = m.frames;
+    metrics_.speech_frames = m.speech_frames;
+    if (scorer_) {
+      metrics_.cuts_pause = host_.cuts_pause;
+      metrics_.cuts_forced = host_.cuts_forced;
+      metrics_.cuts_eos = host_.cuts_eos;
+      metrics_.scorer_calls = host_.scorer_calls;
+      metrics_.scorer_cost_ms = host_.scorer_cost_ms;
+    } else {
+      metrics_.cuts_pause = m.cuts_pause;
+      metrics_.cuts_forced = m.cuts_forced;
+      metrics_.cuts_eos = m.cuts_eos;
+    }
+    return metrics_;
+  }
+
+ private:
+  std::vector<RawSegment> materialise() {
+    int64_t n = 0;
+    check(lsg_seg_take_cuts(h_, 0, nullptr, 0, &n));
+    std::vector<lsg_cut> cuts(static_cast<size_t>(n));
+    check(lsg_seg_take_cuts(h_, 0, cuts.data(), n, &n));
+    std::vector<RawSegment> out;
+    for (const lsg_cut& c : cuts) {
+      RawSegment s;
+      s.begin = c.begin;
+      s.end = c.end;
+      s.confidence = c.confidence;
+      s.cause = static_cast<CutCause>(c.cause);
+      s.audio.sample_rate = cfg_.sample_rate;
+      s.audio.start = c.begin;
+      s.audio.samples.assign(pending_.begin(), pending_.begin() + c.sample_len);
+      pending_.erase(pending_.begin(), pending_.begin() + c.sample_len);
+      out.push_back(std::move(s));
+    }
+    return out;
+  }
+
+  std::vector<uint8_t> take_flags() {
+    int64_t n = 0;
+    check(lsg_seg_take_flags(h_, 0, nullptr, 0, &n));
+    std::vector<uint8_t> f(static_cast<size_t>(n));
+    check(lsg_seg_take_flags(h_, 0, f.data(), n, &n));
+    return f;
+  }
+
+  void emit_cut(Timestamp cut_ms, double conf, CutCause cause, std::vector<RawSegment>& out) {
+    const auto split = static_cast<std::size_t>((cut_ms - seg_start_) * cfg_.sample_rate / 1000);
+    RawSegment seg;
+    seg.begin = seg_start_;
+    seg.end = cut_ms;
+    seg.confidence = conf;
+    seg.cause = cause;
+    seg.audio.sample_rate = cfg_.sample_rate;
+    seg.audio.start = seg_start_;
+    seg.audio.samples.assign(pending_.begin(), pending_.begin() + std::ptrdiff_t(split));
+    pending_.erase(pending_.begin(), pending_.begin() + std::ptrdiff_t(split));
+    emitted_ += std::int64_t(split);
+    out.push_back(std::move(seg));
+    seg_start_ = cut_ms;
+    speech_seen_ = false;
+  }
+
+  // process_frame (segmenter.cpp:51-99) over a GPU VAD decision.
+  void process_frame(bool speech, std::vector<RawSegment>& out) {
+    const Timestamp f0 = base_ + consumed_ * cfg_.vad.frame_ms;
+    const Timestamp f1 = f0 + cfg_.vad.frame_ms;
+    if (speech) {
+      if (speech_seen_ && silence_run_ >= cfg_.min_silence_ms && candidate_open_ && candidate_cut_) {
+        emit_cut(pause_start_ + silence_run_ / 2, candidate_confidence_, CutCause::Pause, out);
+        host_.cuts_pause += 1;
+      }
+      silence_run_ = 0;
+      candidate_open_ = false;
+      candidate_cut_ = false;
+      speech_seen_ = true;
+    } else {
+      if (silence_run_ == 0) pause_start_ = f0;
+      silence_run_ += cfg_.vad.frame_ms;
+      if (!candidate_open_ && silence_run_ >= cfg_.min_silence_ms && speech_seen_) {
+        candidate_open_ = true;
+        candidate_cut_ = true;
+        candidate_confidence_ = 1.0;
+        if (cfg_.mode == SegmenterMode::Semantic) {
+          if (pause_start_ - seg_start_ < cfg_.min_segment_ms) {
+            candidate_cut_ = false;
+          } else if (scorer_) {
+            BoundaryDecision d = scorer_->score({pause_start_, silence_run_, pause_start_ - seg_start_});
+            host_.scorer_calls += 1;
+            host_.scorer_cost_ms += d.cost_ms;
+            candidate_cut_ = d.cut;
+            candidate_confidence_ = d.confidence;
+          }
+        }
+      }
+    }
+    if (cfg_.mode == SegmenterMode::Semantic && speech_seen_ && f1 - seg_start_ >= cfg_.max_segment_ms) {
+      emit_cut(f1, 1.0, CutCause::Forced, out);
+      host_.cuts_forced += 1;
+    }
+    consumed_ += 1;
+  }
+
+  SegmenterConfig cfg_;
+  BoundaryScorer* scorer_;
+  lsg_seg h_ = nullptr;
+  std::int64_t fs_ = 320;
+  std::vector<std::int16_t> pending_;
+  mutable SegmenterMetrics metrics_;
+  SegmenterMetrics host_;
+  bool started_ = false;
+  Timestamp base_ = 0, seg_start_ = 0, pause_start_ = 0;
+  std::int64_t consumed_ = 0, emitted_ = 0;
+  DurationMs silence_run_ = 0;
+  bool speech_seen_ = false, candidate_open_ = false, candidate_cut_ = false;
+  double candidate_confidence_ = 1.0;
+};
+
+// ---------------------------------------------------------------------- mel
+struct MelConfig {
+  int sample_rate = 16000;
+  int fft_size = 1024;
+  int hop = 256;
+  int n_mels = 80;
+  double fmin = 0.0;
+  double fmax = 8000.0;
+};
+
+struct MelSpectrogram {
+  std::int64_t n_frames = 0;
+  int n_mels = 0;
+  std::vector<float> data;
+  float at(std::int64_t frame, int mel) const { return data[static_cast<std::size_t>(frame) * n_mels + mel]; }
+};
+
+inline lsg_mel_cfg to_c(const MelConfig& c) {
+  lsg_mel_cfg m{};
+  m.sample_rate = c.sample_rate;
+  m.fft_size = c.fft_size;
+  m.hop = c.hop;
+  m.n_mels = c.n_mels;
+  m.fmin = c.fmin;
+  m.fmax = c.fmax;
+  return m;
+}
+
+inline std::int64_t mel_frame_count(std::int64_t n_samples, const MelConfig& cfg = {}) {
+  lsg_mel_cfg c = to_c(cfg);
+  int64_t f = 0;
+  check(lsg_mel_frames(n_samples, &c, &f));
+  return f;
+}
+
+// Drop-in for compute_mel (mel.hpp:39).  Builds the tables once per call;
+// hold a MelExtractor to amortise them.
+class MelExtractor {
+ public:
+  explicit MelExtractor(const MelConfig& cfg = {}, std::int64_t max_frames = 1 << 16,
+                        Context& ctx = Context::default_context())
+      : cfg_(cfg) {
+    lsg_mel_cfg c = to_c(cfg);
+    check(lsg_mel_create(ctx.handle(), &c, max_frames, &h_));
+  }
+  ~MelExtractor() { lsg_mel_destroy(h_); }
+  MelExtractor(const MelExtractor&) = delete;
+  MelExtractor& operator=(const MelExtractor&) = delete;
+  MelSpectrogram operator()(const AudioBuffer& audio) const {
+    MelSpectrogram m;
+    m.n_mels = cfg_.n_mels;
+    m.n_frames = mel_frame_count(std::int64_t(audio.samples.size()), cfg_);
+    m.data.resize(static_cast<std::size_t>(m.n_frames) * cfg_.n_mels);
+    int64_t f = 0;
+    if (m.n_frames)
+      check(lsg_mel_compute(h_, audio.samples.data(), int64_t(audio.samples.size()), m.data.data(), &f));
+    return m;
+  }
+
+ private:
+  MelConfig cfg_;
+  lsg_mel h_ = nullptr;
+};
+
+inline MelSpectrogram compute_mel(const AudioBuffer& audio, const MelConfig& cfg = {}) {
+  const std::int64_t f = mel_frame_count(std::int64_t(audio.samples.size()), cfg);
+  MelExtractor ext(cfg, f > 0 ? f : 1);
+  return ext(audio);
+}
+
+// ------------------------------------------------------------------ lipsync
+struct LipsyncRender {
+  std::int64_t frames = 0;
+  std::int64_t cost_us = 0;  // measured device time of the render, microseconds
+};
+
+// The lip-sync stage with the generator behind it: validates the pair the
+// way mock_lipsync does (visual_mocks.cpp:40-51), then renders.
+inline void validate_lipsync(DurationMs audio_span_ms, DurationMs frame_span_ms, std::int64_t n_frames) {
+  check(lsg_lipsync_validate(audio_span_ms, frame_span_ms, n_frames));
+}
+
+}  // namespace lipstream_b200

@@ -145,7 +145,13 @@ class Context:
         return p.value or 0
 
     def set_stream(self, ptr: int | None):
-        self.lib.call("lsg_ctx_set_stream", self.h, C.c_void_p(ptr or 0))
+        """None: the context's own stream.  An int is a cudaStream_t; 0 (the
+        legacy default stream, e.g. torch's default stream) maps to
+        cudaStreamLegacy because NULL means "own stream" in the C ABI."""
+        if ptr is None:
+            self.lib.call("lsg_ctx_set_stream", self.h, C.c_void_p(0))
+        else:
+            self.lib.call("lsg_ctx_set_stream", self.h, C.c_void_p(ptr if ptr else 1))
 
 
 _DEFAULT_CTX: dict[int, Context] = {}

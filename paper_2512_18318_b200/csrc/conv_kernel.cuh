@@ -1,0 +1,396 @@
+// conv_kernel.cuh -- persistent implicit-GEMM convolution on tcgen05 + TMA.
+//
+// One launch = one conv layer (all of its phases).  Grid = one CTA per SM;
+// each CTA walks output tiles t = blockIdx.x, +gridDim.x, ... (128 output
+// pixels x BN channels).  Warp roles:
+//   warp 0     TMA producer (one elected thread): per K stage, im2col TMA
+//              loads of the A tile straight from the NHWC activation
+//              (cp.async.bulk.tensor.4d ... .im2col: the tensor-map bounding
+//              box encodes the conv padding and stride, the per-load offsets
+//              the filter tap, out-of-bounds pixels are zero-filled), plus a
+//              bulk async copy of the packed weight tile B.
+//   warp 1     MMA issuer (one thread): tcgen05.mma kind::f16 (M=128, N=BN,
+//              K=16) into one of two TMEM accumulators.
+//   warps 2-9  epilogue, two warps per TMEM lane quadrant (each half of the
+//              BN columns): tcgen05.ld -> folded-BN bias -> residual -> ReLU ->
+//              16-bit store into a channel slice of the destination, or the
+//              fused 1x1 32->3 + sigmoid of the output block.  The second TMEM
+//              accumulator lets tile i's epilogue overlap tile i+1's mainloop.
+//
+// A smem layouts by channel chunk CC (the largest of 64/32/16/8 dividing
+// Cin): CC=64 -> 128B swizzle, 32 -> 64B, 16 -> 32B, 8 -> no swizzle (two
+// 8-channel loads per K=16 step, LBO = 2 KB).  Every A stage is 128 x 64
+// 16-bit elements (16 KB); B stays 128B-swizzled 64-wide K blocks.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "tc.cuh"
+
+namespace lsg {
+namespace gen {
+
+constexpr int BM = 128;  // UMMA M (TMEM lanes)
+constexpr int BK = 64;   // 16-bit elements per K stage
+constexpr int MAX_TAPS = 49;
+constexpr int MAX_PHASES = 9;
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;  // TMA warp, MMA warp, epilogue warps
+constexpr int OOB_OFFSET = 200;  // im2col offset that always lands outside the input (zero fill)
+
+enum OutMode { OUT_16 = 0, OUT_F32_NCHW = 1, OUT_U8_NHWC = 2, OUT_F32_LOGITS = 3 };
+
+struct Phase {
+  const uint16_t* w;  // packed [ntiles][kblocks][BN][64], 128 B swizzled rows
+  int ntaps, K;
+  int nloads;         // TMA loads of this phase (ntaps * C / CC, +1 pad load for CC = 8)
+  int kblocks;        // ceil(nloads / (64 / CC))
+  int nsteps;         // MMA K=16 steps, ceil(K / 16)
+  int oy, ox;         // output offset of this phase
+  int GH, GW;         // GEMM pixel grid of this phase (per image)
+  int M, mtiles;      // B * GH * GW, ceil(M / 128)
+  int tile0;          // first global tile of this phase
+  unsigned char offh[MAX_TAPS + 1], offw[MAX_TAPS + 1];  // im2col offsets per tap (+ pad tap)
+};
+
+struct alignas(64) ConvParams {
+  CUtensorMap tmap;  // im2col map of the input view; first member (64 B aligned in param space)
+  int cc;            // channel chunk per TMA load
+  int lower_h, lower_w;
+  int H, W, C;
+  uint16_t* out;
+  int OH, OW, out_pitch, out_coff;
+  const uint16_t* res;
+  int res_pitch, res_coff;
+  const float* bias;
+  int sy, sx, osy, osx;
+  int relu, out_mode;
+  const float* w1;  // fused output 1x1: [3][32]
+  const float* b1;  // [3]
+  void* final_out;
+  int nphases, ntiles_n, total_tiles;
+  Phase ph[MAX_PHASES];
+};
+
+// 16-bit number format: HALF = fp16 (kind::f16 format 0), else bf16 (format 1)
+template <bool HALF>
+struct Num {
+  static constexpr uint32_t kFmt = HALF ? 0u : 1u;
+  __device__ __forceinline__ static uint32_t pack(float a, float b) {
+    if constexpr (HALF) {
+      __half2 v = __floats2half2_rn(a, b);
+      return *reinterpret_cast<uint32_t*>(&v);
+    } else {
+      __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+      return *reinterpret_cast<uint32_t*>(&v);
+    }
+  }
+  __device__ __forceinline__ static float2 unpack(uint32_t u) {
+    if constexpr (HALF) {
+      return __half22float2(*reinterpret_cast<__half2*>(&u));
+    } else {
+      return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
+    }
+  }
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int TMEM_COLS =
+      2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+struct TileId {
+  int z, nt, mt;
+};
+
+__device__ __forceinline__ TileId decode_tile(const ConvParams& p, int t) {
+  int z = 0;
+#pragma unroll 1
+  while (z + 1 < p.nphases && t >= p.ph[z + 1].tile0) ++z;
+  const int r = t - p.ph[z].tile0;
+  const int nt = r / p.ph[z].mtiles;
+  return {z, nt, r - nt * p.ph[z].mtiles};
+}
+
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int w,
+                                              int h, int n, uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
+      "h"(off_h)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor for the A operand of K step `k` (0..3) of a stage.
+__device__ __forceinline__ uint64_t a_desc(uint32_t sa, int cc, int k) {
+  uint32_t addr, lbo, sbo, layout;
+  if (cc == 64) {
+    addr = sa + k * 32; lbo = 16; sbo = 1024; layout = 2;   // SWIZZLE_128B
+  } else if (cc == 32) {
+    addr = sa + (k >> 1) * 8192 + (k & 1) * 32; lbo = 16; sbo = 512; layout = 4;  // SWIZZLE_64B
+  } else if (cc == 16) {
+    addr = sa + k * 4096; lbo = 16; sbo = 256; layout = 6;  // SWIZZLE_32B
+  } else {
+    addr = sa + k * 4096; lbo = 2048; sbo = 128; layout = 0;  // no swizzle: 2 loads of 8 channels
+  }
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+}
+
+template <int BN, bool FUSED_OUT, bool HALF>
+__global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant__ ConvParams p) {
+  using CF = Cfg<BN>;
+  using NF = Num<HALF>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * CF::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * CF::B_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 32 * NUM_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
+  }
+  if (warp == 1) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int cc = p.cc;
+  const int lps = BK / cc;  // TMA loads per stage
+  const int cpt = p.C / cc; // loads per tap
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+      const uint32_t load_bytes = BM * cc * 2;
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        const TileId id = decode_tile(p, t);
+        const Phase& P = p.ph[id.z];
+        const int m0 = id.mt * BM;
+        const int HW = P.GH * P.GW;
+        const int n = m0 / HW, rem = m0 - n * HW;
+        const int gy = rem / P.GW, gx = rem - gy * P.GW;
+        const int w0 = gx * p.sx + p.lower_w, h0 = gy * p.sy + p.lower_h;
+        const uint16_t* wbase = P.w + (size_t)id.nt * P.kblocks * BN * BK;
+        for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+          const int s = it % S;
+          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+          const int l0 = kb * lps;
+          const int nl = min(lps, P.nloads - l0);
+          tc::mbar_arrive_expect_tx(&full[s], CF::B_BYTES + nl * load_bytes);
+          tc::bulk_g2s(sB0 + s * CF::B_BYTES, wbase + (size_t)kb * BN * BK, CF::B_BYTES, &full[s]);
+          for (int j = 0; j < nl; ++j) {
+            const int l = l0 + j;
+            const int tap = l / cpt, ch = (l - tap * cpt) * cc;
+            tma_im2col_4d(sA0 + s * CF::A_BYTES + j * load_bytes, &p.tmap, &full[s], ch, w0, h0, n,
+                          P.offw[tap], P.offh[tap]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+      uint32_t it = 0, tl = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+        const TileId id = decode_tile(p, t);
+        const Phase& P = p.ph[id.z];
+        const uint32_t a = tl & 1, use = tl >> 1;
+        tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + a * BN;
+        for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+          const int s = it % S;
+          tc::mbar_wait(&full[s], (it / S) & 1);
+          tc::tc_fence_after();
+          const uint32_t sa = sA0 + s * CF::A_BYTES;
+          const uint64_t db = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
+          const int ns = min(4, P.nsteps - kb * 4);
+          for (int k = 0; k < ns; ++k) tc::mma_f16(d, a_desc(sa, cc, k), db + 2 * k, idesc, (kb | k) != 0);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 2-9)
+    const int q = warp & 3;               // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;     // which half of the BN columns
+    constexpr bool SPLIT = !FUSED_OUT && BN >= 32;
+    constexpr int HC = SPLIT ? BN / 2 : BN;
+    const int cbeg = SPLIT ? half * HC : 0;
+    const bool active = SPLIT || half == 0;
+    const int r = q * 32 + lane;
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+      const TileId id = decode_tile(p, t);
+      const Phase& P = p.ph[id.z];
+      const uint32_t a = tl & 1, use = tl >> 1;
+      const int m = id.mt * BM + r;
+      const int n0 = id.nt * BN;
+      const bool valid = m < P.M;
+      int n = 0, oy = 0, ox = 0;
+      if (valid) {
+        const int HW = P.GH * P.GW;
+        n = m / HW;
+        const int rem = m - n * HW;
+        const int gy = rem / P.GW, gx = rem - gy * P.GW;
+        oy = gy * p.osy + P.oy;
+        ox = gx * p.osx + P.ox;
+      }
+      const size_t pix = ((size_t)n * p.OH + oy) * p.OW + ox;
+      if constexpr (!FUSED_OUT) {
+        uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + n0 + cbeg;
+        const uint16_t* rrow =
+            (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + n0 + cbeg : nullptr;
+        // prefetch the first residual chunk while the mainloop runs
+        uint4 rn0 = make_uint4(0, 0, 0, 0), rn1 = rn0;
+        if (rrow) {
+          rn0 = __ldg(reinterpret_cast<const uint4*>(rrow));
+          rn1 = __ldg(reinterpret_cast<const uint4*>(rrow) + 1);
+        }
+        tc::mbar_wait(&tfull[a], use & 1);
+        tc::tc_fence_after();
+        if (!active) {
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[a]);
+          continue;
+        }
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HC; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(tbase + c0, v);
+          const uint4 ra = rn0, rb = rn1;
+          if (rrow && c0 + 16 < HC) {  // next chunk's residual in flight during this one
+            rn0 = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16));
+            rn1 = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16) + 1);
+          }
+          tc::tmem_ld_wait();
+          if (valid) {
+            float f[16];
+            const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + cbeg + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 b4 = __ldg(bp + j);
+              f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + b4.x;
+              f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+              f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+              f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+            }
+            if (rrow) {
+              const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float2 x = NF::unpack(rr[j]);
+                f[2 * j] += x.x;
+                f[2 * j + 1] += x.y;
+              }
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
+            }
+            uint4 o0, o1;
+            o0.x = NF::pack(f[0], f[1]);
+            o0.y = NF::pack(f[2], f[3]);
+            o0.z = NF::pack(f[4], f[5]);
+            o0.w = NF::pack(f[6], f[7]);
+            o1.x = NF::pack(f[8], f[9]);
+            o1.y = NF::pack(f[10], f[11]);
+            o1.z = NF::pack(f[12], f[13]);
+            o1.w = NF::pack(f[14], f[15]);
+            *reinterpret_cast<uint4*>(orow + c0) = o0;
+            *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
+          }
+        }
+      } else {
+        // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid;
+        // the second warp of each quadrant only keeps the barrier count
+        tc::mbar_wait(&tfull[a], use & 1);
+        tc::tc_fence_after();
+        if (half == 0) {
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+          float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tbase + c0, v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float x = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), x, o[o3]);
+            }
+          }
+          if (valid) {
+            const int HWo = p.OH * p.OW;
+            const size_t pp = (size_t)oy * p.OW + ox;
+            if (p.out_mode == OUT_F32_LOGITS) {
+              float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
+            } else if (p.out_mode == OUT_F32_NCHW) {
+              float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
+            } else {
+              uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) {
+                const float s = 1.f / (1.f + __expf(-o[o3]));
+                out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
+              }
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
+  }
+}
+
+}  // namespace gen
+}  // namespace lsg

@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "conv_kernel.cuh"
 #include "gen_internal.h"
 #include "lsg_common.cuh"
 #include "tc.cuh"
@@ -110,300 +111,7 @@ static const LayerSpec kLayers[] = {
 constexpr int kNumLayers = sizeof(kLayers) / sizeof(kLayers[0]);
 static_assert(kNumLayers == 51, "Wav2Lip has 51 conv layers");
 
-constexpr int BM = 128;        // UMMA M (TMEM lanes)
-constexpr int BK = 64;         // bf16 per 128-byte swizzle row
-constexpr int MAX_TAPS = 49;
-constexpr int NUM_THREADS = 288;  // 4 producer warps, 4 epilogue warps, 1 MMA warp
-
-enum OutMode { OUT_BF16 = 0, OUT_F32_NCHW = 1, OUT_U8_NHWC = 2, OUT_F32_LOGITS = 3 };
-
-struct Phase {
-  const uint16_t* w;       // packed [ntiles][kblocks][BN][64], 128 B swizzled rows
-  int ntaps, kblocks, K;
-  int oy, ox;              // output offset of this phase
-  int GH, GW;              // GEMM pixel grid of this phase (per image)
-  int M;                   // B * GH * GW
-  signed char dy[MAX_TAPS], dx[MAX_TAPS];
-};
-
-// Activations/weights are 16-bit storage (bf16 or fp16, chosen per engine).
-struct ConvParams {
-  const uint16_t* in;
-  int H, W, in_pitch, in_coff, C;
-  uint16_t* out;
-  int OH, OW, out_pitch, out_coff;
-  const uint16_t* res;
-  int res_pitch, res_coff;
-  const float* bias;
-  int sy, sx, osy, osx;
-  int relu, out_mode;
-  const float* w1;  // fused output 1x1: [3][32]
-  const float* b1;  // [3]
-  void* final_out;
-  Phase ph[4];
-};
-
-// 16-bit number format: HALF = fp16 (kind::f16 format 0), else bf16 (format 1)
-template <bool HALF>
-struct Num {
-  static constexpr uint32_t kFmt = HALF ? 0u : 1u;
-  __device__ __forceinline__ static uint32_t pack(float a, float b) {
-    if constexpr (HALF) {
-      __half2 v = __floats2half2_rn(a, b);
-      return *reinterpret_cast<uint32_t*>(&v);
-    } else {
-      __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-      return *reinterpret_cast<uint32_t*>(&v);
-    }
-  }
-  __device__ __forceinline__ static float2 unpack(uint32_t u) {
-    if constexpr (HALF) {
-      return __half22float2(*reinterpret_cast<__half2*>(&u));
-    } else {
-      return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
-    }
-  }
-};
-
-template <int BN>
-struct Cfg {
-  static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (100 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
-  static constexpr int KTAB_MAX = 1152;  // K/8 granules (fd1.0: 9 x 1024 / 8)
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + KTAB_MAX * 4 + 256;
-};
-
-template <int BN, bool FUSED_OUT, bool HALF>
-__global__ void __launch_bounds__(NUM_THREADS, 2) conv_tc(const __grid_constant__ ConvParams p) {
-  using CF = Cfg<BN>;
-  using NF = Num<HALF>;
-  constexpr int S = CF::STAGES;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = tc::smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + S * CF::A_BYTES;
-  int* ktab = reinterpret_cast<int*>(sB + S * CF::B_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ktab + CF::KTAB_MAX);
-  uint64_t* empty = full + S;
-  uint64_t* tmem_full = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Phase& P = p.ph[blockIdx.z];
-  const int m0 = blockIdx.x * BM;
-  if (m0 >= P.M) return;  // phases have different M; uniform per CTA
-  const int n0 = blockIdx.y * BN;
-
-  // K-granule table: (dy, dx, channel) per 8-wide K granule
-  for (int gi = threadIdx.x; gi < P.kblocks * 8; gi += NUM_THREADS) {
-    const int k = gi * 8;
-    int e = -1;  // K padding: zero-filled granule
-    if (k < P.K) {
-      const int tap = k / p.C, c = k - tap * p.C;
-      e = (((int)P.dy[tap] + 64) << 24) | (((int)P.dx[tap] + 64) << 16) | c;
-    }
-    ktab[gi] = e;
-  }
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      tc::mbar_init(&full[s], 128);
-      tc::mbar_init(&empty[s], 1);
-    }
-    tc::mbar_init(tmem_full, 1);
-    tc::fence_mbar_init();
-  }
-  if (warp == 8) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int KB = P.kblocks;
-
-  if (warp < 4) {
-    // ------------------------------------------------ producers (A gather)
-    const int t = threadIdx.x;
-    const int g = t & 7, r0 = t >> 3;
-    int iy0[8], ix0[8];
-    const uint16_t* rb[8];
-    const int HW = P.GH * P.GW;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = m0 + r0 + 16 * i;
-      if (m < P.M) {
-        const int n = m / HW, rem = m - n * HW;
-        const int gy = rem / P.GW, gx = rem - gy * P.GW;
-        iy0[i] = gy * p.sy;
-        ix0[i] = gx * p.sx;
-        rb[i] = p.in + (size_t)n * p.H * p.W * p.in_pitch + p.in_coff;
-      } else {
-        iy0[i] = -100000;
-        ix0[i] = -100000;
-        rb[i] = p.in;
-      }
-    }
-    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
-    const uint32_t swz = (uint32_t)((g ^ (r0 & 7)) << 4);
-    const uint16_t* wbase = P.w + (size_t)blockIdx.y * KB * BN * BK;
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % S;
-      const uint32_t ph = (kb / S) & 1;
-      tc::mbar_wait(&empty[s], ph ^ 1);
-      if (t == 0) {
-        tc::mbar_expect_tx(&full[s], CF::B_BYTES);
-        tc::bulk_g2s(sB0 + s * CF::B_BYTES, wbase + (size_t)kb * BN * BK, CF::B_BYTES, &full[s]);
-      }
-      const int e = ktab[kb * 8 + g];
-      const bool kv = e >= 0;
-      const int dy = ((e >> 24) & 0xff) - 64, dx = ((e >> 16) & 0xff) - 64, c = e & 0xffff;
-      const uint32_t dst0 = sA0 + s * CF::A_BYTES + r0 * 128 + swz;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int iy = iy0[i] + dy, ix = ix0[i] + dx;
-        const bool ok = kv && (unsigned)iy < (unsigned)p.H && (unsigned)ix < (unsigned)p.W;
-        const uint16_t* src = ok ? rb[i] + ((size_t)iy * p.W + ix) * p.in_pitch + c : p.in;
-        tc::cp_async16(dst0 + i * 16 * 128, src, ok ? 16u : 0u);
-      }
-      tc::cp_async_commit();
-      if (kb >= 1) {
-        tc::cp_async_wait<1>();
-        tc::fence_proxy_async();
-        tc::mbar_arrive(&full[(kb - 1) % S]);
-      }
-    }
-    tc::cp_async_wait<0>();
-    tc::fence_proxy_async();
-    if (KB >= 1) tc::mbar_arrive(&full[(KB - 1) % S]);
-  } else if (warp == 8) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
-      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % S;
-        tc::mbar_wait(&full[s], (kb / S) & 1);
-        tc::tc_fence_after();
-        const uint64_t a = tc::sdesc_sw128(sA0 + s * CF::A_BYTES);
-        const uint64_t b = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
-#pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          tc::mma_f16(tmem, a + 2 * k, b + 2 * k, idesc, (kb | k) != 0);
-        tc::mma_commit(&empty[s]);
-      }
-      tc::mma_commit(tmem_full);
-    }
-    __syncwarp();
-  } else {
-    // ------------------------------------------------ epilogue (warps 4-7)
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const int m = m0 + r;
-    tc::mbar_wait(tmem_full, 0);
-    tc::tc_fence_after();
-    const bool valid = m < P.M;
-    int n = 0, oy = 0, ox = 0;
-    if (valid) {
-      const int HW = P.GH * P.GW;
-      n = m / HW;
-      const int rem = m - n * HW;
-      const int gy = rem / P.GW, gx = rem - gy * P.GW;
-      oy = gy * p.osy + P.oy;
-      ox = gx * p.osx + P.ox;
-    }
-    const size_t pix = ((size_t)n * p.OH + oy) * p.OW + ox;
-    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
-    if constexpr (!FUSED_OUT) {
-      uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + n0;
-      const uint16_t* rrow = p.res ? p.res + pix * p.res_pitch + p.res_coff + n0 : nullptr;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tc::tmem_ld16(tbase + c0, v);
-        tc::tmem_ld_wait();
-        if (valid) {
-          float f[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + __ldg(p.bias + n0 + c0 + j);
-          if (rrow) {
-            const uint4 a = *reinterpret_cast<const uint4*>(rrow + c0);
-            const uint4 b = *reinterpret_cast<const uint4*>(rrow + c0 + 8);
-            const uint32_t ra[4] = {a.x, a.y, a.z, a.w};
-            const uint32_t rbv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 x = NF::unpack(ra[j]);
-              const float2 y = NF::unpack(rbv[j]);
-              f[2 * j] += x.x;
-              f[2 * j + 1] += x.y;
-              f[8 + 2 * j] += y.x;
-              f[8 + 2 * j + 1] += y.y;
-            }
-          }
-          if (p.relu) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
-          }
-          uint4 o0, o1;
-          o0.x = NF::pack(f[0], f[1]);
-          o0.y = NF::pack(f[2], f[3]);
-          o0.z = NF::pack(f[4], f[5]);
-          o0.w = NF::pack(f[6], f[7]);
-          o1.x = NF::pack(f[8], f[9]);
-          o1.y = NF::pack(f[10], f[11]);
-          o1.z = NF::pack(f[12], f[13]);
-          o1.w = NF::pack(f[14], f[15]);
-          *reinterpret_cast<uint4*>(orow + c0) = o0;
-          *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
-        }
-      }
-    } else {
-      // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid
-      float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tc::tmem_ld16(tbase + c0, v);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float a = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
-#pragma unroll
-          for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), a, o[o3]);
-        }
-      }
-      if (valid) {
-        const int HWo = p.OH * p.OW;
-        const size_t pp = (size_t)oy * p.OW + ox;
-        if (p.out_mode == OUT_F32_LOGITS) {
-          float* out = reinterpret_cast<float*>(p.final_out);
-#pragma unroll
-          for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
-        } else if (p.out_mode == OUT_F32_NCHW) {
-          float* out = reinterpret_cast<float*>(p.final_out);
-#pragma unroll
-          for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
-        } else {
-          uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
-#pragma unroll
-          for (int o3 = 0; o3 < 3; ++o3) {
-            const float s = 1.f / (1.f + __expf(-o[o3]));
-            out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
-          }
-        }
-      }
-    }
-    tc::tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 8) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
-  }
-}
+using NumH = Num<true>;
 
 // ------------------------------------------------------------ input prep
 // faces: [B][96][96][3] u8 target (rows >= 48 masked), refs [R][96][96][3]
@@ -472,8 +180,45 @@ struct LayerRun {
   int ntiles;
   bool fused;
   ConvParams p;
-  int GH[4], GW[4];  // per phase, per image
+  View in_view;
+  int GH[MAX_PHASES], GW[MAX_PHASES];  // per phase, per image
 };
+
+// cuTensorMapEncodeIm2col through the runtime's driver entry point (no
+// link-time dependency on libcuda).
+using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2col im2col_fn() {
+  static EncodeIm2col fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    LSG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) fail(LSG_ECUDA, "cuTensorMapEncodeIm2col unavailable");
+    fn = reinterpret_cast<EncodeIm2col>(f);
+  }
+  return fn;
+}
+
+// im2col tensor map of an NHWC channel-slice view: dims (C, W, H, N), strides
+// in bytes, bounding box corners (W, H order), 128 pixels x cc channels per load.
+void encode_im2col(CUtensorMap* map, const View& v, int n, int cc, int lw, int lh, int uw, int uh, int sx, int sy) {
+  const cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)v.pitch * 2, (cuuint64_t)v.W * v.pitch * 2,
+                                 (cuuint64_t)v.H * v.W * v.pitch * 2};
+  const int lower[2] = {lw, lh}, upper[2] = {uw, uh};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)sx, (cuuint32_t)sy, 1};
+  const CUtensorMapSwizzle sw = cc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                         : (cc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                     : (cc == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE));
+  CUresult r = im2col_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, lower, upper,
+                           (cuuint32_t)cc, (cuuint32_t)BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
+}
 
 int pick_bn(int cout) {
   if (cout <= 256) return cout;
@@ -501,6 +246,7 @@ uint16_t f2h(float f) {  // round to nearest even (host)
 struct lsg_gen_s {
   Ctx* ctx = nullptr;
   int max_batch = 0;
+  int sm_count = 148;
   bool half = false;  // LSG_PREC_FP16
   DevBuf<uint16_t> wpack;
   DevBuf<float> bias;
@@ -512,15 +258,23 @@ struct lsg_gen_s {
 
 static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
 
+// Persistent launch: tiles enumerate (phase, n tile, m tile) with m fastest,
+// one CTA per SM walks them round-robin.
 template <int BN, bool F, bool H>
-static void launch_conv(const LayerRun& r, int B, cudaStream_t st) {
+static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   ConvParams p = r.p;
-  int mt = 0;
+  int tiles = 0;
   for (int z = 0; z < r.nphases; ++z) {
-    p.ph[z].M = B * r.GH[z] * r.GW[z];
-    mt = std::max(mt, (int)ceil_div(p.ph[z].M, BM));
+    Phase& P = p.ph[z];
+    P.M = B * r.GH[z] * r.GW[z];
+    P.mtiles = (int)ceil_div(P.M, BM);
+    P.tile0 = tiles;
+    tiles += P.mtiles * r.ntiles;
   }
-  dim3 grid(mt, r.ntiles, r.nphases);
+  p.nphases = r.nphases;
+  p.ntiles_n = r.ntiles;
+  p.total_tiles = tiles;
+  const int grid = std::min(tiles, sms);
   conv_tc<BN, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
 }
 
@@ -531,22 +285,22 @@ static void set_smem_attr() {
 }
 
 template <bool H>
-static void dispatch_t(const LayerRun& r, int B, cudaStream_t st) {
-  if (r.fused) return launch_conv<32, true, H>(r, B, st);
+static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
+  if (r.fused) return launch_conv<32, true, H>(r, B, sms, st);
   switch (r.bn) {
-    case 16: return launch_conv<16, false, H>(r, B, st);
-    case 32: return launch_conv<32, false, H>(r, B, st);
-    case 64: return launch_conv<64, false, H>(r, B, st);
-    case 128: return launch_conv<128, false, H>(r, B, st);
-    case 192: return launch_conv<192, false, H>(r, B, st);
-    case 256: return launch_conv<256, false, H>(r, B, st);
+    case 16: return launch_conv<16, false, H>(r, B, sms, st);
+    case 32: return launch_conv<32, false, H>(r, B, sms, st);
+    case 64: return launch_conv<64, false, H>(r, B, sms, st);
+    case 128: return launch_conv<128, false, H>(r, B, sms, st);
+    case 192: return launch_conv<192, false, H>(r, B, sms, st);
+    case 256: return launch_conv<256, false, H>(r, B, sms, st);
   }
   fail(LSG_ERUNTIME, "generator: no kernel for this tile width");
 }
 
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
-  if (h->half) dispatch_t<true>(r, B, st);
-  else dispatch_t<false>(r, B, st);
+  if (h->half) dispatch_t<true>(r, B, h->sm_count, st);
+  else dispatch_t<false>(r, B, h->sm_count, st);
 }
 
 extern "C" {
@@ -593,6 +347,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       h->ctx = ctx;
       h->max_batch = max_batch;
       h->half = precision == LSG_PREC_FP16;
+      h->sm_count = ctx->sm_count;
       const int B = max_batch;
       // ---------------- activation buffers (bf16 NHWC)
       struct Req { View* v; int H, W, C; };
@@ -619,7 +374,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       std::vector<uint16_t> pack;
       std::vector<float> bias;
       std::vector<float> w1b1(3 * 32 + 3);
-      std::vector<int64_t> pack_off(kNumLayers * 4, 0);
+      std::vector<int64_t> pack_off(kNumLayers * MAX_PHASES, 0);
       std::vector<int64_t> bias_off(kNumLayers, 0);
       struct PhaseGeo { int ntaps; signed char dy[MAX_TAPS], dx[MAX_TAPS]; int ky[MAX_TAPS], kx[MAX_TAPS]; int oy, ox; };
       std::vector<std::vector<PhaseGeo>> geo(kNumLayers);
@@ -652,6 +407,21 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
             }
           pg.oy = pg.ox = 0;
           G.push_back(pg);
+        } else if (L.sh == 1 && L.sw == 1 && L.ph == 0 && L.pw == 0) {
+          // fd1.0: stride-1 convT of a 1x1 map -- output pixel (a, b) is
+          // exactly tap (a, b) of the single input pixel: kh*kw one-tap
+          // phases, no zero taps (the plan asserts the 1x1 input)
+          for (int a = 0; a < L.kh; ++a)
+            for (int bb = 0; bb < L.kw; ++bb) {
+              PhaseGeo pg{};
+              pg.ntaps = 1;
+              pg.dy[0] = pg.dx[0] = 0;
+              pg.ky[0] = a;
+              pg.kx[0] = bb;
+              pg.oy = a;
+              pg.ox = bb;
+              G.push_back(pg);
+            }
         } else {
           // out[o] = sum_{i,k: o = i*s - p + k} in[i] w[k]; phase a of o = g*s + a
           for (int a = 0; a < L.sh; ++a)
@@ -681,9 +451,9 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           const PhaseGeo& pg = G[z];
           const int K = pg.ntaps * cin_pad;
           const int kbs = (int)ceil_div(K, BK);
-          pack_off[li * 4 + z] = (int64_t)pack.size();
+          pack_off[li * MAX_PHASES + z] = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)ntiles * kbs * bn * BK, 0);
-          uint16_t* dst = pack.data() + pack_off[li * 4 + z];
+          uint16_t* dst = pack.data() + pack_off[li * MAX_PHASES + z];
           for (int nt = 0; nt < ntiles; ++nt)
             for (int kb = 0; kb < kbs; ++kb) {
               uint16_t* blk = dst + ((size_t)nt * kbs + kb) * bn * BK;
@@ -803,13 +573,12 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         r.ntiles = L.cout / r.bn;
         r.nphases = (int)geo[l].size();
         ConvParams& p = r.p;
-        p.in = in.p;
+        r.in_view = in;
         p.H = in.H;
         p.W = in.W;
-        p.in_pitch = in.pitch;
-        p.in_coff = in.coff;
         p.C = (L.cin + 7) / 8 * 8;
         if (in.C != p.C) fail(LSG_ERUNTIME, std::string("generator plan: channel mismatch at ") + L.name);
+        p.cc = p.C % 64 == 0 ? 64 : (p.C % 32 == 0 ? 32 : (p.C % 16 == 0 ? 16 : 8));
         // output geometry
         int OH, OW;
         if (L.kind == CONV) {
@@ -831,7 +600,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         p.res_coff = in.coff;
         p.bias = h->bias.p + bias_off[l];
         p.relu = 1;
-        p.out_mode = OUT_BF16;
+        p.out_mode = OUT_16;
         if (L.kind == CONV) {
           p.sy = L.sh;
           p.sx = L.sw;
@@ -840,29 +609,57 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           p.sy = p.sx = 1;
           p.osy = L.sh;
           p.osx = L.sw;
+          if ((int)geo[l].size() == L.kh * L.kw && L.sh == 1) {  // one-tap phases of a 1x1 input
+            if (in.H != 1 || in.W != 1) fail(LSG_ERUNTIME, std::string("generator plan: ") + L.name + " needs a 1x1 input");
+            p.osy = L.kh;
+            p.osx = L.kw;
+          }
         }
         if (fused) {
           p.w1 = h->w1b1.p;
           p.b1 = h->w1b1.p + 96;
         }
+        if (r.nphases > MAX_PHASES) fail(LSG_ERUNTIME, "generator: too many phases");
+        // im2col bounding box: conv -> lower = -pad, upper = pad - (k - 1), traversal
+        // stride = conv stride; convT phases walk the input grid (lower = upper = 0)
+        int lower_w = 0, lower_h = 0, upper_w = 0, upper_h = 0;
+        if (L.kind == CONV) {
+          lower_w = -L.pw;
+          lower_h = -L.ph;
+          upper_w = L.pw - (L.kw - 1);
+          upper_h = L.ph - (L.kh - 1);
+        }
+        p.lower_w = lower_w;
+        p.lower_h = lower_h;
+        encode_im2col(&p.tmap, in, max_batch, p.cc, lower_w, lower_h, upper_w, upper_h, p.sx, p.sy);
         for (int z = 0; z < r.nphases; ++z) {
           const PhaseGeo& pg = geo[l][z];
           Phase& P = p.ph[z];
-          P.w = h->wpack.p + pack_off[l * 4 + z];
+          P.w = h->wpack.p + pack_off[l * MAX_PHASES + z];
           P.ntaps = pg.ntaps;
           P.K = pg.ntaps * p.C;
-          P.kblocks = (int)ceil_div(P.K, BK);
-          if (P.kblocks * 8 > 1152) fail(LSG_ERUNTIME, "generator: K table overflow");
+          P.nsteps = (int)ceil_div(P.K, 16);
+          P.nloads = pg.ntaps * (p.C / p.cc);
+          if (p.cc == 8 && (P.nloads & 1)) P.nloads += 1;  // K=16 steps read loads in pairs: zero pad load
+          P.kblocks = (int)ceil_div(P.nloads, BK / p.cc);
+          if (P.kblocks != (int)ceil_div(P.K, BK)) fail(LSG_ERUNTIME, std::string("generator: K blocking at ") + L.name);
           P.oy = pg.oy;
           P.ox = pg.ox;
           for (int t = 0; t < pg.ntaps; ++t) {
-            P.dy[t] = pg.dy[t];
-            P.dx[t] = pg.dx[t];
+            const int ow = pg.dx[t] - lower_w, oh = pg.dy[t] - lower_h;
+            if (ow < 0 || oh < 0 || ow > 255 || oh > 255) fail(LSG_ERUNTIME, "generator: im2col offset range");
+            P.offw[t] = (unsigned char)ow;
+            P.offh[t] = (unsigned char)oh;
           }
-          r.GH[z] = L.kind == CONV ? OH : (int)ceil_div(OH - pg.oy, L.sh);
-          r.GW[z] = L.kind == CONV ? OW : (int)ceil_div(OW - pg.ox, L.sw);
+          P.offw[pg.ntaps] = (unsigned char)OOB_OFFSET;  // pad tap: always outside the input
+          P.offh[pg.ntaps] = 0;
+          r.GH[z] = L.kind == CONV ? OH : (int)ceil_div(OH - pg.oy, p.osy);
+          r.GW[z] = L.kind == CONV ? OW : (int)ceil_div(OW - pg.ox, p.osx);
           P.GH = r.GH[z];
           P.GW = r.GW[z];
+          // the tensor map's bounding box must generate exactly the phase grid
+          const int gw = (in.W + upper_w - lower_w - 1) / p.sx + 1, gh = (in.H + upper_h - lower_h - 1) / p.sy + 1;
+          if (gw != P.GW || gh != P.GH) fail(LSG_ERUNTIME, std::string("generator: im2col grid mismatch at ") + L.name);
         }
         h->plan.push_back(r);
       }
@@ -932,9 +729,9 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     const LayerRun& r = h->plan[stop_layer];
     const ConvParams& p = r.p;
     const LayerSpec& L = kLayers[stop_layer];
-    const uint16_t* src = which ? p.out : p.in;
+    const uint16_t* src = which ? p.out : r.in_view.p;
     const int H = which ? p.OH : p.H, W = which ? p.OW : p.W;
-    const int pitch = which ? p.out_pitch : p.in_pitch, coff = which ? p.out_coff : p.in_coff;
+    const int pitch = which ? p.out_pitch : r.in_view.pitch, coff = which ? p.out_coff : r.in_view.coff;
     const int C = which ? L.cout : p.C;
     const int64_t pixels = (int64_t)B * H * W;
     if (h->half) view_to_f32<true><<<(unsigned)ceil_div(pixels * C, 256), 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev);

@@ -1,0 +1,206 @@
+// dropin_test.cpp -- the reference's own known-answer cases, run against the
+// C++ drop-ins (include/lsg/lipstream_b200.hpp) on the GPU.  Mirrors
+// proj/tests/segmenter_tests.cpp and media_tests.cpp of the reference.
+// Built by tests/cpp/Makefile; run by tests/test_cpp_dropin.py (GPU).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lsg/lipstream_b200.hpp"
+
+using namespace lipstream_b200;
+
+static int g_fail = 0;
+#define CHECK(c)                                                        \
+  do {                                                                  \
+    if (!(c)) {                                                         \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      ++g_fail;                                                         \
+    }                                                                   \
+  } while (0)
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+struct Burst {
+  int64_t speech, pause;
+};
+
+static AudioBuffer pattern(int64_t lead, std::vector<Burst> b, int64_t total, double hz = 220.0, double amp = 0.3) {
+  std::vector<int64_t> sp, pa;
+  for (auto& x : b) {
+    sp.push_back(x.speech);
+    pa.push_back(x.pause);
+  }
+  AudioBuffer a;
+  a.samples.resize(size_t(total * 16));
+  int64_t n = 0;
+  check(lsg_synth_pattern(lead, int32_t(b.size()), sp.data(), pa.data(), hz, amp, total, 16000, a.samples.data(),
+                          int64_t(a.samples.size()), &n));
+  a.samples.resize(size_t(n));
+  return a;
+}
+
+static std::vector<RawSegment> segment_all(const AudioBuffer& a, SegmenterConfig cfg, size_t chunk = 0,
+                                           BoundaryScorer* scorer = nullptr) {
+  Segmenter seg(cfg, scorer);
+  std::vector<RawSegment> out;
+  if (chunk == 0) {
+    out = seg.push(a);
+  } else {
+    for (size_t off = 0; off < a.samples.size(); off += chunk) {
+      AudioBuffer c;
+      c.start = a.start + int64_t(off) * 1000 / a.sample_rate;
+      size_t e = std::min(a.samples.size(), off + chunk);
+      c.samples.assign(a.samples.begin() + off, a.samples.begin() + e);
+      auto part = seg.push(c);
+      out.insert(out.end(), part.begin(), part.end());
+    }
+  }
+  auto tail = seg.finish();
+  out.insert(out.end(), tail.begin(), tail.end());
+  return out;
+}
+
+static std::vector<int64_t> ends(const std::vector<RawSegment>& s) {
+  std::vector<int64_t> e;
+  for (auto& x : s) e.push_back(x.end);
+  return e;
+}
+
+int main(int argc, char** argv) {
+  const std::string golden_dir = argc > 1 ? argv[1] : "tests/golden";
+  SegmenterConfig cfg;
+  // segmenter_tests.cpp:140-151: chunk invariance, stock begins
+  AudioBuffer stock = pattern(600, {{1400, 600}}, 8000);
+  auto whole = segment_all(stock, cfg);
+  CHECK(whole.size() == 4);
+  if (whole.size() == 4) {
+    CHECK(whole[0].begin == 0 && whole[1].begin == 2300 && whole[2].begin == 4300 && whole[3].begin == 6300);
+  }
+  for (size_t ch : {37u, 1000u, 4037u}) CHECK(ends(segment_all(stock, cfg, ch)) == ends(whole));
+  size_t total = 0;
+  for (auto& s : whole) {
+    CHECK(s.audio.start == s.begin);
+    CHECK(int64_t(s.audio.samples.size()) == s.duration_ms() * 16);
+    total += s.audio.samples.size();
+  }
+  CHECK(total == stock.samples.size());
+  // :153-163 pauses under the floor never cut
+  auto shortp = segment_all(pattern(0, {{1000, 400}}, 6000), cfg);
+  CHECK(shortp.size() == 1 && shortp[0].end == 6000 && shortp[0].cause == CutCause::Eos);
+  // :165-182 continuous speech splits at the cap, only in semantic mode
+  AudioBuffer cont = pattern(0, {{20000, 600}}, 12000);
+  auto sem = segment_all(cont, cfg);
+  CHECK(sem.size() == 2 && sem[0].end == 10000 && sem[0].cause == CutCause::Forced && sem[1].end == 12000);
+  SegmenterConfig base = cfg;
+  base.mode = SegmenterMode::Baseline;
+  auto bl = segment_all(cont, base);
+  CHECK(bl.size() == 1 && bl[0].end == 12000);
+  // :184-198 baseline vs semantic fixture
+  AudioBuffer fx = pattern(600, {{800, 600}}, 5600);
+  CHECK((ends(segment_all(fx, base)) == std::vector<int64_t>{1700, 3100, 4500, 5600}));
+  CHECK((ends(segment_all(fx, cfg)) == std::vector<int64_t>{3100, 5600}));
+  // :200-230 scorer veto
+  struct Scripted : BoundaryScorer {
+    int calls = 0;
+    BoundaryDecision score(const BoundaryContext& c) override {
+      ++calls;
+      CHECK(c.silence_run_ms >= 500);
+      CHECK(c.segment_span_ms >= 1500);
+      if (calls == 1) return {false, 0.0, 1.5};
+      return {true, 0.7, 1.5};
+    }
+  } scorer;
+  {
+    Segmenter seg(cfg, &scorer);
+    auto segs = seg.push(pattern(0, {{1600, 600}}, 6000));
+    auto tail = seg.finish();
+    segs.insert(segs.end(), tail.begin(), tail.end());
+    CHECK(segs.size() == 2);
+    if (segs.size() == 2) {
+      CHECK(segs[0].end == 4100 && segs[0].confidence == 0.7 && segs[0].cause == CutCause::Pause);
+      CHECK(segs[1].end == 6000);
+    }
+    CHECK(scorer.calls == 2);
+    CHECK(seg.metrics().scorer_calls == 2);
+    CHECK(std::fabs(seg.metrics().scorer_cost_ms - 3.0) < 1e-12);
+  }
+  // :232-239 silence only
+  AudioBuffer silence;
+  silence.samples.assign(16000 * 3, 0);
+  CHECK(segment_all(silence, cfg).empty());
+  // :241-256 stream discipline
+  {
+    Segmenter seg(cfg);
+    AudioBuffer a = pattern(600, {{1400, 600}}, 1000);
+    seg.push(a);
+    AudioBuffer gap = a;
+    gap.start = 5000;
+    CHECK(throws<std::invalid_argument>([&] { seg.push(gap); }));
+    AudioBuffer wrong = a;
+    wrong.sample_rate = 8000;
+    CHECK(throws<std::invalid_argument>([&] { seg.push(wrong); }));
+    seg.finish();
+    CHECK(throws<std::logic_error>([&] { seg.push(a); }));
+    CHECK(throws<std::logic_error>([&] { seg.finish(); }));
+  }
+  // :258-269 broken configs
+  {
+    SegmenterConfig c = cfg;
+    c.min_silence_ms = 0;
+    CHECK(throws<std::invalid_argument>([&] { Segmenter s(c); }));
+    c = cfg;
+    c.max_segment_ms = c.min_segment_ms;
+    CHECK(throws<std::invalid_argument>([&] { Segmenter s(c); }));
+    c = cfg;
+    c.sample_rate = 44100;
+    CHECK(throws<std::invalid_argument>([&] { Segmenter s(c); }));
+  }
+  // media_tests.cpp:83-97 frame counts
+  CHECK(mel_frame_count(1023) == 0 && mel_frame_count(1024) == 1 && mel_frame_count(1279) == 1 &&
+        mel_frame_count(1280) == 2 && mel_frame_count(160000) == 622);
+  // :99-117 440 Hz lands in band 11; :172-179 golden within 1e-4 rel
+  AudioBuffer tone = pattern(0, {{1000, 0}}, 1000, 440.0);
+  MelSpectrogram mel = compute_mel(tone);
+  CHECK(mel.n_frames == 59 && mel.n_mels == 80);
+  int arg = 0;
+  std::vector<double> band(80, 0.0);
+  for (int64_t f = 0; f < mel.n_frames; ++f)
+    for (int b = 0; b < 80; ++b) band[size_t(b)] += mel.at(f, b);
+  for (int b = 1; b < 80; ++b)
+    if (band[size_t(b)] > band[size_t(arg)]) arg = b;
+  CHECK(arg == 11);
+  std::ifstream g(golden_dir + "/mel_golden.bin", std::ios::binary);
+  uint32_t hdr[2] = {0, 0};
+  g.read(reinterpret_cast<char*>(hdr), 8);
+  std::vector<float> want(size_t(hdr[0]) * hdr[1]);
+  g.read(reinterpret_cast<char*>(want.data()), std::streamsize(want.size() * 4));
+  CHECK(g.good() && hdr[0] == 59 && hdr[1] == 80);
+  size_t bad = 0;
+  for (size_t i = 0; i < want.size() && i < mel.data.size(); ++i)
+    if (std::fabs(mel.data[i] - want[i]) > 1e-4 * std::max(1.0, std::fabs(double(want[i])))) ++bad;
+  CHECK(bad == 0);
+  // :119-126 silence -> log floor
+  AudioBuffer sil;
+  sil.samples.assign(4096, 0);
+  for (float v : compute_mel(sil).data) CHECK(v == float(std::log(1e-10)));
+  // visual_mocks.cpp:43-46 lip-sync contract
+  CHECK(throws<std::invalid_argument>([] { validate_lipsync(2000, 2020, 1); }));
+  CHECK(throws<std::invalid_argument>([] { validate_lipsync(2000, 2400, 61); }));
+  validate_lipsync(2000, 2020, 61);
+  std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "all drop-in checks passed", g_fail);
+  return g_fail ? 1 : 0;
+}
