@@ -133,23 +133,31 @@ __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* m
       : "memory");
 }
 
-// UMMA shared-memory descriptor for the A operand of K step `k` (0..3) of a stage.
-__device__ __forceinline__ uint64_t a_desc(uint32_t sa, int cc, int k) {
-  uint32_t addr, lbo, sbo, layout;
-  if (cc == 64) {
-    addr = sa + k * 32; lbo = 16; sbo = 1024; layout = 2;   // SWIZZLE_128B
-  } else if (cc == 32) {
-    addr = sa + (k >> 1) * 8192 + (k & 1) * 32; lbo = 16; sbo = 512; layout = 4;  // SWIZZLE_64B
-  } else if (cc == 16) {
-    addr = sa + k * 4096; lbo = 16; sbo = 256; layout = 6;  // SWIZZLE_32B
-  } else {
-    addr = sa + k * 4096; lbo = 2048; sbo = 128; layout = 0;  // no swizzle: 2 loads of 8 channels
-  }
-  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)layout << 61);
+// A descriptor of a stage: constant fields per channel chunk CC, start address
+// advanced per K=16 step by a compile-time offset (16-byte units).
+template <int CC>
+__device__ __forceinline__ uint64_t a_desc_base(uint32_t sa) {
+  constexpr uint64_t lbo = CC == 8 ? 2048 : 16;
+  constexpr uint64_t sbo = CC == 64 ? 1024 : (CC == 32 ? 512 : (CC == 16 ? 256 : 128));
+  constexpr uint64_t layout = CC == 64 ? 2 : (CC == 32 ? 4 : (CC == 16 ? 6 : 0));
+  return (uint64_t)((sa >> 4) & 0x3FFF) | ((lbo >> 4) << 16) | ((sbo >> 4) << 32) | (1ull << 46) | (layout << 61);
+}
+template <int CC>
+__device__ __forceinline__ constexpr uint32_t a_koff(int k) {
+  return CC == 64 ? k * 2 : (CC == 32 ? (k >> 1) * 512 + (k & 1) * 2 : k * 256);
 }
 
-template <int BN, bool FUSED_OUT, bool HALF>
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred));
+  return pred != 0;
+}
+
+template <int BN, int CC, bool FUSED_OUT, bool HALF>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant__ ConvParams p) {
   using CF = Cfg<BN>;
   using NF = Num<HALF>;
@@ -184,69 +192,84 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int cc = p.cc;
-  const int lps = BK / cc;  // TMA loads per stage
-  const int cpt = p.C / cc; // loads per tap
+  constexpr int LPS = BK / CC;  // TMA loads per stage
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
-      const uint32_t load_bytes = BM * cc * 2;
-      uint32_t it = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        const TileId id = decode_tile(p, t);
-        const Phase& P = p.ph[id.z];
-        const int m0 = id.mt * BM;
-        const int HW = P.GH * P.GW;
-        const int n = m0 / HW, rem = m0 - n * HW;
-        const int gy = rem / P.GW, gx = rem - gy * P.GW;
-        const int w0 = gx * p.sx + p.lower_w, h0 = gy * p.sy + p.lower_h;
-        const uint16_t* wbase = P.w + (size_t)id.nt * P.kblocks * BN * BK;
-        for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
-          const int s = it % S;
-          tc::mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-          const int l0 = kb * lps;
-          const int nl = min(lps, P.nloads - l0);
-          tc::mbar_arrive_expect_tx(&full[s], CF::B_BYTES + nl * load_bytes);
+    // ------------------------------------------------ TMA producer (whole warp;
+    // lane j issues load j of a stage, lane 0 the weights + expect_tx)
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    constexpr uint32_t LOAD_BYTES = BM * CC * 2;
+    const int cpt = p.C / CC;  // loads per tap
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      const TileId id = decode_tile(p, t);
+      const Phase& P = p.ph[id.z];
+      const int KB = P.kblocks, NL = P.nloads;
+      const int m0 = id.mt * BM;
+      const int HW = P.GH * P.GW;
+      const int n = m0 / HW, rem = m0 - n * HW;
+      const int gy = rem / P.GW, gx = rem - gy * P.GW;
+      const int w0 = gx * p.sx + p.lower_w, h0 = gy * p.sy + p.lower_h;
+      const uint16_t* wbase = P.w + (size_t)id.nt * KB * BN * BK;
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        const int l = kb * LPS + lane;
+        const int nl = min(LPS, NL - kb * LPS);
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&full[s], CF::B_BYTES + nl * LOAD_BYTES);
           tc::bulk_g2s(sB0 + s * CF::B_BYTES, wbase + (size_t)kb * BN * BK, CF::B_BYTES, &full[s]);
-          for (int j = 0; j < nl; ++j) {
-            const int l = l0 + j;
-            const int tap = l / cpt, ch = (l - tap * cpt) * cc;
-            tma_im2col_4d(sA0 + s * CF::A_BYTES + j * load_bytes, &p.tmap, &full[s], ch, w0, h0, n,
-                          P.offw[tap], P.offh[tap]);
-          }
+        }
+        if (lane < nl) {
+          const int tap = l / cpt, ch = (l - tap * cpt) * CC;
+          tma_im2col_4d(sA0 + s * CF::A_BYTES + lane * LOAD_BYTES, &p.tmap, &full[s], ch, w0, h0, n,
+                        P.offw[tap], P.offh[tap]);
+        }
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
-      const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
-      uint32_t it = 0, tl = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
-        const TileId id = decode_tile(p, t);
-        const Phase& P = p.ph[id.z];
-        const uint32_t a = tl & 1, use = tl >> 1;
-        tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
+    // ------------------------------------------------ MMA issuer (whole warp
+    // runs the loop, one elected lane issues: descriptors stay uniform)
+    constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+    const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
+    int s = 0;
+    uint32_t ph = 0, tl = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+      const TileId id = decode_tile(p, t);
+      const int KB = p.ph[id.z].kblocks, NS = p.ph[id.z].nsteps;
+      const uint32_t a = tl & 1, use = tl >> 1;
+      tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint32_t d = tmem + a * BN;
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::mbar_wait(&full[s], ph);
         tc::tc_fence_after();
-        const uint32_t d = tmem + a * BN;
-        for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
-          const int s = it % S;
-          tc::mbar_wait(&full[s], (it / S) & 1);
-          tc::tc_fence_after();
-          const uint32_t sa = sA0 + s * CF::A_BYTES;
-          const uint64_t db = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
-          const int ns = min(4, P.nsteps - kb * 4);
-          for (int k = 0; k < ns; ++k) tc::mma_f16(d, a_desc(sa, cc, k), db + 2 * k, idesc, (kb | k) != 0);
+        const uint64_t da = a_desc_base<CC>(sA0 + s * CF::A_BYTES);
+        const uint64_t db = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
+        if (elect_one()) {
+          if (kb * 4 + 4 <= NS) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) tc::mma_f16(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+          } else {
+            const int ns = NS - kb * 4;
+            for (int k = 0; k < ns; ++k) tc::mma_f16(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+          }
           tc::mma_commit(&empty[s]);
         }
-        tc::mma_commit(&tfull[a]);
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      if (elect_one()) tc::mma_commit(&tfull[a]);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
     const int q = warp & 3;               // TMEM lane quadrant this warp may access

@@ -260,7 +260,7 @@ static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout
 
 // Persistent launch: tiles enumerate (phase, n tile, m tile) with m fastest,
 // one CTA per SM walks them round-robin.
-template <int BN, bool F, bool H>
+template <int BN, int CC, bool F, bool H>
 static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   ConvParams p = r.p;
   int tiles = 0;
@@ -275,27 +275,41 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   p.ntiles_n = r.ntiles;
   p.total_tiles = tiles;
   const int grid = std::min(tiles, sms);
-  conv_tc<BN, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
+  conv_tc<BN, CC, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
 }
 
-template <int BN, bool F>
-static void set_smem_attr() {
-  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
-  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+// (tile width BN, channel chunk CC, fused output) combinations the Wav2Lip
+// layers use; every combination is compiled for fp16 and bf16.
+#define LSG_CONV_VARIANTS(X) \
+  X(16, 8, false)            \
+  X(32, 8, false)            \
+  X(32, 16, false)           \
+  X(32, 32, false)           \
+  X(64, 32, false)           \
+  X(64, 64, false)           \
+  X(128, 64, false)          \
+  X(192, 64, false)          \
+  X(256, 64, false)          \
+  X(32, 16, true)
+
+static void set_smem_attrs() {
+#define LSG_SET_ATTR(BN, CC, F)                                                                                   \
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                Cfg<BN>::SMEM));                                                                  \
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                                Cfg<BN>::SMEM));
+  LSG_CONV_VARIANTS(LSG_SET_ATTR)
+#undef LSG_SET_ATTR
 }
 
 template <bool H>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
-  if (r.fused) return launch_conv<32, true, H>(r, B, sms, st);
-  switch (r.bn) {
-    case 16: return launch_conv<16, false, H>(r, B, sms, st);
-    case 32: return launch_conv<32, false, H>(r, B, sms, st);
-    case 64: return launch_conv<64, false, H>(r, B, sms, st);
-    case 128: return launch_conv<128, false, H>(r, B, sms, st);
-    case 192: return launch_conv<192, false, H>(r, B, sms, st);
-    case 256: return launch_conv<256, false, H>(r, B, sms, st);
-  }
-  fail(LSG_ERUNTIME, "generator: no kernel for this tile width");
+#define LSG_DISPATCH(BN, CC, F) \
+  if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, H>(r, B, sms, st);
+  LSG_CONV_VARIANTS(LSG_DISPATCH)
+#undef LSG_DISPATCH
+  fail(LSG_ERUNTIME, "generator: no conv kernel for tile width " + std::to_string(r.bn) + " / channel chunk " +
+                         std::to_string(r.p.cc));
 }
 
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
@@ -663,13 +677,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         }
         h->plan.push_back(r);
       }
-      set_smem_attr<16, false>();
-      set_smem_attr<32, false>();
-      set_smem_attr<64, false>();
-      set_smem_attr<128, false>();
-      set_smem_attr<192, false>();
-      set_smem_attr<256, false>();
-      set_smem_attr<32, true>();
+      set_smem_attrs();
     } catch (...) {
       delete h;
       throw;
