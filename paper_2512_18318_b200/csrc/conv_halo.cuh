@@ -1,0 +1,323 @@
+// conv_halo.cuh -- stride-1 3x3 convolution with shared-memory halo reuse.
+//
+// For the narrow, high-resolution layers (96x96x64, 48x48x128, the 80->32
+// output conv, ...) the im2col kernel re-reads every input pixel once per
+// filter tap (9x) and the weights once per 128-pixel tile, so it is bound by
+// operand traffic, not the tensor pipe.  Here an output tile is a 16-row x
+// 8-column pixel block of one image; per 64-channel block the TMA (tile mode,
+// zero fill outside the image) loads the (16+2) x (8+2) input patch ONCE, as
+// eight 8-channel "granule planes" of [18][10][8] elements.  Every filter tap
+// is then a UMMA operand view into that patch: a no-swizzle K-major
+// descriptor whose start address is shifted by (ky*10 + kx)*16 bytes, core
+// matrices = 8 consecutive patch pixels x 16 B, SBO = one patch row (160 B),
+// LBO = one granule plane.  So a patch buffer feeds 9 taps x 4 K-steps = 36
+// tcgen05.mma; the weights stay resident in shared memory for the whole
+// persistent CTA when they fit (all Wav2Lip layers routed here but fd5.x),
+// otherwise they stream per (channel block, tap) through their own ring.
+// Epilogue identical to conv_tc (bias, residual, ReLU, channel-slice store,
+// fused 1x1+sigmoid output).
+#pragma once
+
+#include "conv_kernel.cuh"
+
+namespace lsg {
+namespace gen {
+
+constexpr int HTH = 16, HTW = 8;  // output tile: 16 rows x 8 columns = 128 pixels
+
+struct alignas(64) HaloParams {
+  CUtensorMap tmap;  // tiled map of the input view (C, W, H, N), box (8, HTW+k-1, HTH+k-1, 1)
+  int H, W, C, B;
+  int k, pad;
+  int pw, ph;        // patch width / height (HTW + k - 1, HTH + k - 1)
+  int plane;         // bytes per granule plane in smem (pw*ph*16, 128-aligned)
+  int ngran;         // C / 8
+  int ncb;           // channel blocks of <= 8 granules
+  int tiles_x, tiles_y, tiles_per_img, total_tiles;
+  const uint16_t* w; // packed [ntile][cb][tap][BN][64] (128 B swizzled rows)
+  int wblocks;       // cb * taps blocks per n tile
+  // epilogue (as ConvParams)
+  uint16_t* out;
+  int out_pitch, out_coff;
+  const uint16_t* res;
+  int res_pitch, res_coff;
+  const float* bias;
+  int relu, out_mode;
+  const float* w1;
+  const float* b1;
+  void* final_out;
+  int ntiles_n;
+};
+
+template <int BN, bool B_RES>
+struct HaloCfg {
+  static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B, rounded to 128
+  static constexpr int HSTAGE = 8 * PLANE_MAX;
+  static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
+  static constexpr int B_RES_BYTES = 96 * 1024;
+  static constexpr int HS = B_RES ? 4 : 3;
+  static constexpr int BS = B_RES ? 1 : ((200 * 1024 - HS * HSTAGE) / BBLK > 8 ? 8 : (200 * 1024 - HS * HSTAGE) / BBLK);
+  static constexpr int B_BYTES = B_RES ? B_RES_BYTES : BS * BBLK;
+  static constexpr int SMEM = 1024 + HS * HSTAGE + B_BYTES + 512;
+  static constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
+};
+
+__device__ __forceinline__ void tma_tile_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int x, int y,
+                                            int n) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(bar)), "r"(c), "r"(x), "r"(y), "r"(n)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
+}
+
+template <int BN, bool FUSED_OUT, bool HALF, bool B_RES>
+__global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
+  using CF = HaloCfg<BN, B_RES>;
+  using NF = Num<HALF>;
+  constexpr int HS = CF::HS, BS = CF::BS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + HS * CF::HSTAGE;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + CF::B_BYTES);
+  uint64_t* hempty = hfull + HS;
+  uint64_t* bfull = hempty + HS;
+  uint64_t* bempty = bfull + BS;
+  uint64_t* tfull = bempty + BS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int taps = p.k * p.k;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < HS; ++s) {
+      tc::mbar_init(&hfull[s], 1);
+      tc::mbar_init(&hempty[s], 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      tc::mbar_init(&bfull[s], 1);
+      tc::mbar_init(&bempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 32 * NUM_EPI_WARPS);
+    }
+    tc::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
+  }
+  if (warp == 1) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t box_bytes = (uint32_t)(p.pw * p.ph * 16);
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
+    if constexpr (B_RES) {
+      if (lane == 0) {  // every weight block of this layer, once per CTA
+        const uint32_t bytes = (uint32_t)(p.wblocks * CF::BBLK);
+        tc::mbar_arrive_expect_tx(&bfull[0], bytes);
+        for (uint32_t off = 0; off < bytes; off += 32768) {
+          const uint32_t chunk = bytes - off < 32768 ? bytes - off : 32768;
+          tc::bulk_g2s(sB0 + off, reinterpret_cast<const uint8_t*>(p.w) + off, chunk, &bfull[0]);
+        }
+      }
+      __syncwarp();
+    }
+    int hs = 0, bs = 0;
+    uint32_t hph = 0, bph = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      const int n = t / p.tiles_per_img, r = t - n * p.tiles_per_img;
+      const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
+      const int y0 = ty * HTH - p.pad, x0 = tx * HTW - p.pad;
+      for (int cb = 0; cb < p.ncb; ++cb) {
+        const int g0 = cb * 8, ng = min(8, p.ngran - g0);
+        tc::mbar_wait(&hempty[hs], hph ^ 1);
+        if (lane == 0) tc::mbar_arrive_expect_tx(&hfull[hs], ng * box_bytes);
+        __syncwarp();
+        if (lane < ng)
+          tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * 8, x0, y0, n);
+        if (++hs == HS) {
+          hs = 0;
+          hph ^= 1;
+        }
+        if constexpr (!B_RES) {
+          const uint16_t* wb = p.w + (size_t)cb * taps * BN * BK;  // single n tile when streaming
+          for (int tap = 0; tap < taps; ++tap) {
+            tc::mbar_wait(&bempty[bs], bph ^ 1);
+            if (lane == 0) {
+              tc::mbar_arrive_expect_tx(&bfull[bs], CF::BBLK);
+              tc::bulk_g2s(sB0 + bs * CF::BBLK, wb + (size_t)tap * BN * BK, CF::BBLK, &bfull[bs]);
+            }
+            __syncwarp();
+            if (++bs == BS) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+    const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
+    const uint32_t sbo = (uint32_t)(p.pw * 16);
+    if constexpr (B_RES) {
+      tc::mbar_wait(&bfull[0], 0);
+      tc::tc_fence_after();
+    }
+    // One elected lane issues everything; the rest of the warp idles at the
+    // final __syncwarp.  Descriptors are linear in the start address (14-bit
+    // field, smem < 256 KB never carries), so each tap / K-step is a constant
+    // add to a per-patch base: no division or re-encoding in the issue loop,
+    // which otherwise costs more than the MMAs themselves (profiles/r01).
+    if (elect_one()) {
+      const uint64_t plane2 = (uint64_t)((2 * p.plane) >> 4);  // one K-step = two granule planes
+      uint64_t toff[9];
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) toff[tap] = (uint64_t)((tap / 3) * p.pw + tap % 3);
+      const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)p.plane, sbo);
+      const uint64_t b_desc0 = tc::sdesc_sw128(sB0);
+      constexpr uint64_t BBLK16 = CF::BBLK >> 4;
+      constexpr uint64_t HST16 = CF::HSTAGE >> 4;
+      int hs = 0, bs = 0;
+      uint32_t hph = 0, bph = 0, tl = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+        const uint32_t a = tl & 1, use = tl >> 1;
+        tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + a * BN;
+        for (int cb = 0; cb < p.ncb; ++cb) {
+          const int ksteps = min(8, p.ngran - cb * 8) >> 1;
+          tc::mbar_wait(&hfull[hs], hph);
+          tc::tc_fence_after();
+          const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            uint64_t db;
+            if constexpr (B_RES) {
+              db = b_desc0 + (uint64_t)(cb * 9 + tap) * BBLK16;
+            } else {
+              tc::mbar_wait(&bfull[bs], bph);
+              tc::tc_fence_after();
+              db = b_desc0 + (uint64_t)bs * BBLK16;
+            }
+            const uint64_t at = ah + toff[tap];
+            if (ksteps == 4) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                tc::mma_f16(d, at + ks * plane2, db + 2 * ks, idesc, (cb | tap | ks) != 0);
+            } else {
+              for (int ks = 0; ks < ksteps; ++ks)
+                tc::mma_f16(d, at + ks * plane2, db + 2 * ks, idesc, (cb | tap | ks) != 0);
+            }
+            if constexpr (!B_RES) {
+              tc::mma_commit(&bempty[bs]);
+              if (++bs == BS) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+          }
+          tc::mma_commit(&hempty[hs]);
+          if (++hs == HS) {
+            hs = 0;
+            hph ^= 1;
+          }
+        }
+        tc::mma_commit(&tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ epilogue (warps 2-9)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr bool SPLIT = !FUSED_OUT && BN >= 32;
+    constexpr int HC = SPLIT ? BN / 2 : BN;
+    const int cbeg = SPLIT ? half * HC : 0;
+    const bool active = SPLIT || half == 0;
+    const int r = q * 32 + lane;  // tile pixel: row r / 8, column r % 8
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+      const uint32_t a = tl & 1, use = tl >> 1;
+      const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
+      const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
+      const int y = ty * HTH + (r >> 3), x = tx * HTW + (r & 7);
+      const bool valid = y < p.H && x < p.W;
+      const size_t pix = ((size_t)n * p.H + y) * p.W + x;
+      if constexpr (!FUSED_OUT) {
+        uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + cbeg;
+        const uint16_t* rrow = (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + cbeg : nullptr;
+        if (!active) {
+          tc::mbar_wait(&tfull[a], use & 1);
+          tc::tc_fence_after();
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[a]);
+          continue;
+        }
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
+        epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
+      } else {
+        tc::mbar_wait(&tfull[a], use & 1);
+        tc::tc_fence_after();
+        if (half == 0) {
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+          float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
+#pragma unroll
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tbase + c0, v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float xx = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
+            }
+          }
+          if (valid) {
+            const int HWo = p.H * p.W;
+            const size_t pp = (size_t)y * p.W + x;
+            if (p.out_mode == OUT_F32_LOGITS) {
+              float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
+            } else if (p.out_mode == OUT_F32_NCHW) {
+              float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
+            } else {
+              uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) {
+                const float s = 1.f / (1.f + __expf(-o[o3]));
+                out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
+              }
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
+  }
+}
+
+}  // namespace gen
+}  // namespace lsg

@@ -147,6 +147,76 @@ __device__ __forceinline__ constexpr uint32_t a_koff(int k) {
   return CC == 64 ? k * 2 : (CC == 32 ? (k >> 1) * 512 + (k & 1) * 2 : k * 256);
 }
 
+// One epilogue thread's share of an output row: HC accumulator columns ->
+// + bias (+ residual) (ReLU) -> 16-bit store.  The whole residual slice is
+// requested before the accumulator wait (HC <= 64: 32 registers), so its
+// latency hides under the mainloop instead of once per 16-column chunk.
+template <int HC, bool HALF>
+__device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, const uint16_t* rrow, const float* bias,
+                                             bool relu, bool valid, uint64_t* tfull_bar, uint32_t parity) {
+  using NF = Num<HALF>;
+  constexpr int NR = HC <= 64 ? HC / 8 : 2;
+  uint4 rv[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) rv[i] = rrow ? __ldg(reinterpret_cast<const uint4*>(rrow) + i) : make_uint4(0, 0, 0, 0);
+  tc::mbar_wait(tfull_bar, parity);
+  tc::tc_fence_after();
+#pragma unroll
+  for (int c0 = 0; c0 < HC; c0 += 16) {
+    uint32_t v[16];
+    tc::tmem_ld16(tbase + c0, v);
+    uint4 ra, rb;
+    if constexpr (HC <= 64) {
+      ra = rv[c0 / 8];
+      rb = rv[c0 / 8 + 1];
+    } else {
+      ra = rv[0];
+      rb = rv[1];
+      if (rrow && c0 + 16 < HC) {
+        rv[0] = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16));
+        rv[1] = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16) + 1);
+      }
+    }
+    tc::tmem_ld_wait();
+    if (valid) {
+      float f[16];
+      const float4* bp = reinterpret_cast<const float4*>(bias + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 b4 = __ldg(bp + j);
+        f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + b4.x;
+        f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
+        f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
+        f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
+      }
+      if (rrow) {
+        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 x = NF::unpack(rr[j]);
+          f[2 * j] += x.x;
+          f[2 * j + 1] += x.y;
+        }
+      }
+      if (relu) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
+      }
+      uint4 o0, o1;
+      o0.x = NF::pack(f[0], f[1]);
+      o0.y = NF::pack(f[2], f[3]);
+      o0.z = NF::pack(f[4], f[5]);
+      o0.w = NF::pack(f[6], f[7]);
+      o1.x = NF::pack(f[8], f[9]);
+      o1.y = NF::pack(f[10], f[11]);
+      o1.z = NF::pack(f[12], f[13]);
+      o1.w = NF::pack(f[14], f[15]);
+      *reinterpret_cast<uint4*>(orow + c0) = o0;
+      *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
+    }
+  }
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -301,67 +371,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
         uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + n0 + cbeg;
         const uint16_t* rrow =
             (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + n0 + cbeg : nullptr;
-        // prefetch the first residual chunk while the mainloop runs
-        uint4 rn0 = make_uint4(0, 0, 0, 0), rn1 = rn0;
-        if (rrow) {
-          rn0 = __ldg(reinterpret_cast<const uint4*>(rrow));
-          rn1 = __ldg(reinterpret_cast<const uint4*>(rrow) + 1);
-        }
-        tc::mbar_wait(&tfull[a], use & 1);
-        tc::tc_fence_after();
         if (!active) {
+          tc::mbar_wait(&tfull[a], use & 1);
+          tc::tc_fence_after();
           tc::tc_fence_before();
           tc::mbar_arrive(&tempty[a]);
           continue;
         }
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
-#pragma unroll 1
-        for (int c0 = 0; c0 < HC; c0 += 16) {
-          uint32_t v[16];
-          tc::tmem_ld16(tbase + c0, v);
-          const uint4 ra = rn0, rb = rn1;
-          if (rrow && c0 + 16 < HC) {  // next chunk's residual in flight during this one
-            rn0 = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16));
-            rn1 = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16) + 1);
-          }
-          tc::tmem_ld_wait();
-          if (valid) {
-            float f[16];
-            const float4* bp = reinterpret_cast<const float4*>(p.bias + n0 + cbeg + c0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 b4 = __ldg(bp + j);
-              f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + b4.x;
-              f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
-              f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
-              f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
-            }
-            if (rrow) {
-              const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float2 x = NF::unpack(rr[j]);
-                f[2 * j] += x.x;
-                f[2 * j + 1] += x.y;
-              }
-            }
-            if (p.relu) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
-            }
-            uint4 o0, o1;
-            o0.x = NF::pack(f[0], f[1]);
-            o0.y = NF::pack(f[2], f[3]);
-            o0.z = NF::pack(f[4], f[5]);
-            o0.w = NF::pack(f[6], f[7]);
-            o1.x = NF::pack(f[8], f[9]);
-            o1.y = NF::pack(f[10], f[11]);
-            o1.z = NF::pack(f[12], f[13]);
-            o1.w = NF::pack(f[14], f[15]);
-            *reinterpret_cast<uint4*>(orow + c0) = o0;
-            *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
-          }
-        }
+        epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + n0 + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
       } else {
         // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid;
         // the second warp of each quadrant only keeps the barrier count

@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include "conv_halo.cuh"
 #include "conv_kernel.cuh"
 #include "gen_internal.h"
 #include "lsg_common.cuh"
@@ -182,7 +183,46 @@ struct LayerRun {
   ConvParams p;
   View in_view;
   int GH[MAX_PHASES], GW[MAX_PHASES];  // per phase, per image
+  bool halo = false;                   // routed to conv_halo
+  bool halo_bres = false;              // weights resident in shared memory
+  HaloParams hp;
 };
+
+// Stride-1 3x3 "same" convs on maps at least 16 wide with Cout <= 128 go to
+// the halo kernel (conv_halo.cuh); everything else to the im2col kernel.
+bool halo_eligible(const LayerSpec& L, const View& in) {
+  return L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 &&
+         L.cout <= 128 && in.W >= 16 && L.cin % 16 == 0;
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled tiled_fn() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    LSG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) fail(LSG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiled>(f);
+  }
+  return fn;
+}
+
+// tiled map of an NHWC channel-slice view, box = 8 channels x pw x ph x 1 image
+void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph) {
+  const cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)v.pitch * 2, (cuuint64_t)v.W * v.pitch * 2,
+                                 (cuuint64_t)v.H * v.W * v.pitch * 2};
+  const cuuint32_t box[4] = {8, (cuuint32_t)pw, (cuuint32_t)ph, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+}
 
 // cuTensorMapEncodeIm2col through the runtime's driver entry point (no
 // link-time dependency on libcuda).
@@ -292,6 +332,13 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(256, 64, false)          \
   X(32, 16, true)
 
+// halo kernel variants: (tile width, fused output, weights resident)
+#define LSG_HALO_VARIANTS(X) \
+  X(32, false, true)         \
+  X(64, false, true)         \
+  X(128, false, false)       \
+  X(32, true, true)
+
 static void set_smem_attrs() {
 #define LSG_SET_ATTR(BN, CC, F)                                                                                   \
   LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
@@ -300,10 +347,33 @@ static void set_smem_attrs() {
                                 Cfg<BN>::SMEM));
   LSG_CONV_VARIANTS(LSG_SET_ATTR)
 #undef LSG_SET_ATTR
+#define LSG_SET_HALO_ATTR(BN, F, R)                                                                               \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                HaloCfg<BN, R>::SMEM));                                                           \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                HaloCfg<BN, R>::SMEM));
+  LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
+#undef LSG_SET_HALO_ATTR
+}
+
+template <int BN, bool F, bool H, bool R>
+static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
+  HaloParams hp = r.hp;
+  hp.B = B;
+  hp.total_tiles = B * hp.tiles_per_img;
+  const int grid = std::min(hp.total_tiles, sms);
+  conv_halo<BN, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, R>::SMEM, st>>>(hp);
 }
 
 template <bool H>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
+  if (r.halo) {
+#define LSG_HALO_DISPATCH(BN, F, R) \
+  if (r.bn == BN && r.fused == F && r.halo_bres == R) return launch_halo<BN, F, H, R>(r, B, sms, st);
+    LSG_HALO_VARIANTS(LSG_HALO_DISPATCH)
+#undef LSG_HALO_DISPATCH
+    fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn));
+  }
 #define LSG_DISPATCH(BN, CC, F) \
   if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, H>(r, B, sms, st);
   LSG_CONV_VARIANTS(LSG_DISPATCH)
@@ -390,6 +460,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       std::vector<float> w1b1(3 * 32 + 3);
       std::vector<int64_t> pack_off(kNumLayers * MAX_PHASES, 0);
       std::vector<int64_t> bias_off(kNumLayers, 0);
+      std::vector<int64_t> halo_off(kNumLayers, -1);  // (channel block, tap) packing for conv_halo
       struct PhaseGeo { int ntaps; signed char dy[MAX_TAPS], dx[MAX_TAPS]; int ky[MAX_TAPS], kx[MAX_TAPS]; int oy, ox; };
       std::vector<std::vector<PhaseGeo>> geo(kNumLayers);
       const float* wp = weights;
@@ -456,6 +527,25 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
               pg.oy = a;
               pg.ox = bb;
               G.push_back(pg);
+            }
+        }
+        if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 &&
+            L.cout <= 128 && L.cin % 16 == 0) {
+          // [cb][tap][cout][64]: K block = 64 channels of one tap, 128 B swizzled rows
+          const int ncb = (L.cin + 63) / 64, bnh = L.cout;
+          halo_off[li] = (int64_t)pack.size();
+          pack.resize(pack.size() + (size_t)ncb * 9 * bnh * BK, 0);
+          uint16_t* dst = pack.data() + halo_off[li];
+          for (int cb = 0; cb < ncb; ++cb)
+            for (int tap = 0; tap < 9; ++tap) {
+              uint16_t* blk = dst + ((size_t)cb * 9 + tap) * bnh * BK;
+              const int ky = tap / 3, kx = tap % 3;
+              for (int r = 0; r < bnh; ++r)
+                for (int j = 0; j < BK; ++j) {
+                  const int c = cb * 64 + j;
+                  const float v = c < L.cin ? w[(((int64_t)r * L.cin + c) * 3 + ky) * 3 + kx] : 0.f;
+                  blk[r * BK + (((j >> 3) ^ (r & 7)) << 3) + (j & 7)] = h->half ? f2h(v) : f2bf(v);
+                }
             }
         }
         const int cin_pad = (L.cin + 7) / 8 * 8;
@@ -675,6 +765,40 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           const int gw = (in.W + upper_w - lower_w - 1) / p.sx + 1, gh = (in.H + upper_h - lower_h - 1) / p.sy + 1;
           if (gw != P.GW || gh != P.GH) fail(LSG_ERUNTIME, std::string("generator: im2col grid mismatch at ") + L.name);
         }
+        if (halo_off[l] >= 0 && halo_eligible(L, in)) {
+          HaloParams& hp = r.hp;
+          r.halo = true;
+          hp.H = in.H;
+          hp.W = in.W;
+          hp.C = p.C;
+          hp.k = 3;
+          hp.pad = 1;
+          hp.pw = HTW + 2;
+          hp.ph = HTH + 2;
+          hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
+          hp.ngran = p.C / 8;
+          hp.ncb = (hp.ngran + 7) / 8;
+          hp.tiles_x = (int)ceil_div(in.W, HTW);
+          hp.tiles_y = (int)ceil_div(in.H, HTH);
+          hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
+          hp.w = h->wpack.p + halo_off[l];
+          hp.wblocks = hp.ncb * 9;
+          hp.ntiles_n = 1;
+          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, true>::B_RES_BYTES;
+          if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
+          hp.out = p.out;
+          hp.out_pitch = p.out_pitch;
+          hp.out_coff = p.out_coff;
+          hp.res = p.res;
+          hp.res_pitch = p.res_pitch;
+          hp.res_coff = p.res_coff;
+          hp.bias = p.bias;
+          hp.relu = p.relu;
+          hp.out_mode = p.out_mode;
+          hp.w1 = p.w1;
+          hp.b1 = p.b1;
+          encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph);
+        }
         h->plan.push_back(r);
       }
       set_smem_attrs();
@@ -778,8 +902,8 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
                                                   : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
   for (auto& r : h->plan) {
     if (r.fused) {
-      r.p.out_mode = mode;
-      r.p.final_out = out;
+      r.p.out_mode = r.hp.out_mode = mode;
+      r.p.final_out = r.hp.final_out = out;
     }
     dispatch(h, r, B, st);
     LSG_LAUNCHED(ctx);

@@ -43,7 +43,10 @@ def main(path, B=512):
         tot += t
         dram = (m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)) / 1e6
         lname, tf, frac = "", 0.0, 0.0
-        if Ls and "conv_tc" in name:
+        if Ls and ("conv_tc" in name or "conv_halo" in name):
+            if li == len(names):  # next forward of a multi-rep capture
+                print(f"subtotal {tot - t:.1f} us")
+                li = 0
             L = Ls[li]
             hi, wi, ho, wo = shapes[li]
             pix = ho * wo if L.kind == 0 else hi * wi
