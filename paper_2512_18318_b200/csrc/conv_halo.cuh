@@ -1,21 +1,28 @@
-// conv_halo.cuh -- stride-1 3x3 convolution with shared-memory halo reuse.
+// conv_halo.cuh -- patch-reuse convolution: one input patch in shared memory
+// feeds every filter tap of a 128-position output tile.
 //
-// For the narrow, high-resolution layers (96x96x64, 48x48x128, the 80->32
-// output conv, ...) the im2col kernel re-reads every input pixel once per
-// filter tap (9x) and the weights once per 128-pixel tile, so it is bound by
-// operand traffic, not the tensor pipe.  Here an output tile is a 16-row x
-// 8-column pixel block of one image; per 64-channel block the TMA (tile mode,
-// zero fill outside the image) loads the (16+2) x (8+2) input patch ONCE, as
-// eight 8-channel "granule planes" of [18][10][8] elements.  Every filter tap
-// is then a UMMA operand view into that patch: a no-swizzle K-major
-// descriptor whose start address is shifted by (ky*10 + kx)*16 bytes, core
-// matrices = 8 consecutive patch pixels x 16 B, SBO = one patch row (160 B),
-// LBO = one granule plane.  So a patch buffer feeds 9 taps x 4 K-steps = 36
-// tcgen05.mma; the weights stay resident in shared memory for the whole
-// persistent CTA when they fit (all Wav2Lip layers routed here but fd5.x),
-// otherwise they stream per (channel block, tap) through their own ring.
-// Epilogue identical to conv_tc (bias, residual, ReLU, channel-slice store,
-// fused 1x1+sigmoid output).
+// The im2col kernel (conv_kernel.cuh) re-reads each input pixel once per
+// filter tap and is bound by L2->SM operand traffic on the narrow (N <= 64),
+// high-resolution layers.  Here a tile is a 16-row x 8-column block of grid
+// positions of one image.  Per channel block the TMA (tile mode, zero fill
+// outside the image) loads the input patch around it ONCE as up to eight
+// "planes" of [ph][pw][8] elements (16 B per pixel); every tap is then a
+// UMMA operand view into the patch: a no-swizzle K-major descriptor whose
+// start address is shifted by the tap's patch offset, core matrices = 8
+// consecutive patch pixels x 16 B, SBO = one patch row, LBO = one plane, two
+// planes per K=16 step.  The layer supplies a tap list (patch offset, output
+// phase, first-tap-of-phase), which covers
+//   * 3x3 stride-1 convs: 1 phase, 9 taps, planes = 8-channel granules;
+//   * stride-2 3x3 ConvTranspose (fd5.0/fd6.0 shapes): the grid is the INPUT
+//     grid, 4 output phases (oy, ox) with 1/2/2/4 taps, each phase its own
+//     TMEM accumulator, all fed by the same patch;
+//   * the 7x7 stem on 8-channel faces (fe0): planes are the patch shifted by
+//     kx = 0..7 columns, so one K block = 8 horizontal taps x 8 channels and
+//     the tap list is the 7 rows.
+// Weights are resident in shared memory for the whole persistent CTA when
+// they fit, otherwise they stream per (channel block, tap) through a ring.
+// Epilogue as conv_tc (bias, residual, ReLU, channel-slice store, fused
+// 1x1 + sigmoid output), per phase.
 #pragma once
 
 #include "conv_kernel.cuh"
@@ -23,21 +30,31 @@
 namespace lsg {
 namespace gen {
 
-constexpr int HTH = 16, HTW = 8;  // output tile: 16 rows x 8 columns = 128 pixels
+constexpr int HTH = 16, HTW = 8;  // tile: 16 rows x 8 columns = 128 grid positions
+constexpr int MAX_HTAPS = 9;
 
 struct alignas(64) HaloParams {
-  CUtensorMap tmap;  // tiled map of the input view (C, W, H, N), box (8, HTW+k-1, HTH+k-1, 1)
-  int H, W, C, B;
-  int k, pad;
-  int pw, ph;        // patch width / height (HTW + k - 1, HTH + k - 1)
-  int plane;         // bytes per granule plane in smem (pw*ph*16, 128-aligned)
-  int ngran;         // C / 8
-  int ncb;           // channel blocks of <= 8 granules
+  CUtensorMap tmap;  // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
+  int H, W, C, B;    // input view
+  int GH, GW;        // grid (output positions for convs, input positions for ConvT)
+  int oy0, ox0;      // patch origin relative to the tile origin (-pad for convs)
+  int pw, ph;        // patch width / height in pixels
+  int plane;         // bytes per plane in smem (pw*ph*16, 128-aligned)
+  int ngran;         // planes per tile over all channel blocks (C/8, or 8 shifted copies)
+  int ncb;           // channel blocks of <= 8 planes
+  int shift_planes;  // planes are x-shifted copies of channels 0..7 (fe0)
+  int ntaps;
+  int aoff[MAX_HTAPS];   // tap start offset in the patch, 16-byte units (= pixels)
+  int tphase[MAX_HTAPS]; // output phase the tap accumulates into
+  int tfirst;            // bit t: tap t is the first tap of its phase
+  int osy, osx;          // output stride of the grid (2 for ConvT phases)
+  int poy[4], pox[4];    // per-phase output offset
   int tiles_x, tiles_y, tiles_per_img, total_tiles;
-  const uint16_t* w; // packed [ntile][cb][tap][BN][64] (128 B swizzled rows)
-  int wblocks;       // cb * taps blocks per n tile
+  const uint16_t* w;  // packed [cb][tap][BN][64] (128 B swizzled rows)
+  int wblocks;        // ncb * ntaps
   // epilogue (as ConvParams)
   uint16_t* out;
+  int OH, OW;
   int out_pitch, out_coff;
   const uint16_t* res;
   int res_pitch, res_coff;
@@ -46,12 +63,11 @@ struct alignas(64) HaloParams {
   const float* w1;
   const float* b1;
   void* final_out;
-  int ntiles_n;
 };
 
-template <int BN, bool B_RES>
+template <int BN, int NPH, bool B_RES>
 struct HaloCfg {
-  static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B, rounded to 128
+  static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
   static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
   static constexpr int B_RES_BYTES = 96 * 1024;
@@ -59,7 +75,14 @@ struct HaloCfg {
   static constexpr int BS = B_RES ? 1 : ((200 * 1024 - HS * HSTAGE) / BBLK > 8 ? 8 : (200 * 1024 - HS * HSTAGE) / BBLK);
   static constexpr int B_BYTES = B_RES ? B_RES_BYTES : BS * BBLK;
   static constexpr int SMEM = 1024 + HS * HSTAGE + B_BYTES + 512;
-  static constexpr int TMEM_COLS = Cfg<BN>::TMEM_COLS;
+  static constexpr int ACC_COLS = NPH * BN;                // one accumulator: every phase
+  static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;  // double-buffered when TMEM allows
+  static constexpr int TMEM_COLS = NACC * ACC_COLS <= 32    ? 32
+                                   : NACC * ACC_COLS <= 64  ? 64
+                                   : NACC * ACC_COLS <= 128 ? 128
+                                   : NACC * ACC_COLS <= 256 ? 256
+                                                            : 512;
+  static_assert(NACC * ACC_COLS <= 512, "accumulators exceed TMEM");
 };
 
 __device__ __forceinline__ void tma_tile_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int x, int y,
@@ -76,11 +99,12 @@ __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
 }
 
-template <int BN, bool FUSED_OUT, bool HALF, bool B_RES>
+template <int BN, int NPH, bool FUSED_OUT, bool HALF, bool B_RES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
-  using CF = HaloCfg<BN, B_RES>;
+  using CF = HaloCfg<BN, NPH, B_RES>;
   using NF = Num<HALF>;
-  constexpr int HS = CF::HS, BS = CF::BS;
+  constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
+  static_assert(!FUSED_OUT || NPH == 1, "fused output conv has one phase");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = tc::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -94,7 +118,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int taps = p.k * p.k;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < HS; ++s) {
@@ -133,26 +156,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       }
       __syncwarp();
     }
+    // plane g of channel block cb: channels (cb*8 + g)*8 at x0, or channels 0..7 at x0 + g
+    const int cstep = p.shift_planes ? 0 : 8, xstep = p.shift_planes ? 1 : 0;
     int hs = 0, bs = 0;
     uint32_t hph = 0, bph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       const int n = t / p.tiles_per_img, r = t - n * p.tiles_per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-      const int y0 = ty * HTH - p.pad, x0 = tx * HTW - p.pad;
+      const int y0 = ty * HTH + p.oy0, x0 = tx * HTW + p.ox0;
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
         tc::mbar_wait(&hempty[hs], hph ^ 1);
         if (lane == 0) tc::mbar_arrive_expect_tx(&hfull[hs], ng * box_bytes);
         __syncwarp();
         if (lane < ng)
-          tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * 8, x0, y0, n);
+          tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * cstep,
+                      x0 + lane * xstep, y0, n);
         if (++hs == HS) {
           hs = 0;
           hph ^= 1;
         }
         if constexpr (!B_RES) {
-          const uint16_t* wb = p.w + (size_t)cb * taps * BN * BK;  // single n tile when streaming
-          for (int tap = 0; tap < taps; ++tap) {
+          const uint16_t* wb = p.w + (size_t)cb * p.ntaps * BN * BK;
+          for (int tap = 0; tap < p.ntaps; ++tap) {
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             if (lane == 0) {
               tc::mbar_arrive_expect_tx(&bfull[bs], CF::BBLK);
@@ -169,63 +195,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // One elected lane issues everything.  Descriptors are linear in the
+    // start address (14-bit field; smem < 256 KB never carries), so every
+    // tap / K step is a constant add to a per-patch base: no division or
+    // re-encoding in the issue loop, which otherwise costs more than the
+    // MMAs themselves (profiles/r01).
     constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
-    const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
-    const uint32_t sbo = (uint32_t)(p.pw * 16);
-    if constexpr (B_RES) {
-      tc::mbar_wait(&bfull[0], 0);
-      tc::tc_fence_after();
-    }
-    // One elected lane issues everything; the rest of the warp idles at the
-    // final __syncwarp.  Descriptors are linear in the start address (14-bit
-    // field, smem < 256 KB never carries), so each tap / K-step is a constant
-    // add to a per-patch base: no division or re-encoding in the issue loop,
-    // which otherwise costs more than the MMAs themselves (profiles/r01).
     if (elect_one()) {
-      const uint64_t plane2 = (uint64_t)((2 * p.plane) >> 4);  // one K-step = two granule planes
-      uint64_t toff[9];
+      const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
+      if constexpr (B_RES) {
+        tc::mbar_wait(&bfull[0], 0);
+        tc::tc_fence_after();
+      }
+      const uint64_t plane2 = (uint64_t)((2 * p.plane) >> 4);  // one K step = two planes
+      uint64_t toff[MAX_HTAPS];
+      uint32_t tcol[MAX_HTAPS];
 #pragma unroll
-      for (int tap = 0; tap < 9; ++tap) toff[tap] = (uint64_t)((tap / 3) * p.pw + tap % 3);
-      const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)p.plane, sbo);
+      for (int tap = 0; tap < MAX_HTAPS; ++tap) {
+        toff[tap] = (uint64_t)p.aoff[tap];
+        tcol[tap] = (uint32_t)(p.tphase[tap] * BN);
+      }
+      const int ntaps = p.ntaps, tfirst = p.tfirst;
+      const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)p.plane, (uint32_t)(p.pw * 16));
       const uint64_t b_desc0 = tc::sdesc_sw128(sB0);
       constexpr uint64_t BBLK16 = CF::BBLK >> 4;
       constexpr uint64_t HST16 = CF::HSTAGE >> 4;
       int hs = 0, bs = 0;
       uint32_t hph = 0, bph = 0, tl = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
-        const uint32_t a = tl & 1, use = tl >> 1;
+        const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
         tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
         tc::tc_fence_after();
-        const uint32_t d = tmem + a * BN;
+        const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < p.ncb; ++cb) {
           const int ksteps = min(8, p.ngran - cb * 8) >> 1;
           tc::mbar_wait(&hfull[hs], hph);
           tc::tc_fence_after();
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
-            uint64_t db;
-            if constexpr (B_RES) {
-              db = b_desc0 + (uint64_t)(cb * 9 + tap) * BBLK16;
-            } else {
-              tc::mbar_wait(&bfull[bs], bph);
-              tc::tc_fence_after();
-              db = b_desc0 + (uint64_t)bs * BBLK16;
-            }
-            const uint64_t at = ah + toff[tap];
-            if (ksteps == 4) {
+          for (int tap = 0; tap < MAX_HTAPS; ++tap) {
+            if (tap < ntaps) {
+              uint64_t db;
+              if constexpr (B_RES) {
+                db = b_desc0 + (uint64_t)(cb * ntaps + tap) * BBLK16;
+              } else {
+                tc::mbar_wait(&bfull[bs], bph);
+                tc::tc_fence_after();
+                db = b_desc0 + (uint64_t)bs * BBLK16;
+              }
+              const uint64_t at = ah + toff[tap];
+              const uint32_t dd = d + tcol[tap];
+              const uint32_t acc0 = (cb == 0 && ((tfirst >> tap) & 1)) ? 0u : 1u;
+              if (ksteps == 4) {
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks)
-                tc::mma_f16(d, at + ks * plane2, db + 2 * ks, idesc, (cb | tap | ks) != 0);
-            } else {
-              for (int ks = 0; ks < ksteps; ++ks)
-                tc::mma_f16(d, at + ks * plane2, db + 2 * ks, idesc, (cb | tap | ks) != 0);
-            }
-            if constexpr (!B_RES) {
-              tc::mma_commit(&bempty[bs]);
-              if (++bs == BS) {
-                bs = 0;
-                bph ^= 1;
+                for (int ks = 0; ks < 4; ++ks) tc::mma_f16(dd, at + ks * plane2, db + 2 * ks, idesc, ks ? 1u : acc0);
+              } else {
+                for (int ks = 0; ks < ksteps; ++ks)
+                  tc::mma_f16(dd, at + ks * plane2, db + 2 * ks, idesc, ks ? 1u : acc0);
+              }
+              if constexpr (!B_RES) {
+                tc::mma_commit(&bempty[bs]);
+                if (++bs == BS) {
+                  bs = 0;
+                  bph ^= 1;
+                }
               }
             }
           }
@@ -247,32 +280,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     constexpr int HC = SPLIT ? BN / 2 : BN;
     const int cbeg = SPLIT ? half * HC : 0;
     const bool active = SPLIT || half == 0;
-    const int r = q * 32 + lane;  // tile pixel: row r / 8, column r % 8
+    const int r = q * 32 + lane;  // tile position: row r / 8, column r % 8
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
-      const uint32_t a = tl & 1, use = tl >> 1;
+      const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
       const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
       const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
-      const int y = ty * HTH + (r >> 3), x = tx * HTW + (r & 7);
-      const bool valid = y < p.H && x < p.W;
-      const size_t pix = ((size_t)n * p.H + y) * p.W + x;
+      const int gy = ty * HTH + (r >> 3), gx = tx * HTW + (r & 7);
+      const bool gvalid = gy < p.GH && gx < p.GW;
       if constexpr (!FUSED_OUT) {
-        uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + cbeg;
-        const uint16_t* rrow = (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + cbeg : nullptr;
         if (!active) {
           tc::mbar_wait(&tfull[a], use & 1);
           tc::tc_fence_after();
-          tc::tc_fence_before();
-          tc::mbar_arrive(&tempty[a]);
-          continue;
+        } else {
+#pragma unroll
+          for (int z = 0; z < NPH; ++z) {
+            const int y = gy * p.osy + p.poy[z], x = gx * p.osx + p.pox[z];
+            const bool valid = gvalid && y < p.OH && x < p.OW;
+            const size_t pix = ((size_t)n * p.OH + y) * p.OW + x;
+            uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + cbeg;
+            const uint16_t* rrow = (p.res && valid) ? p.res + pix * p.res_pitch + p.res_coff + cbeg : nullptr;
+            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS + z * BN + cbeg;
+            epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
+          }
         }
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
-        epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
       } else {
         tc::mbar_wait(&tfull[a], use & 1);
         tc::tc_fence_after();
         if (half == 0) {
-          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS;
           float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
 #pragma unroll
           for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -286,9 +322,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
               for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
             }
           }
-          if (valid) {
-            const int HWo = p.H * p.W;
-            const size_t pp = (size_t)y * p.W + x;
+          if (gvalid) {
+            const int HWo = p.OH * p.OW;
+            const size_t pp = (size_t)gy * p.OW + gx;
             if (p.out_mode == OUT_F32_LOGITS) {
               float* out = reinterpret_cast<float*>(p.final_out);
 #pragma unroll

@@ -73,6 +73,7 @@ struct alignas(64) ConvParams {
   const float* b1;  // [3]
   void* final_out;
   int nphases, ntiles_n, total_tiles;
+  int interleave;  // all phases have equal mtiles: t = (mt * nphases + z) * ntiles_n + nt
   Phase ph[MAX_PHASES];
 };
 
@@ -115,12 +116,26 @@ struct TileId {
 };
 
 __device__ __forceinline__ TileId decode_tile(const ConvParams& p, int t) {
+  // Tiles that read the same input rows are adjacent in t, so the ~148 CTAs
+  // in flight share them through L2: n tiles of one m tile, and (when the
+  // phases are congruent, i.e. a stride-2 ConvT) the 4 output phases of one
+  // input region.  Otherwise phase-major, n tile fastest within a phase.
+  if (p.interleave) {
+    // the phase rotates with the m tile: a grid stride that is a multiple of
+    // nphases (148 = 37 x 4) would otherwise pin each CTA to one phase, and
+    // ConvT phases carry 1/2/2/4 taps
+    const int q = t / p.ntiles_n, nt = t - q * p.ntiles_n;
+    const int mt = q / p.nphases;
+    int z = q - mt * p.nphases + mt;
+    z -= (z / p.nphases) * p.nphases;
+    return {z, nt, mt};
+  }
   int z = 0;
 #pragma unroll 1
   while (z + 1 < p.nphases && t >= p.ph[z + 1].tile0) ++z;
   const int r = t - p.ph[z].tile0;
-  const int nt = r / p.ph[z].mtiles;
-  return {z, nt, r - nt * p.ph[z].mtiles};
+  const int mt = r / p.ntiles_n;
+  return {z, r - mt * p.ntiles_n, mt};
 }
 
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int w,

@@ -185,15 +185,35 @@ struct LayerRun {
   int GH[MAX_PHASES], GW[MAX_PHASES];  // per phase, per image
   bool halo = false;                   // routed to conv_halo
   bool halo_bres = false;              // weights resident in shared memory
+  int halo_nph = 1;                    // output phases (4 for a stride-2 ConvT)
   HaloParams hp;
 };
 
-// Stride-1 3x3 "same" convs on maps at least 16 wide with Cout <= 128 go to
-// the halo kernel (conv_halo.cuh); everything else to the im2col kernel.
-bool halo_eligible(const LayerSpec& L, const View& in) {
-  return L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 &&
-         L.cout <= 128 && in.W >= 16 && L.cin % 16 == 0;
+// Layers routed to the patch-reuse kernel (conv_halo.cuh); everything else
+// goes to the im2col kernel.
+enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3 };
+
+HaloMode halo_mode(const LayerSpec& L) {
+  if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 && L.cout <= 128 &&
+      L.cin % 16 == 0)
+    return HALO_CONV3;  // 3x3 "same": fe1.x, fe2.x, ae1-5, fd5.x, fd6.x, out0
+  if (L.kind != CONV && L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2 && L.ph == 1 && L.pw == 1 && L.oph == 1 &&
+      L.opw == 1 && L.cout <= 64 && L.cin % 16 == 0)
+    return HALO_CONVT2;  // fd6.0: 4 output phases share one accumulator set
+  if (L.kind == CONV && L.kh == 7 && L.kw == 7 && L.sh == 1 && L.sw == 1 && L.ph == 3 && L.pw == 3 && L.cin <= 8 &&
+      L.cout <= 16)
+    return HALO_STEM7;  // fe0 on the 8-channel face tensor
+  return HALO_NONE;
 }
+
+// Geometry + tap list of a halo-routed layer (see HaloParams).
+struct HaloGeo {
+  HaloMode mode = HALO_NONE;
+  int oy0 = 0, ox0 = 0, pw = 0, ph = 0, nph = 1, ntaps = 0, tfirst = 0;
+  int aoff[MAX_HTAPS] = {}, tphase[MAX_HTAPS] = {}, ky[MAX_HTAPS] = {}, kx[MAX_HTAPS] = {};
+  int poy[4] = {}, pox[4] = {};
+  int64_t off = -1;  // packed weights
+};
 
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -298,8 +318,8 @@ struct lsg_gen_s {
 
 static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
 
-// Persistent launch: tiles enumerate (phase, n tile, m tile) with m fastest,
-// one CTA per SM walks them round-robin.
+// Persistent launch: one CTA per SM walks the tiles round-robin in the
+// L2-friendly order of decode_tile().
 template <int BN, int CC, bool F, bool H>
 static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   ConvParams p = r.p;
@@ -314,6 +334,8 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   p.nphases = r.nphases;
   p.ntiles_n = r.ntiles;
   p.total_tiles = tiles;
+  p.interleave = 1;
+  for (int z = 1; z < r.nphases; ++z) p.interleave &= p.ph[z].mtiles == p.ph[0].mtiles;
   const int grid = std::min(tiles, sms);
   conv_tc<BN, CC, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
 }
@@ -332,12 +354,14 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(256, 64, false)          \
   X(32, 16, true)
 
-// halo kernel variants: (tile width, fused output, weights resident)
+// halo kernel variants: (tile width, output phases, fused output, weights resident)
 #define LSG_HALO_VARIANTS(X) \
-  X(32, false, true)         \
-  X(64, false, true)         \
-  X(128, false, false)       \
-  X(32, true, true)
+  X(16, 1, false, true)      \
+  X(32, 1, false, true)      \
+  X(64, 1, false, true)      \
+  X(128, 1, false, false)    \
+  X(64, 4, false, false)     \
+  X(32, 1, true, true)
 
 static void set_smem_attrs() {
 #define LSG_SET_ATTR(BN, CC, F)                                                                                   \
@@ -347,32 +371,34 @@ static void set_smem_attrs() {
                                 Cfg<BN>::SMEM));
   LSG_CONV_VARIANTS(LSG_SET_ATTR)
 #undef LSG_SET_ATTR
-#define LSG_SET_HALO_ATTR(BN, F, R)                                                                               \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                                HaloCfg<BN, R>::SMEM));                                                           \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                                HaloCfg<BN, R>::SMEM));
+#define LSG_SET_HALO_ATTR(BN, NP, F, R)                                                                           \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, NP, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                HaloCfg<BN, NP, R>::SMEM));                                                       \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, NP, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                HaloCfg<BN, NP, R>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
 }
 
-template <int BN, bool F, bool H, bool R>
+template <int BN, int NP, bool F, bool H, bool R>
 static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   HaloParams hp = r.hp;
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img;
   const int grid = std::min(hp.total_tiles, sms);
-  conv_halo<BN, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, R>::SMEM, st>>>(hp);
+  conv_halo<BN, NP, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, NP, R>::SMEM, st>>>(hp);
 }
 
 template <bool H>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
   if (r.halo) {
-#define LSG_HALO_DISPATCH(BN, F, R) \
-  if (r.bn == BN && r.fused == F && r.halo_bres == R) return launch_halo<BN, F, H, R>(r, B, sms, st);
+#define LSG_HALO_DISPATCH(BN, NP, F, R)                                                       \
+  if (r.bn == BN && r.halo_nph == NP && r.fused == F && r.halo_bres == R)                     \
+    return launch_halo<BN, NP, F, H, R>(r, B, sms, st);
     LSG_HALO_VARIANTS(LSG_HALO_DISPATCH)
 #undef LSG_HALO_DISPATCH
-    fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn));
+    fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / phases " +
+                           std::to_string(r.halo_nph) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
 #define LSG_DISPATCH(BN, CC, F) \
   if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, H>(r, B, sms, st);
@@ -460,7 +486,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       std::vector<float> w1b1(3 * 32 + 3);
       std::vector<int64_t> pack_off(kNumLayers * MAX_PHASES, 0);
       std::vector<int64_t> bias_off(kNumLayers, 0);
-      std::vector<int64_t> halo_off(kNumLayers, -1);  // (channel block, tap) packing for conv_halo
+      std::vector<HaloGeo> hgeo(kNumLayers);  // conv_halo routing, taps and packing
       struct PhaseGeo { int ntaps; signed char dy[MAX_TAPS], dx[MAX_TAPS]; int ky[MAX_TAPS], kx[MAX_TAPS]; int oy, ox; };
       std::vector<std::vector<PhaseGeo>> geo(kNumLayers);
       const float* wp = weights;
@@ -529,21 +555,65 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
               G.push_back(pg);
             }
         }
-        if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 &&
-            L.cout <= 128 && L.cin % 16 == 0) {
-          // [cb][tap][cout][64]: K block = 64 channels of one tap, 128 B swizzled rows
-          const int ncb = (L.cin + 63) / 64, bnh = L.cout;
-          halo_off[li] = (int64_t)pack.size();
-          pack.resize(pack.size() + (size_t)ncb * 9 * bnh * BK, 0);
-          uint16_t* dst = pack.data() + halo_off[li];
+        if (const HaloMode hm = halo_mode(L); hm != HALO_NONE) {
+          HaloGeo& hg = hgeo[li];
+          hg.mode = hm;
+          auto add_tap = [&](int aoff, int z, int ky, int kx) {
+            if (hg.ntaps == MAX_HTAPS) fail(LSG_ERUNTIME, std::string("generator: halo tap list overflow at ") + L.name);
+            bool first = true;
+            for (int t = 0; t < hg.ntaps; ++t) first &= hg.tphase[t] != z;
+            if (first) hg.tfirst |= 1 << hg.ntaps;
+            hg.aoff[hg.ntaps] = aoff;
+            hg.tphase[hg.ntaps] = z;
+            hg.ky[hg.ntaps] = ky;
+            hg.kx[hg.ntaps] = kx;
+            ++hg.ntaps;
+          };
+          if (hm == HALO_CONV3) {  // patch = tile + 1-pixel halo, taps = (ky, kx)
+            hg.oy0 = hg.ox0 = -1;
+            hg.pw = HTW + 2;
+            hg.ph = HTH + 2;
+            for (int ky = 0; ky < 3; ++ky)
+              for (int kx = 0; kx < 3; ++kx) add_tap(ky * hg.pw + kx, 0, ky, kx);
+          } else if (hm == HALO_CONVT2) {  // grid = input positions, patch = tile + 1 (bottom/right)
+            hg.pw = HTW + 1;
+            hg.ph = HTH + 1;
+            hg.nph = (int)G.size();
+            if (hg.nph != 4) fail(LSG_ERUNTIME, std::string("generator: ConvT phase count at ") + L.name);
+            for (int z = 0; z < hg.nph; ++z) {
+              hg.poy[z] = G[z].oy;
+              hg.pox[z] = G[z].ox;
+              for (int t = 0; t < G[z].ntaps; ++t) {
+                if (G[z].dy[t] < 0 || G[z].dy[t] > 1 || G[z].dx[t] < 0 || G[z].dx[t] > 1)
+                  fail(LSG_ERUNTIME, std::string("generator: ConvT tap outside patch at ") + L.name);
+                add_tap(G[z].dy[t] * hg.pw + G[z].dx[t], z, G[z].ky[t], G[z].kx[t]);
+              }
+            }
+          } else {  // stem: planes = x shifts 0..7, taps = the 7 kernel rows
+            hg.oy0 = hg.ox0 = -3;
+            hg.pw = HTW;
+            hg.ph = HTH + 6;
+            for (int ky = 0; ky < 7; ++ky) add_tap(ky * hg.pw, 0, ky, -1);
+          }
+          // [cb][tap][cout][64]: one K block per (channel block, tap), 128 B swizzled rows
+          const int ncb = hm == HALO_STEM7 ? 1 : (L.cin + 63) / 64, bnh = L.cout;
+          hg.off = (int64_t)pack.size();
+          pack.resize(pack.size() + (size_t)ncb * hg.ntaps * bnh * BK, 0);
+          uint16_t* dst = pack.data() + hg.off;
           for (int cb = 0; cb < ncb; ++cb)
-            for (int tap = 0; tap < 9; ++tap) {
-              uint16_t* blk = dst + ((size_t)cb * 9 + tap) * bnh * BK;
-              const int ky = tap / 3, kx = tap % 3;
+            for (int tap = 0; tap < hg.ntaps; ++tap) {
+              uint16_t* blk = dst + ((size_t)cb * hg.ntaps + tap) * bnh * BK;
               for (int r = 0; r < bnh; ++r)
                 for (int j = 0; j < BK; ++j) {
-                  const int c = cb * 64 + j;
-                  const float v = c < L.cin ? w[(((int64_t)r * L.cin + c) * 3 + ky) * 3 + kx] : 0.f;
+                  int c = cb * 64 + j, ky = hg.ky[tap], kx = hg.kx[tap];
+                  if (hm == HALO_STEM7) {
+                    kx = j >> 3;
+                    c = j & 7;
+                  }
+                  float v = 0.f;
+                  if (c < L.cin && kx < L.kw)
+                    v = L.kind == CONV ? w[(((int64_t)r * L.cin + c) * L.kh + ky) * L.kw + kx]
+                                       : w[(((int64_t)c * L.cout + r) * L.kh + ky) * L.kw + kx];
                   blk[r * BK + (((j >> 3) ^ (r & 7)) << 3) + (j & 7)] = h->half ? f2h(v) : f2bf(v);
                 }
             }
@@ -765,27 +835,45 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           const int gw = (in.W + upper_w - lower_w - 1) / p.sx + 1, gh = (in.H + upper_h - lower_h - 1) / p.sy + 1;
           if (gw != P.GW || gh != P.GH) fail(LSG_ERUNTIME, std::string("generator: im2col grid mismatch at ") + L.name);
         }
-        if (halo_off[l] >= 0 && halo_eligible(L, in)) {
+        const HaloGeo& hg = hgeo[l];
+        if (hg.mode != HALO_NONE && (hg.mode != HALO_CONV3 || in.W >= 16)) {
           HaloParams& hp = r.hp;
           r.halo = true;
+          r.halo_nph = hg.nph;
           hp.H = in.H;
           hp.W = in.W;
           hp.C = p.C;
-          hp.k = 3;
-          hp.pad = 1;
-          hp.pw = HTW + 2;
-          hp.ph = HTH + 2;
+          hp.GH = hg.mode == HALO_CONVT2 ? in.H : OH;
+          hp.GW = hg.mode == HALO_CONVT2 ? in.W : OW;
+          hp.oy0 = hg.oy0;
+          hp.ox0 = hg.ox0;
+          hp.pw = hg.pw;
+          hp.ph = hg.ph;
           hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
-          hp.ngran = p.C / 8;
+          if (hp.plane > HaloCfg<32, 1, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
+          hp.shift_planes = hg.mode == HALO_STEM7;
+          hp.ngran = hp.shift_planes ? 8 : p.C / 8;
           hp.ncb = (hp.ngran + 7) / 8;
-          hp.tiles_x = (int)ceil_div(in.W, HTW);
-          hp.tiles_y = (int)ceil_div(in.H, HTH);
+          hp.ntaps = hg.ntaps;
+          for (int t = 0; t < MAX_HTAPS; ++t) {
+            hp.aoff[t] = hg.aoff[t];
+            hp.tphase[t] = hg.tphase[t];
+          }
+          hp.tfirst = hg.tfirst;
+          hp.osy = hp.osx = hg.mode == HALO_CONVT2 ? 2 : 1;
+          for (int z = 0; z < 4; ++z) {
+            hp.poy[z] = hg.poy[z];
+            hp.pox[z] = hg.pox[z];
+          }
+          hp.tiles_x = (int)ceil_div(hp.GW, HTW);
+          hp.tiles_y = (int)ceil_div(hp.GH, HTH);
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
-          hp.w = h->wpack.p + halo_off[l];
-          hp.wblocks = hp.ncb * 9;
-          hp.ntiles_n = 1;
-          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, true>::B_RES_BYTES;
+          hp.w = h->wpack.p + hg.off;
+          hp.wblocks = hp.ncb * hg.ntaps;
+          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, 1, true>::B_RES_BYTES;
           if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
+          hp.OH = OH;
+          hp.OW = OW;
           hp.out = p.out;
           hp.out_pitch = p.out_pitch;
           hp.out_coff = p.out_coff;
