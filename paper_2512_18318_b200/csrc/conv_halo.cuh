@@ -33,6 +33,35 @@ namespace gen {
 constexpr int HTH = 16, HTW = 8;  // tile: 16 rows x 8 columns = 128 grid positions
 constexpr int MAX_HTAPS = 9;
 
+// Routing modes and their compile-time tap tables (patch offset in pixels,
+// output phase).  The host builds the same lists from the layer geometry and
+// checks them against these (generator.cu), so packing and issue agree.
+enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3 };
+
+template <int MODE>
+struct HaloTaps;
+template <>
+struct HaloTaps<HALO_CONV3> {  // 3x3 "same": patch (16+2) x (8+2), taps (ky, kx)
+  static constexpr int NPH = 1, NT = 9, PW = HTW + 2, PH = HTH + 2;
+  __host__ __device__ static constexpr int aoff(int t) { return (t / 3) * PW + t % 3; }
+  __host__ __device__ static constexpr int phase(int) { return 0; }
+};
+template <>
+struct HaloTaps<HALO_CONVT2> {  // stride-2 ConvT: patch (16+1) x (8+1) of the input, 4 phases (oy, ox)
+  static constexpr int NPH = 4, NT = 9, PW = HTW + 1, PH = HTH + 1;
+  // (dy, dx) per tap: phase 0 (0,0) | 1 (0,1) (0,0) | 2 (1,0) (0,0) | 3 (1,1) (1,0) (0,1) (0,0)
+  __host__ __device__ static constexpr int aoff(int t) {
+    return t == 1 || t == 7 ? 1 : (t == 3 || t == 6 ? PW : (t == 5 ? PW + 1 : 0));
+  }
+  __host__ __device__ static constexpr int phase(int t) { return t == 0 ? 0 : (t < 3 ? 1 : (t < 5 ? 2 : 3)); }
+};
+template <>
+struct HaloTaps<HALO_STEM7> {  // 7x7 on 8 channels: planes = x shifts, taps = kernel rows
+  static constexpr int NPH = 1, NT = 7, PW = HTW, PH = HTH + 6;
+  __host__ __device__ static constexpr int aoff(int t) { return t * PW; }
+  __host__ __device__ static constexpr int phase(int) { return 0; }
+};
+
 struct alignas(64) HaloParams {
   CUtensorMap tmap;  // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
   int H, W, C, B;    // input view
@@ -65,8 +94,9 @@ struct alignas(64) HaloParams {
   void* final_out;
 };
 
-template <int BN, int NPH, bool B_RES>
+template <int BN, int MODE, bool B_RES>
 struct HaloCfg {
+  static constexpr int NPH = HaloTaps<MODE>::NPH;
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
   static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
@@ -99,9 +129,11 @@ __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
 }
 
-template <int BN, int NPH, bool FUSED_OUT, bool HALF, bool B_RES>
+template <int BN, int MODE, bool FUSED_OUT, bool HALF, bool B_RES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
-  using CF = HaloCfg<BN, NPH, B_RES>;
+  using CF = HaloCfg<BN, MODE, B_RES>;
+  using TT = HaloTaps<MODE>;
+  constexpr int NPH = TT::NPH;
   using NF = Num<HALF>;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
   static_assert(!FUSED_OUT || NPH == 1, "fused output conv has one phase");
@@ -197,78 +229,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     // ------------------------------------------------ MMA issuer
     // One elected lane issues everything.  Descriptors are linear in the
     // start address (14-bit field; smem < 256 KB never carries), so every
-    // tap / K step is a constant add to a per-patch base: no division or
-    // re-encoding in the issue loop, which otherwise costs more than the
-    // MMAs themselves (profiles/r01).
+    // tap / K step is a compile-time add to a per-patch base, and the
+    // clobber-free wrappers let parameters stay in registers: the issue loop
+    // is a handful of uniform adds per 4 MMAs (profiles/r01: with divisions,
+    // parameter reloads and per-tap warp reconvergence it cost more than the
+    // MMAs themselves).
     constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+    constexpr int NT = TT::NT;
+    constexpr uint64_t PLANE2 = (uint64_t)((2 * ((TT::PW * TT::PH * 16 + 127) / 128 * 128)) >> 4);
+    constexpr uint64_t BBLK16 = CF::BBLK >> 4;
+    constexpr uint64_t HST16 = CF::HSTAGE >> 4;
     if (elect_one()) {
       const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
       if constexpr (B_RES) {
-        tc::mbar_wait(&bfull[0], 0);
-        tc::tc_fence_after();
+        tc::mbar_wait_nc(&bfull[0], 0);
+        tc::tc_fence_after_nc();
       }
-      const uint64_t plane2 = (uint64_t)((2 * p.plane) >> 4);  // one K step = two planes
-      uint64_t toff[MAX_HTAPS];
-      uint32_t tcol[MAX_HTAPS];
-#pragma unroll
-      for (int tap = 0; tap < MAX_HTAPS; ++tap) {
-        toff[tap] = (uint64_t)p.aoff[tap];
-        tcol[tap] = (uint32_t)(p.tphase[tap] * BN);
-      }
-      const int ntaps = p.ntaps, tfirst = p.tfirst;
-      const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)p.plane, (uint32_t)(p.pw * 16));
+      const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)(PLANE2 << 3), (uint32_t)(TT::PW * 16));
       const uint64_t b_desc0 = tc::sdesc_sw128(sB0);
-      constexpr uint64_t BBLK16 = CF::BBLK >> 4;
-      constexpr uint64_t HST16 = CF::HSTAGE >> 4;
+      const int ncb = p.ncb, ngran = p.ngran, total = p.total_tiles;
       int hs = 0, bs = 0;
       uint32_t hph = 0, bph = 0, tl = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-        tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
-        tc::tc_fence_after();
+        tc::mbar_wait_nc(&tempty[a], (use & 1) ^ 1);
+        tc::tc_fence_after_nc();
         const uint32_t d = tmem + a * CF::ACC_COLS;
-        for (int cb = 0; cb < p.ncb; ++cb) {
-          const int ksteps = min(8, p.ngran - cb * 8) >> 1;
-          tc::mbar_wait(&hfull[hs], hph);
-          tc::tc_fence_after();
+        for (int cb = 0; cb < ncb; ++cb) {
+          const int ksteps = min(8, ngran - cb * 8) >> 1;
+          tc::mbar_wait_nc(&hfull[hs], hph);
+          tc::tc_fence_after_nc();
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
+          const uint64_t bcb = b_desc0 + (uint64_t)(cb * NT) * BBLK16;
 #pragma unroll
-          for (int tap = 0; tap < MAX_HTAPS; ++tap) {
-            if (tap < ntaps) {
-              uint64_t db;
-              if constexpr (B_RES) {
-                db = b_desc0 + (uint64_t)(cb * ntaps + tap) * BBLK16;
-              } else {
-                tc::mbar_wait(&bfull[bs], bph);
-                tc::tc_fence_after();
-                db = b_desc0 + (uint64_t)bs * BBLK16;
-              }
-              const uint64_t at = ah + toff[tap];
-              const uint32_t dd = d + tcol[tap];
-              const uint32_t acc0 = (cb == 0 && ((tfirst >> tap) & 1)) ? 0u : 1u;
-              if (ksteps == 4) {
+          for (int tap = 0; tap < NT; ++tap) {
+            uint64_t db;
+            if constexpr (B_RES) {
+              db = bcb + (uint64_t)tap * BBLK16;
+            } else {
+              tc::mbar_wait_nc(&bfull[bs], bph);
+              tc::tc_fence_after_nc();
+              db = b_desc0 + (uint64_t)bs * BBLK16;
+            }
+            const uint64_t at = ah + (uint64_t)TT::aoff(tap);
+            const uint32_t dd = d + (uint32_t)(TT::phase(tap) * BN);
+            bool first = true;  // first tap of its phase (compile time)
 #pragma unroll
-                for (int ks = 0; ks < 4; ++ks) tc::mma_f16(dd, at + ks * plane2, db + 2 * ks, idesc, ks ? 1u : acc0);
-              } else {
-                for (int ks = 0; ks < ksteps; ++ks)
-                  tc::mma_f16(dd, at + ks * plane2, db + 2 * ks, idesc, ks ? 1u : acc0);
-              }
-              if constexpr (!B_RES) {
-                tc::mma_commit(&bempty[bs]);
-                if (++bs == BS) {
-                  bs = 0;
-                  bph ^= 1;
-                }
+            for (int u = 0; u < tap; ++u) first = first && TT::phase(u) != TT::phase(tap);
+            const uint32_t acc0 = (first && cb == 0) ? 0u : 1u;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              if (ks < ksteps) tc::mma_f16_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+            if constexpr (!B_RES) {
+              tc::mma_commit_nc(&bempty[bs]);
+              if (++bs == BS) {
+                bs = 0;
+                bph ^= 1;
               }
             }
           }
-          tc::mma_commit(&hempty[hs]);
+          tc::mma_commit_nc(&hempty[hs]);
           if (++hs == HS) {
             hs = 0;
             hph ^= 1;
           }
         }
-        tc::mma_commit(&tfull[a]);
+        tc::mma_commit_nc(&tfull[a]);
       }
     }
     __syncwarp();

@@ -185,14 +185,12 @@ struct LayerRun {
   int GH[MAX_PHASES], GW[MAX_PHASES];  // per phase, per image
   bool halo = false;                   // routed to conv_halo
   bool halo_bres = false;              // weights resident in shared memory
-  int halo_nph = 1;                    // output phases (4 for a stride-2 ConvT)
+  int halo_mode = 0;                   // HaloMode of a conv_halo layer
   HaloParams hp;
 };
 
 // Layers routed to the patch-reuse kernel (conv_halo.cuh); everything else
 // goes to the im2col kernel.
-enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3 };
-
 HaloMode halo_mode(const LayerSpec& L) {
   if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 && L.cout <= 128 &&
       L.cin % 16 == 0)
@@ -354,14 +352,25 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(256, 64, false)          \
   X(32, 16, true)
 
-// halo kernel variants: (tile width, output phases, fused output, weights resident)
-#define LSG_HALO_VARIANTS(X) \
-  X(16, 1, false, true)      \
-  X(32, 1, false, true)      \
-  X(64, 1, false, true)      \
-  X(128, 1, false, false)    \
-  X(64, 4, false, false)     \
-  X(32, 1, true, true)
+// halo kernel variants: (tile width, mode, fused output, weights resident)
+#define LSG_HALO_VARIANTS(X)             \
+  X(16, HALO_STEM7, false, true)         \
+  X(32, HALO_CONV3, false, true)         \
+  X(64, HALO_CONV3, false, true)         \
+  X(128, HALO_CONV3, false, false)       \
+  X(64, HALO_CONVT2, false, false)       \
+  X(32, HALO_CONV3, true, true)
+
+// The host-built tap list of a halo layer must be the kernel's compile-time
+// table (conv_halo.cuh HaloTaps): packing order == issue order.
+template <int MODE>
+bool taps_match(const HaloGeo& g) {
+  using TT = HaloTaps<MODE>;
+  if (g.ntaps != TT::NT || g.nph != TT::NPH || g.pw != TT::PW || g.ph != TT::PH) return false;
+  for (int t = 0; t < TT::NT; ++t)
+    if (g.aoff[t] != TT::aoff(t) || g.tphase[t] != TT::phase(t)) return false;
+  return true;
+}
 
 static void set_smem_attrs() {
 #define LSG_SET_ATTR(BN, CC, F)                                                                                   \
@@ -371,34 +380,34 @@ static void set_smem_attrs() {
                                 Cfg<BN>::SMEM));
   LSG_CONV_VARIANTS(LSG_SET_ATTR)
 #undef LSG_SET_ATTR
-#define LSG_SET_HALO_ATTR(BN, NP, F, R)                                                                           \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, NP, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                HaloCfg<BN, NP, R>::SMEM));                                                       \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, NP, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                HaloCfg<BN, NP, R>::SMEM));
+#define LSG_SET_HALO_ATTR(BN, MD, F, R)                                                                           \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                HaloCfg<BN, MD, R>::SMEM));                                                       \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                HaloCfg<BN, MD, R>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
 }
 
-template <int BN, int NP, bool F, bool H, bool R>
+template <int BN, int MD, bool F, bool H, bool R>
 static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   HaloParams hp = r.hp;
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img;
   const int grid = std::min(hp.total_tiles, sms);
-  conv_halo<BN, NP, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, NP, R>::SMEM, st>>>(hp);
+  conv_halo<BN, MD, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, MD, R>::SMEM, st>>>(hp);
 }
 
 template <bool H>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
   if (r.halo) {
-#define LSG_HALO_DISPATCH(BN, NP, F, R)                                                       \
-  if (r.bn == BN && r.halo_nph == NP && r.fused == F && r.halo_bres == R)                     \
-    return launch_halo<BN, NP, F, H, R>(r, B, sms, st);
+#define LSG_HALO_DISPATCH(BN, MD, F, R)                                                       \
+  if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
+    return launch_halo<BN, MD, F, H, R>(r, B, sms, st);
     LSG_HALO_VARIANTS(LSG_HALO_DISPATCH)
 #undef LSG_HALO_DISPATCH
-    fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / phases " +
-                           std::to_string(r.halo_nph) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
+    fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / mode " +
+                           std::to_string(r.halo_mode) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
 #define LSG_DISPATCH(BN, CC, F) \
   if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, H>(r, B, sms, st);
@@ -595,6 +604,10 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
             hg.ph = HTH + 6;
             for (int ky = 0; ky < 7; ++ky) add_tap(ky * hg.pw, 0, ky, -1);
           }
+          const bool ok = hm == HALO_CONV3    ? taps_match<HALO_CONV3>(hg)
+                          : hm == HALO_CONVT2 ? taps_match<HALO_CONVT2>(hg)
+                                              : taps_match<HALO_STEM7>(hg);
+          if (!ok) fail(LSG_ERUNTIME, std::string("generator: halo tap table mismatch at ") + L.name);
           // [cb][tap][cout][64]: one K block per (channel block, tap), 128 B swizzled rows
           const int ncb = hm == HALO_STEM7 ? 1 : (L.cin + 63) / 64, bnh = L.cout;
           hg.off = (int64_t)pack.size();
@@ -839,7 +852,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         if (hg.mode != HALO_NONE && (hg.mode != HALO_CONV3 || in.W >= 16)) {
           HaloParams& hp = r.hp;
           r.halo = true;
-          r.halo_nph = hg.nph;
+          r.halo_mode = hg.mode;
           hp.H = in.H;
           hp.W = in.W;
           hp.C = p.C;
@@ -850,7 +863,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.pw = hg.pw;
           hp.ph = hg.ph;
           hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
-          if (hp.plane > HaloCfg<32, 1, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
+          if (hp.plane > HaloCfg<32, HALO_CONV3, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
           hp.shift_planes = hg.mode == HALO_STEM7;
           hp.ngran = hp.shift_planes ? 8 : p.C / 8;
           hp.ncb = (hp.ngran + 7) / 8;
@@ -870,7 +883,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
-          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, 1, true>::B_RES_BYTES;
+          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, true>::B_RES_BYTES;
           if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
           hp.OH = OH;
           hp.OW = OW;

@@ -113,6 +113,42 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Variants for a thread that only ISSUES tensor-core work (reads no shared
+// or global data the async proxies write): no "memory" clobber, so the
+// compiler keeps kernel parameters and descriptors in registers across the
+// issue loop instead of re-loading them after every instruction.  volatile
+// asm statements keep their relative order.
+__device__ __forceinline__ bool mbar_try_wait_nc(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity));
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_nc(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait_nc(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try_wait_nc(bar, parity)) {
+    if ((++spins & 0xfff) == 0 && clock64() - t0 > 40000000000LL) __trap();
+  }
+}
+__device__ __forceinline__ void tc_fence_after_nc() { asm volatile("tcgen05.fence::after_thread_sync;"); }
+__device__ __forceinline__ void mma_f16_nc(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_nc(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)));
+}
+
 // Instruction descriptor, kind::f16: A/B format fmt (0 fp16, 1 bf16) -> f32
 // accumulate, K-major A and B, M x N.
 __host__ __device__ constexpr uint32_t idesc_f16kind(int M, int N, uint32_t fmt) {

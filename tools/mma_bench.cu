@@ -4,6 +4,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_2512_18318_b200/csrc -o mma_bench mma_bench.cu
 // modes: 0 SW128 A fixed | 1 SW128 A cycling over 4 stages | 2 no-swizzle A
 //        3 = 1 + bulk-copy fill traffic from L2 into a separate region
+//        4 no-swizzle, SBO 160 (halo patch rows), start +16 B (shifted tap)
+//        5 no-swizzle, SBO 160, 128-aligned start | 6 no-swizzle, SBO 128, start +16 B
 #include <cstdio>
 #include <cstdint>
 
@@ -18,8 +20,8 @@ __device__ __forceinline__ uint64_t desc_noswz(uint32_t addr, uint32_t lbo, uint
 
 constexpr int SMEM = 200 * 1024;
 
-template <int M, int N>
-__global__ void bench(long long* out, int iters, int mode, const uint8_t* src, unsigned long long* fill_bytes) {
+template <int M, int N, int mode>
+__global__ void bench(long long* out, int iters, const uint8_t* src, unsigned long long* fill_bytes) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw = tc::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -46,14 +48,30 @@ __global__ void bench(long long* out, int iters, int mode, const uint8_t* src, u
     const uint32_t b = base + 65536;
     const uint64_t db = tc::sdesc_sw128(b);
     constexpr uint32_t idesc = tc::idesc_f16kind(M, N, 0);
+    // descriptor of K step 0 and the per-step increment (16-byte units)
+    uint64_t da0;
+    uint64_t kstep;
+    if constexpr (mode == 2) {
+      da0 = desc_noswz(base, 2048, 128);
+      kstep = 4096 >> 4;
+    } else if constexpr (mode == 4) {
+      da0 = desc_noswz(base + 16, 2944, 160);
+      kstep = 5888 >> 4;
+    } else if constexpr (mode == 5) {
+      da0 = desc_noswz(base, 2944, 160);
+      kstep = 5888 >> 4;
+    } else if constexpr (mode == 6) {
+      da0 = desc_noswz(base + 16, 2048, 128);
+      kstep = 4096 >> 4;
+    } else {
+      da0 = tc::sdesc_sw128(base);
+      kstep = 2;
+    }
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      const uint32_t a = base + (mode == 0 || mode == 2 ? 0u : (uint32_t)((i & 3) * 16384));
+      const uint64_t da = da0 + (mode == 1 || mode == 3 ? (uint64_t)((i & 3) * (16384 >> 4)) : 0ull);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint64_t da = mode == 2 ? desc_noswz(a + k * 4096, 2048, 128) : tc::sdesc_sw128(a) + 2 * k;
-        tc::mma_f16(tmem, da, db + 2 * k, idesc, 1);
-      }
+      for (int k = 0; k < 4; ++k) tc::mma_f16(tmem, da + k * kstep, db + 2 * k, idesc, 1);
     }
     tc::mma_commit(&bar);
     tc::mbar_wait(&bar, 0);
@@ -93,15 +111,15 @@ __global__ void bench(long long* out, int iters, int mode, const uint8_t* src, u
 static uint8_t* g_src;
 static unsigned long long* g_fill;
 
-template <int M, int N>
-void run(int blocks, int mode) {
+template <int M, int N, int mode>
+void run(int blocks) {
   long long* d;
   cudaMalloc(&d, sizeof(long long) * blocks);
   cudaMemset(g_fill, 0, sizeof(unsigned long long) * 148);
-  cudaFuncSetAttribute(bench<M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  cudaFuncSetAttribute(bench<M, N, mode>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   const int iters = 4000;
-  bench<M, N><<<blocks, 128, SMEM>>>(d, 10, mode, g_src, g_fill);
-  bench<M, N><<<blocks, 128, SMEM>>>(d, iters, mode, g_src, g_fill);
+  bench<M, N, mode><<<blocks, 128, SMEM>>>(d, 10, g_src, g_fill);
+  bench<M, N, mode><<<blocks, 128, SMEM>>>(d, iters, g_src, g_fill);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   unsigned long long f[148];
@@ -125,11 +143,17 @@ int main() {
   cudaMalloc(&g_src, 148 * 65536);
   cudaMemset(g_src, 1, 148 * 65536);
   cudaMalloc(&g_fill, sizeof(unsigned long long) * 148);
-  for (int mode : {0, 1, 2, 3}) {
-    run<128, 32>(148, mode);
-    run<128, 64>(148, mode);
-    run<128, 128>(148, mode);
-    run<128, 256>(148, mode);
-  }
+#define RUN(MODE)            \
+  run<128, 32, MODE>(148);   \
+  run<128, 64, MODE>(148);   \
+  run<128, 128, MODE>(148);  \
+  run<128, 256, MODE>(148);
+  RUN(0)
+  RUN(1)
+  RUN(2)
+  RUN(3)
+  RUN(4)
+  RUN(5)
+  RUN(6)
   return 0;
 }
