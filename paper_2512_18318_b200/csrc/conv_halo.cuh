@@ -63,7 +63,9 @@ struct HaloTaps<HALO_STEM7> {  // 7x7 on 8 channels: planes = x shifts, taps = k
 };
 
 struct alignas(64) HaloParams {
-  CUtensorMap tmap;  // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
+  CUtensorMap tmap;      // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
+  CUtensorMap tmap_out;  // output view, box (min(BN,64), 8, 16, 1) output positions (x2 stride for ConvT)
+  CUtensorMap tmap_res;  // residual view, box (min(BN,64), 8, 16, 1)
   int H, W, C, B;    // input view
   int GH, GW;        // grid (output positions for convs, input positions for ConvT)
   int oy0, ox0;      // patch origin relative to the tile origin (-pad for convs)
@@ -94,17 +96,36 @@ struct alignas(64) HaloParams {
   void* final_out;
 };
 
-template <int BN, int MODE, bool B_RES>
+// Shared memory plan (bytes): patch ring | weights (resident or ring) |
+// output staging (TMA-store source) | residual tiles (TMA-load target) |
+// barriers.  Staging / residual tiles are [128 positions][IB bytes] boxes in
+// the tensor map's swizzle (IB = 128 -> 128B, 64 -> 64B, 32 -> 32B) so the
+// epilogue's per-position 16-byte accesses are bank-conflict free.
+template <int BN, int MODE, bool FUSED, bool B_RES>
 struct HaloCfg {
   static constexpr int NPH = HaloTaps<MODE>::NPH;
+  static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
+  static constexpr int HS = 3;
   static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
-  static constexpr int B_RES_BYTES = 96 * 1024;
-  static constexpr int HS = B_RES ? 4 : 3;
-  static constexpr int BS = B_RES ? 1 : ((200 * 1024 - HS * HSTAGE) / BBLK > 8 ? 8 : (200 * 1024 - HS * HSTAGE) / BBLK);
-  static constexpr int B_BYTES = B_RES ? B_RES_BYTES : BS * BBLK;
-  static constexpr int SMEM = 1024 + HS * HSTAGE + B_BYTES + 512;
+  static constexpr int W_RES_BYTES = 72 * 1024;
+  static constexpr int IB = (BN < 64 ? BN : 64) * 2;   // bytes per position per box
+  static constexpr int NCH = BN > 64 ? BN / 64 : 1;    // boxes across the channels
+  static constexpr int BOX = 128 * IB;                 // one [128][IB] box
+  static constexpr int STG_BYTES = FUSED ? 0 : NPH * NCH * BOX;
+  static constexpr int NSTG = FUSED ? 0 : (B_RES ? 2 : 1);
+  static constexpr int RES_BYTES = HAS_RES ? NCH * BOX : 0;
+  static constexpr int NRES = HAS_RES ? (B_RES ? 2 : 1) : 0;
+  static constexpr int FIXED = HS * HSTAGE + NSTG * STG_BYTES + NRES * RES_BYTES;
+  static constexpr int BS_FIT = (220 * 1024 - FIXED) / BBLK;
+  static constexpr int BS = B_RES ? 1 : (BS_FIT > 8 ? 8 : BS_FIT);
+  static constexpr int B_BYTES = B_RES ? W_RES_BYTES : BS * BBLK;
+  static constexpr int OFF_B = HS * HSTAGE;
+  static constexpr int OFF_STG = OFF_B + B_BYTES;
+  static constexpr int OFF_RES = OFF_STG + NSTG * STG_BYTES;
+  static constexpr int OFF_BAR = OFF_RES + NRES * RES_BYTES;
+  static constexpr int SMEM = 1024 + OFF_BAR + 512;
   static constexpr int ACC_COLS = NPH * BN;                // one accumulator: every phase
   static constexpr int NACC = 2 * ACC_COLS <= 512 ? 2 : 1;  // double-buffered when TMEM allows
   static constexpr int TMEM_COLS = NACC * ACC_COLS <= 32    ? 32
@@ -113,7 +134,33 @@ struct HaloCfg {
                                    : NACC * ACC_COLS <= 256 ? 256
                                                             : 512;
   static_assert(NACC * ACC_COLS <= 512, "accumulators exceed TMEM");
+  static_assert(B_RES || BS >= 2, "weight ring too small");
+  static_assert(SMEM <= 227 * 1024, "shared memory plan exceeds 227 KB");
 };
+
+// byte offset of 16-byte chunk j of box row r under the box's swizzle
+template <int IB>
+__device__ __forceinline__ uint32_t swz(int r, int j) {
+  const uint32_t off = (uint32_t)(r * IB + j * 16);
+  constexpr uint32_t mask = IB == 128 ? 7u : (IB == 64 ? 3u : 1u);
+  return off ^ (((off >> 7) & mask) << 4);
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c, int x, int y, int n) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c), "r"(x), "r"(y), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void tma_tile_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int x, int y,
                                             int n) {
@@ -131,24 +178,33 @@ __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint3
 
 template <int BN, int MODE, bool FUSED_OUT, bool HALF, bool B_RES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
-  using CF = HaloCfg<BN, MODE, B_RES>;
+  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES>;
   using TT = HaloTaps<MODE>;
   constexpr int NPH = TT::NPH;
   using NF = Num<HALF>;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
   static_assert(!FUSED_OUT || NPH == 1, "fused output conv has one phase");
+  // epilogue warps 2-9 = two groups of four (one per TMEM lane quadrant).
+  // SPLIT: both groups take every tile, half the channels each.  Otherwise
+  // (BN = 16, or the fused 1x1 output) the groups alternate tiles, group g
+  // owning accumulator g.
+  constexpr bool SPLIT = !FUSED_OUT && BN >= 32;
+  constexpr bool EPI_ALT = !SPLIT && NACC == 2;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = tc::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint8_t* sH = smem;
-  uint8_t* sB = smem + HS * CF::HSTAGE;
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + CF::B_BYTES);
+  uint8_t* sB = smem + CF::OFF_B;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(smem + CF::OFF_BAR);
   uint64_t* hempty = hfull + HS;
   uint64_t* bfull = hempty + HS;
   uint64_t* bempty = bfull + BS;
   uint64_t* tfull = bempty + BS;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
+  constexpr int EPI_THREADS = EPI_ALT ? 32 * NUM_EPI_WARPS / 2 : 32 * NUM_EPI_WARPS;  // per tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -162,10 +218,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], 32 * NUM_EPI_WARPS);
+      tc::mbar_init(&tempty[a], EPI_THREADS);
+      tc::mbar_init(&rfull[a], 1);
+      tc::mbar_init(&rempty[a], EPI_THREADS);
     }
     tc::fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap)) : "memory");
+    if constexpr (!FUSED_OUT)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_out)) : "memory");
+    if constexpr (CF::HAS_RES)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_res)) : "memory");
   }
   if (warp == 1) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
@@ -190,12 +252,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     }
     // plane g of channel block cb: channels (cb*8 + g)*8 at x0, or channels 0..7 at x0 + g
     const int cstep = p.shift_planes ? 0 : 8, xstep = p.shift_planes ? 1 : 0;
-    int hs = 0, bs = 0;
-    uint32_t hph = 0, bph = 0;
+    int hs = 0, bs = 0, rs = 0;
+    uint32_t hph = 0, bph = 0, rph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       const int n = t / p.tiles_per_img, r = t - n * p.tiles_per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
       const int y0 = ty * HTH + p.oy0, x0 = tx * HTW + p.ox0;
+
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
         tc::mbar_wait(&hempty[hs], hph ^ 1);
@@ -222,6 +285,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
               bph ^= 1;
             }
           }
+        }
+      }
+      if constexpr (CF::HAS_RES) {
+        tc::mbar_wait(&rempty[rs], rph ^ 1);
+        if (lane == 0) {
+          tc::mbar_arrive_expect_tx(&rfull[rs], CF::RES_BYTES);
+          const uint32_t dst = tc::smem_u32(smem + CF::OFF_RES + rs * CF::RES_BYTES);
+#pragma unroll
+          for (int cc = 0; cc < CF::NCH; ++cc)
+            tma_tile_4d(dst + cc * CF::BOX, &p.tmap_res, &rfull[rs], cc * 64, tx * HTW, ty * HTH, n);
+        }
+        __syncwarp();
+        if (++rs == CF::NRES) {
+          rs = 0;
+          rph ^= 1;
         }
       }
     }
@@ -302,76 +380,159 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     // ------------------------------------------------ epilogue (warps 2-9)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
-    constexpr bool SPLIT = !FUSED_OUT && BN >= 32;
     constexpr int HC = SPLIT ? BN / 2 : BN;
     const int cbeg = SPLIT ? half * HC : 0;
-    const bool active = SPLIT || half == 0;
     const int r = q * 32 + lane;  // tile position: row r / 8, column r % 8
-    uint32_t tl = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
-      const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-      const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
+    const int step = EPI_ALT ? 2 : 1;
+    uint32_t tl = EPI_ALT ? (uint32_t)half : 0u;
+    // grid position of tile t for this thread
+    auto gpos = [&](int t, int& n, int& gy, int& gx) {
+      n = t / p.tiles_per_img;
+      const int rr = t - n * p.tiles_per_img;
       const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
-      const int gy = ty * HTH + (r >> 3), gx = tx * HTW + (r & 7);
-      const bool gvalid = gy < p.GH && gx < p.GW;
-      if constexpr (!FUSED_OUT) {
-        if (!active) {
-          tc::mbar_wait(&tfull[a], use & 1);
-          tc::tc_fence_after();
-        } else {
-#pragma unroll
-          for (int z = 0; z < NPH; ++z) {
-            const int y = gy * p.osy + p.poy[z], x = gx * p.osx + p.pox[z];
-            const bool valid = gvalid && y < p.OH && x < p.OW;
-            const size_t pix = ((size_t)n * p.OH + y) * p.OW + x;
-            uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + cbeg;
-            const uint16_t* rrow = (p.res && valid) ? p.res + pix * p.res_pitch + p.res_coff + cbeg : nullptr;
-            const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS + z * BN + cbeg;
-            epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
-          }
-        }
-      } else {
+      gy = ty * HTH + (r >> 3);
+      gx = tx * HTW + (r & 7);
+    };
+    if constexpr (!FUSED_OUT) {
+      // Staged epilogue: TMEM -> +bias (+residual from the TMA-loaded tile)
+      // -> ReLU -> 16-bit -> swizzled staging box -> one TMA tensor store per
+      // (phase, 64-channel chunk).  Coalescing is the TMA's job; the 16-byte
+      // row accesses of the threads stay bank-conflict free.
+      constexpr int IB = CF::IB;
+      const int grp = EPI_ALT ? half : 0;
+      const bool leader = (warp == 2 + 4 * grp) && lane == 0;  // issues the group's stores
+      int sb = 0, rs = 0;
+      uint32_t rph = 0;
+      for (int t = blockIdx.x + (int)tl * gridDim.x; t < p.total_tiles; t += step * gridDim.x, tl += step) {
+        const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
+        const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
+        const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
+        uint8_t* stg = smem + CF::OFF_STG + (EPI_ALT ? grp : sb) * CF::STG_BYTES;
+        // the store that last read this staging buffer must have drained
+        if (leader) bulk_wait_read<EPI_ALT ? 0 : CF::NSTG - 1>();
+        named_bar(1 + grp, EPI_THREADS);
+        const uint8_t* res = smem + CF::OFF_RES + rs * CF::RES_BYTES;
+        if constexpr (CF::HAS_RES) tc::mbar_wait(&rfull[rs], rph);
         tc::mbar_wait(&tfull[a], use & 1);
         tc::tc_fence_after();
-        if (half == 0) {
-          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS;
-          float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
 #pragma unroll
-          for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int z = 0; z < NPH; ++z) {
+          const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS + z * BN + cbeg;
+#pragma unroll
+          for (int c0 = 0; c0 < HC; c0 += 16) {
             uint32_t v[16];
             tc::tmem_ld16(tbase + c0, v);
+            const int ch = cbeg + c0;  // first channel of this 16-column chunk
+            const int cc = ch >> 6, j0 = (ch & 63) >> 3;
+            float f[16];
+            const float4* bp = reinterpret_cast<const float4*>(p.bias + ch);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float4 b4 = __ldg(bp + k);
+              f[4 * k + 0] = b4.x;
+              f[4 * k + 1] = b4.y;
+              f[4 * k + 2] = b4.z;
+              f[4 * k + 3] = b4.w;
+            }
+            if constexpr (CF::HAS_RES) {
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const uint4 rv = *reinterpret_cast<const uint4*>(res + cc * CF::BOX + swz<IB>(r, j0 + h2));
+                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const float2 x2 = NF::unpack(rw[k]);
+                  f[8 * h2 + 2 * k] += x2.x;
+                  f[8 * h2 + 2 * k + 1] += x2.y;
+                }
+              }
+            }
             tc::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float xx = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+            for (int k = 0; k < 16; ++k) {
+              f[k] += __uint_as_float(v[k]);
+              if (p.relu) f[k] = fmaxf(f[k], 0.f);
+            }
 #pragma unroll
-              for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
+            for (int h2 = 0; h2 < 2; ++h2) {
+              uint4 o;
+              o.x = NF::pack(f[8 * h2 + 0], f[8 * h2 + 1]);
+              o.y = NF::pack(f[8 * h2 + 2], f[8 * h2 + 3]);
+              o.z = NF::pack(f[8 * h2 + 4], f[8 * h2 + 5]);
+              o.w = NF::pack(f[8 * h2 + 6], f[8 * h2 + 7]);
+              *reinterpret_cast<uint4*>(stg + (z * CF::NCH + cc) * CF::BOX + swz<IB>(r, j0 + h2)) = o;
             }
           }
-          if (gvalid) {
-            const int HWo = p.OH * p.OW;
-            const size_t pp = (size_t)gy * p.OW + gx;
-            if (p.out_mode == OUT_F32_LOGITS) {
-              float* out = reinterpret_cast<float*>(p.final_out);
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tempty[a]);
+        if constexpr (CF::HAS_RES) {
+          tc::mbar_arrive(&rempty[rs]);
+          if (++rs == CF::NRES) {
+            rs = 0;
+            rph ^= 1;
+          }
+        }
+        tc::fence_proxy_async();  // staging writes -> visible to the TMA (async proxy)
+        named_bar(1 + grp, EPI_THREADS);
+        if (leader) {
+          const uint32_t src = tc::smem_u32(stg);
 #pragma unroll
-              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
-            } else if (p.out_mode == OUT_F32_NCHW) {
-              float* out = reinterpret_cast<float*>(p.final_out);
+          for (int z = 0; z < NPH; ++z)
 #pragma unroll
-              for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
-            } else {
-              uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
+            for (int cc = 0; cc < CF::NCH; ++cc)
+              tma_store_4d(&p.tmap_out, src + (z * CF::NCH + cc) * CF::BOX, cc * 64,
+                           tx * HTW * p.osx + p.pox[z], ty * HTH * p.osy + p.poy[z], n);
+          bulk_commit();
+        }
+        if (++sb == CF::NSTG) sb = 0;
+      }
+      if (leader) bulk_wait_all();
+    } else {
+      for (int t = blockIdx.x + (int)tl * gridDim.x; t < p.total_tiles; t += step * gridDim.x, tl += step) {
+        const uint32_t a = tl & 1, use = tl >> 1;
+        int n, gy, gx;
+        gpos(t, n, gy, gx);
+        const bool gvalid = gy < p.GH && gx < p.GW;
+        tc::mbar_wait(&tfull[a], use & 1);
+        tc::tc_fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS;
+        float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
 #pragma unroll
-              for (int o3 = 0; o3 < 3; ++o3) {
-                const float s = 1.f / (1.f + __expf(-o[o3]));
-                out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
-              }
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          tc::tmem_ld16(tbase + c0, v);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float xx = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+#pragma unroll
+            for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
+          }
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tempty[a]);  // accumulator drained: stores below overlap the next tile's MMAs
+        if (gvalid) {
+          const int HWo = p.OH * p.OW;
+          const size_t pp = (size_t)gy * p.OW + gx;
+          if (p.out_mode == OUT_F32_LOGITS) {
+            float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+            for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = o[o3];
+          } else if (p.out_mode == OUT_F32_NCHW) {
+            float* out = reinterpret_cast<float*>(p.final_out);
+#pragma unroll
+            for (int o3 = 0; o3 < 3; ++o3) out[((size_t)n * 3 + o3) * HWo + pp] = 1.f / (1.f + __expf(-o[o3]));
+          } else {
+            uint8_t* out = reinterpret_cast<uint8_t*>(p.final_out) + ((size_t)n * HWo + pp) * 3;
+#pragma unroll
+            for (int o3 = 0; o3 < 3; ++o3) {
+              const float s = 1.f / (1.f + __expf(-o[o3]));
+              out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
             }
           }
         }
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tempty[a]);
     }
   }
   __syncthreads();

@@ -232,6 +232,65 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
   }
 }
 
+// As epilogue_row, with the residual slice already in registers (loaded a
+// tile ahead by the caller, so its latency hides under the previous tile's
+// epilogue when the epilogue, not the MMA, is the bottleneck).  HC <= 64.
+template <int HC, bool HALF>
+__device__ __forceinline__ void epilogue_row_pre(uint32_t tbase, uint16_t* orow, const uint4 (&rv)[HC / 8],
+                                                 bool has_res, const float* bias, bool relu, bool valid,
+                                                 uint64_t* tfull_bar, uint32_t parity) {
+  using NF = Num<HALF>;
+  static_assert(HC % 16 == 0 && HC <= 64, "epilogue_row_pre: HC");
+  tc::mbar_wait(tfull_bar, parity);
+  tc::tc_fence_after();
+#pragma unroll
+  for (int c0 = 0; c0 < HC; c0 += 16) {
+    uint32_t v[16];
+    tc::tmem_ld16(tbase + c0, v);
+    float bf[16];
+    const float4* bp = reinterpret_cast<const float4*>(bias + c0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 b4 = __ldg(bp + j);
+      bf[4 * j + 0] = b4.x;
+      bf[4 * j + 1] = b4.y;
+      bf[4 * j + 2] = b4.z;
+      bf[4 * j + 3] = b4.w;
+    }
+    tc::tmem_ld_wait();
+    if (valid) {
+      float f[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + bf[j];
+      if (has_res) {
+        const uint4 ra = rv[c0 / 8], rb = rv[c0 / 8 + 1];
+        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 x = NF::unpack(rr[j]);
+          f[2 * j] += x.x;
+          f[2 * j + 1] += x.y;
+        }
+      }
+      if (relu) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
+      }
+      uint4 o0, o1;
+      o0.x = NF::pack(f[0], f[1]);
+      o0.y = NF::pack(f[2], f[3]);
+      o0.z = NF::pack(f[4], f[5]);
+      o0.w = NF::pack(f[6], f[7]);
+      o1.x = NF::pack(f[8], f[9]);
+      o1.y = NF::pack(f[10], f[11]);
+      o1.z = NF::pack(f[12], f[13]);
+      o1.w = NF::pack(f[14], f[15]);
+      *reinterpret_cast<uint4*>(orow + c0) = o0;
+      *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
+    }
+  }
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

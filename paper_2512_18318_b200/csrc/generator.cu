@@ -242,6 +242,24 @@ void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph) {
   if (r != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+// tiled map of an NHWC channel-slice view for the staged epilogue: box =
+// (bc channels, bx, by, 1) with element strides (1, ex, ey, 1); the swizzle
+// matches the box row width (bc * 2 bytes = 128 / 64 / 32).
+void encode_box(CUtensorMap* map, const View& v, int n, int bc, int bx, int by, int ex, int ey) {
+  const cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)v.pitch * 2, (cuuint64_t)v.W * v.pitch * 2,
+                                 (cuuint64_t)v.H * v.W * v.pitch * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)ex, (cuuint32_t)ey, 1};
+  const CUtensorMapSwizzle sw = bc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                         : (bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  if (bc != 64 && bc != 32 && bc != 16) fail(LSG_ERUNTIME, "encode_box: channel box must be 16, 32 or 64");
+  CUresult r = tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled (box) failed (" + std::to_string((int)r) + ")");
+}
+
 // cuTensorMapEncodeIm2col through the runtime's driver entry point (no
 // link-time dependency on libcuda).
 using EncodeIm2col = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -382,9 +400,9 @@ static void set_smem_attrs() {
 #undef LSG_SET_ATTR
 #define LSG_SET_HALO_ATTR(BN, MD, F, R)                                                                           \
   LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                HaloCfg<BN, MD, R>::SMEM));                                                       \
+                                HaloCfg<BN, MD, F, R>::SMEM));                                                       \
   LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                HaloCfg<BN, MD, R>::SMEM));
+                                HaloCfg<BN, MD, F, R>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
 }
@@ -395,7 +413,7 @@ static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img;
   const int grid = std::min(hp.total_tiles, sms);
-  conv_halo<BN, MD, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, MD, R>::SMEM, st>>>(hp);
+  conv_halo<BN, MD, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, MD, F, R>::SMEM, st>>>(hp);
 }
 
 template <bool H>
@@ -863,7 +881,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.pw = hg.pw;
           hp.ph = hg.ph;
           hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
-          if (hp.plane > HaloCfg<32, HALO_CONV3, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
+          if (hp.plane > HaloCfg<32, HALO_CONV3, false, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
           hp.shift_planes = hg.mode == HALO_STEM7;
           hp.ngran = hp.shift_planes ? 8 : p.C / 8;
           hp.ncb = (hp.ngran + 7) / 8;
@@ -883,7 +901,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
-          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, true>::B_RES_BYTES;
+          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;
           if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
           hp.OH = OH;
           hp.OW = OW;
@@ -899,6 +917,12 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.w1 = p.w1;
           hp.b1 = p.b1;
           encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph);
+          const int bc = std::min(r.bn, 64);
+          if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
+          if (hg.mode == HALO_CONV3 && !fused) {
+            if (!L.res || in.C != L.cout) fail(LSG_ERUNTIME, std::string("generator: halo 3x3 block without residual at ") + L.name);
+            encode_box(&hp.tmap_res, in, max_batch, bc, HTW, HTH, 1, 1);
+          }
         }
         h->plan.push_back(r);
       }
