@@ -107,8 +107,9 @@ struct HaloCfg {
   static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
-  static constexpr int HS = 3;
   static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
+  static constexpr int WG = 3;              // streamed weights: taps per ring slot (one wait + commit each)
+  static constexpr int GBLK = WG * BBLK;
   static constexpr int W_RES_BYTES = 72 * 1024;
   static constexpr int IB = (BN < 64 ? BN : 64) * 2;   // bytes per position per box
   static constexpr int NCH = BN > 64 ? BN / 64 : 1;    // boxes across the channels
@@ -117,10 +118,12 @@ struct HaloCfg {
   static constexpr int NSTG = FUSED ? 0 : (B_RES ? 2 : 1);
   static constexpr int RES_BYTES = HAS_RES ? NCH * BOX : 0;
   static constexpr int NRES = HAS_RES ? (B_RES ? 2 : 1) : 0;
-  static constexpr int FIXED = HS * HSTAGE + NSTG * STG_BYTES + NRES * RES_BYTES;
-  static constexpr int BS_FIT = (220 * 1024 - FIXED) / BBLK;
-  static constexpr int BS = B_RES ? 1 : (BS_FIT > 8 ? 8 : BS_FIT);
-  static constexpr int B_BYTES = B_RES ? W_RES_BYTES : BS * BBLK;
+  static constexpr int EPI_BYTES = NSTG * STG_BYTES + NRES * RES_BYTES;
+  static constexpr int HS = (B_RES || 3 * HSTAGE + EPI_BYTES + 2 * GBLK <= 220 * 1024) ? 3 : 2;
+  static constexpr int FIXED = HS * HSTAGE + EPI_BYTES;
+  static constexpr int BS_FIT = (220 * 1024 - FIXED) / GBLK;
+  static constexpr int BS = B_RES ? 1 : (BS_FIT > 4 ? 4 : BS_FIT);
+  static constexpr int B_BYTES = B_RES ? W_RES_BYTES : BS * GBLK;
   static constexpr int OFF_B = HS * HSTAGE;
   static constexpr int OFF_STG = OFF_B + B_BYTES;
   static constexpr int OFF_RES = OFF_STG + NSTG * STG_BYTES;
@@ -271,13 +274,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           hs = 0;
           hph ^= 1;
         }
-        if constexpr (!B_RES) {
+        if constexpr (!B_RES) {  // taps [g*WG, g*WG+WG) of this channel block per ring slot
           const uint16_t* wb = p.w + (size_t)cb * p.ntaps * BN * BK;
-          for (int tap = 0; tap < p.ntaps; ++tap) {
+          for (int t0 = 0; t0 < p.ntaps; t0 += CF::WG) {
+            const uint32_t bytes = (uint32_t)(min(CF::WG, p.ntaps - t0) * CF::BBLK);
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             if (lane == 0) {
-              tc::mbar_arrive_expect_tx(&bfull[bs], CF::BBLK);
-              tc::bulk_g2s(sB0 + bs * CF::BBLK, wb + (size_t)tap * BN * BK, CF::BBLK, &bfull[bs]);
+              tc::mbar_arrive_expect_tx(&bfull[bs], bytes);
+              tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * BN * BK, bytes, &bfull[bs]);
             }
             __syncwarp();
             if (++bs == BS) {
@@ -319,10 +323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     constexpr uint64_t HST16 = CF::HSTAGE >> 4;
     if (elect_one()) {
       const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
-      if constexpr (B_RES) {
-        tc::mbar_wait_nc(&bfull[0], 0);
-        tc::tc_fence_after_nc();
-      }
+      if constexpr (B_RES) tc::mbar_wait_nc(&bfull[0], 0);
       const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)(PLANE2 << 3), (uint32_t)(TT::PW * 16));
       const uint64_t b_desc0 = tc::sdesc_sw128(sB0);
       const int ncb = p.ncb, ngran = p.ngran, total = p.total_tiles;
@@ -330,13 +331,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       uint32_t hph = 0, bph = 0, tl = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-        tc::mbar_wait_nc(&tempty[a], (use & 1) ^ 1);
-        tc::tc_fence_after_nc();
+        tc::mbar_wait_fast(&tempty[a], (use & 1) ^ 1);
+        tc::tc_fence_after_nc();  // TMEM reuse after the epilogue's reads
         const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < ncb; ++cb) {
           const int ksteps = min(8, ngran - cb * 8) >> 1;
-          tc::mbar_wait_nc(&hfull[hs], hph);
-          tc::tc_fence_after_nc();
+          tc::mbar_wait_fast(&hfull[hs], hph);  // TMA data: the mbarrier alone orders it
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
           const uint64_t bcb = b_desc0 + (uint64_t)(cb * NT) * BBLK16;
 #pragma unroll
@@ -345,9 +345,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             if constexpr (B_RES) {
               db = bcb + (uint64_t)tap * BBLK16;
             } else {
-              tc::mbar_wait_nc(&bfull[bs], bph);
-              tc::tc_fence_after_nc();
-              db = b_desc0 + (uint64_t)bs * BBLK16;
+              if (tap % CF::WG == 0) tc::mbar_wait_fast(&bfull[bs], bph);
+              db = b_desc0 + (uint64_t)bs * (CF::GBLK >> 4) + (uint64_t)(tap % CF::WG) * BBLK16;
             }
             const uint64_t at = ah + (uint64_t)TT::aoff(tap);
             const uint32_t dd = d + (uint32_t)(TT::phase(tap) * BN);
@@ -359,10 +358,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             for (int ks = 0; ks < 4; ++ks)
               if (ks < ksteps) tc::mma_f16_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
             if constexpr (!B_RES) {
-              tc::mma_commit_nc(&bempty[bs]);
-              if (++bs == BS) {
-                bs = 0;
-                bph ^= 1;
+              if (tap % CF::WG == CF::WG - 1 || tap == NT - 1) {
+                tc::mma_commit_nc(&bempty[bs]);
+                if (++bs == BS) {
+                  bs = 0;
+                  bph ^= 1;
+                }
               }
             }
           }

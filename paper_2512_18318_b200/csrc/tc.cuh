@@ -136,6 +136,19 @@ __device__ __forceinline__ void mbar_wait_nc(uint64_t* bar, uint32_t parity) {
     if ((++spins & 0xfff) == 0 && clock64() - t0 > 40000000000LL) __trap();
   }
 }
+// Probe first: mbarrier.test_wait costs ~60 cycles of issue latency on the
+// MMA thread, a completed try_wait ~160 (tools/sync_bench.cu), and the tensor
+// pipe idles for every cycle the issuing thread is not issuing.
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity));
+  if (!ok) mbar_wait_nc(bar, parity);
+}
 __device__ __forceinline__ void tc_fence_after_nc() { asm volatile("tcgen05.fence::after_thread_sync;"); }
 __device__ __forceinline__ void mma_f16_nc(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
