@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t box_bytes = (uint32_t)(p.pw * p.ph * 16);
+  tc::griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       }
       __syncwarp();
     }
+    tc::griddep_wait();  // weights are constant; activations come from the previous layer
     // plane g of channel block cb: channels (cb*8 + g)*8 at x0, or channels 0..7 at x0 + g
     const int cstep = p.shift_planes ? 0 : 8, xstep = p.shift_planes ? 1 : 0;
     int hs = 0, bs = 0, rs = 0;
@@ -379,6 +381,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     __syncwarp();
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
+    tc::griddep_wait();
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     constexpr int HC = SPLIT ? BN / 2 : BN;

@@ -337,10 +337,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr int LPS = BK / CC;  // TMA loads per stage
+  tc::griddep_launch();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (whole warp;
     // lane j issues load j of a stage, lane 0 the weights + expect_tx)
+    tc::griddep_wait();  // previous layer's activations complete
     const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
     constexpr uint32_t LOAD_BYTES = BM * CC * 2;
     const int cpt = p.C / CC;  // loads per tap
@@ -416,6 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
+    tc::griddep_wait();  // the output / residual buffers are free / complete
     const int q = warp & 3;               // TMEM lane quadrant this warp may access
     const int half = (warp - 2) >> 2;     // which half of the BN columns
     constexpr bool SPLIT = !FUSED_OUT && BN >= 32;

@@ -334,6 +334,23 @@ struct lsg_gen_s {
 
 static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
 
+// Every layer kernel is launched with programmatic stream serialization so its
+// prologue overlaps the previous layer's tail (tc.cuh griddep_*).
+template <typename P>
+static void launch_pdl(void (*kernel)(P), int grid, int block, int smem, cudaStream_t st, const P& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  LSG_CUDA(cudaLaunchKernelEx(&cfg, kernel, p));
+}
+
 // Persistent launch: one CTA per SM walks the tiles round-robin in the
 // L2-friendly order of decode_tile().
 template <int BN, int CC, bool F, bool H>
@@ -353,7 +370,7 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   p.interleave = 1;
   for (int z = 1; z < r.nphases; ++z) p.interleave &= p.ph[z].mtiles == p.ph[0].mtiles;
   const int grid = std::min(tiles, sms);
-  conv_tc<BN, CC, F, H><<<grid, NUM_THREADS, Cfg<BN>::SMEM, st>>>(p);
+  launch_pdl(conv_tc<BN, CC, F, H>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
 }
 
 // (tile width BN, channel chunk CC, fused output) combinations the Wav2Lip
@@ -413,7 +430,7 @@ static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img;
   const int grid = std::min(hp.total_tiles, sms);
-  conv_halo<BN, MD, F, H, R><<<grid, NUM_THREADS, HaloCfg<BN, MD, F, R>::SMEM, st>>>(hp);
+  launch_pdl(conv_halo<BN, MD, F, H, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R>::SMEM, st, hp);
 }
 
 template <bool H>
