@@ -71,11 +71,10 @@ def make_workload(rank: int, n_streams: int, seconds: int, fps: float, api, gene
         n_video = int(np.ceil(seconds * fps / 1000.0 * 1000.0))
         rng = np.random.default_rng(sid)
         sh = rng.integers(-3, 4, (n_video, 2))
-        v = np.empty((n_video, 96, 96, 3), np.uint8)
-        # seeded +-3 px wobble of the reference crop (mock_face_detect, visual_mocks.cpp:10-22)
-        for f in range(n_video):
-            v[f] = np.roll(ref, (int(sh[f, 0]), int(sh[f, 1])), axis=(0, 1))
-        video.append(v)
+        # seeded +-3 px wobble of the reference crop (mock_face_detect, visual_mocks.cpp:10-22):
+        # frame f = np.roll(ref, sh[f]) taken from the 49 precomputed shifts
+        shifted = np.stack([np.roll(ref, (dy, dx), axis=(0, 1)) for dy in range(-3, 4) for dx in range(-3, 4)])
+        video.append(shifted[(sh[:, 0] + 3) * 7 + (sh[:, 1] + 3)])
     return pcm, video, np.stack(refs)
 
 
@@ -195,6 +194,9 @@ def main():
     ap.add_argument("--batch", type=int, default=512, help="generator frames per launch sequence")
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--paced-seconds", type=int, default=20, help="config-5 paced leg length (0: skip)")
+    ap.add_argument("--paced-streams", type=int, default=256, help="config-5 paced streams over all GPUs")
+    ap.add_argument("--scaled-streams", type=int, default=512, help="segmenter/mel roofline set: streams x 60 s")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -327,12 +329,19 @@ def main():
     e2e = n_e2e * world / (ms_e2e / 1000.0)
     h2d = sum(p.nbytes for p in pcm) + sum(v.nbytes for v in video) + refs.nbytes
     d2h = n_e2e * CROP
+    # ------------------------------------------- config-5 paced (real time)
+    paced = None
+    if args.paced_seconds > 0:
+        paced = paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, fps)
+        ctx.set_stream(torch_stream.cuda_stream)
+    # ------------------------------- segmenter / mel rooflines (scaled set)
+    scaled = scaled_leg(args, local, torch, ctx, torch_stream, api) if args.scaled_streams > 0 else None
     # -------------------------------------------- generator kernel roofline
     B = args.batch
     gen_ms = measure_generator(eng, torch, torch_stream, local, B, reps=10)
     peaks = measured_peaks()
     achieved = FLOPS_PER_FRAME * B / (gen_ms / 1000.0) / 1e12
-    peak = peaks.get("bf16_tflops", 1590.0)
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
     gen_b128_ms = measure_generator(eng, torch, torch_stream, local, 128, reps=10) if B >= 128 else None
     clocks = clk.summary()
     if rank != 0:
@@ -354,14 +363,25 @@ def main():
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "tensor", "kernel": f"generator forward (51 tcgen05 conv launches, batch {B})",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense fp16 == bf16 rate)",
-                     "ms_per_launch_sequence": gen_ms, "flops_per_frame": FLOPS_PER_FRAME, "traffic": None},
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (the forward runs back to back "
+                                    "inside a long step; dense fp16 == bf16 rate)",
+                     "frac_vs_burst_peak": achieved / peaks.get("bf16_tflops", 1590.0),
+                     "ms_per_launch_sequence": gen_ms, "flops_per_frame": FLOPS_PER_FRAME,
+                     "traffic": generator_traffic(B),
+                     "traffic_source": "profiles/r01_gen512_launches.csv: sum of dram__bytes_read+write over the "
+                                       "forward's launches (ncu), bytes per launch sequence of 512 frames"},
         "generator_b128": ({"ms": gen_b128_ms, "frames_per_s": 128 / (gen_b128_ms / 1000.0),
                             "tflops": FLOPS_PER_FRAME * 128 / (gen_b128_ms / 1000.0) / 1e12}
                            if gen_b128_ms else None),
         "clocks": clocks,
         "gpu_launches": launches,
     }
+    if paced:
+        out["paced"] = paced
+        out["p50_segment_latency_ms"] = paced["p50_ms"]
+        out["p99_segment_latency_ms"] = paced["p99_ms"]
+    if scaled:
+        out["stage_rooflines"] = scaled
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
@@ -372,6 +392,155 @@ def main():
     print(json.dumps(out))
     if dist:
         dist.destroy_process_group()
+
+
+def generator_traffic(B):
+    """DRAM bytes of one generator forward from the committed ncu launch list
+    (profiles/r01_gen512_launches.csv, B=512), or None."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_gen512_launches.csv")
+    if B != 512 or not os.path.exists(path):
+        return None
+    rows = list(csv.reader(open(path)))
+    try:
+        i0 = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    except StopIteration:
+        return None
+    h = rows[i0]
+    ik, im, iv = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    tot = 0.0
+    for r in rows[i0 + 1:]:
+        if len(r) > iv and r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum") and "conv_" in r[ik]:
+            tot += float(r[iv].replace(",", ""))
+    return tot or None
+
+
+def cuda_core_peaks():
+    """Measured FP32/FP64 FMA peaks (tools/fma_peak.cu, profiles/r01_cuda_core_peaks.jsonl)."""
+    out = {"fp32": 72.5, "fp64": 34.1, "source": "fallback (tools/fma_peak.cu on B200, round 1)"}
+    path = os.path.join(ROOT, "profiles", "r01_cuda_core_peaks.jsonl")
+    if os.path.exists(path):
+        for line in open(path):
+            try:
+                d = json.loads(line)
+                out[d["dtype"]] = d["tflops"]
+                out["source"] = "profiles/r01_cuda_core_peaks.jsonl (tools/fma_peak.cu)"
+            except (ValueError, KeyError):
+                pass
+    return out
+
+
+def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, fps):
+    """Config 5 paced: this rank's share of --paced-streams released in real
+    time; p50/p99 of (segment's last frame rendered - media time of its cut)
+    over all ranks' segments (paper_2512_18318_b200/paced.py)."""
+    from paper_2512_18318_b200.paced import PacedRunner, summarize
+    per = max(1, args.paced_streams // world)
+    secs = args.paced_seconds
+    pcm, video, refs = make_workload(rank + 1000, per, secs + 1, fps, api, generator)
+    dev = f"cuda:{local}"
+    ms = max(len(p) for p in pcm)
+    pcm_dev = torch.zeros((per, ms), dtype=torch.int16, device=dev)
+    for s, p in enumerate(pcm):
+        pcm_dev[s, :len(p)] = torch.from_numpy(p)
+    mv = max(len(v) for v in video)
+    vid_dev = torch.zeros((per, mv, 96, 96, 3), dtype=torch.uint8, device=dev)
+    for s, v in enumerate(video):
+        vid_dev[s, :len(v)] = torch.from_numpy(v)
+    refs_dev = torch.from_numpy(refs).to(dev)
+    n_samples = [secs * 16000] * per
+    s_run = torch.cuda.Stream(device=local)
+    with torch.cuda.stream(s_run):
+        ctx.set_stream(s_run.cuda_stream)
+        runner = PacedRunner(eng, ctx, torch, per, fps=fps)
+        runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, dev, seconds=2)  # warm-up
+        if dist:
+            dist.barrier()
+        res = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, dev)
+    if dist:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (res.latencies_ms.tolist(), res.decision_ms.tolist(),
+                                          res.render_ms.tolist(), res.frames, res.late_ticks, res.ticks))
+        res.latencies_ms = np.array(sum((g[0] for g in gathered), []))
+        res.decision_ms = np.array(sum((g[1] for g in gathered), []))
+        res.render_ms = np.array(sum((g[2] for g in gathered), []))
+        res.frames = sum(g[3] for g in gathered)
+        res.late_ticks = max(g[4] for g in gathered)
+        res.segments = len(res.latencies_ms)
+    out = summarize(res, per * world, secs)
+    out["streams_per_gpu"] = per
+    out["definition"] = ("latency = wall time the segment's last frame is rendered on the device - wall time media "
+                         "time reached the segment end (audio and 25 fps video released in real time, 40 ms "
+                         "ticks); decision = when the segmenter emitted the cut; render = decision -> rendered")
+    out["rendered_fps_demand"] = res.frames / secs
+    return out
+
+
+def scaled_leg(args, local, torch, ctx, stream, api):
+    """Segmenter (HBM roofline, 2 B/sample) and mel (FP64 roofline, 25,600
+    fp64 + 4,645 fp32 flops per frame) on streams x 60 s of
+    synthetic speech (>> 126 MB L2), device-resident PCM, CUDA events."""
+    from paper_2512_18318_b200.api import MelConfig, MelExtractor, MultiStreamSegmenter, SegmenterConfig
+    S, secs = args.scaled_streams, 60
+    dev = f"cuda:{local}"
+    n = secs * 16000
+    pcm_dev = torch.empty((S, n), dtype=torch.int16, device=dev)
+    for s in range(S):
+        lead, bursts, hz, amp = stream_pattern(5000 + s)
+        pcm_dev[s] = torch.from_numpy(api.synth_pattern(lead, bursts, hz, amp, secs * 1000)[:n])
+    seg = MultiStreamSegmenter(SegmenterConfig(), S, n, ctx=ctx)
+    mel = MelExtractor(MelConfig(), max_frames=1 << 22, ctx=ctx)
+    base = pcm_dev.data_ptr()
+    chunks = [(base + s * n * 2, n) for s in range(S)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    seg_ms, mel_ms, cuts = [], [], []
+    with torch.cuda.stream(stream):
+        ctx.set_stream(stream.cuda_stream)
+        for rep in range(4):
+            lib = ctx.lib
+            lib.call("lsg_seg_reset", seg.h)
+            flush.zero_()
+            e0.record(stream)
+            seg.push(list(range(S)), chunks, [0] * S, on_device=True)
+            seg.finish(list(range(S)))
+            e1.record(stream)
+            stream.synchronize()
+            cuts = seg.take_all_cuts()
+            if rep:
+                seg_ms.append(e0.elapsed_time(e1))
+        N, hop = 1024, 256
+        offs = [c.stream * n + c.sample_off for c in cuts]
+        lens = [c.sample_len for c in cuts]
+        frames = [0 if ln < N else 1 + (ln - N) // hop for ln in lens]
+        row0 = list(np.cumsum([0] + frames[:-1]))
+        rows = torch.empty((max(sum(frames), 1), 80), dtype=torch.float32, device=dev)
+        for rep in range(4):
+            flush.zero_()
+            e0.record(stream)
+            mel.batch_device(base, offs, lens, rows.data_ptr(), row0)
+            e1.record(stream)
+            stream.synchronize()
+            if rep:
+                mel_ms.append(e0.elapsed_time(e1))
+    peaks, cc = measured_peaks(), cuda_core_peaks()
+    t_seg = float(np.median(seg_ms))
+    nbytes = S * n * 2
+    F = int(sum(frames))
+    t_mel = float(np.median(mel_ms))
+    t_roof = F * 25600 / (cc["fp64"] * 1e12) + F * 4645 / (cc["fp32"] * 1e12)
+    return {
+        "set": f"{S} streams x {secs} s (16 kHz int16, {nbytes / 1e6:.0f} MB, > L2), L2 flushed before each timed run",
+        "segmenter": {"bound": "hbm", "ms": t_seg, "bytes": nbytes, "achieved": nbytes / (t_seg / 1e3) / 1e9,
+                      "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
+                      "frac": nbytes / (t_seg / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0), "segments": len(cuts),
+                      "timed": "lsg_seg_push + lsg_seg_finish over all streams (device events, includes the cut "
+                               "readback sync)"},
+        "mel": {"bound": "fp64", "ms": t_mel, "frames": F, "flops_fp64_per_frame": 25600,
+                "flops_fp32_per_frame": 4645, "achieved_fp64_tflops": F * 25600 / (t_mel / 1e3) / 1e12,
+                "peak_fp64_tflops": cc["fp64"], "peak_source": cc["source"], "t_roof_ms": t_roof * 1e3,
+                "frac": t_roof * 1e3 / t_mel, "timed": "lsg_mel_compute_batch over every segment of the set"},
+    }
 
 
 def measure_generator(eng, torch, stream, local, B, reps=10):
