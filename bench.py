@@ -59,11 +59,14 @@ def stream_pattern(seed: int):
     return lead, bursts, hz, 0.2 + 0.1 * (seed % 5)
 
 
-def make_workload(rank: int, n_streams: int, seconds: int, fps: float, api, generator):
-    """Host inputs of one rank: PCM, per-frame face crops, reference crops."""
+def make_workload(rank: int, n_streams: int, seconds: int, fps: float, api, generator, world: int = 1,
+                  seed_base: int = 0):
+    """Host inputs of one rank: PCM, per-frame face crops, reference crops of
+    the streams it owns (global stream s lives on GPU s mod world)."""
+    from paper_2512_18318_b200.shard import streams_for_rank
     pcm, video, refs = [], [], []
-    for i in range(n_streams):
-        sid = rank * n_streams + i
+    for sid in streams_for_rank(n_streams, rank, world):
+        sid += seed_base
         lead, bursts, hz, amp = stream_pattern(sid + 1)
         pcm.append(api.synth_pattern(lead, bursts, hz, amp, seconds * 1000))
         ref = generator.synthetic_face(10_000 + sid)
@@ -252,7 +255,7 @@ def main():
     eng = generator.LipsyncEngine(weights, max_batch=args.batch, ctx=ctx, precision=prec)
     pipe = Pipeline(PipelineConfig(args.streams, args.seconds * 1000, fps, 50, args.batch, True), eng, ctx=ctx)
 
-    pcm, video, refs = make_workload(rank, args.streams, args.seconds, fps, api, generator)
+    pcm, video, refs = make_workload(rank, args.streams, args.seconds, fps, api, generator, world)
     # pinned host copies (e2e leg) and device-resident copies (value leg)
     lib = ctx.lib
     import ctypes as C
@@ -288,11 +291,8 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(x):
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        from paper_2512_18318_b200.shard import max_over_ranks as mor
+        return mor(x, dist, device=f"cuda:{local}")
 
     for _ in range(max(args.warmup, 3)):
         n_frames, st = step_device()
@@ -437,7 +437,7 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
     from paper_2512_18318_b200.paced import PacedRunner, summarize
     per = max(1, args.paced_streams // world)
     secs = args.paced_seconds
-    pcm, video, refs = make_workload(rank + 1000, per, secs + 1, fps, api, generator)
+    pcm, video, refs = make_workload(rank, per, secs + 1, fps, api, generator, world, seed_base=1000)
     dev = f"cuda:{local}"
     ms = max(len(p) for p in pcm)
     pcm_dev = torch.zeros((per, ms), dtype=torch.int16, device=dev)
@@ -458,14 +458,10 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
             dist.barrier()
         res = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, dev)
     if dist:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, (res.latencies_ms.tolist(), res.decision_ms.tolist(),
-                                          res.render_ms.tolist(), res.frames, res.late_ticks, res.ticks))
-        res.latencies_ms = np.array(sum((g[0] for g in gathered), []))
-        res.decision_ms = np.array(sum((g[1] for g in gathered), []))
-        res.render_ms = np.array(sum((g[2] for g in gathered), []))
-        res.frames = sum(g[3] for g in gathered)
-        res.late_ticks = max(g[4] for g in gathered)
+        from paper_2512_18318_b200.shard import gather_arrays
+        res.latencies_ms, res.decision_ms, res.render_ms, fr, lt = gather_arrays(
+            [res.latencies_ms, res.decision_ms, res.render_ms, [res.frames], [res.late_ticks]], dist, world)
+        res.frames, res.late_ticks = int(fr.sum()), int(lt.max())
         res.segments = len(res.latencies_ms)
     out = summarize(res, per * world, secs)
     out["streams_per_gpu"] = per
