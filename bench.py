@@ -514,7 +514,8 @@ def scaled_leg(args, local, torch, ctx, stream, api):
         for rep in range(4):
             flush.zero_()
             e0.record(stream)
-            mel.batch_device(base, offs, lens, rows.data_ptr(), row0)
+            for a in range(0, len(offs), 4096):  # lsg_mel_compute_batch takes <= 4096 segments per call
+                mel.batch_device(base, offs[a:a + 4096], lens[a:a + 4096], rows.data_ptr(), row0[a:a + 4096])
             e1.record(stream)
             stream.synchronize()
             if rep:

@@ -40,58 +40,35 @@ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
 __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return {a.x + b.x, a.y + b.y}; }
 __device__ __forceinline__ cplx csub(cplx a, cplx b) { return {a.x - b.x, a.y - b.y}; }
 
-struct Tables {
-  const double* window;   // [N]
-  const cplx* tw;         // [N/2] W_{N/2}^j  (fast path: W512^j)
-  const cplx* tw_half;    // [N/2+1] W_N^k for the real split
-  const int32_t* band_lo; // [n_mels] first non-zero bin
-  const int32_t* band_n;  // [n_mels] non-zeros
-  const int32_t* band_off;// [n_mels] offset into weights
-  const double* weights;  // [nnz]
-};
-
-// In-register 16-point DFT (decimation in time), twiddles W16^j = tw[32 j].
-__device__ __forceinline__ void dft16(cplx (&v)[16], const cplx* __restrict__ tw512) {
-  // bit reversal permutation of 4 bits
-  const int rev[16] = {0, 8, 4, 12, 2, 10, 6, 14, 1, 9, 5, 13, 3, 11, 7, 15};
-  cplx a[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = v[rev[i]];
-#pragma unroll
-  for (int len = 2; len <= 16; len <<= 1) {
-#pragma unroll
-    for (int i = 0; i < 16; i += len) {
-#pragma unroll
-      for (int k = 0; k < len / 2; ++k) {
-        const int e = k * (16 / len);  // W16^e
-        cplx w;
-        if (e == 0) w = {1.0, 0.0};
-        else if (e == 4) w = {0.0, -1.0};
-        else {
-          const double2 d = __ldg(reinterpret_cast<const double2*>(tw512) + 32 * e);
-          w = {d.x, d.y};
-        }
-        cplx u = a[i + k];
-        cplx t = (e == 0) ? a[i + k + len / 2] : (e == 4 ? cplx{a[i + k + len / 2].y, -a[i + k + len / 2].x} : cmul(a[i + k + len / 2], w));
-        a[i + k] = cadd(u, t);
-        a[i + k + len / 2] = csub(u, t);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = a[i];
-}
-
 __device__ __forceinline__ cplx ld_tw(const cplx* t, int i) {
   double2 d = __ldg(reinterpret_cast<const double2*>(t) + i);
   return {d.x, d.y};
 }
 
-constexpr int MEL_WARPS = 8;
+constexpr int MEL_WARPS = 16;                      // one CTA per SM: 16 warps x 128 registers
 constexpr int S_STRIDE = 33;                       // padded row (complex) for the transpose
-constexpr int S_CPLX = 16 * S_STRIDE;              // 528 complex per warp
-constexpr int P_DBL = 516;                         // 513 bins, padded
-constexpr size_t SMEM_PER_WARP = S_CPLX * 16 + P_DBL * 8;
+constexpr int S_CPLX = 16 * S_STRIDE;              // 528 complex per warp (the power spectrum aliases it)
+constexpr size_t SMEM_PER_WARP = S_CPLX * 16;
+
+// Block-shared tables of the 1024 fast path (staged once per CTA, so the
+// per-frame loop never reads tables through L1 with divergent addresses).
+struct FastTables {
+  const double* window;   // [1024]
+  const cplx* tw;         // [512] W512^j
+  const cplx* tw_half;    // [513] W1024^k
+  const int32_t* band_lo; // [M]
+  const int32_t* band_n;  // [M]
+  const double* fbq;      // [maxnb][M]: weight q of band m (0 past the band)
+  int maxnb;
+};
+__host__ __device__ constexpr size_t fast_table_bytes(int M, int maxnb) {
+  return 1024 * 8                 // window
+         + 16 * 32 * 16           // step-1 twiddles per (k1, lane)
+         + 32 * 16                // W512^(16 c), c < 32 (W32^c; W16^e = W32^(2e))
+         + 264 * 16               // real-split twiddles k <= 256
+         + (size_t)maxnb * M * 8  // filterbank, q-major
+         + (size_t)M * 8;         // band lo | n
+}
 
 struct Batch {
   const int16_t* pcm;
@@ -115,15 +92,92 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ f0, int n, i
   return lo;
 }
 
-__global__ void __launch_bounds__(MEL_WARPS * 32)
-mel1024_kernel(Batch B, Tables T) {
+// In-register 16-point DFT (decimation in time); w32[c] = W512^(16 c), so
+// W16^e = w32[2 e] (shared memory, broadcast reads).
+__host__ __device__ constexpr int bitrev4(int i) {
+  return ((i & 1) << 3) | ((i & 2) << 1) | ((i & 4) >> 1) | ((i & 8) >> 3);
+}
+// One radix-2 stage of the 16-point DIT, LEN a compile-time constant so every
+// loop unrolls and the arrays stay in registers.
+template <int LEN>
+__device__ __forceinline__ void dit_stage(cplx (&a)[16], const cplx* __restrict__ w32) {
+#pragma unroll
+  for (int i = 0; i < 16; i += LEN) {
+#pragma unroll
+    for (int k = 0; k < LEN / 2; ++k) {
+      constexpr int step = 16 / LEN;
+      const int e = k * step;  // W16^e
+      const cplx u = a[i + k];
+      cplx t;
+      if (e == 0) t = a[i + k + LEN / 2];
+      else if (e == 4) t = cplx{a[i + k + LEN / 2].y, -a[i + k + LEN / 2].x};
+      else t = cmul(a[i + k + LEN / 2], w32[2 * e]);
+      a[i + k] = cadd(u, t);
+      a[i + k + LEN / 2] = csub(u, t);
+    }
+  }
+}
+__device__ __forceinline__ void dft16s(cplx (&v)[16], const cplx* __restrict__ w32) {
+  cplx a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = v[bitrev4(i)];
+  dit_stage<2>(a, w32);
+  dit_stage<4>(a, w32);
+  dit_stage<8>(a, w32);
+  dit_stage<16>(a, w32);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = a[i];
+}
+
+__global__ void __launch_bounds__(MEL_WARPS * 32, 1)
+mel1024_kernel(Batch B, FastTables T) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  cplx* S = reinterpret_cast<cplx*>(smem + warp * SMEM_PER_WARP);
-  double* P = reinterpret_cast<double*>(smem + warp * SMEM_PER_WARP + S_CPLX * 16);
+  const int M = B.n_mels, maxnb = T.maxnb;
+  // ---- block tables
+  double* s_win = reinterpret_cast<double*>(smem);
+  cplx* s_tw1 = reinterpret_cast<cplx*>(s_win + 1024);   // [16][32]
+  cplx* s_w32 = s_tw1 + 16 * 32;                         // [32]
+  cplx* s_twh = s_w32 + 32;                              // [264]
+  double* s_fbq = reinterpret_cast<double*>(s_twh + 264);  // [maxnb][M]
+  int32_t* s_blo = reinterpret_cast<int32_t*>(s_fbq + (size_t)maxnb * M);
+  int32_t* s_bn = s_blo + M;
+  cplx* S = reinterpret_cast<cplx*>(smem + fast_table_bytes(M, maxnb)) + warp * S_CPLX;
+  double* P = reinterpret_cast<double*>(S);  // |X|^2 after the spectrum has been read
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_win[i] = __ldg(T.window + i);
+  for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {
+    const int k1 = i >> 5, l = i & 31;
+    const double2 d = __ldg(reinterpret_cast<const double2*>(T.tw) + ((l * k1) & 511));
+    s_tw1[i] = {d.x, d.y};
+  }
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) {
+    const double2 d = __ldg(reinterpret_cast<const double2*>(T.tw) + 16 * i);
+    s_w32[i] = {d.x, d.y};
+  }
+  for (int i = threadIdx.x; i <= 256; i += blockDim.x) {
+    const double2 d = __ldg(reinterpret_cast<const double2*>(T.tw_half) + i);
+    s_twh[i] = {d.x, d.y};
+  }
+  for (int i = threadIdx.x; i < maxnb * M; i += blockDim.x) s_fbq[i] = __ldg(T.fbq + i);
+  for (int i = threadIdx.x; i < M; i += blockDim.x) {
+    s_blo[i] = __ldg(T.band_lo + i);
+    s_bn[i] = __ldg(T.band_n + i);
+  }
+  __syncthreads();
+  // Each warp takes a contiguous run of frames: one binary search for the
+  // run's first segment, then a linear advance, and consecutive frames of a
+  // segment share 75% of their PCM through L1.
   const int64_t nwarps = (int64_t)gridDim.x * MEL_WARPS;
-  for (int64_t f = (int64_t)blockIdx.x * MEL_WARPS + warp; f < B.total_frames; f += nwarps) {
-    const int s = find_seg(B.seg_frame0, B.n_seg, f);
+  const int64_t wid = (int64_t)blockIdx.x * MEL_WARPS + warp;
+  const int64_t per = (B.total_frames + nwarps - 1) / nwarps;
+  const int64_t f_beg = wid * per, f_end = min(B.total_frames, f_beg + per);
+  int s = f_beg < f_end ? find_seg(B.seg_frame0, B.n_seg, f_beg) : 0;
+  int64_t s_next = __ldg(B.seg_frame0 + s + 1);
+  for (int64_t f = f_beg; f < f_end; ++f) {
+    while (f >= s_next) {  // next non-empty segment
+      ++s;
+      s_next = __ldg(B.seg_frame0 + s + 1);
+    }
     const int64_t j = f - __ldg(B.seg_frame0 + s);
     const int16_t* x = B.pcm + __ldg(B.seg_pcm_off + s) + j * B.hop;
     // ---- step 1: lane m2 = lane; z[32*m1 + m2] = (x[64 m1 + 2 m2], x[64 m1 + 2 m2 + 1])
@@ -132,15 +186,14 @@ mel1024_kernel(Batch B, Tables T) {
     for (int m1 = 0; m1 < 16; ++m1) {
       const int i0 = 64 * m1 + 2 * lane;
       const double s0 = (double)__ldg(x + i0), s1 = (double)__ldg(x + i0 + 1);
-      v[m1].x = __dmul_rn(s0 * (1.0 / 32768.0), __ldg(T.window + i0));
-      v[m1].y = __dmul_rn(s1 * (1.0 / 32768.0), __ldg(T.window + i0 + 1));
+      v[m1].x = __dmul_rn(s0 * (1.0 / 32768.0), s_win[i0]);
+      v[m1].y = __dmul_rn(s1 * (1.0 / 32768.0), s_win[i0 + 1]);
     }
-    dft16(v, T.tw);
-    __syncwarp();
+    dft16s(v, s_w32);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) {
       cplx y = v[k1];
-      if (k1) y = cmul(y, ld_tw(T.tw, (lane * k1) & 511));
+      if (k1) y = cmul(y, s_tw1[k1 * 32 + lane]);  // W512^(lane k1)
       S[k1 * S_STRIDE + lane] = y;
     }
     __syncwarp();
@@ -148,10 +201,10 @@ mel1024_kernel(Batch B, Tables T) {
     const int k1 = lane & 15, b = lane >> 4;
 #pragma unroll
     for (int a = 0; a < 16; ++a) v[a] = S[k1 * S_STRIDE + 2 * a + b];
-    dft16(v, T.tw);
+    dft16s(v, s_w32);
     if (b) {
 #pragma unroll
-      for (int c = 1; c < 16; ++c) v[c] = cmul(v[c], ld_tw(T.tw, 16 * c));  // W32^c
+      for (int c = 1; c < 16; ++c) v[c] = cmul(v[c], s_w32[c]);  // W32^c
     }
     __syncwarp();
 #pragma unroll
@@ -164,31 +217,57 @@ mel1024_kernel(Batch B, Tables T) {
       S[k1 + 16 * c + 256 * b] = z;  // Z[k], k = k1 + 16c + 256b
     }
     __syncwarp();
-    // ---- step 3: real split, P[k] = |X[k]|^2 (mel.cpp:118)
-    for (int k = lane; k <= 256; k += 32) {
-      const cplx zk = S[k & 511];
-      const cplx zn = S[(512 - k) & 511];
-      // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i);  X[k] = E + W^k O, X[512-k] = conj(E - W^k O)
-      const cplx E = {0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y)};
-      const cplx O = {0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x)};
-      const cplx wo = cmul(ld_tw(T.tw_half, k), O);
-      const cplx X1 = cadd(E, wo);
-      const cplx X2 = csub(E, wo);  // conj(X[512-k]); |.|^2 is the same
-      P[k] = __dadd_rn(__dmul_rn(X1.x, X1.x), __dmul_rn(X1.y, X1.y));
-      P[512 - k] = __dadd_rn(__dmul_rn(X2.x, X2.x), __dmul_rn(X2.y, X2.y));
+    // ---- step 3: real split, P[k] = |X[k]|^2 (mel.cpp:118).  The lane's
+    // spectrum pairs go to registers first: P overwrites S in place.
+    double pk[9], pn[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const int k = lane + 32 * i;
+      if (k <= 256) {
+        const cplx zk = S[k & 511];
+        const cplx zn = S[(512 - k) & 511];
+        // E = (Zk + conj Zn)/2, O = (Zk - conj Zn)/(2i);  X[k] = E + W^k O, X[512-k] = conj(E - W^k O)
+        const cplx E = {0.5 * (zk.x + zn.x), 0.5 * (zk.y - zn.y)};
+        const cplx O = {0.5 * (zk.y + zn.y), -0.5 * (zk.x - zn.x)};
+        const cplx wo = cmul(s_twh[k], O);
+        const cplx X1 = cadd(E, wo);
+        const cplx X2 = csub(E, wo);  // conj(X[512-k]); |.|^2 is the same
+        pk[i] = __dadd_rn(__dmul_rn(X1.x, X1.x), __dmul_rn(X1.y, X1.y));
+        pn[i] = __dadd_rn(__dmul_rn(X2.x, X2.x), __dmul_rn(X2.y, X2.y));
+      }
     }
     __syncwarp();
-    // ---- step 4: sparse filterbank + log (mel.cpp:119-124)
-    float* orow = B.out + (__ldg(B.seg_out_row + s) + j) * B.n_mels;
-    for (int m = lane; m < B.n_mels; m += 32) {
-      const int lo = __ldg(T.band_lo + m), nb = __ldg(T.band_n + m), off = __ldg(T.band_off + m);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const int k = lane + 32 * i;
+      if (k <= 256) {
+        P[k] = pk[i];
+        P[512 - k] = pn[i];
+      }
+    }
+    __syncwarp();
+    // ---- step 4: sparse filterbank + log (mel.cpp:119-124), bin order, unfused
+    float* orow = B.out + (__ldg(B.seg_out_row + s) + j) * M;
+    for (int m = lane; m < M; m += 32) {
+      const int lo = s_blo[m], nb = s_bn[m];
       double acc = 0.0;
-      for (int q = 0; q < nb; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(T.weights + off + q), P[lo + q]));
+      for (int q = 0; q < nb; ++q) acc = __dadd_rn(acc, __dmul_rn(s_fbq[q * M + m], P[lo + q]));
       orow[m] = (float)log(acc > 1e-10 ? acc : 1e-10);
     }
     __syncwarp();
   }
 }
+
+// Generic-path tables
+struct Tables {
+  const double* window;   // [N]
+  const cplx* tw;         // [N/2] W_N^j
+  const cplx* tw_half;    // [N/2+1] W_N^k
+  const int32_t* band_lo; // [n_mels] first non-zero bin
+  const int32_t* band_n;  // [n_mels] non-zeros
+  const int32_t* band_off;// [n_mels] offset into weights
+  const double* weights;  // [nnz]
+};
 
 // Generic power-of-two path: one CTA per frame, radix-2 in shared memory.
 __global__ void mel_generic_kernel(Batch B, Tables T, int N) {
@@ -270,6 +349,11 @@ struct lsg_mel_s {
   DevBuf<int16_t> pcm_stage;
   DevBuf<float> out_stage;
   Tables T{};
+  // fast path (fft 1024): q-major filterbank + block-shared tables
+  DevBuf<double> fbq;
+  FastTables FT{};
+  bool fast = false;
+  size_t fast_smem = 0;
 };
 
 static void launch(lsg_mel h, const int16_t* pcm, int32_t n_seg, int64_t total_frames, float* out) {
@@ -286,10 +370,9 @@ static void launch(lsg_mel h, const int16_t* pcm, int32_t n_seg, int64_t total_f
   B.total_frames = total_frames;
   B.out = out;
   const int N = h->cfg.fft_size;
-  if (N == 1024) {
-    const size_t smem = MEL_WARPS * SMEM_PER_WARP;
-    const int64_t blocks = std::min<int64_t>(ceil_div(total_frames, MEL_WARPS), (int64_t)ctx->sm_count * 2);
-    mel1024_kernel<<<(unsigned)blocks, MEL_WARPS * 32, smem, ctx->stream>>>(B, h->T);
+  if (h->fast) {
+    const int64_t blocks = std::min<int64_t>(ceil_div(total_frames, MEL_WARPS), (int64_t)ctx->sm_count);
+    mel1024_kernel<<<(unsigned)blocks, MEL_WARPS * 32, h->fast_smem, ctx->stream>>>(B, h->FT);
   } else {
     const size_t smem = (size_t)N * 16 + (size_t)(N / 2 + 1) * 8;
     const int64_t blocks = std::min<int64_t>(total_frames, (int64_t)ctx->sm_count * 4);
@@ -366,10 +449,16 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
           for (int b = first; b <= last; ++b) wts.push_back(row[b]);
         }
       }
+      // fast path (fft 1024): q-major filterbank [maxnb][M]; its block tables
+      // + per-warp buffers must fit in shared memory, else the generic kernel
+      int maxnb = 0;
+      for (int m = 0; m < M; ++m) maxnb = std::max(maxnb, bn[m]);
+      h->fast_smem = fast_table_bytes(M, maxnb) + MEL_WARPS * SMEM_PER_WARP;
+      h->fast = N == 1024 && h->fast_smem <= 227 * 1024;
       // twiddles: fast path W512^j, generic path W_N^j; real split W_N^k
       const int half = N / 2;
       std::vector<cplx> tw, twh(half + 1);
-      if (N == 1024) {
+      if (h->fast) {
         tw.resize(512);
         for (int j = 0; j < 512; ++j) tw[j] = {std::cos(-2.0 * kPi * j / 512), std::sin(-2.0 * kPi * j / 512)};
       } else {
@@ -404,9 +493,15 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
       const int64_t max_samples = (max_frames - 1) * cfg->hop + N;
       h->pcm_stage.alloc((size_t)max_samples);
       h->out_stage.alloc((size_t)max_frames * M);
-      if (N == 1024) {
+      if (h->fast) {
+        std::vector<double> fbq((size_t)std::max(maxnb, 1) * M, 0.0);
+        for (int m = 0; m < M; ++m)
+          for (int q = 0; q < bn[m]; ++q) fbq[(size_t)q * M + m] = wts[(size_t)boff[m] + q];
+        h->fbq.alloc(fbq.size());
+        LSG_CUDA(cudaMemcpy(h->fbq.p, fbq.data(), fbq.size() * 8, cudaMemcpyHostToDevice));
+        h->FT = {h->window.p, h->tw.p, h->tw_half.p, h->band.p, h->band.p + M, h->fbq.p, maxnb};
         LSG_CUDA(cudaFuncSetAttribute(mel1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(MEL_WARPS * SMEM_PER_WARP)));
+                                      (int)h->fast_smem));
       } else {
         LSG_CUDA(cudaFuncSetAttribute(mel_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)((size_t)N * 16 + (size_t)(N / 2 + 1) * 8)));

@@ -79,15 +79,24 @@ struct alignas(16) FrameStat {
 constexpr int K1_WARPS = 8;
 constexpr int K1_FPW = 2;  // frames per warp per block
 
-__device__ __forceinline__ void acc8(int4 v, long long& ss, int& mx) {
+// 8 samples: squares summed pairwise in uint32 (each pair <= 2^31, exact),
+// one 64-bit add per pair; max |s| from packed int16 max/min (exact for
+// -32768, whose magnitude does not fit int16).
+__device__ __forceinline__ void acc8(int4 v, unsigned long long& ss, unsigned& pmax, unsigned& pmin) {
   const int w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    int lo = (int)(int16_t)(w[k] & 0xffff);
-    int hi = w[k] >> 16;
-    ss += (long long)(lo * lo) + (long long)(hi * hi);
-    mx = max(mx, max(abs(lo), abs(hi)));
+    const int lo = (int)(int16_t)(w[k] & 0xffff);
+    const int hi = w[k] >> 16;
+    ss += (unsigned)(lo * lo) + (unsigned)(hi * hi);
+    pmax = __vmaxs2(pmax, (unsigned)w[k]);
+    pmin = __vmins2(pmin, (unsigned)w[k]);
   }
+}
+__device__ __forceinline__ int absmax_packed(unsigned pmax, unsigned pmin) {
+  const int mx = max((int)(int16_t)(pmax & 0xffff), (int)pmax >> 16);
+  const int mn = min((int)(int16_t)(pmin & 0xffff), (int)pmin >> 16);
+  return max(mx, -mn);
 }
 
 __global__ void __launch_bounds__(K1_WARPS * 32)
@@ -111,7 +120,11 @@ seg_frame_stats(const Chunk* __restrict__ chunks, const int16_t* __restrict__ ca
       const int64_t f = f0 + j;
       if (f >= c.nframes) break;
       const int4* p = reinterpret_cast<const int4*>(c.pcm + f * fs);
-      for (int q = lane; q < nv; q += 32) acc8(__ldg(p + q), ss[j], mx[j]);
+      unsigned long long s2 = 0;
+      unsigned pmax = 0x80008000u, pmin = 0x7fff7fffu;
+      for (int q = lane; q < nv; q += 32) acc8(__ldg(p + q), s2, pmax, pmin);
+      ss[j] = (long long)s2;
+      mx[j] = absmax_packed(pmax, pmin);
     }
   } else {
     const int16_t* cs = carry + (int64_t)c.stream * fs;
@@ -416,7 +429,24 @@ seg_scan(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, 
     __syncthreads();
     if (tid == 0) {
       if (P.peak_mode == 0) {
-        for (int i = 0; i < n; ++i) {
+        // the chain is DMUL -> max per frame; frame maxima come in 8 at a
+        // time so shared-memory latency stays off it (n is a multiple of 8
+        // except in the last tile)
+        int i = 0;
+        for (; i + 8 <= n; i += 8) {
+          double m[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m[k] = s_peak[i + k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            peak = __dmul_rn(peak, P.decay);
+            peak = m[k] > peak ? m[k] : peak;
+            m[k] = peak;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) s_peak[i + k] = m[k];
+        }
+        for (; i < n; ++i) {
           peak = __dmul_rn(peak, P.decay);
           const double fm = s_peak[i];
           peak = fm > peak ? fm : peak;
@@ -518,32 +548,61 @@ __global__ void seg_finish(const int32_t* __restrict__ streams, const int64_t* _
   S->m_eos += 1;
 }
 
-// Compacts the touched streams' cuts + state (+flags) into mapped host memory.
-__global__ void seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
-                            const lsg_cut* __restrict__ cuts_all, const uint32_t* __restrict__ flags_all,
-                            Params P, DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts,
-                            uint32_t* h_flags, int cut_cap_total) {
-  __shared__ int s_off[1025];
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int i = 0; i < n; ++i) {
-      s_off[i] = acc;
-      acc += st[streams[i]].n_cuts;
-    }
-    s_off[n] = acc;
-  }
+// Compacts the touched streams' cuts + state (+flags) into mapped host
+// memory: block-wide scan of the per-stream cut counts, then one warp per
+// stream copying its cuts as coalesced 16-byte words (lsg_cut is 48 B).
+constexpr int COLLECT_THREADS = 1024;
+constexpr int COLLECT_MAX = 4096;  // streams per push / finish
+__global__ void __launch_bounds__(COLLECT_THREADS)
+seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
+            const lsg_cut* __restrict__ cuts_all, const uint32_t* __restrict__ flags_all, Params P,
+            DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts, uint32_t* h_flags, int cut_cap_total) {
+  __shared__ int s_off[COLLECT_MAX + 1];
+  __shared__ int s_warp[COLLECT_THREADS / 32];
+  __shared__ int s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i <= n; i += blockDim.x) h_offsets[i] = s_off[i];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) h_state[i] = st[streams[i]];
-  for (int i = 0; i < n; ++i) {
+  for (int base = 0; base < n; base += COLLECT_THREADS) {
+    const int i = base + tid;
+    const int v = i < n ? st[streams[i]].n_cuts : 0;
+    int x = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int excl = s_carry + (warp ? s_warp[warp - 1] : 0) + x - v;
+    if (i < n) s_off[i] = excl;
+    __syncthreads();
+    if (tid == 0) s_carry += s_warp[31];
+    __syncthreads();
+  }
+  if (tid == 0) s_off[n] = s_carry;
+  __syncthreads();
+  for (int i = tid; i <= n; i += COLLECT_THREADS) h_offsets[i] = s_off[i];
+  for (int i = tid; i < n; i += COLLECT_THREADS) h_state[i] = st[streams[i]];
+  for (int i = warp; i < n; i += COLLECT_THREADS / 32) {
     const int s = streams[i];
-    const int k = st[s].n_cuts;
-    for (int j = threadIdx.x; j < k; j += blockDim.x)
-      if (s_off[i] + j < cut_cap_total) h_cuts[s_off[i] + j] = cuts_all[(int64_t)s * P.cut_cap + j];
+    const int k = min(st[s].n_cuts, max(0, cut_cap_total - s_off[i]));
+    const uint4* src = reinterpret_cast<const uint4*>(cuts_all + (int64_t)s * P.cut_cap);
+    uint4* dst = reinterpret_cast<uint4*>(h_cuts + s_off[i]);
+    for (int u = lane; u < k * 3; u += 32) dst[u] = src[u];
     if (P.flags_only) {
       const int nw = (st[s].n_flag_frames + 31) >> 5;
-      for (int j = threadIdx.x; j < nw; j += blockDim.x)
-        h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
+      for (int j = lane; j < nw; j += 32) h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
     }
   }
 }
@@ -565,7 +624,7 @@ struct StreamHost {
   lsg_seg_metrics metrics{};
 };
 
-constexpr int kMaxCollect = 1024;  // streams per push call handled by one collect launch
+constexpr int kMaxCollect = seg::COLLECT_MAX;  // streams per push call handled by one collect launch
 
 struct lsg_seg_s {
   Ctx* ctx = nullptr;
@@ -619,7 +678,7 @@ static void validate_cfg(const lsg_seg_cfg* c) {
 // Runs collect for the listed streams, synchronises, and distributes results.
 static void collect(lsg_seg h, int n, bool finishing) {
   Ctx* ctx = h->ctx;
-  seg_collect<<<1, 256, 0, ctx->stream>>>(h->streams_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
+  seg_collect<<<1, COLLECT_THREADS, 0, ctx->stream>>>(h->streams_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
                                           h->h_state, h->h_off, h->h_cuts, h->h_flags,
                                           (int)h->h_cut_cap);
   LSG_LAUNCHED(ctx);
