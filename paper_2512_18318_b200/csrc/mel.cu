@@ -190,11 +190,18 @@ mel1024_kernel(Batch B, FastTables T) {
       v[m1].y = __dmul_rn(s1 * (1.0 / 32768.0), s_win[i0 + 1]);
     }
     dft16s(v, s_w32);
+    {
+      // W512^(lane k1) by recurrence from W512^lane (mel.cpp:46-70 builds its
+      // twiddles by recurrence too); re-anchored from the table at k1 = 8
+      const cplx w1 = s_tw1[32 + lane];
+      cplx w = w1;
+      S[lane] = v[0];
 #pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) {
-      cplx y = v[k1];
-      if (k1) y = cmul(y, s_tw1[k1 * 32 + lane]);  // W512^(lane k1)
-      S[k1 * S_STRIDE + lane] = y;
+      for (int k1 = 1; k1 < 16; ++k1) {
+        if (k1 == 8) w = s_tw1[8 * 32 + lane];
+        S[k1 * S_STRIDE + lane] = cmul(v[k1], w);
+        w = cmul(w, w1);
+      }
     }
     __syncwarp();
     // ---- step 2: lane = k1 + 16 b; a = 0..15 over m2 = 2a + b
