@@ -74,9 +74,19 @@ struct lsg_pipe_s {
   PinnedBuf<int32_t> h_chunk_row, h_ref_idx;
   PinnedBuf<int64_t> h_frame_idx, h_pad_tab;
   cudaEvent_t ev[5] = {};
+  // copy/compute overlap: video H2D per stream and rendered frames D2H per
+  // generator batch run on their own streams, ordered by events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev_vid, ev_out;
+  cudaEvent_t ev_start = nullptr;
   ~lsg_pipe_s() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ev_vid) cudaEventDestroy(e);
+    for (auto& e : ev_out) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
     if (seg) lsg_seg_destroy(seg);
     if (mel) lsg_mel_destroy(mel);
   }
@@ -117,6 +127,11 @@ lsg_status lsg_pipe_create(lsg_ctx ctx, const lsg_pipe_cfg* cfg, const lsg_seg_c
       h->video.alloc((size_t)cfg->n_streams * h->max_video * kCrop);
       h->refs.alloc((size_t)cfg->n_streams * kCrop);
       for (auto& e : h->ev) LSG_CUDA(cudaEventCreate(&e));
+      LSG_CUDA(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+      LSG_CUDA(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+      LSG_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+      h->ev_vid.resize((size_t)cfg->n_streams);
+      for (auto& e : h->ev_vid) LSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     } catch (...) {
       delete h;
       throw;
@@ -148,15 +163,22 @@ lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_
       if (n_video[s] < 0 || n_video[s] > h->max_video) invalid("lsg_pipe_run: too many video frames");
     }
     // ---------------------------------------------------------------- H2D
+    // PCM and reference crops on the compute stream (the segmenter needs them
+    // first); face crops per stream on the H2D stream, overlapping the
+    // segmenter, mel and the generator batches of earlier streams.
     LSG_CUDA(cudaEventRecord(h->ev[0], st));
-    for (int s = 0; s < S; ++s) {
+    LSG_CUDA(cudaEventRecord(h->ev_start, st));  // previous run's readers of video are done
+    LSG_CUDA(cudaStreamWaitEvent(h->h2d, h->ev_start, 0));
+    for (int s = 0; s < S; ++s)
       if (n_samples[s])
         LSG_CUDA(cudaMemcpyAsync(h->pcm.p + (size_t)s * h->max_samples, pcm[s], n_samples[s] * 2, cudaMemcpyDefault, st));
+    LSG_CUDA(cudaMemcpyAsync(h->refs.p, refs, (size_t)S * kCrop, cudaMemcpyDefault, st));
+    for (int s = 0; s < S; ++s) {
       if (n_video[s])
         LSG_CUDA(cudaMemcpyAsync(h->video.p + (size_t)s * h->max_video * kCrop, video[s], n_video[s] * kCrop,
-                                 cudaMemcpyDefault, st));
+                                 cudaMemcpyDefault, h->h2d));
+      LSG_CUDA(cudaEventRecord(h->ev_vid[s], h->h2d));
     }
-    LSG_CUDA(cudaMemcpyAsync(h->refs.p, refs, (size_t)S * kCrop, cudaMemcpyDefault, st));
     // ---------------------------------------------------------- segmenter
     LSG_CUDA(cudaEventRecord(h->ev[1], st));
     {
@@ -255,16 +277,36 @@ lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_
       LSG_CUDA(cudaMemcpyAsync(h->frame_idx.p, h->h_frame_idx.p, J * 8, cudaMemcpyHostToDevice, st));
     }
     const int MB = h->cfg.max_batch;
-    for (int64_t b0 = 0; b0 < J; b0 += MB) {
+    const int64_t n_copy = frames ? std::min<int64_t>(J, cap) : 0;
+    const size_t n_batches = (size_t)ceil_div(std::max<int64_t>(J, 1), MB);
+    while (h->ev_out.size() < n_batches) {
+      cudaEvent_t e;
+      LSG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->ev_out.push_back(e);
+    }
+    int waited = -1;  // face crops of streams <= waited are resident
+    for (int64_t b0 = 0, bi = 0; b0 < J; b0 += MB, ++bi) {
       const int B = (int)std::min<int64_t>(MB, J - b0);
+      int need = 0;
+      for (int64_t j = b0; j < b0 + B; ++j) need = std::max(need, (int)jobs[j].stream);
+      if (need > waited) {  // jobs are stream-major, so this wait is rarely more than one stream ahead
+        LSG_CUDA(cudaStreamWaitEvent(st, h->ev_vid[need], 0));
+        waited = need;
+      }
       gen::forward_gather(h->gen, h->mel_rows.p, h->chunk_row.p + b0, h->video.p, h->frame_idx.p + b0, h->refs.p,
                           h->ref_idx.p + b0, h->out.p + b0 * px, h->cfg.out_format, B);
+      // ------------------------------------------------------------ D2H
+      if (b0 < n_copy) {
+        LSG_CUDA(cudaEventRecord(h->ev_out[bi], st));
+        LSG_CUDA(cudaStreamWaitEvent(h->d2h, h->ev_out[bi], 0));
+        const int64_t nb = std::min<int64_t>(B, n_copy - b0);
+        LSG_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(frames) + b0 * px, h->out.p + b0 * px, nb * px,
+                                 cudaMemcpyDeviceToHost, h->d2h));
+      }
     }
+    if (waited < S - 1) LSG_CUDA(cudaStreamWaitEvent(st, h->ev_vid[S - 1], 0));  // leave no copy in flight
     LSG_CUDA(cudaEventRecord(h->ev[4], st));
-    // ---------------------------------------------------------------- D2H
-    const int64_t n_copy = std::min<int64_t>(J, cap);
-    if (n_copy > 0 && frames)
-      LSG_CUDA(cudaMemcpyAsync(frames, h->out.p, n_copy * px, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(h->d2h));
     ctx->sync();
     for (int64_t j = 0; j < n_copy && recs; ++j)
       recs[j] = {jobs[j].stream, jobs[j].seg, jobs[j].frame, jobs[j].ts, jobs[j].k, 0};
