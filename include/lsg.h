@@ -165,6 +165,8 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
  * tcgen05 tensor cores. */
 #define LSG_PREC_BF16 0         /* bf16 weights/activations, f32 accumulate */
 #define LSG_PREC_FP16 1         /* fp16 weights/activations, f32 accumulate (same tcgen05 rate) */
+#define LSG_PREC_FP8 2          /* e4m3 weights (per output channel scale) and activations (per tensor
+                                   scale from lsg_gen_calibrate), f32 accumulate */
 #define LSG_OUT_F32_NCHW 0      /* [B][3][96][96] f32 in [0,1] */
 #define LSG_OUT_U8_NHWC 1       /* [B][96][96][3] u8, round(255*x) */
 #define LSG_OUT_F32_LOGITS 2    /* [B][3][96][96] f32 pre-sigmoid (parity checks) */
@@ -178,6 +180,17 @@ lsg_status lsg_gen_param_count(int64_t* n);
 lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap_layers, int32_t* n_layers);
 lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights /*[host]*/, int64_t n_floats,
                           int32_t precision, int32_t max_batch, lsg_gen* out);
+/* As lsg_gen_create; LSG_PREC_FP8 requires act_absmax [host], the n_act
+ * activation ranges lsg_gen_calibrate returns (ignored otherwise). */
+lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights /*[host]*/, int64_t n_floats, int32_t precision,
+                            const float* act_absmax, int32_t n_act, int32_t max_batch, lsg_gen* out);
+/* On a bf16/fp16 engine: run a calibration batch (inputs as lsg_gen_forward)
+ * and return max |x| of every fp8 scale group -- face input, mel input, the
+ * seven concat buffers (shared by both producers), each other layer output.
+ * *n_tensors = groups; nothing is written when cap < *n_tensors. */
+lsg_status lsg_gen_calibrate(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
+                             const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
+                             int32_t B, float* absmax /*[host]*/, int32_t cap, int32_t* n_tensors);
 lsg_status lsg_gen_destroy(lsg_gen h);
 /* Forward of B frames, all inputs [dev]:
  *   mel_rows  [rows][80] f32 log-mel rows (lsg_mel output)

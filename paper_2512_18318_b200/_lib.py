@@ -105,6 +105,8 @@ _SIGS = {
     "lsg_gen_param_count": [PI64],
     "lsg_gen_layer_info": [PI32, I32, PI32],
     "lsg_gen_create": [P, P, I64, I32, I32, PP],
+    "lsg_gen_create_q": [P, P, I64, I32, P, I32, I32, PP],
+    "lsg_gen_calibrate": [P, P, P, P, P, P, I32, P, I32, PI32],
     "lsg_gen_destroy": [P],
     "lsg_gen_forward": [P, P, P, P, P, P, P, I32, I32],
     "lsg_lipsync_validate": [I64, I64, I64],

@@ -90,6 +90,9 @@ struct alignas(64) HaloParams {
   const uint16_t* res;
   int res_pitch, res_coff;
   const float* bias;
+  const float* oscale;  // fp8: per output channel s_in * s_w[co], else null
+  float res_scale;      // fp8: residual tensor scale, else 1
+  float out_inv;        // fp8: 1 / output tensor scale, else 1
   int relu, out_mode;
   const float* w1;
   const float* b1;
@@ -101,7 +104,7 @@ struct alignas(64) HaloParams {
 // barriers.  Staging / residual tiles are [128 positions][IB bytes] boxes in
 // the tensor map's swizzle (IB = 128 -> 128B, 64 -> 64B, 32 -> 32B) so the
 // epilogue's per-position 16-byte accesses are bank-conflict free.
-template <int BN, int MODE, bool FUSED, bool B_RES>
+template <int BN, int MODE, bool FUSED, bool B_RES, int ES = 2>  // ES: bytes per channel (2, or 1 for fp8)
 struct HaloCfg {
   static constexpr int NPH = HaloTaps<MODE>::NPH;
   static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
@@ -111,8 +114,8 @@ struct HaloCfg {
   static constexpr int WG = 3;              // streamed weights: taps per ring slot (one wait + commit each)
   static constexpr int GBLK = WG * BBLK;
   static constexpr int W_RES_BYTES = 72 * 1024;
-  static constexpr int IB = (BN < 64 ? BN : 64) * 2;   // bytes per position per box
-  static constexpr int NCH = BN > 64 ? BN / 64 : 1;    // boxes across the channels
+  static constexpr int IB = BN * ES < 128 ? BN * ES : 128;  // bytes per position per box
+  static constexpr int NCH = BN * ES > 128 ? BN * ES / 128 : 1;  // boxes across the channels
   static constexpr int BOX = 128 * IB;                 // one [128][IB] box
   static constexpr int STG_BYTES = FUSED ? 0 : NPH * NCH * BOX;
   static constexpr int NSTG = FUSED ? 0 : (B_RES ? 2 : 1);
@@ -145,7 +148,7 @@ struct HaloCfg {
 template <int IB>
 __device__ __forceinline__ uint32_t swz(int r, int j) {
   const uint32_t off = (uint32_t)(r * IB + j * 16);
-  constexpr uint32_t mask = IB == 128 ? 7u : (IB == 64 ? 3u : 1u);
+  constexpr uint32_t mask = IB == 128 ? 7u : (IB == 64 ? 3u : (IB == 32 ? 1u : 0u));  // 16 B rows: no swizzle
   return off ^ (((off >> 7) & mask) << 4);
 }
 
@@ -179,12 +182,12 @@ __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint3
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
 }
 
-template <int BN, int MODE, bool FUSED_OUT, bool HALF, bool B_RES>
+template <int BN, int MODE, bool FUSED_OUT, int PR, bool B_RES>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
-  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES>;
+  using NF = Num<PR>;
+  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::F8 ? 1 : 2>;
   using TT = HaloTaps<MODE>;
   constexpr int NPH = TT::NPH;
-  using NF = Num<HALF>;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
   static_assert(!FUSED_OUT || NPH == 1, "fused output conv has one phase");
   // epilogue warps 2-9 = two groups of four (one per TMEM lane quadrant).
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             const uint32_t acc0 = (first && cb == 0) ? 0u : 1u;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              if (ks < ksteps) tc::mma_f16_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+              if (ks < ksteps) NF::mma_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
             if constexpr (!B_RES) {
               if (tap % CF::WG == CF::WG - 1 || tap == NT - 1) {
                 tc::mma_commit_nc(&bempty[bs]);
@@ -426,46 +429,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           for (int c0 = 0; c0 < HC; c0 += 16) {
             uint32_t v[16];
             tc::tmem_ld16(tbase + c0, v);
-            const int ch = cbeg + c0;  // first channel of this 16-column chunk
-            const int cc = ch >> 6, j0 = (ch & 63) >> 3;
-            float f[16];
-            const float4* bp = reinterpret_cast<const float4*>(p.bias + ch);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float4 b4 = __ldg(bp + k);
-              f[4 * k + 0] = b4.x;
-              f[4 * k + 1] = b4.y;
-              f[4 * k + 2] = b4.z;
-              f[4 * k + 3] = b4.w;
-            }
+            // 16 channels = W16 16-byte chunks of the position's box row
+            constexpr int W16 = NF::U4, ES = NF::F8 ? 1 : 2;
+            const int byte0 = (cbeg + c0) * ES;
+            const int cc = byte0 >> 7, j0 = (byte0 & 127) >> 4;
+            uint4 rv[W16];
             if constexpr (CF::HAS_RES) {
 #pragma unroll
-              for (int h2 = 0; h2 < 2; ++h2) {
-                const uint4 rv = *reinterpret_cast<const uint4*>(res + cc * CF::BOX + swz<IB>(r, j0 + h2));
-                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const float2 x2 = NF::unpack(rw[k]);
-                  f[8 * h2 + 2 * k] += x2.x;
-                  f[8 * h2 + 2 * k + 1] += x2.y;
-                }
-              }
+              for (int w = 0; w < W16; ++w)
+                rv[w] = *reinterpret_cast<const uint4*>(res + cc * CF::BOX + swz<IB>(r, j0 + w));
             }
             tc::tmem_ld_wait();
+            uint4 o[W16];
+            epi16<PR>(v, p.bias + cbeg + c0, p.oscale + (NF::F8 ? cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
+                      p.res_scale, p.relu != 0, p.out_inv, o);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              f[k] += __uint_as_float(v[k]);
-              if (p.relu) f[k] = fmaxf(f[k], 0.f);
-            }
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              uint4 o;
-              o.x = NF::pack(f[8 * h2 + 0], f[8 * h2 + 1]);
-              o.y = NF::pack(f[8 * h2 + 2], f[8 * h2 + 3]);
-              o.z = NF::pack(f[8 * h2 + 4], f[8 * h2 + 5]);
-              o.w = NF::pack(f[8 * h2 + 6], f[8 * h2 + 7]);
-              *reinterpret_cast<uint4*>(stg + (z * CF::NCH + cc) * CF::BOX + swz<IB>(r, j0 + h2)) = o;
-            }
+            for (int w = 0; w < W16; ++w)
+              *reinterpret_cast<uint4*>(stg + (z * CF::NCH + cc) * CF::BOX + swz<IB>(r, j0 + w)) = o[w];
           }
         }
         tc::tc_fence_before();
@@ -509,7 +489,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           tc::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float xx = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+            const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
+            const float xx = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
 #pragma unroll
             for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
           }

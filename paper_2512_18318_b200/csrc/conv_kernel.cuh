@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <cstdint>
 
@@ -67,6 +68,9 @@ struct alignas(64) ConvParams {
   const uint16_t* res;
   int res_pitch, res_coff;
   const float* bias;
+  const float* oscale;  // fp8: per output channel s_in * s_w[co] (dequantizes the accumulator), else null
+  float res_scale;      // fp8: scale of the residual tensor, else 1
+  float out_inv;        // fp8: 1 / scale of the output tensor, else 1
   int sy, sx, osy, osx;
   int relu, out_mode;
   const float* w1;  // fused output 1x1: [3][32]
@@ -77,12 +81,22 @@ struct alignas(64) ConvParams {
   Phase ph[MAX_PHASES];
 };
 
-// 16-bit number format: HALF = fp16 (kind::f16 format 0), else bf16 (format 1)
-template <bool HALF>
+// Element formats.  Activations and weights are always moved as 16-bit
+// "units": a bf16/fp16 value, or a PAIR of fp8 e4m3 values.  One MMA step
+// is 32 bytes of a row either way (kind::f16 K=16, kind::f8f6f4 K=32), so
+// tensor maps, shared-memory layouts, descriptors and K loops are identical
+// across formats; only the MMA kind, the weight packing and the epilogue's
+// (de)quantisation differ.
+enum Prec { PR_BF16 = 0, PR_FP16 = 1, PR_FP8 = 2 };
+
+template <int PR>
 struct Num {
-  static constexpr uint32_t kFmt = HALF ? 0u : 1u;
-  __device__ __forceinline__ static uint32_t pack(float a, float b) {
-    if constexpr (HALF) {
+  static constexpr bool F8 = PR == PR_FP8;
+  static constexpr uint32_t kFmt = PR == PR_BF16 ? 1u : 0u;  // bf16 = 1; fp16 = 0; e4m3 = 0
+  static constexpr int CPU = F8 ? 2 : 1;                     // channels per 16-bit unit
+  static constexpr int U4 = F8 ? 1 : 2;                      // uint4 words per 16 channels
+  __device__ __forceinline__ static uint32_t pack(float a, float b) {  // 16-bit formats
+    if constexpr (PR == PR_FP16) {
       __half2 v = __floats2half2_rn(a, b);
       return *reinterpret_cast<uint32_t*>(&v);
     } else {
@@ -91,13 +105,108 @@ struct Num {
     }
   }
   __device__ __forceinline__ static float2 unpack(uint32_t u) {
-    if constexpr (HALF) {
+    if constexpr (PR == PR_FP16) {
       return __half22float2(*reinterpret_cast<__half2*>(&u));
     } else {
       return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
     }
   }
+  // 16 channels <-> their U4 uint4 words
+  __device__ __forceinline__ static void to_float16(const uint4* w, float (&x)[16]) {
+    if constexpr (F8) {
+      const uint32_t r[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(r[k] >> (16 * h)), __NV_E4M3);
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hr));
+          x[4 * k + 2 * h] = f.x;
+          x[4 * k + 2 * h + 1] = f.y;
+        }
+      }
+    } else {
+      const uint32_t r[8] = {w[0].x, w[0].y, w[0].z, w[0].w, w[1].x, w[1].y, w[1].z, w[1].w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 f = unpack(r[k]);
+        x[2 * k] = f.x;
+        x[2 * k + 1] = f.y;
+      }
+    }
+  }
+  __device__ __forceinline__ static void from_float16(const float (&f)[16], uint4* w) {
+    if constexpr (F8) {
+      uint32_t r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(f[4 * k], f[4 * k + 1]), __NV_SATFINITE, __NV_E4M3);
+        const uint32_t hi =
+            __nv_cvt_float2_to_fp8x2(make_float2(f[4 * k + 2], f[4 * k + 3]), __NV_SATFINITE, __NV_E4M3);
+        r[k] = lo | (hi << 16);
+      }
+      w[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    } else {
+      w[0] = make_uint4(pack(f[0], f[1]), pack(f[2], f[3]), pack(f[4], f[5]), pack(f[6], f[7]));
+      w[1] = make_uint4(pack(f[8], f[9]), pack(f[10], f[11]), pack(f[12], f[13]), pack(f[14], f[15]));
+    }
+  }
+  __device__ __forceinline__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (F8) tc::mma_f8(d, a, b, idesc, acc);
+    else tc::mma_f16(d, a, b, idesc, acc);
+  }
+  __device__ __forceinline__ static void mma_nc(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (F8) tc::mma_f8_nc(d, a, b, idesc, acc);
+    else tc::mma_f16_nc(d, a, b, idesc, acc);
+  }
 };
+
+// The per-channel math of every epilogue, 16 channels at a time:
+// y = acc * oscale + bias (+ residual * res_scale), ReLU, * out_inv (fp8).
+template <int PR>
+__device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias, const float* oscale,
+                                      const uint4* res, float res_scale, bool relu, float out_inv, uint4* out) {
+  using NF = Num<PR>;
+  float f[16];
+  const float4* bp = reinterpret_cast<const float4*>(bias);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 b4 = __ldg(bp + j);
+    f[4 * j + 0] = b4.x;
+    f[4 * j + 1] = b4.y;
+    f[4 * j + 2] = b4.z;
+    f[4 * j + 3] = b4.w;
+  }
+  if constexpr (NF::F8) {
+    const float4* sp = reinterpret_cast<const float4*>(oscale);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 s4 = __ldg(sp + j);
+      f[4 * j + 0] = fmaf(__uint_as_float(v[4 * j + 0]), s4.x, f[4 * j + 0]);
+      f[4 * j + 1] = fmaf(__uint_as_float(v[4 * j + 1]), s4.y, f[4 * j + 1]);
+      f[4 * j + 2] = fmaf(__uint_as_float(v[4 * j + 2]), s4.z, f[4 * j + 2]);
+      f[4 * j + 3] = fmaf(__uint_as_float(v[4 * j + 3]), s4.w, f[4 * j + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] += __uint_as_float(v[j]);
+  }
+  if (res) {
+    float x[16];
+    NF::to_float16(res, x);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = NF::F8 ? fmaf(x[j], res_scale, f[j]) : f[j] + x[j];
+  }
+  if (relu) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
+  }
+  if constexpr (NF::F8) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] *= out_inv;
+  }
+  NF::from_float16(f, out);
+}
 
 template <int BN>
 struct Cfg {
@@ -163,14 +272,16 @@ __device__ __forceinline__ constexpr uint32_t a_koff(int k) {
 }
 
 // One epilogue thread's share of an output row: HC accumulator columns ->
-// + bias (+ residual) (ReLU) -> 16-bit store.  The whole residual slice is
-// requested before the accumulator wait (HC <= 64: 32 registers), so its
-// latency hides under the mainloop instead of once per 16-column chunk.
-template <int HC, bool HALF>
+// epi16 -> 16-bit-unit store (orow/rrow point at the row's first channel).
+// The whole residual slice is requested before the accumulator wait
+// (HC <= 64), so its latency hides under the mainloop.
+template <int HC, int PR>
 __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, const uint16_t* rrow, const float* bias,
-                                             bool relu, bool valid, uint64_t* tfull_bar, uint32_t parity) {
-  using NF = Num<HALF>;
-  constexpr int NR = HC <= 64 ? HC / 8 : 2;
+                                             const float* oscale, float res_scale, float out_inv, bool relu,
+                                             bool valid, uint64_t* tfull_bar, uint32_t parity) {
+  using NF = Num<PR>;
+  constexpr int W16 = NF::U4;                 // uint4 per 16 channels
+  constexpr int NR = HC <= 64 ? HC / 16 * W16 : 2 * W16;
   uint4 rv[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) rv[i] = rrow ? __ldg(reinterpret_cast<const uint4*>(rrow) + i) : make_uint4(0, 0, 0, 0);
@@ -180,113 +291,25 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
   for (int c0 = 0; c0 < HC; c0 += 16) {
     uint32_t v[16];
     tc::tmem_ld16(tbase + c0, v);
-    uint4 ra, rb;
+    uint4 rcur[W16];
     if constexpr (HC <= 64) {
-      ra = rv[c0 / 8];
-      rb = rv[c0 / 8 + 1];
-    } else {
-      ra = rv[0];
-      rb = rv[1];
+#pragma unroll
+      for (int w = 0; w < W16; ++w) rcur[w] = rv[c0 / 16 * W16 + w];
+    } else {  // rolling two-chunk prefetch
+#pragma unroll
+      for (int w = 0; w < W16; ++w) rcur[w] = rv[w];
       if (rrow && c0 + 16 < HC) {
-        rv[0] = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16));
-        rv[1] = __ldg(reinterpret_cast<const uint4*>(rrow + c0 + 16) + 1);
+#pragma unroll
+        for (int w = 0; w < W16; ++w)
+          rv[w] = __ldg(reinterpret_cast<const uint4*>(rrow) + (c0 + 16) / 16 * W16 + w);
       }
     }
     tc::tmem_ld_wait();
     if (valid) {
-      float f[16];
-      const float4* bp = reinterpret_cast<const float4*>(bias + c0);
+      uint4 o[W16];
+      epi16<PR>(v, bias + c0, oscale + (NF::F8 ? c0 : 0), rrow ? rcur : nullptr, res_scale, relu, out_inv, o);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float4 b4 = __ldg(bp + j);
-        f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + b4.x;
-        f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + b4.y;
-        f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + b4.z;
-        f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + b4.w;
-      }
-      if (rrow) {
-        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 x = NF::unpack(rr[j]);
-          f[2 * j] += x.x;
-          f[2 * j + 1] += x.y;
-        }
-      }
-      if (relu) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
-      }
-      uint4 o0, o1;
-      o0.x = NF::pack(f[0], f[1]);
-      o0.y = NF::pack(f[2], f[3]);
-      o0.z = NF::pack(f[4], f[5]);
-      o0.w = NF::pack(f[6], f[7]);
-      o1.x = NF::pack(f[8], f[9]);
-      o1.y = NF::pack(f[10], f[11]);
-      o1.z = NF::pack(f[12], f[13]);
-      o1.w = NF::pack(f[14], f[15]);
-      *reinterpret_cast<uint4*>(orow + c0) = o0;
-      *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
-    }
-  }
-}
-
-// As epilogue_row, with the residual slice already in registers (loaded a
-// tile ahead by the caller, so its latency hides under the previous tile's
-// epilogue when the epilogue, not the MMA, is the bottleneck).  HC <= 64.
-template <int HC, bool HALF>
-__device__ __forceinline__ void epilogue_row_pre(uint32_t tbase, uint16_t* orow, const uint4 (&rv)[HC / 8],
-                                                 bool has_res, const float* bias, bool relu, bool valid,
-                                                 uint64_t* tfull_bar, uint32_t parity) {
-  using NF = Num<HALF>;
-  static_assert(HC % 16 == 0 && HC <= 64, "epilogue_row_pre: HC");
-  tc::mbar_wait(tfull_bar, parity);
-  tc::tc_fence_after();
-#pragma unroll
-  for (int c0 = 0; c0 < HC; c0 += 16) {
-    uint32_t v[16];
-    tc::tmem_ld16(tbase + c0, v);
-    float bf[16];
-    const float4* bp = reinterpret_cast<const float4*>(bias + c0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 b4 = __ldg(bp + j);
-      bf[4 * j + 0] = b4.x;
-      bf[4 * j + 1] = b4.y;
-      bf[4 * j + 2] = b4.z;
-      bf[4 * j + 3] = b4.w;
-    }
-    tc::tmem_ld_wait();
-    if (valid) {
-      float f[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]) + bf[j];
-      if (has_res) {
-        const uint4 ra = rv[c0 / 8], rb = rv[c0 / 8 + 1];
-        const uint32_t rr[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 x = NF::unpack(rr[j]);
-          f[2 * j] += x.x;
-          f[2 * j + 1] += x.y;
-        }
-      }
-      if (relu) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
-      }
-      uint4 o0, o1;
-      o0.x = NF::pack(f[0], f[1]);
-      o0.y = NF::pack(f[2], f[3]);
-      o0.z = NF::pack(f[4], f[5]);
-      o0.w = NF::pack(f[6], f[7]);
-      o1.x = NF::pack(f[8], f[9]);
-      o1.y = NF::pack(f[10], f[11]);
-      o1.z = NF::pack(f[12], f[13]);
-      o1.w = NF::pack(f[14], f[15]);
-      *reinterpret_cast<uint4*>(orow + c0) = o0;
-      *reinterpret_cast<uint4*>(orow + c0 + 8) = o1;
+      for (int w = 0; w < W16; ++w) reinterpret_cast<uint4*>(orow)[c0 / 16 * W16 + w] = o[w];
     }
   }
 }
@@ -301,10 +324,10 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-template <int BN, int CC, bool FUSED_OUT, bool HALF>
+template <int BN, int CC, bool FUSED_OUT, int PR>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant__ ConvParams p) {
   using CF = Cfg<BN>;
-  using NF = Num<HALF>;
+  using NF = Num<PR>;
   constexpr int S = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = tc::smem_u32(smem_raw);
@@ -400,10 +423,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
         if (elect_one()) {
           if (kb * 4 + 4 <= NS) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) tc::mma_f16(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
           } else {
             const int ns = NS - kb * 4;
-            for (int k = 0; k < ns; ++k) tc::mma_f16(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < ns; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
           }
           tc::mma_commit(&empty[s]);
         }
@@ -445,9 +468,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
       }
       const size_t pix = ((size_t)n * p.OH + oy) * p.OW + ox;
       if constexpr (!FUSED_OUT) {
-        uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + n0 + cbeg;
+        // channel offsets in 16-bit units (fp8: two channels per unit)
+        uint16_t* orow = p.out + pix * p.out_pitch + p.out_coff + (n0 + cbeg) / NF::CPU;
         const uint16_t* rrow =
-            (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + n0 + cbeg : nullptr;
+            (p.res && valid && active) ? p.res + pix * p.res_pitch + p.res_coff + (n0 + cbeg) / NF::CPU : nullptr;
         if (!active) {
           tc::mbar_wait(&tfull[a], use & 1);
           tc::tc_fence_after();
@@ -456,7 +480,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
           continue;
         }
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
-        epilogue_row<HC, HALF>(tbase, orow, rrow, p.bias + n0 + cbeg, p.relu != 0, valid, &tfull[a], use & 1);
+        epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::F8 ? n0 + cbeg : 0), p.res_scale,
+                             p.out_inv, p.relu != 0, valid, &tfull[a], use & 1);
       } else {
         // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid;
         // the second warp of each quadrant only keeps the barrier count
@@ -472,7 +497,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
             tc::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float x = fmaxf(__uint_as_float(v[j]) + __ldg(p.bias + c0 + j), 0.f);
+              const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
+              const float x = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
 #pragma unroll
               for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), x, o[o3]);
             }

@@ -112,16 +112,30 @@ static const LayerSpec kLayers[] = {
 constexpr int kNumLayers = sizeof(kLayers) / sizeof(kLayers[0]);
 static_assert(kNumLayers == 51, "Wav2Lip has 51 conv layers");
 
-using NumH = Num<true>;
-
 // ------------------------------------------------------------ input prep
+// Both inputs are 16 bytes per pixel: 8 channels of bf16/fp16, or 16 fp8
+// channels (values * inv_scale) -- the same tensor-map geometry either way.
+template <int PR>
+__device__ __forceinline__ uint4 pack_px(const float (&c)[6], float inv_scale) {
+  using NF = Num<PR>;
+  if constexpr (NF::F8) {
+    float f[16] = {};
+#pragma unroll
+    for (int j = 0; j < 6; ++j) f[j] = c[j] * inv_scale;
+    uint4 o;
+    NF::from_float16(f, &o);
+    return o;
+  } else {
+    return make_uint4(NF::pack(c[0], c[1]), NF::pack(c[2], c[3]), NF::pack(c[4], c[5]), 0u);
+  }
+}
+
 // faces: [B][96][96][3] u8 target (rows >= 48 masked), refs [R][96][96][3]
-// -> [B][96][96][8] bf16 = (target/255 masked, ref/255, 0, 0)
-template <bool HALF>
+// -> [B][96][96][16 B] = (target/255 masked, ref/255, 0...)
+template <int PR>
 __global__ void prep_faces(const uint8_t* __restrict__ target, const int64_t* __restrict__ target_idx,
                            const uint8_t* __restrict__ refs, const int32_t* __restrict__ ref_index,
-                           uint16_t* __restrict__ out, int B) {
-  using NF = Num<HALF>;
+                           uint16_t* __restrict__ out, int B, float inv_scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel
   const int64_t total = (int64_t)B * 96 * 96;
   if (i >= total) return;
@@ -133,32 +147,40 @@ __global__ void prep_faces(const uint8_t* __restrict__ target, const int64_t* __
   const uint8_t* r = refs + ((int64_t)__ldg(ref_index + b) * 96 * 96 + pix) * 3;
   const float k = 1.f / 255.f;
   const bool mask = y >= 48;
-  uint4 o;
-  o.x = NF::pack(mask ? 0.f : t[0] * k, mask ? 0.f : t[1] * k);
-  o.y = NF::pack(mask ? 0.f : t[2] * k, r[0] * k);
-  o.z = NF::pack(r[1] * k, r[2] * k);
-  o.w = 0;
-  reinterpret_cast<uint4*>(out)[i] = o;
+  const float c[6] = {mask ? 0.f : t[0] * k, mask ? 0.f : t[1] * k, mask ? 0.f : t[2] * k,
+                      r[0] * k, r[1] * k, r[2] * k};
+  reinterpret_cast<uint4*>(out)[i] = pack_px<PR>(c, inv_scale);
 }
 
-// mel rows [rows][80] f32, chunk_row [B] -> [B][80][16][8] bf16, chunk[h][w] = rows[r0 + w][h]
-template <bool HALF>
+// mel rows [rows][80] f32, chunk_row [B] -> [B][80][16][16 B], chunk[h][w] = rows[r0 + w][h]
+template <int PR>
 __global__ void prep_mel(const float* __restrict__ rows, const int32_t* __restrict__ chunk_row,
-                         uint16_t* __restrict__ out, int B) {
-  using NF = Num<HALF>;
+                         uint16_t* __restrict__ out, int B, float inv_scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, h, w)
   const int64_t total = (int64_t)B * 80 * 16;
   if (i >= total) return;
   const int b = (int)(i / (80 * 16));
   const int hw = (int)(i - (int64_t)b * 80 * 16);
   const int h = hw / 16, w = hw - h * 16;
-  const float v = __ldg(rows + ((int64_t)__ldg(chunk_row + b) + w) * 80 + h);
-  uint4 o;
-  o.x = NF::pack(v, 0.f);
-  o.y = 0;
-  o.z = 0;
-  o.w = 0;
-  reinterpret_cast<uint4*>(out)[i] = o;
+  const float c[6] = {__ldg(rows + ((int64_t)__ldg(chunk_row + b) + w) * 80 + h), 0.f, 0.f, 0.f, 0.f, 0.f};
+  reinterpret_cast<uint4*>(out)[i] = pack_px<PR>(c, inv_scale);
+}
+
+// max |x| over a 16-bit (bf16/fp16) channel-slice view (calibration)
+template <int PR>
+__global__ void absmax_view(const uint16_t* __restrict__ src, int pitch, int coff, int C, int64_t pixels,
+                            unsigned* __restrict__ out) {
+  using NF = Num<PR>;
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pixels * C; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t px = i / C;
+    const int c = (int)(i - px * C);
+    const uint32_t u = __ldg(src + px * pitch + coff + c);
+    m = fmaxf(m, fabsf(NF::unpack(u).x));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // non-negative floats order as uints
 }
 
 }  // namespace gen
@@ -251,9 +273,11 @@ void encode_box(CUtensorMap* map, const View& v, int n, int bc, int bx, int by, 
                                  (cuuint64_t)v.H * v.W * v.pitch * 2};
   const cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)bx, (cuuint32_t)by, 1};
   const cuuint32_t estr[4] = {1, (cuuint32_t)ex, (cuuint32_t)ey, 1};
-  const CUtensorMapSwizzle sw = bc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                         : (bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-  if (bc != 64 && bc != 32 && bc != 16) fail(LSG_ERUNTIME, "encode_box: channel box must be 16, 32 or 64");
+  const CUtensorMapSwizzle sw = bc == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : bc == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (bc != 64 && bc != 32 && bc != 16 && bc != 8) fail(LSG_ERUNTIME, "encode_box: channel box must be 8..64 units");
   CUresult r = tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -323,9 +347,14 @@ struct lsg_gen_s {
   Ctx* ctx = nullptr;
   int max_batch = 0;
   int sm_count = 148;
-  bool half = false;  // LSG_PREC_FP16
+  int prec = PR_BF16;  // Prec (conv_kernel.cuh): LSG_PREC_BF16 / FP16 / FP8
+  int cpu = 1;         // channels per 16-bit storage unit (2 for fp8)
+  float inv_face = 1.f, inv_mel = 1.f;  // fp8 input quantisation (1 / scale)
   DevBuf<uint16_t> wpack;
   DevBuf<float> bias;
+  DevBuf<float> oscale;  // fp8: per layer, per output channel s_in * s_w[co]
+  std::vector<int> plan_in_id, plan_out_id;  // tensor ids (kTensors) of each layer's input / output
+  std::vector<float> ascale;                 // fp8: scale per tensor id (1 otherwise)
   DevBuf<float> w1b1;
   DevBuf<uint16_t> act;  // all activation buffers
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
@@ -353,7 +382,7 @@ static void launch_pdl(void (*kernel)(P), int grid, int block, int smem, cudaStr
 
 // Persistent launch: one CTA per SM walks the tiles round-robin in the
 // L2-friendly order of decode_tile().
-template <int BN, int CC, bool F, bool H>
+template <int BN, int CC, bool F, int PR>
 static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   ConvParams p = r.p;
   int tiles = 0;
@@ -370,11 +399,13 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   p.interleave = 1;
   for (int z = 1; z < r.nphases; ++z) p.interleave &= p.ph[z].mtiles == p.ph[0].mtiles;
   const int grid = std::min(tiles, sms);
-  launch_pdl(conv_tc<BN, CC, F, H>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
+  launch_pdl(conv_tc<BN, CC, F, PR>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
 }
 
-// (tile width BN, channel chunk CC, fused output) combinations the Wav2Lip
-// layers use; every combination is compiled for fp16 and bf16.
+// (tile width BN, channel chunk CC in 16-bit units, fused output)
+// combinations the Wav2Lip layers use; every combination is compiled for
+// bf16, fp16 and fp8 (fp8 halves the units per channel, hence CC 8/16/32 with
+// the wider tiles).
 #define LSG_CONV_VARIANTS(X) \
   X(16, 8, false)            \
   X(32, 8, false)            \
@@ -385,7 +416,12 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(128, 64, false)          \
   X(192, 64, false)          \
   X(256, 64, false)          \
-  X(32, 16, true)
+  X(32, 16, true)            \
+  X(64, 16, false)           \
+  X(128, 32, false)          \
+  X(192, 32, false)          \
+  X(256, 32, false)          \
+  X(32, 8, true)
 
 // halo kernel variants: (tile width, mode, fused output, weights resident)
 #define LSG_HALO_VARIANTS(X)             \
@@ -407,45 +443,47 @@ bool taps_match(const HaloGeo& g) {
   return true;
 }
 
-static void set_smem_attrs() {
+template <int PR>
+static void set_smem_attrs_t() {
 #define LSG_SET_ATTR(BN, CC, F)                                                                                   \
-  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
-                                Cfg<BN>::SMEM));                                                                  \
-  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
-                                Cfg<BN>::SMEM));
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc<BN, CC, F, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
   LSG_CONV_VARIANTS(LSG_SET_ATTR)
 #undef LSG_SET_ATTR
 #define LSG_SET_HALO_ATTR(BN, MD, F, R)                                                                           \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                HaloCfg<BN, MD, F, R>::SMEM));                                                       \
-  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
-                                HaloCfg<BN, MD, F, R>::SMEM));
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, PR, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
 }
+static void set_smem_attrs(int prec) {
+  if (prec == PR_FP8) set_smem_attrs_t<PR_FP8>();
+  else if (prec == PR_FP16) set_smem_attrs_t<PR_FP16>();
+  else set_smem_attrs_t<PR_BF16>();
+}
 
-template <int BN, int MD, bool F, bool H, bool R>
+template <int BN, int MD, bool F, int PR, bool R>
 static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   HaloParams hp = r.hp;
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img;
   const int grid = std::min(hp.total_tiles, sms);
-  launch_pdl(conv_halo<BN, MD, F, H, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R>::SMEM, st, hp);
+  launch_pdl(conv_halo<BN, MD, F, PR, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM, st,
+             hp);
 }
 
-template <bool H>
+template <int PR>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
   if (r.halo) {
 #define LSG_HALO_DISPATCH(BN, MD, F, R)                                                       \
   if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
-    return launch_halo<BN, MD, F, H, R>(r, B, sms, st);
+    return launch_halo<BN, MD, F, PR, R>(r, B, sms, st);
     LSG_HALO_VARIANTS(LSG_HALO_DISPATCH)
 #undef LSG_HALO_DISPATCH
     fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / mode " +
                            std::to_string(r.halo_mode) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
 #define LSG_DISPATCH(BN, CC, F) \
-  if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, H>(r, B, sms, st);
+  if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st);
   LSG_CONV_VARIANTS(LSG_DISPATCH)
 #undef LSG_DISPATCH
   fail(LSG_ERUNTIME, "generator: no conv kernel for tile width " + std::to_string(r.bn) + " / channel chunk " +
@@ -453,9 +491,15 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
 }
 
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
-  if (h->half) dispatch_t<true>(r, B, h->sm_count, st);
-  else dispatch_t<false>(r, B, h->sm_count, st);
+  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st);
+  else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st);
+  else dispatch_t<PR_BF16>(r, B, h->sm_count, st);
 }
+
+// Activation tensors for fp8 scales: 0 face input, 1 mel input, 2..8 the
+// concat buffers cat0..cat6 (both producers share the scale), 9 + l the
+// output of layer l when it is not a concat slice.
+constexpr int kTensors = 9 + kNumLayers;
 
 extern "C" {
 
@@ -485,36 +529,48 @@ lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap, int32_t* n_layers) {
   });
 }
 
-lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, int32_t precision, int32_t max_batch,
-                          lsg_gen* out) {
+lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats, int32_t precision,
+                            const float* act_absmax, int32_t n_act, int32_t max_batch, lsg_gen* out) {
   return guard([&] {
     *out = nullptr;
     int64_t want = 0;
     lsg_gen_param_count(&want);
     if (n_floats != want) invalid("lsg_gen_create: weight blob has " + std::to_string(n_floats) + " floats, expected " +
                                   std::to_string(want));
-    if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16) invalid("lsg_gen_create: unsupported precision");
+    if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16 && precision != LSG_PREC_FP8)
+      invalid("lsg_gen_create: unsupported precision");
+    if (precision == LSG_PREC_FP8 && (!act_absmax || n_act != kTensors))
+      invalid("lsg_gen_create: fp8 needs the calibrated activation ranges (lsg_gen_calibrate)");
     if (max_batch <= 0 || max_batch > 4096) invalid("lsg_gen_create: max_batch out of range");
     DeviceGuard g(ctx);
     auto h = new lsg_gen_s();
     try {
       h->ctx = ctx;
       h->max_batch = max_batch;
-      h->half = precision == LSG_PREC_FP16;
+      h->prec = precision == LSG_PREC_FP8 ? PR_FP8 : (precision == LSG_PREC_FP16 ? PR_FP16 : PR_BF16);
+      const bool f8 = h->prec == PR_FP8;
+      const int cpu = h->cpu = f8 ? 2 : 1;
       h->sm_count = ctx->sm_count;
       const int B = max_batch;
-      // ---------------- activation buffers (bf16 NHWC)
+      // fp8 activation scales: calibrated |x| max with 10% headroom onto e4m3's 448
+      std::vector<float> ascale(kTensors, 1.f);
+      if (f8)
+        for (int i = 0; i < kTensors; ++i) ascale[i] = std::max(act_absmax[i], 1e-6f) * 1.1f / 448.f;
+      h->inv_face = 1.f / ascale[0];
+      h->inv_mel = 1.f / ascale[1];
+      h->ascale = ascale;
+      // ---------------- activation buffers (NHWC, 16-bit units: bf16/fp16, or fp8 pairs)
       struct Req { View* v; int H, W, C; };
       const int cat_hw[7] = {1, 3, 6, 12, 24, 48, 96};
       const int cat_c[7] = {1024, 1024, 768, 512, 320, 160, 80};
       std::vector<Req> reqs;
-      reqs.push_back({&h->x_face, 96, 96, 8});
+      reqs.push_back({&h->x_face, 96, 96, 8});  // 16 bytes per pixel in every format
       reqs.push_back({&h->x_mel, 80, 16, 8});
-      for (int l = 0; l < 7; ++l) reqs.push_back({&h->cat[l], cat_hw[l], cat_hw[l], cat_c[l]});
-      reqs.push_back({&h->S0, 96, 96, 64});
-      reqs.push_back({&h->S1, 96, 96, 64});
-      reqs.push_back({&h->A0, 80, 16, 32});
-      reqs.push_back({&h->A1, 80, 16, 32});
+      for (int l = 0; l < 7; ++l) reqs.push_back({&h->cat[l], cat_hw[l], cat_hw[l], cat_c[l] / cpu});
+      reqs.push_back({&h->S0, 96, 96, 64 / cpu});
+      reqs.push_back({&h->S1, 96, 96, 64 / cpu});
+      reqs.push_back({&h->A0, 80, 16, 32 / cpu});
+      reqs.push_back({&h->A1, 80, 16, 32 / cpu});
       size_t tot = 0;
       for (auto& r : reqs) tot += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
       h->act.alloc(tot);
@@ -524,6 +580,20 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         *r.v = View{h->act.p + off, r.H, r.W, r.C, 0, r.C};
         off += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
       }
+      // K-block element j of row r (a row = 128 bytes = 64 units): 16-bit
+      // value, or fp8 byte (value / s_w[row's channel]); 16-byte chunks
+      // 128B-swizzled as the UMMA K-major SW128 layout expects
+      const int KE = 64 * cpu;  // elements per K block
+      auto store = [&](uint16_t* blk, int r, int j, float v, float inv_sw) {
+        if (f8) {
+          uint8_t* b8 = reinterpret_cast<uint8_t*>(blk);
+          b8[r * 128 + (((j >> 4) ^ (r & 7)) << 4) + (j & 15)] =
+              (uint8_t)__nv_cvt_float_to_fp8(v * inv_sw, __NV_SATFINITE, __NV_E4M3);
+        } else {
+          blk[r * BK + (((j >> 3) ^ (r & 7)) << 3) + (j & 7)] = h->prec == PR_FP16 ? f2h(v) : f2bf(v);
+        }
+      };
+      std::vector<std::vector<float>> wscale(kNumLayers);  // fp8: per output channel max|w| / 448
       // ---------------- weights: pack per layer / phase / N tile / K block
       std::vector<uint16_t> pack;
       std::vector<float> bias;
@@ -547,6 +617,20 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         }
         bias_off[li] = (int64_t)bias.size();
         bias.insert(bias.end(), b, b + L.cout);
+        auto wat = [&](int co, int ci, int ky, int kx) {  // conv [co][ci][ky][kx], convT [ci][co][ky][kx]
+          return L.kind == CONV ? w[(((int64_t)co * L.cin + ci) * L.kh + ky) * L.kw + kx]
+                                : w[(((int64_t)ci * L.cout + co) * L.kh + ky) * L.kw + kx];
+        };
+        std::vector<float>& sw = wscale[li];
+        sw.assign(L.cout, 1.f);
+        if (f8)
+          for (int co = 0; co < L.cout; ++co) {
+            float m = 0.f;
+            for (int ci = 0; ci < L.cin; ++ci)
+              for (int ky = 0; ky < L.kh; ++ky)
+                for (int kx = 0; kx < L.kw; ++kx) m = std::max(m, std::fabs(wat(co, ci, ky, kx)));
+            sw[co] = m > 0.f ? m / 448.f : 1.f;
+          }
         // phases
         std::vector<PhaseGeo>& G = geo[li];
         if (L.kind == CONV) {
@@ -643,36 +727,35 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
                           : hm == HALO_CONVT2 ? taps_match<HALO_CONVT2>(hg)
                                               : taps_match<HALO_STEM7>(hg);
           if (!ok) fail(LSG_ERUNTIME, std::string("generator: halo tap table mismatch at ") + L.name);
-          // [cb][tap][cout][64]: one K block per (channel block, tap), 128 B swizzled rows
-          const int ncb = hm == HALO_STEM7 ? 1 : (L.cin + 63) / 64, bnh = L.cout;
+          // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap)
+          const int ncb = hm == HALO_STEM7 ? 1 : (L.cin + KE - 1) / KE, bnh = L.cout;
           hg.off = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)ncb * hg.ntaps * bnh * BK, 0);
           uint16_t* dst = pack.data() + hg.off;
+          const int gch = 8 * cpu;  // channels per 16-byte granule (stem: one x-shifted plane)
           for (int cb = 0; cb < ncb; ++cb)
             for (int tap = 0; tap < hg.ntaps; ++tap) {
               uint16_t* blk = dst + ((size_t)cb * hg.ntaps + tap) * bnh * BK;
               for (int r = 0; r < bnh; ++r)
-                for (int j = 0; j < BK; ++j) {
-                  int c = cb * 64 + j, ky = hg.ky[tap], kx = hg.kx[tap];
+                for (int j = 0; j < KE; ++j) {
+                  int c = cb * KE + j, ky = hg.ky[tap], kx = hg.kx[tap];
                   if (hm == HALO_STEM7) {
-                    kx = j >> 3;
-                    c = j & 7;
+                    kx = j / gch;
+                    c = j % gch;
                   }
-                  float v = 0.f;
-                  if (c < L.cin && kx < L.kw)
-                    v = L.kind == CONV ? w[(((int64_t)r * L.cin + c) * L.kh + ky) * L.kw + kx]
-                                       : w[(((int64_t)c * L.cout + r) * L.kh + ky) * L.kw + kx];
-                  blk[r * BK + (((j >> 3) ^ (r & 7)) << 3) + (j & 7)] = h->half ? f2h(v) : f2bf(v);
+                  const float v = (c < L.cin && kx < L.kw) ? wat(r, c, ky, kx) : 0.f;
+                  store(blk, r, j, v, 1.f / sw[r]);
                 }
             }
         }
-        const int cin_pad = (L.cin + 7) / 8 * 8;
+        // input channels padded to whole 16-byte granules (8 units)
+        const int cin_pad = (L.cin + 8 * cpu - 1) / (8 * cpu) * (8 * cpu);
         const int bn = (li == kNumLayers - 2) ? 32 : pick_bn(L.cout);
         const int ntiles = L.cout / bn;
         for (size_t z = 0; z < G.size(); ++z) {
           const PhaseGeo& pg = G[z];
-          const int K = pg.ntaps * cin_pad;
-          const int kbs = (int)ceil_div(K, BK);
+          const int K = pg.ntaps * cin_pad;  // elements
+          const int kbs = (int)ceil_div(K, KE);
           pack_off[li * MAX_PHASES + z] = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)ntiles * kbs * bn * BK, 0);
           uint16_t* dst = pack.data() + pack_off[li * MAX_PHASES + z];
@@ -681,20 +764,14 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
               uint16_t* blk = dst + ((size_t)nt * kbs + kb) * bn * BK;
               for (int r = 0; r < bn; ++r) {
                 const int co = nt * bn + r;
-                for (int j = 0; j < BK; ++j) {
-                  const int k = kb * BK + j;
+                for (int j = 0; j < KE; ++j) {
+                  const int k = kb * KE + j;
                   float v = 0.f;
                   if (k < K) {
                     const int t = k / cin_pad, ci = k % cin_pad;
-                    if (ci < L.cin) {
-                      const int ky = pg.ky[t], kx = pg.kx[t];
-                      v = L.kind == CONV ? w[(((int64_t)co * L.cin + ci) * L.kh + ky) * L.kw + kx]
-                                         : w[(((int64_t)ci * L.cout + co) * L.kh + ky) * L.kw + kx];
-                    }
+                    if (ci < L.cin) v = wat(co, ci, pg.ky[t], pg.kx[t]);
                   }
-                  // 128-byte swizzle: 16-byte chunk (j/8) of row r lands at chunk (j/8) ^ (r%8)
-                  const int chunk = (j >> 3) ^ (r & 7);
-                  blk[r * BK + chunk * 8 + (j & 7)] = h->half ? f2h(v) : f2bf(v);
+                  store(blk, r, j, v, 1.f / sw[co]);
                 }
               }
             }
@@ -708,19 +785,20 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       LSG_CUDA(cudaMemcpy(h->w1b1.p, w1b1.data(), w1b1.size() * 4, cudaMemcpyHostToDevice));
 
       // ---------------- plan: input/output views per layer
-      auto slice = [](View v, int coff, int C) {
+      // channel arguments below are real channels; views count 16-bit units
+      auto slice = [cpu](View v, int coff, int C) {
         View s = v;
         s.pitch = v.C;
-        s.coff = coff;
-        s.C = C;
+        s.coff = coff / cpu;
+        s.C = C / cpu;
         return s;
       };
-      auto resize = [](View v, int H, int W, int C) {
+      auto resize = [cpu](View v, int H, int W, int C) {
         View s = v;
         s.H = H;
         s.W = W;
-        s.C = C;
-        s.pitch = C;
+        s.C = C / cpu;
+        s.pitch = C / cpu;
         s.coff = 0;
         return s;
       };
@@ -784,6 +862,53 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
       io[li++] = {cat[6], View{}};  // out0 (+ out1 fused)
       if (li != kNumLayers - 1) fail(LSG_ERUNTIME, "generator plan does not cover every layer");
 
+      // tensor ids (fp8 scales): fixed for inputs / concat buffers, per layer otherwise
+      std::vector<int> in_id(kNumLayers, 0), out_id(kNumLayers, 0);
+      {
+        auto fixed = [&](const View& v) -> int {
+          if (v.p == h->x_face.p) return 0;
+          if (v.p == h->x_mel.p) return 1;
+          for (int k = 0; k < 7; ++k)
+            if (v.p == h->cat[k].p) return 2 + k;
+          return -1;
+        };
+        std::vector<std::pair<const uint16_t*, int>> last;  // scratch buffer -> tensor id it holds
+        auto holder = [&](const uint16_t* p0) {
+          for (auto& e : last)
+            if (e.first == p0) return e.second;
+          fail(LSG_ERUNTIME, "generator plan: read of an unwritten scratch buffer");
+          return -1;
+        };
+        for (int l = 0; l < kNumLayers - 1; ++l) {
+          const View& in = io[l].first;
+          const View& ov = io[l].second;
+          in_id[l] = fixed(in) >= 0 ? fixed(in) : holder(in.p);
+          if (l == kNumLayers - 2) continue;  // fused output layer: no stored tensor
+          const int f = fixed(ov);
+          out_id[l] = f >= 0 ? f : 9 + l;
+          if (f < 0) {
+            bool found = false;
+            for (auto& e : last)
+              if (e.first == ov.p) {
+                e.second = out_id[l];
+                found = true;
+              }
+            if (!found) last.push_back({ov.p, out_id[l]});
+          }
+        }
+      }
+      h->plan_in_id = in_id;
+      h->plan_out_id = out_id;
+      std::vector<float> osc;
+      std::vector<int64_t> osc_off(kNumLayers, 0);
+      if (f8) {
+        for (int l = 0; l < kNumLayers - 1; ++l) {
+          osc_off[l] = (int64_t)osc.size();
+          for (int co = 0; co < kLayers[l].cout; ++co) osc.push_back(ascale[in_id[l]] * wscale[l][co]);
+        }
+        h->oscale.alloc(osc.size());
+        LSG_CUDA(cudaMemcpy(h->oscale.p, osc.data(), osc.size() * 4, cudaMemcpyHostToDevice));
+      }
       for (int l = 0; l < kNumLayers - 1; ++l) {
         const LayerSpec& L = kLayers[l];
         const View in = io[l].first, ov = io[l].second;
@@ -798,7 +923,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         r.in_view = in;
         p.H = in.H;
         p.W = in.W;
-        p.C = (L.cin + 7) / 8 * 8;
+        p.C = (L.cin + 8 * cpu - 1) / (8 * cpu) * 8;  // 16-bit units, whole 16-byte granules
         if (in.C != p.C) fail(LSG_ERUNTIME, std::string("generator plan: channel mismatch at ") + L.name);
         p.cc = p.C % 64 == 0 ? 64 : (p.C % 32 == 0 ? 32 : (p.C % 16 == 0 ? 16 : 8));
         // output geometry
@@ -810,7 +935,7 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           OH = (in.H - 1) * L.sh - 2 * L.ph + L.kh + L.oph;
           OW = (in.W - 1) * L.sw - 2 * L.pw + L.kw + L.opw;
         }
-        if (!fused && (ov.H != OH || ov.W != OW || ov.C != L.cout))
+        if (!fused && (ov.H != OH || ov.W != OW || ov.C != L.cout / cpu))
           fail(LSG_ERUNTIME, std::string("generator plan: shape mismatch at ") + L.name);
         p.out = ov.p;
         p.OH = OH;
@@ -821,6 +946,9 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
         p.res_pitch = in.pitch;
         p.res_coff = in.coff;
         p.bias = h->bias.p + bias_off[l];
+        p.oscale = f8 ? h->oscale.p + osc_off[l] : nullptr;
+        p.res_scale = f8 ? ascale[in_id[l]] : 1.f;
+        p.out_inv = f8 && !fused ? 1.f / ascale[out_id[l]] : 1.f;
         p.relu = 1;
         p.out_mode = OUT_16;
         if (L.kind == CONV) {
@@ -900,7 +1028,9 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
           if (hp.plane > HaloCfg<32, HALO_CONV3, false, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
           hp.shift_planes = hg.mode == HALO_STEM7;
-          hp.ngran = hp.shift_planes ? 8 : p.C / 8;
+          // planes come in pairs per K step; an odd last plane reads channels past the
+          // view, which the TMA zero-fills (fp8 out0: 80 channels = 5 planes)
+          hp.ngran = hp.shift_planes ? 8 : ((p.C / 8 + 1) & ~1);
           hp.ncb = (hp.ngran + 7) / 8;
           hp.ntaps = hg.ntaps;
           for (int t = 0; t < MAX_HTAPS; ++t) {
@@ -929,21 +1059,24 @@ lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, i
           hp.res_pitch = p.res_pitch;
           hp.res_coff = p.res_coff;
           hp.bias = p.bias;
+          hp.oscale = p.oscale;
+          hp.res_scale = p.res_scale;
+          hp.out_inv = p.out_inv;
           hp.relu = p.relu;
           hp.out_mode = p.out_mode;
           hp.w1 = p.w1;
           hp.b1 = p.b1;
           encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph);
-          const int bc = std::min(r.bn, 64);
+          const int bc = std::min(r.bn * 2 / cpu, 128) / 2;  // box channels in 16-bit units (128-byte rows max)
           if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
           if (hg.mode == HALO_CONV3 && !fused) {
-            if (!L.res || in.C != L.cout) fail(LSG_ERUNTIME, std::string("generator: halo 3x3 block without residual at ") + L.name);
+            if (!L.res || in.C != L.cout / cpu) fail(LSG_ERUNTIME, std::string("generator: halo 3x3 block without residual at ") + L.name);
             encode_box(&hp.tmap_res, in, max_batch, bc, HTW, HTH, 1, 1);
           }
         }
         h->plan.push_back(r);
       }
-      set_smem_attrs();
+      set_smem_attrs(h->prec);
     } catch (...) {
       delete h;
       throw;
@@ -971,17 +1104,99 @@ lsg_status lsg_gen_forward(lsg_gen h, const float* mel_rows, const int32_t* chun
 
 }  // extern "C"
 
+// ------------------------------------------------------ input prep launch
+static void prep_inputs(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
+                        const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, int B,
+                        cudaStream_t st) {
+  const unsigned gf = (unsigned)ceil_div((int64_t)B * 96 * 96, 256), gm = (unsigned)ceil_div((int64_t)B * 80 * 16, 256);
+  if (h->prec == PR_FP8) {
+    prep_faces<PR_FP8><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, h->inv_face);
+    prep_mel<PR_FP8><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, h->inv_mel);
+  } else if (h->prec == PR_FP16) {
+    prep_faces<PR_FP16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
+    prep_mel<PR_FP16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
+  } else {
+    prep_faces<PR_BF16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
+    prep_mel<PR_BF16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
+  }
+}
+
+static void absmax_into(lsg_gen h, const uint16_t* src, int pitch, int coff, int C, int64_t pixels, unsigned* dst,
+                        cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(pixels * C, 256), 4096);
+  if (h->prec == PR_FP16) absmax_view<PR_FP16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, dst);
+  else absmax_view<PR_BF16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, dst);
+}
+
+extern "C" {
+
+// max |activation| of every fp8 scale group (kTensors: face, mel, cat0..6,
+// per-layer outputs) over a calibration batch, on a 16-bit engine
+lsg_status lsg_gen_calibrate(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
+                             const uint8_t* refs, const int32_t* ref_index, int32_t B, float* absmax, int32_t cap,
+                             int32_t* n_tensors) {
+  return guard([&] {
+    *n_tensors = kTensors;
+    if (cap < kTensors) return;
+    if (h->prec == PR_FP8) invalid("lsg_gen_calibrate: calibrate on a bf16/fp16 engine");
+    if (B <= 0 || B > h->max_batch) invalid("lsg_gen_calibrate: batch out of range");
+    Ctx* ctx = h->ctx;
+    DeviceGuard g(ctx);
+    cudaStream_t st = ctx->stream;
+    DevBuf<unsigned> acc;
+    acc.alloc(kTensors);
+    LSG_CUDA(cudaMemsetAsync(acc.p, 0, kTensors * sizeof(unsigned), st));
+    prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
+    absmax_into(h, h->x_face.p, h->x_face.pitch, h->x_face.coff, h->x_face.C, (int64_t)B * 96 * 96, acc.p + 0, st);
+    absmax_into(h, h->x_mel.p, h->x_mel.pitch, h->x_mel.coff, h->x_mel.C, (int64_t)B * 80 * 16, acc.p + 1, st);
+    for (size_t l = 0; l < h->plan.size(); ++l) {
+      LayerRun& r = h->plan[l];
+      if (r.fused) {
+        r.p.out_mode = r.hp.out_mode = OUT_F32_LOGITS;
+        r.p.final_out = r.hp.final_out = nullptr;
+        continue;  // its result is not stored as a tensor
+      }
+      dispatch(h, r, B, st);
+      const ConvParams& p = r.p;
+      absmax_into(h, p.out, p.out_pitch, p.out_coff, kLayers[l].cout, (int64_t)B * p.OH * p.OW,
+                  acc.p + h->plan_out_id[l], st);
+    }
+    std::vector<unsigned> hv(kTensors);
+    LSG_CUDA(cudaMemcpyAsync(hv.data(), acc.p, kTensors * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < kTensors; ++i) {
+      float f;
+      std::memcpy(&f, &hv[i], 4);
+      absmax[i] = f;
+    }
+  });
+}
+
+lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights, int64_t n_floats, int32_t precision, int32_t max_batch,
+                          lsg_gen* out) {
+  return lsg_gen_create_q(ctx, weights, n_floats, precision, nullptr, 0, max_batch, out);
+}
+
+}  // extern "C"
+
 // ---------------------------------------------------------------- debug
 // Not part of include/lsg.h: test-only introspection used by
 // tests/test_generator.py to check each layer in isolation.
-template <bool HALF>
-__global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int64_t pixels, float* dst) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+template <int PR>
+__global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int64_t pixels, float* dst, float scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // unit index
   if (i >= pixels * C) return;
   const int64_t px = i / C;
   const int c = (int)(i - px * C);
   const uint16_t u = src[px * pitch + coff + c];
-  dst[i] = HALF ? __half2float(__ushort_as_half(u)) : __bfloat162float(__ushort_as_bfloat16(u));
+  if constexpr (PR == PR_FP8) {
+    const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)u, __NV_E4M3);
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hr));
+    dst[2 * i] = f.x * scale;
+    dst[2 * i + 1] = f.y * scale;
+  } else {
+    dst[i] = PR == PR_FP16 ? __half2float(__ushort_as_half(u)) : __bfloat162float(__ushort_as_bfloat16(u));
+  }
 }
 
 extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
@@ -992,12 +1207,7 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     cudaStream_t st = ctx->stream;
-    const int64_t n = (int64_t)B * 96 * 96;
-    if (h->half) prep_faces<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target, nullptr, refs, ref_index, h->x_face.p, B);
-    else prep_faces<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target, nullptr, refs, ref_index, h->x_face.p, B);
-    const int64_t m = (int64_t)B * 80 * 16;
-    if (h->half) prep_mel<true><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
-    else prep_mel<false><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
+    prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
     if (stop_layer < 0 || stop_layer >= (int)h->plan.size() - 1) invalid("lsgdbg_run_until: bad layer");
     for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
     const LayerRun& r = h->plan[stop_layer];
@@ -1006,15 +1216,18 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     const uint16_t* src = which ? p.out : r.in_view.p;
     const int H = which ? p.OH : p.H, W = which ? p.OW : p.W;
     const int pitch = which ? p.out_pitch : r.in_view.pitch, coff = which ? p.out_coff : r.in_view.coff;
-    const int C = which ? L.cout : p.C;
+    const int C = which ? L.cout / h->cpu : p.C;  // units
+    const float scale = h->ascale[which ? h->plan_out_id[stop_layer] : h->plan_in_id[stop_layer]];
     const int64_t pixels = (int64_t)B * H * W;
-    if (h->half) view_to_f32<true><<<(unsigned)ceil_div(pixels * C, 256), 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev);
-    else view_to_f32<false><<<(unsigned)ceil_div(pixels * C, 256), 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev);
+    const unsigned grid = (unsigned)ceil_div(pixels * C, 256);
+    if (h->prec == PR_FP8) view_to_f32<PR_FP8><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, scale);
+    else if (h->prec == PR_FP16) view_to_f32<PR_FP16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, 1.f);
+    else view_to_f32<PR_BF16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, 1.f);
     LSG_CUDA(cudaGetLastError());
     shape4[0] = B;
     shape4[1] = H;
     shape4[2] = W;
-    shape4[3] = C;
+    shape4[3] = C * h->cpu;
   });
 }
 
@@ -1030,15 +1243,8 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
   if (out_format < 0 || out_format > 2) invalid("lsg_gen_forward: unknown output format");
   Ctx* ctx = h->ctx;
   cudaStream_t st = ctx->stream;
-  const int64_t n = (int64_t)B * 96 * 96;
-  if (h->half)
-    prep_faces<true><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target_base, target_idx, refs, ref_index, h->x_face.p, B);
-  else
-    prep_faces<false><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(target_base, target_idx, refs, ref_index, h->x_face.p, B);
+  prep_inputs(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
   LSG_LAUNCHED(ctx);
-  const int64_t m = (int64_t)B * 80 * 16;
-  if (h->half) prep_mel<true><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
-  else prep_mel<false><<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B);
   LSG_LAUNCHED(ctx);
   const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
                                                   : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);

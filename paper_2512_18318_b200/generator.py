@@ -208,21 +208,84 @@ def face_input(target_u8: np.ndarray, ref_u8: np.ndarray) -> np.ndarray:
     return np.concatenate([t, r], axis=2).transpose(2, 0, 1).copy()
 
 
+def calibration_batch(seed: int = 7, frames: int = 64):
+    """Seeded calibration inputs for the fp8 activation ranges (SURVEY §8 d:
+    a 64-frame seeded batch): mel rows of synthetic speech through the
+    library's own mel stage (silence included, so the log floor is in range),
+    jittered synthetic faces.  Returns host arrays
+    (mel_rows [R,80] f32, chunk_row [B] i32, target [B,96,96,3] u8,
+     refs [R,96,96,3] u8, ref_index [B] i32)."""
+    from .api import AudioBuffer, compute_mel, synth_pattern
+    rng = np.random.default_rng(seed)
+    pcm = synth_pattern(300, [(900, 500), (1200, 700), (800, 600)], 220.0, 0.3, 6000)
+    mel = compute_mel(AudioBuffer(samples=pcm)).data.reshape(-1, 80).astype(np.float32)
+    chunk = rng.integers(0, mel.shape[0] - 16, frames).astype(np.int32)
+    refs = np.stack([synthetic_face(seed * 1000 + i) for i in range(4)])
+    ridx = rng.integers(0, 4, frames).astype(np.int32)
+    target = np.stack([np.roll(refs[r], (int(a), int(b)), axis=(0, 1))
+                       for r, a, b in zip(ridx, rng.integers(-3, 4, frames), rng.integers(-3, 4, frames))])
+    return mel, chunk, target.astype(np.uint8), refs.astype(np.uint8), ridx
+
+
+class _Dev:
+    """Device copies of host arrays through the library's allocator."""
+
+    def __init__(self, ctx, arrays):
+        self.ctx, self.ptrs = ctx, []
+        for a in arrays:
+            a = np.ascontiguousarray(a)
+            p = C.c_void_p()
+            ctx.lib.call("lsg_dev_alloc", ctx.h, max(a.nbytes, 1), C.byref(p))
+            ctx.lib.call("lsg_copy", ctx.h, p, C.c_void_p(a.ctypes.data), a.nbytes)
+            self.ptrs.append(p)
+        ctx.sync()
+
+    def free(self):
+        for p in self.ptrs:
+            self.ctx.lib.lsg_dev_free(self.ctx.h, p)
+        self.ptrs = []
+
+
+def calibrate(weights: np.ndarray, ctx, batch=None) -> np.ndarray:
+    """max |x| per fp8 scale group (lsg_gen_calibrate on an fp16 engine)."""
+    mel, chunk, target, refs, ridx = batch or calibration_batch()
+    B = len(chunk)
+    eng = LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=LipsyncEngine.PREC_FP16)
+    dev = _Dev(ctx, [mel, chunk, target, refs, ridx])
+    try:
+        n = C.c_int32()
+        eng.lib.call("lsg_gen_calibrate", eng.h, *dev.ptrs[:5], B, None, 0, C.byref(n))
+        out = np.zeros(n.value, np.float32)
+        eng.lib.call("lsg_gen_calibrate", eng.h, *dev.ptrs[:5], B, C.c_void_p(out.ctypes.data), n.value, C.byref(n))
+    finally:
+        dev.free()
+        eng.close()
+    return out
+
+
 class LipsyncEngine:
     """The lip-sync stage on the GPU (lsg_gen): replaces mock_lipsync's cost
-    model (visual_mocks.hpp:41-43) with the generator forward."""
+    model (visual_mocks.hpp:41-43) with the generator forward.  precision
+    PREC_FP8 calibrates per-tensor activation ranges first (calibrate())."""
 
-    PREC_BF16, PREC_FP16 = 0, 1
+    PREC_BF16, PREC_FP16, PREC_FP8 = 0, 1, 2
 
-    def __init__(self, weights: np.ndarray, max_batch: int = 128, ctx=None, precision: int = 1):
+    def __init__(self, weights: np.ndarray, max_batch: int = 128, ctx=None, precision: int = 1, calib=None):
         from .api import default_context
         self.ctx = ctx or default_context()
         self.lib = self.ctx.lib
         w = np.ascontiguousarray(weights, np.float32)
         h = C.c_void_p()
         self.precision = precision
-        self.lib.call("lsg_gen_create", self.ctx.h, C.c_void_p(w.ctypes.data), w.size, precision, max_batch,
-                      C.byref(h))
+        self.act_absmax = None
+        if precision == self.PREC_FP8:
+            self.act_absmax = calibrate(w, self.ctx, calib)
+            a = self.act_absmax
+            self.lib.call("lsg_gen_create_q", self.ctx.h, C.c_void_p(w.ctypes.data), w.size, precision,
+                          C.c_void_p(a.ctypes.data), a.size, max_batch, C.byref(h))
+        else:
+            self.lib.call("lsg_gen_create", self.ctx.h, C.c_void_p(w.ctypes.data), w.size, precision, max_batch,
+                          C.byref(h))
         self.h = h
         self.max_batch = max_batch
 

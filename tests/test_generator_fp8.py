@@ -1,0 +1,174 @@
+"""FP8 (e4m3) generator: per-output-channel weight
+scales, per-tensor activation scales from lsg_gen_calibrate (the fp16
+engine's |x| maxima on a seeded 64-frame batch; concat buffers share one
+scale), f32 accumulation.
+
+Checks: every layer in isolation against an fp32 conv of the GPU's own
+dequantised input with the same e4m3-quantised weights -- the only error left
+is the output's e4m3 rounding (half an ulp = 1/16 relative) -- and the whole
+forward against a CPU fp8 rounding model with the engine's scales."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from test_generator import _inputs, _oracle  # noqa: F401
+
+
+@pytest.fixture(scope="module")
+def gref():
+    return _oracle()
+
+
+@pytest.fixture(scope="module")
+def weights(lsg):
+    from paper_2512_18318_b200 import generator
+    return generator.synthetic_weights(seed=0)
+
+
+def _wq(torch, w, kind):
+    """e4m3 with one scale per output channel (dim 0 for conv, 1 for convT),
+    as lsg_gen_create_q packs them."""
+    t = torch.from_numpy(np.ascontiguousarray(w)).float()
+    co_dim = 0 if kind == 0 else 1
+    red = [d for d in range(4) if d != co_dim]
+    m = t.abs().amax(dim=red, keepdim=True)
+    s = torch.where(m > 0, m / 448.0, torch.ones_like(m))
+    return (t / s).to(torch.float8_e4m3fn).float() * s
+
+
+@pytest.mark.gpu
+def test_calibration_groups(weights, lsg):
+    torch = pytest.importorskip("torch")  # noqa: F841
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    a = generator.calibrate(weights, ctx)
+    assert a.shape == (9 + 51,)
+    assert 0.5 <= a[0] <= 1.0          # faces in [0, 1]
+    assert 20.0 < a[1] < 30.0          # mel: log floor ln(1e-10) = -23
+    assert (a[2:9] > 0).all()          # every concat buffer written
+    assert np.isfinite(a).all()
+
+
+@pytest.mark.gpu
+def test_fp8_every_layer_in_isolation(weights, gref):
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    B = 3
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
+    rows, chunk_row, target, refs, ref_index = _inputs(B, 77)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    buf = torch.empty(B * 96 * 96 * 1024, dtype=torch.float32, device="cuda")
+    shape = (C.c_int32 * 4)()
+    fn = eng.lib.dll.lsgdbg_run_until
+    params = gref.split_blob(weights)
+    Ls = generator.layers()
+
+    def dump(layer, which):
+        rc = fn(eng.h, *[C.c_void_p(t.data_ptr()) for t in d], B, layer, which, C.c_void_p(buf.data_ptr()), shape)
+        assert rc == 0
+        torch.cuda.synchronize()
+        n = shape[0] * shape[1] * shape[2] * shape[3]
+        return buf[:n].reshape(*shape).permute(0, 3, 1, 2).cpu()
+    worst = 0.0
+    for i in range(len(Ls) - 2):  # out0+out1 fused: covered end to end
+        L = Ls[i]
+        x, y = dump(i, 0)[:, :L.cin], dump(i, 1)
+        w = _wq(torch, params[i][0], L.kind)
+        b = torch.from_numpy(np.ascontiguousarray(params[i][1]))
+        ref = F.conv2d(x, w, b, (L.sh, L.sw), (L.ph, L.pw)) if L.kind == 0 else \
+            F.conv_transpose2d(x, w, b, (L.sh, L.sw), (L.ph, L.pw), (L.oph, L.opw))
+        ref = torch.relu(ref + x if L.res else ref)
+        rel = (y - ref).abs().max().item() / (ref.abs().max().item() + 1e-6)
+        worst = max(worst, rel)
+        assert rel < 0.07, f"layer {i}: rel err {rel:.4f}"  # e4m3 half-ulp = 1/16
+    print(f"fp8 worst per-layer error {worst:.4f} of the layer max")
+    eng.close()
+    ctx.set_stream(None)
+
+
+def fp8_rounding_model(gref, blob, mel, faces, absmax):
+    """The fp32 oracle with e4m3 weights (per output channel) and every stored
+    activation rounded to e4m3 with its calibrated per-tensor scale -- face /
+    mel inputs, concat buffers (shared by both producers), other layer
+    outputs -- exactly the quantisation points of the fp8 engine."""
+    import torch
+    import torch.nn.functional as F
+    scale = np.maximum(absmax, 1e-6) * 1.1 / 448.0
+
+    def q(t, s):
+        return (t / s).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).float() * s
+    layers = list(zip(gref.layer_table(), gref.split_blob(blob)))
+    li = [0]
+
+    def conv(x):
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        wq = _wq(torch, w, kind)
+        b = torch.from_numpy(np.ascontiguousarray(b))
+        y = F.conv2d(x, wq, b, s_, p) if kind == 0 else F.conv_transpose2d(x, wq, b, s_, p, op)
+        if res:
+            y = y + x
+        li[0] += 1
+        return torch.relu(y)
+    with torch.no_grad():
+        x = q(torch.from_numpy(faces), scale[0])
+        feats = []
+        for j, blk in enumerate(gref.FACE):
+            for n, _ in enumerate(blk):
+                tid = 2 + (6 - j) if n == len(blk) - 1 else 9 + li[0]
+                x = q(conv(x), scale[tid])
+            feats.append(x)
+        a = q(torch.from_numpy(mel), scale[1])
+        for _ in gref.AUDIO:
+            a = q(conv(a), scale[9 + li[0]])
+        x = a
+        for j, blk in enumerate(gref.DECODER):
+            for n, _ in enumerate(blk):
+                tid = 2 + j if n == len(blk) - 1 else 9 + li[0]
+                x = q(conv(x), scale[tid])
+            x = torch.cat([x, feats.pop()], 1)
+        x = conv(x)  # out0: kept in f32 by the fused epilogue
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        y = F.conv2d(x, torch.from_numpy(np.ascontiguousarray(w)), torch.from_numpy(np.ascontiguousarray(b)))
+        return torch.sigmoid(y).numpy()
+
+
+@pytest.mark.gpu
+def test_fp8_forward_tracks_fp8_rounding_model(weights, gref):
+    """End to end, this random-weight network amplifies rounding noise
+    enormously (bf16, half-ulp 2^-9: ~30 dB; e4m3, half-ulp 2^-4: ~6 dB vs
+    fp32), so, as for bf16, the bound is that the GPU lands within 3 dB of
+    the CPU fp8 rounding model built from the engine's own scales; the
+    per-layer test above is the exactness check."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    B = 16
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
+    rows, chunk_row, target, refs, ref_index = _inputs(B, 116)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    out = torch.empty(B, 3, 96, 96, dtype=torch.float32, device="cuda")
+    u8 = torch.empty(B, 96, 96, 3, dtype=torch.uint8, device="cuda")
+    eng.forward_device(*[t.data_ptr() for t in d], out.data_ptr(), 0, B)
+    eng.forward_device(*[t.data_ptr() for t in d], u8.data_ptr(), 1, B)
+    torch.cuda.synchronize()
+    mel = np.stack([gref.mel_chunk(rows, int(r))[None] for r in chunk_row])
+    faces = np.stack([gref.face_input(target[b], refs[ref_index[b]]) for b in range(B)])
+    want = gref.forward(weights, mel, faces)
+    got = out.cpu().numpy()
+    assert np.isfinite(got).all()
+    p = gref.psnr(got, want)
+    model = fp8_rounding_model(gref, weights, mel, faces, eng.act_absmax)
+    pm = gref.psnr(model, want)
+    print(f"fp8 PSNR vs fp32 oracle: GPU {p:.1f} dB, CPU fp8 rounding model {pm:.1f} dB")
+    assert abs(p - pm) <= 3.0, f"fp8 GPU {p:.1f} dB vs rounding model {pm:.1f} dB"
+    assert np.abs(u8.cpu().numpy().astype(int) - np.round(got.transpose(0, 2, 3, 1) * 255).astype(int)).max() <= 1
+    eng.close()
+    ctx.set_stream(None)
