@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--paced-seconds", type=int, default=20, help="config-5 paced leg length (0: skip)")
     ap.add_argument("--paced-streams", type=int, default=256, help="config-5 paced streams over all GPUs")
     ap.add_argument("--scaled-streams", type=int, default=512, help="segmenter/mel roofline set: streams x 60 s")
+    ap.add_argument("--config4-streams", type=int, default=8, help="fp8 leg (config 4): streams per GPU (0: skip)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -336,6 +337,9 @@ def main():
         ctx.set_stream(torch_stream.cuda_stream)
     # ------------------------------- segmenter / mel rooflines (scaled set)
     scaled = scaled_leg(args, local, torch, ctx, torch_stream, api) if args.scaled_streams > 0 else None
+    # ---------------------------------- config 4: fp8 generator, batches of 128
+    cfg4 = config4_leg(args, rank, world, local, dist, torch, ctx, torch_stream, api, generator, weights, fps) \
+        if args.config4_streams > 0 else None
     # -------------------------------------------- generator kernel roofline
     B = args.batch
     gen_ms = measure_generator(eng, torch, torch_stream, local, B, reps=10)
@@ -382,6 +386,8 @@ def main():
         out["p99_segment_latency_ms"] = paced["p99_ms"]
     if scaled:
         out["stage_rooflines"] = scaled
+    if cfg4:
+        out["config4_fp8"] = cfg4
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
@@ -538,6 +544,66 @@ def scaled_leg(args, local, torch, ctx, stream, api):
                 "peak_fp64_tflops": cc["fp64"], "peak_source": cc["source"], "t_roof_ms": t_roof * 1e3,
                 "frac": t_roof * 1e3 / t_mel, "timed": "lsg_mel_compute_batch over every segment of the set"},
     }
+
+
+def fp8_peaks():
+    path = os.path.join(ROOT, "profiles", "r01_fp8_peak.json")
+    try:
+        d = json.load(open(path))
+        return d["tflops_burst"], d["tflops_sustained"], "profiles/r01_fp8_peak.json (tools/fp8_peak.py, cuBLASLt 8192^3)"
+    except (OSError, ValueError, KeyError):
+        pk = measured_peaks()
+        return 2 * pk.get("bf16_tflops", 1590.0), 2 * pk.get("bf16_tflops_sustained", 1400.0), "2x bf16 (fallback)"
+
+
+def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generator, weights, fps):
+    """Config 4: the fp8-quantised generator (per-channel weight / per-tensor
+    activation scales calibrated on device) behind the same unpaced
+    segmenter -> mel -> generator pipeline, config4_streams streams per GPU
+    (64 over 8 GPUs), generator batches of 128; plus the B=128 forward alone
+    against the measured fp8 tensor peak."""
+    from paper_2512_18318_b200.pipeline import Pipeline, PipelineConfig
+    S, secs = args.config4_streams, 30
+    eng8 = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
+    pipe = Pipeline(PipelineConfig(S, secs * 1000, fps, 50, 128, True), eng8, ctx=ctx)
+    pcm, video, refs = make_workload(rank, S, secs, fps, api, generator, world, seed_base=2000)
+    dev = f"cuda:{local}"
+    d_pcm = [torch.from_numpy(p).to(dev) for p in pcm]
+    d_vid = [torch.from_numpy(v).to(dev) for v in video]
+    d_refs = torch.from_numpy(refs).to(dev)
+    torch.cuda.synchronize()
+    ns, nv = [len(p) for p in pcm], [len(v) for v in video]
+
+    def step():
+        return pipe.run_ptrs([t.data_ptr() for t in d_pcm], ns, [t.data_ptr() for t in d_vid], nv, d_refs.data_ptr(),
+                             0, 0, None)
+    for _ in range(3):
+        step()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(3):
+        frames, _ = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    from paper_2512_18318_b200.shard import max_over_ranks
+    ms = max_over_ranks(e0.elapsed_time(e1) / 3, dist, device=dev)
+    gms = measure_generator(eng8, torch, stream, local, 128, reps=20)
+    burst, sust, src = fp8_peaks()
+    tf = FLOPS_PER_FRAME * 128 / (gms / 1e3) / 1e12
+    out = {"workload": f"config 4: fp8 generator, {S} streams/GPU x {secs} s, unpaced, batch 128",
+           "dtype": "fp8_e4m3 (f32 accumulate)", "value": frames * world / (ms / 1e3), "unit": "frames/s",
+           "ms_per_step": ms, "frames_per_step": frames * world,
+           "generator_b128": {"ms": gms, "frames_per_s": 128 / (gms / 1e3), "achieved_tflops": tf,
+                              "peak_tflops": sust, "frac": tf / sust, "frac_vs_burst": tf / burst,
+                              "peak_source": src},
+           "quality": "per-layer exact up to e4m3 output rounding; end to end tracks the CPU fp8 rounding model "
+                      "(tests/test_generator_fp8.py)"}
+    pipe.close()
+    eng8.close()
+    return out
 
 
 def measure_generator(eng, torch, stream, local, B, reps=10):
