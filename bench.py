@@ -347,6 +347,10 @@ def main():
     achieved = FLOPS_PER_FRAME * B / (gen_ms / 1000.0) / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
     gen_b128_ms = measure_generator(eng, torch, torch_stream, local, 128, reps=10) if B >= 128 else None
+    # config 3 as BASELINE.json states it: bf16, batch 128
+    eng_bf = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_BF16)
+    bf16_b128_ms = measure_generator(eng_bf, torch, torch_stream, local, 128, reps=10)
+    eng_bf.close()
     clocks = clk.summary()
     if rank != 0:
         if dist:
@@ -377,6 +381,9 @@ def main():
         "generator_b128": ({"ms": gen_b128_ms, "frames_per_s": 128 / (gen_b128_ms / 1000.0),
                             "tflops": FLOPS_PER_FRAME * 128 / (gen_b128_ms / 1000.0) / 1e12}
                            if gen_b128_ms else None),
+        "config3_bf16_b128": {"ms": bf16_b128_ms, "frames_per_s": 128 / (bf16_b128_ms / 1000.0),
+                              "achieved_tflops": FLOPS_PER_FRAME * 128 / (bf16_b128_ms / 1000.0) / 1e12,
+                              "frac": FLOPS_PER_FRAME * 128 / (bf16_b128_ms / 1000.0) / 1e12 / peak},
         "clocks": clocks,
         "gpu_launches": launches,
     }
