@@ -533,6 +533,44 @@ def scaled_leg(args, local, torch, ctx, stream, api):
             stream.synchronize()
             if rep:
                 mel_ms.append(e0.elapsed_time(e1))
+        # ---- A/V alignment (row f2): energy envelope of every stream (HBM:
+        # 2 B/sample in, 8 B/ms out), then NCC of each segment's envelope
+        # against a motion envelope lagging it by a known offset
+        import ctypes as Cc
+        lib = ctx.lib
+        env = torch.empty(S * secs * 1000, dtype=torch.float64, device=dev)
+        i64 = lambda xs: (Cc.c_int64 * len(xs))(*[int(x) for x in xs])  # noqa: E731
+        olen = (Cc.c_int64 * S)()
+        en_ms = []
+        for rep in range(4):
+            flush.zero_()
+            e0.record(stream)
+            lib.call("lsg_align_energy", ctx.h, S, Cc.c_void_p(base), i64([s * n for s in range(S)]), i64([n] * S),
+                     16000, Cc.c_void_p(env.data_ptr()), i64([s * secs * 1000 for s in range(S)]), olen)
+            e1.record(stream)
+            stream.synchronize()
+            if rep:
+                en_ms.append(e0.elapsed_time(e1))
+        segs = [c for c in cuts if c.end - c.begin > 120][:4096]
+        shift = [((i * 7) % 21) - 10 for i in range(len(segs))]
+        e_off = [c.stream * secs * 1000 + c.begin for c in segs]
+        e_len = [c.end - c.begin for c in segs]
+        m_off = [o - sh for o, sh in zip(e_off, shift)]  # motion[t] = energy[t - shift]: lags by `shift`
+        m_off = [max(0, o) for o in m_off]
+        res = (Cc.c_char * (24 * len(segs)))()
+        al_ms = []
+        for rep in range(3):
+            e0.record(stream)
+            lib.call("lsg_align_batch", ctx.h, len(segs), Cc.c_void_p(env.data_ptr()), i64(e_off), i64(e_len),
+                     Cc.c_void_p(env.data_ptr()), i64(m_off), i64(e_len), 50, res)
+            e1.record(stream)
+            stream.synchronize()
+            if rep:
+                al_ms.append(e0.elapsed_time(e1))
+        import struct
+        offs = [struct.unpack_from("<qdii", bytes(res), 24 * i)[0] for i in range(len(segs))]
+        recovered = sum(1 for o, sh, mo in zip(offs, shift, m_off) if mo > 0 and o == sh)
+        checkable = sum(1 for mo in m_off if mo > 0)
     peaks, cc = measured_peaks(), cuda_core_peaks()
     t_seg = float(np.median(seg_ms))
     nbytes = S * n * 2
@@ -546,6 +584,17 @@ def scaled_leg(args, local, torch, ctx, stream, api):
                       "frac": nbytes / (t_seg / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0), "segments": len(cuts),
                       "timed": "lsg_seg_push + lsg_seg_finish over all streams (device events, includes the cut "
                                "readback sync)"},
+        "align": {"energy_envelope": {"bound": "hbm", "ms": float(np.median(en_ms)),
+                                      "bytes": nbytes + S * secs * 1000 * 8,
+                                      "achieved": (nbytes + S * secs * 1000 * 8) / (float(np.median(en_ms)) / 1e3) / 1e9,
+                                      "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
+                                      "frac": (nbytes + S * secs * 1000 * 8) / (float(np.median(en_ms)) / 1e3) / 1e9
+                                      / peaks.get("hbm_gbs", 6650.0)},
+                  "ncc": {"pairs": len(segs), "ms": float(np.median(al_ms)), "max_lag": 50,
+                          "lag_ms_products": int(sum(101 * max(0, l - 100) for l in e_len)),
+                          "offsets_recovered": f"{recovered}/{checkable}",
+                          "note": "one CTA per segment, one thread per lag, sequential sums (bit-identical to "
+                                  "align.cpp): latency-bound by design"}},
         "mel": {"bound": "fp64", "ms": t_mel, "frames": F, "flops_fp64_per_frame": 25600,
                 "flops_fp32_per_frame": 4645, "achieved_fp64_tflops": F * 25600 / (t_mel / 1e3) / 1e12,
                 "peak_fp64_tflops": cc["fp64"], "peak_source": cc["source"], "t_roof_ms": t_roof * 1e3,

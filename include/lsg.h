@@ -205,6 +205,33 @@ lsg_status lsg_gen_forward(lsg_gen h, const float* mel_rows, const int32_t* chun
  * n_frames < 2 or |audio_span - frame_span| > 150 ms. */
 lsg_status lsg_lipsync_validate(int64_t audio_span_ms, int64_t frame_span_ms, int64_t n_frames);
 
+/* ------------------------------------------------------------ alignment
+ * A/V alignment, batched and bit-identical to align.cpp.
+ * Offsets / lengths are [host]; *_base pointers [dev]. */
+typedef struct {
+  int64_t offset_ms;           /* positive: motion lags the audio            */
+  double peak_corr;
+  int32_t low_confidence;
+  int32_t pad;
+} lsg_align_result;            /* AlignResult (align.hpp:17-21)              */
+/* energy_envelope_ms (align.cpp:10-32) of n PCM segments: segment i is
+ * n_samples[i] samples at pcm_base + pcm_off[i]; its llround(1000 n / rate)
+ * ms envelope goes to out_base + out_off[i]; out_len[i] [host] on return. */
+lsg_status lsg_align_energy(lsg_ctx ctx, int32_t n, const int16_t* pcm_base, const int64_t* pcm_off,
+                            const int64_t* n_samples, int32_t sample_rate, double* out_base,
+                            const int64_t* out_off, int64_t* out_len);
+/* motion_envelope_ms (align.cpp:34-50): segment i reads n_frames[i]
+ * (ts, mouth_motion) records from frame_off[i] (sorted by ts) and writes
+ * span[i] ms starting at t0[i] to out_base + out_off[i]. */
+lsg_status lsg_align_motion(lsg_ctx ctx, int32_t n, const int64_t* ts_base, const double* motion_base,
+                            const int64_t* frame_off, const int64_t* n_frames, const int64_t* t0,
+                            const int64_t* span, double* out_base, const int64_t* out_off);
+/* align_envelopes (align.cpp:52-116) for n (energy, motion) pairs; results
+ * [host].  EINVAL for max_lag < 0 (the reference's throw) or > 511. */
+lsg_status lsg_align_batch(lsg_ctx ctx, int32_t n, const double* energy_base, const int64_t* e_off,
+                           const int64_t* e_len, const double* motion_base, const int64_t* m_off,
+                           const int64_t* m_len, int64_t max_lag, lsg_align_result* out);
+
 /* -------------------------------------------------------------- pipeline
  * Replaces the per-clip driver run_pipeline_input (runner.cpp:239-351) for
  * the GPU stages: segment -> mel per segment -> gather frames -> generator,

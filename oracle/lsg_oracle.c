@@ -333,3 +333,116 @@ int64_t or_compute_mel(const int16_t* pcm, int64_t n, const or_mel_cfg* c, float
   free(win); free(w); free(buf); free(pw);
   return frames;
 }
+
+/* ======================================================== A/V alignment */
+
+/* align.cpp:10-32: RMS over 10 ms hops of v = s / 32768, held for each ms of
+ * the hop; sequential sums, no contraction (the reference's x86-64 build). */
+int64_t or_energy_envelope(const int16_t* pcm, int64_t n, int rate, double* out, int64_t cap) {
+  if (rate <= 0) return -1;
+  const int64_t total = llround(1000.0 * (double)n / rate);
+  if (total <= 0) return 0;
+  const int64_t hop = (int64_t)rate * 10 / 1000;
+  if (hop <= 0) return -1;
+  if (total > cap) return total;
+  for (int64_t t = 0; t < total; t += 10) {
+    const int64_t s0 = t / 10 * hop;
+    const int64_t s1 = s0 + hop < n ? s0 + hop : n;
+    volatile double sumsq = 0.0;
+    for (int64_t s = s0; s < s1; ++s) {
+      const volatile double v = pcm[s] / 32768.0;
+      const volatile double vv = v * v;
+      sumsq = sumsq + vv;
+    }
+    const double rms = s1 > s0 ? sqrt(sumsq / (double)(s1 - s0)) : 0.0;
+    for (int64_t k = t; k < (t + 10 < total ? t + 10 : total); ++k) out[k] = rms;
+  }
+  return total;
+}
+
+/* align.cpp:34-50: each frame's value holds until the next frame; 0 before
+ * the first frame. */
+int or_motion_envelope(const int64_t* ts, const double* motion, int64_t nf, int64_t t0, int64_t span, double* out) {
+  if (span < 0) return -1;
+  int64_t f = 0;
+  double held = 0.0;
+  int have = 0;
+  for (int64_t t = 0; t < span; ++t) {
+    while (f < nf && ts[f] <= t0 + t) {
+      held = motion[f];
+      have = 1;
+      ++f;
+    }
+    out[t] = have ? held : 0.0;
+  }
+  return 0;
+}
+
+/* align.cpp:52-116: normalised cross-correlation over lags in
+ * [-max_lag, max_lag] on the full-overlap region [max_lag, D - max_lag);
+ * ties prefer the smaller |lag|, then the negative one. */
+int or_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm, int64_t max_lag,
+                       or_align_result* r) {
+  if (max_lag < 0) return -1;
+  r->offset_ms = 0;
+  r->peak_corr = 0.0;
+  r->low_confidence = 0;
+  const int64_t d = ne < nm ? ne : nm;
+  const int64_t lo = max_lag, hi = d - max_lag;
+  if (hi - lo < 2) {
+    r->low_confidence = 1;
+    return 0;
+  }
+  const double n = (double)(hi - lo);
+  volatile double e_mean = 0.0;
+  for (int64_t t = lo; t < hi; ++t) e_mean = e_mean + e[t];
+  e_mean = e_mean / n;
+  volatile double e_var = 0.0;
+  for (int64_t t = lo; t < hi; ++t) {
+    const volatile double v = e[t] - e_mean;
+    const volatile double vv = v * v;
+    e_var = e_var + vv;
+  }
+  const double e_sigma = sqrt(e_var);
+  if (e_sigma < 1e-12) {
+    r->low_confidence = 1;
+    return 0;
+  }
+  int any = 0;
+  double best = 0.0;
+  int64_t best_lag = 0;
+  for (int64_t lag = -max_lag; lag <= max_lag; ++lag) {
+    volatile double m_mean = 0.0;
+    for (int64_t t = lo; t < hi; ++t) m_mean = m_mean + m[t + lag];
+    m_mean = m_mean / n;
+    volatile double m_var = 0.0, dot = 0.0;
+    for (int64_t t = lo; t < hi; ++t) {
+      const volatile double me = m[t + lag] - m_mean;
+      const volatile double mm = me * me;
+      m_var = m_var + mm;
+      const volatile double de = e[t] - e_mean;
+      const volatile double p = de * me;
+      dot = dot + p;
+    }
+    const double m_sigma = sqrt(m_var);
+    if (m_sigma < 1e-12) continue;
+    const double corr = dot / (e_sigma * m_sigma);
+    int better = !any || corr > best;
+    if (any && corr == best) {
+      const int64_t al = lag < 0 ? -lag : lag, ab = best_lag < 0 ? -best_lag : best_lag;
+      better = al < ab || (al == ab && lag < best_lag);
+    }
+    if (better) {
+      any = 1;
+      best = corr;
+      best_lag = lag;
+    }
+  }
+  if (!any) {
+    r->low_confidence = 1;
+    return 0;
+  }
+  r->offset_ms = best_lag;
+  r->peak_corr = best;
+  return 0;
+}

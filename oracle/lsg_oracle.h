@@ -107,6 +107,22 @@ int64_t or_compute_mel(const int16_t* pcm, int64_t n, const or_mel_cfg* c, float
 /* filterbank W[m][b] (n_mels x (fft/2+1)) exactly as mel.cpp builds it */
 int or_mel_filterbank(const or_mel_cfg* c, double* w);
 
+/* ---------------------------------------------------------- A/V alignment
+ * Restatement of align.cpp. */
+typedef struct {
+  int64_t offset_ms;
+  double peak_corr;
+  int low_confidence;
+} or_align_result;
+/* energy_envelope_ms (align.cpp:10-32): returns the length (whole ms of the
+ * buffer, llround(1000 n / rate)), writes it when cap allows */
+int64_t or_energy_envelope(const int16_t* pcm, int64_t n, int rate, double* out, int64_t cap);
+/* motion_envelope_ms (align.cpp:34-50): frames sorted by ts */
+int or_motion_envelope(const int64_t* ts, const double* motion, int64_t nf, int64_t t0, int64_t span, double* out);
+/* align_envelopes (align.cpp:52-116) */
+int or_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm, int64_t max_lag,
+                       or_align_result* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,7 @@
 // ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference
 // sources (lipstream::Segmenter, VadTracker, compute_mel, render_pattern,
-// expected_segment_durations), compiled from /root/reference by
+// expected_segment_durations, the A/V alignment of align.cpp), compiled
+// from /root/reference by
 // oracle/Makefile into oracle/_ref/libref_lipstream.so.
 //
 // TEST INFRASTRUCTURE ONLY: used by tests/ to pin the C restatement
@@ -11,6 +12,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "lipstream/align.hpp"
 #include "lipstream/mel.hpp"
 #include "lipstream/rng.hpp"
 #include "lipstream/segmenter.hpp"
@@ -251,5 +253,46 @@ int ref_write_mel(const char* path, const float* data, int64_t frames, int n_mel
 }
 
 uint64_t ref_splitmix64(uint64_t* state) { return splitmix64(*state); }
+double ref_u64_to_unit(uint64_t v) { return u64_to_unit(v); }
+
+// energy_envelope_ms (align.cpp:10-32); returns the length, writes when cap allows
+int64_t ref_energy_envelope(const int16_t* pcm, int64_t n, int rate, double* out, int64_t cap) {
+  AudioBuffer a;
+  a.samples.assign(pcm, pcm + n);
+  a.sample_rate = rate;
+  std::vector<double> e = energy_envelope_ms(a);
+  if ((int64_t)e.size() <= cap) std::memcpy(out, e.data(), e.size() * sizeof(double));
+  return (int64_t)e.size();
+}
+
+// motion_envelope_ms (align.cpp:34-50) from frame (ts, mouth_motion) pairs
+int ref_motion_envelope(const int64_t* ts, const double* motion, int64_t nf, int64_t t0, int64_t span, double* out) {
+  try {
+    std::vector<FrameRecord> fr((size_t)nf);
+    for (int64_t i = 0; i < nf; ++i) {
+      fr[(size_t)i].ts = ts[i];
+      fr[(size_t)i].mouth_motion = motion[i];
+    }
+    std::vector<double> e = motion_envelope_ms(fr, t0, span);
+    std::memcpy(out, e.data(), e.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// align_envelopes (align.cpp:52-116)
+int ref_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm, int64_t max_lag, int64_t* offset,
+                        double* corr, int* low) {
+  try {
+    AlignResult r = align_envelopes(std::vector<double>(e, e + ne), std::vector<double>(m, m + nm), max_lag);
+    *offset = r.offset_ms;
+    *corr = r.peak_corr;
+    *low = r.low_confidence ? 1 : 0;
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
 
 }  // extern "C"

@@ -110,6 +110,9 @@ _SIGS = {
     "lsg_gen_destroy": [P],
     "lsg_gen_forward": [P, P, P, P, P, P, P, I32, I32],
     "lsg_lipsync_validate": [I64, I64, I64],
+    "lsg_align_energy": [P, I32, P, PI64, PI64, I32, P, PI64, PI64],
+    "lsg_align_motion": [P, I32, P, P, PI64, PI64, PI64, PI64, P, PI64],
+    "lsg_align_batch": [P, I32, P, PI64, PI64, P, PI64, PI64, I64, P],
     "lsg_pipe_create": [P, C.POINTER(PipeCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), P, PP],
     "lsg_pipe_destroy": [P],
     "lsg_pipe_run": [P, PP, PI64, PP, PI64, P, C.POINTER(FrameRec), P, I64, PI64, C.POINTER(PipeStats)],

@@ -471,3 +471,115 @@ __all__ = ["AudioBuffer", "BoundaryContext", "BoundaryDecision", "Context", "Cut
            "LogicError", "MelConfig", "MelExtractor", "MelSpectrogram", "MultiStreamSegmenter", "PeakMode",
            "RawSegment", "Segmenter", "SegmenterConfig", "SegmenterMetrics", "SegmenterMode", "VadConfig",
            "compute_mel", "default_context", "mel_frame_count", "synth_pattern"]
+
+
+# ------------------------------------------------------------ A/V alignment
+@dataclass
+class AlignResult:
+    """align.hpp:17-21."""
+    offset_ms: int = 0  # positive: motion lags the audio
+    peak_corr: float = 0.0
+    low_confidence: bool = False
+
+
+class AlignRes(C.Structure):
+    _fields_ = [("offset_ms", C.c_int64), ("peak_corr", C.c_double), ("low_confidence", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class _DevArrays:
+    """Device copies of host arrays (the drop-ins take host data, like the
+    reference's const references)."""
+
+    def __init__(self, ctx: Context, *arrays):
+        self.ctx, self.ptrs = ctx, []
+        for a in arrays:
+            p = C.c_void_p()
+            ctx.lib.call("lsg_dev_alloc", ctx.h, max(a.nbytes, 16), C.byref(p))
+            if a.nbytes:
+                ctx.lib.call("lsg_copy", ctx.h, p, _ptr(a), a.nbytes)
+            self.ptrs.append(p)
+
+    def free(self):
+        for p in self.ptrs:
+            self.ctx.lib.lsg_dev_free(self.ctx.h, p)
+        self.ptrs = []
+
+
+def _i64(xs):
+    return (C.c_int64 * max(len(xs), 1))(*[int(x) for x in xs])
+
+
+def energy_envelope_ms(audio: AudioBuffer, ctx: Context | None = None) -> np.ndarray:
+    """Drop-in for energy_envelope_ms (align.hpp:12): RMS of 10 ms hops, held per ms (GPU)."""
+    return energy_envelopes([audio], ctx)[0]
+
+
+def energy_envelopes(audios, ctx: Context | None = None) -> list[np.ndarray]:
+    """Batched energy_envelope_ms: one lsg_align_energy call for many buffers."""
+    ctx = ctx or default_context()
+    if not audios:
+        return []
+    rate = audios[0].sample_rate
+    if any(a.sample_rate != rate for a in audios):
+        raise ValueError("energy_envelopes: one sample rate per batch")
+    pcm = [np.ascontiguousarray(a.samples, np.int16) for a in audios]
+    offs = np.cumsum([0] + [len(p) for p in pcm[:-1]])
+    lens = [int(round(1000.0 * len(p) / rate)) if rate > 0 else 0 for p in pcm]
+    oo = np.cumsum([0] + lens[:-1])
+    allpcm = np.concatenate(pcm) if sum(len(p) for p in pcm) else np.zeros(1, np.int16)
+    out = np.zeros(max(sum(lens), 1), np.float64)
+    dev = _DevArrays(ctx, allpcm, out)
+    try:
+        got = (C.c_int64 * len(pcm))()
+        ctx.lib.call("lsg_align_energy", ctx.h, len(pcm), dev.ptrs[0], _i64(offs), _i64([len(p) for p in pcm]), rate,
+                     dev.ptrs[1], _i64(oo), got)
+        ctx.lib.call("lsg_copy", ctx.h, _ptr(out), dev.ptrs[1], out.nbytes)
+        ctx.sync()
+    finally:
+        dev.free()
+    return [out[o:o + n].copy() for o, n in zip(oo, lens)]
+
+
+def motion_envelope_ms(frames, t0: int, span: int, ctx: Context | None = None) -> np.ndarray:
+    """Drop-in for motion_envelope_ms (align.hpp:16): frames = [(ts, mouth_motion)] sorted by ts (GPU)."""
+    if span < 0:
+        raise ValueError("align: negative span")
+    ctx = ctx or default_context()
+    ts = np.ascontiguousarray([f[0] for f in frames] or [0], np.int64)
+    mo = np.ascontiguousarray([f[1] for f in frames] or [0.0], np.float64)
+    out = np.zeros(max(span, 1), np.float64)
+    dev = _DevArrays(ctx, ts, mo, out)
+    try:
+        ctx.lib.call("lsg_align_motion", ctx.h, 1, dev.ptrs[0], dev.ptrs[1], _i64([0]), _i64([len(frames)]),
+                     _i64([t0]), _i64([span]), dev.ptrs[2], _i64([0]))
+        ctx.lib.call("lsg_copy", ctx.h, _ptr(out), dev.ptrs[2], out.nbytes)
+        ctx.sync()
+    finally:
+        dev.free()
+    return out[:span].copy()
+
+
+def align_envelopes(energy, motion, max_lag: int = 50, ctx: Context | None = None) -> AlignResult:
+    """Drop-in for align_envelopes (align.hpp:33-35) (GPU)."""
+    return align_batch([(energy, motion)], max_lag, ctx)[0]
+
+
+def align_batch(pairs, max_lag: int = 50, ctx: Context | None = None) -> list[AlignResult]:
+    """align_envelopes for many (energy, motion) pairs in one lsg_align_batch call."""
+    ctx = ctx or default_context()
+    if not pairs:
+        return []
+    es = [np.ascontiguousarray(e, np.float64) for e, _ in pairs]
+    ms = [np.ascontiguousarray(m, np.float64) for _, m in pairs]
+    eo, mo = np.cumsum([0] + [len(e) for e in es[:-1]]), np.cumsum([0] + [len(m) for m in ms[:-1]])
+    ea = np.concatenate(es) if sum(len(e) for e in es) else np.zeros(1)
+    ma = np.concatenate(ms) if sum(len(m) for m in ms) else np.zeros(1)
+    dev = _DevArrays(ctx, ea, ma)
+    res = (AlignRes * len(pairs))()
+    try:
+        ctx.lib.call("lsg_align_batch", ctx.h, len(pairs), dev.ptrs[0], _i64(eo), _i64([len(e) for e in es]),
+                     dev.ptrs[1], _i64(mo), _i64([len(m) for m in ms]), max_lag, res)
+    finally:
+        dev.free()
+    return [AlignResult(int(r.offset_ms), float(r.peak_corr), bool(r.low_confidence)) for r in res]

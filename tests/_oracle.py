@@ -97,6 +97,45 @@ class Reference:
             raise ValueError(f"render_pattern rc={rc}")
         return out[: n.value].copy()
 
+    # ---- A/V alignment (align.cpp)
+    def energy_envelope(self, pcm: np.ndarray, rate: int = 16000) -> np.ndarray:
+        pcm = np.ascontiguousarray(pcm, np.int16)
+        f = self.lib.ref_energy_envelope
+        f.restype = C.c_int64
+        n = f(pcm.ctypes.data_as(C.c_void_p), C.c_int64(len(pcm)), C.c_int(rate), None, C.c_int64(0))
+        out = np.zeros(max(n, 1), np.float64)
+        f(pcm.ctypes.data_as(C.c_void_p), C.c_int64(len(pcm)), C.c_int(rate), out.ctypes.data_as(C.c_void_p),
+          C.c_int64(n))
+        return out[:n]
+
+    def motion_envelope(self, frames, t0: int, span: int) -> np.ndarray:
+        ts = np.ascontiguousarray([f[0] for f in frames] or [0], np.int64)
+        mo = np.ascontiguousarray([f[1] for f in frames] or [0.0], np.float64)
+        out = np.zeros(max(span, 1), np.float64)
+        rc = self.lib.ref_motion_envelope(ts.ctypes.data_as(C.c_void_p), mo.ctypes.data_as(C.c_void_p),
+                                          C.c_int64(len(frames)), C.c_int64(t0), C.c_int64(span),
+                                          out.ctypes.data_as(C.c_void_p))
+        if rc:
+            raise ValueError("motion_envelope")
+        return out[:span]
+
+    def align(self, e, m, max_lag: int = 50):
+        e = np.ascontiguousarray(e, np.float64)
+        m = np.ascontiguousarray(m, np.float64)
+        off, corr, low = C.c_int64(), C.c_double(), C.c_int()
+        rc = self.lib.ref_align_envelopes(e.ctypes.data_as(C.c_void_p), C.c_int64(len(e)),
+                                          m.ctypes.data_as(C.c_void_p), C.c_int64(len(m)), C.c_int64(max_lag),
+                                          C.byref(off), C.byref(corr), C.byref(low))
+        if rc:
+            raise ValueError("align_envelopes")
+        return off.value, corr.value, bool(low.value)
+
+    def u64_to_unit(self, v: int) -> float:
+        f = self.lib.ref_u64_to_unit
+        f.restype = C.c_double
+        f.argtypes = [C.c_uint64]
+        return f(v)
+
     def ends_in_speech(self, p: Pattern, total_ms: int) -> bool:
         sp = _i64arr([b[0] for b in p.bursts])
         pa = _i64arr([b[1] for b in p.bursts])
@@ -225,6 +264,41 @@ class Restated:
         self.SEG_BYTES = self.lib.or_seg_sizeof()
         self.lib.or_compute_mel.restype = C.c_int64
         self.lib.or_mel_frame_count.restype = C.c_int64
+
+    # ---- A/V alignment (lsg_oracle.c or_*align*)
+    def energy_envelope(self, pcm: np.ndarray, rate: int = 16000) -> np.ndarray:
+        pcm = np.ascontiguousarray(pcm, np.int16)
+        f = self.lib.or_energy_envelope
+        f.restype = C.c_int64
+        n = f(pcm.ctypes.data_as(C.c_void_p), C.c_int64(len(pcm)), C.c_int(rate), None, C.c_int64(0))
+        out = np.zeros(max(n, 1), np.float64)
+        f(pcm.ctypes.data_as(C.c_void_p), C.c_int64(len(pcm)), C.c_int(rate), out.ctypes.data_as(C.c_void_p),
+          C.c_int64(n))
+        return out[:n]
+
+    def motion_envelope(self, frames, t0: int, span: int) -> np.ndarray:
+        ts = np.ascontiguousarray([f[0] for f in frames] or [0], np.int64)
+        mo = np.ascontiguousarray([f[1] for f in frames] or [0.0], np.float64)
+        out = np.zeros(max(span, 1), np.float64)
+        rc = self.lib.or_motion_envelope(ts.ctypes.data_as(C.c_void_p), mo.ctypes.data_as(C.c_void_p),
+                                         C.c_int64(len(frames)), C.c_int64(t0), C.c_int64(span),
+                                         out.ctypes.data_as(C.c_void_p))
+        if rc:
+            raise ValueError("motion_envelope")
+        return out[:span]
+
+    def align(self, e, m, max_lag: int = 50):
+        class R(C.Structure):
+            _fields_ = [("offset_ms", C.c_int64), ("peak_corr", C.c_double), ("low", C.c_int)]
+        e = np.ascontiguousarray(e, np.float64)
+        m = np.ascontiguousarray(m, np.float64)
+        r = R()
+        rc = self.lib.or_align_envelopes(e.ctypes.data_as(C.c_void_p), C.c_int64(len(e)),
+                                         m.ctypes.data_as(C.c_void_p), C.c_int64(len(m)), C.c_int64(max_lag),
+                                         C.byref(r))
+        if rc:
+            raise ValueError("align_envelopes")
+        return r.offset_ms, r.peak_corr, bool(r.low)
 
     def segment(self, pcm: np.ndarray, cfg: dict | None = None, chunks=None, start_ms: int = 0, scorer=None):
         c = seg_cfg(cfg)
