@@ -571,6 +571,37 @@ def scaled_leg(args, local, torch, ctx, stream, api):
         offs = [struct.unpack_from("<qdii", bytes(res), 24 * i)[0] for i in range(len(segs))]
         recovered = sum(1 for o, sh, mo in zip(offs, shift, m_off) if mo > 0 and o == sh)
         checkable = sum(1 for mo in m_off if mo > 0)
+        # ---- face-crop preparation (row f1): detect + Kalman per segment of
+        # 60 frames, bilinear 96x96 crops out of 640x448 frames
+        nsg, per = 400, 60
+        ts_f = torch.tensor([int(np.floor(i * 40 + 0.5)) for i in range(per)] * nsg, dtype=torch.int64, device=dev)
+        fi_f = torch.arange(nsg * per, dtype=torch.int64, device=dev)
+        box = torch.empty(nsg * per, 4, dtype=torch.float64, device=dev)
+        kc = (Cc.c_double * 3)(1e-2, 25.0, 1e6)
+        stt = (Cc.c_int32 * nsg)()
+        tr_ms = []
+        for rep in range(3):
+            e0.record(stream)
+            lib.call("lsg_face_track", ctx.h, nsg, i64([k * per for k in range(nsg)]), i64([per] * nsg),
+                     Cc.c_void_p(ts_f.data_ptr()), Cc.c_void_p(fi_f.data_ptr()), None, None, Cc.c_uint64(7), kc,
+                     Cc.c_void_p(box.data_ptr()), None, stt)
+            e1.record(stream)
+            stream.synchronize()
+            if rep:
+                tr_ms.append(e0.elapsed_time(e1))
+        fr640 = torch.randint(0, 256, (64, 448, 640, 3), dtype=torch.uint8, device=dev)
+        ncrop = nsg * per
+        fof = torch.arange(ncrop, dtype=torch.int64, device=dev) % 64
+        crops = torch.empty(ncrop, 96, 96, 3, dtype=torch.uint8, device=dev)
+        cr_ms = []
+        for rep in range(4):
+            e0.record(stream)
+            lib.call("lsg_face_crop", ctx.h, ncrop, Cc.c_void_p(fr640.data_ptr()), 448, 640,
+                     Cc.c_void_p(fof.data_ptr()), Cc.c_void_p(box.data_ptr()), Cc.c_void_p(crops.data_ptr()))
+            e1.record(stream)
+            stream.synchronize()
+            if rep:
+                cr_ms.append(e0.elapsed_time(e1))
     peaks, cc = measured_peaks(), cuda_core_peaks()
     t_seg = float(np.median(seg_ms))
     nbytes = S * n * 2
@@ -595,6 +626,15 @@ def scaled_leg(args, local, torch, ctx, stream, api):
                           "offsets_recovered": f"{recovered}/{checkable}",
                           "note": "one CTA per segment, one thread per lag, sequential sums (bit-identical to "
                                   "align.cpp): latency-bound by design"}},
+        "face": {"track": {"segments": nsg, "frames_per_segment": per, "ms": float(np.median(tr_ms)),
+                           "note": "one thread per segment: the Kalman recurrence is sequential per segment; "
+                                   "bit-identical to kalman.cpp"},
+                 "crop": {"crops": ncrop, "ms": float(np.median(cr_ms)),
+                          "crops_per_s": ncrop / (float(np.median(cr_ms)) / 1e3),
+                          "bytes": ncrop * 96 * 96 * 3 * 2, "achieved_gbs":
+                              ncrop * 96 * 96 * 3 * 2 / (float(np.median(cr_ms)) / 1e3) / 1e9,
+                          "note": "640x448 source frames, bilinear; bytes = 96x96x3 written + the same read "
+                                  "(box area ~ output area)"}},
         "mel": {"bound": "fp64", "ms": t_mel, "frames": F, "flops_fp64_per_frame": 25600,
                 "flops_fp32_per_frame": 4645, "achieved_fp64_tflops": F * 25600 / (t_mel / 1e3) / 1e12,
                 "peak_fp64_tflops": cc["fp64"], "peak_source": cc["source"], "t_roof_ms": t_roof * 1e3,

@@ -232,6 +232,35 @@ lsg_status lsg_align_batch(lsg_ctx ctx, int32_t n, const double* energy_base, co
                            const int64_t* e_len, const double* motion_base, const int64_t* m_off,
                            const int64_t* m_len, int64_t max_lag, lsg_align_result* out);
 
+/* ----------------------------------------------------------------- face
+ * Face-crop preparation: the detect + KalmanBoxFilter
+ * smoothing loop of orchestrator.cpp:115-129 per segment (bit-identical to
+ * kalman.cpp), and a bilinear 96x96 crop of the smoothed box. */
+typedef struct {
+  double process_noise;        /* 1e-2 per second (kalman.hpp:8-12)          */
+  double measurement_noise;    /* 25 px^2                                    */
+  double initial_variance;     /* 1e6                                        */
+} lsg_kalman_cfg;
+lsg_status lsg_kalman_cfg_default(lsg_kalman_cfg* c);
+/* mock_face_detect (visual_mocks.cpp:10-22): box4 = {cx, cy, w, h} [host] */
+lsg_status lsg_face_mock_detect(int64_t frame_index, uint64_t seed, double* box4);
+/* n segments; segment i = frames [seg_off[i], seg_off[i] + seg_len[i]) of
+ * the frame arrays ([dev]: ts, frame_index, optional has_face / faces
+ * [F][4]); a frame without a face uses mock_face_detect(frame_index, seed).
+ * Writes the smoothed box [F][4] and (optional) velocity [F][2] [dev];
+ * status[i] [host] = 0, or -1 where KalmanBoxFilter would throw (non-finite
+ * box, bad time step, S not SPD) -- that segment's later frames are left
+ * unwritten.  seg_off / seg_len [host]. */
+lsg_status lsg_face_track(lsg_ctx ctx, int32_t n, const int64_t* seg_off, const int64_t* seg_len,
+                          const int64_t* ts, const int64_t* frame_index, const int32_t* has_face,
+                          const double* faces, uint64_t seed, const lsg_kalman_cfg* cfg,
+                          double* out_box, double* out_vel, int32_t* status);
+/* n crops: crop k resamples box boxes[k] of frame frame_of[k] of frames
+ * [F][H][W][3] u8 into out [n][96][96][3] u8 (bilinear, clamp to edge);
+ * all pointers [dev]; asynchronous on the context stream. */
+lsg_status lsg_face_crop(lsg_ctx ctx, int32_t n, const uint8_t* frames, int32_t H, int32_t W,
+                         const int64_t* frame_of, const double* boxes, uint8_t* out);
+
 /* -------------------------------------------------------------- pipeline
  * Replaces the per-clip driver run_pipeline_input (runner.cpp:239-351) for
  * the GPU stages: segment -> mel per segment -> gather frames -> generator,

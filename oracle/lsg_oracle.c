@@ -446,3 +446,200 @@ int or_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm,
   r->peak_corr = best;
   return 0;
 }
+
+/* ==================================================== face track (f1) */
+
+static uint64_t or_splitmix64(uint64_t* s) {
+  uint64_t z = (*s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+static uint64_t or_mix_u64(uint64_t h, uint64_t v) { /* rng.hpp:21-25 */
+  h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  uint64_t s = h;
+  return or_splitmix64(&s);
+}
+
+/* visual_mocks.cpp:10-22 */
+void or_mock_face_detect(int64_t frame_index, uint64_t seed, double* box4) {
+  const char* tag = "facedetect";
+  uint64_t h = seed;
+  for (const char* c = tag; *c; ++c) h = or_mix_u64(h, (uint8_t)*c);
+  h = or_mix_u64(h, (uint64_t)frame_index);
+  box4[0] = 320.0 + ((double)(or_splitmix64(&h) % 7) - 3.0);
+  box4[1] = 240.0 + ((double)(or_splitmix64(&h) % 7) - 3.0);
+  box4[2] = 160.0;
+  box4[3] = 200.0;
+}
+
+typedef struct {
+  int init;
+  double x[6], p[6][6];
+  double pn, mn, iv;
+} or_kf;
+
+/* kalman.cpp:16-49: 4x4 Cholesky and solve */
+static int or_chol4(double a[4][4], double l[4][4]) {
+  memset(l, 0, 16 * sizeof(double));
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j <= i; ++j) {
+      volatile double sum = a[i][j];
+      for (int k = 0; k < j; ++k) {
+        const volatile double pr = l[i][k] * l[j][k];
+        sum = sum - pr;
+      }
+      if (i == j) {
+        if (sum <= 0.0 || !isfinite(sum)) return 0;
+        l[i][i] = sqrt(sum);
+      } else {
+        l[i][j] = sum / l[j][j];
+      }
+    }
+  return 1;
+}
+static void or_chol_solve4(double l[4][4], const double b[4], double x[4]) {
+  double y[4];
+  for (int i = 0; i < 4; ++i) {
+    volatile double sum = b[i];
+    for (int k = 0; k < i; ++k) {
+      const volatile double pr = l[i][k] * y[k];
+      sum = sum - pr;
+    }
+    y[i] = sum / l[i][i];
+  }
+  for (int i = 3; i >= 0; --i) {
+    volatile double sum = y[i];
+    for (int k = i + 1; k < 4; ++k) {
+      const volatile double pr = l[k][i] * x[k];
+      sum = sum - pr;
+    }
+    x[i] = sum / l[i][i];
+  }
+}
+
+/* kalman.cpp:58-77 */
+static void or_kf_predict(or_kf* f, double dt) {
+  volatile double t;
+  t = f->x[4] * dt; f->x[0] = f->x[0] + t;
+  t = f->x[5] * dt; f->x[1] = f->x[1] + t;
+  double fp[6][6];
+  for (int j = 0; j < 6; ++j) {
+    for (int i = 0; i < 6; ++i) fp[i][j] = f->p[i][j];
+    t = dt * f->p[4][j]; fp[0][j] = fp[0][j] + t;
+    t = dt * f->p[5][j]; fp[1][j] = fp[1][j] + t;
+  }
+  for (int i = 0; i < 6; ++i) {
+    for (int j = 0; j < 6; ++j) f->p[i][j] = fp[i][j];
+    t = dt * fp[i][4]; f->p[i][0] = f->p[i][0] + t;
+    t = dt * fp[i][5]; f->p[i][1] = f->p[i][1] + t;
+  }
+  const double q = f->pn * dt;
+  for (int i = 0; i < 6; ++i) f->p[i][i] = f->p[i][i] + q;
+}
+
+/* kalman.cpp:79-135 (update), Joseph form */
+static int or_kf_update(or_kf* f, const double z[4], double dt) {
+  for (int i = 0; i < 4; ++i)
+    if (!isfinite(z[i])) return -1;
+  if (!f->init) {
+    for (int i = 0; i < 4; ++i) f->x[i] = z[i];
+    f->x[4] = f->x[5] = 0.0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = 0; j < 6; ++j) f->p[i][j] = i == j ? f->iv : 0.0;
+    f->init = 1;
+    return 0;
+  }
+  if (dt < 0 || !isfinite(dt)) return -1;
+  or_kf_predict(f, dt);
+  double s[4][4], l[4][4], k[6][4];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) s[i][j] = f->p[i][j] + (i == j ? f->mn : 0.0);
+  if (!or_chol4(s, l)) return -1;
+  for (int i = 0; i < 6; ++i) {
+    double row[4], sol[4];
+    for (int j = 0; j < 4; ++j) row[j] = f->p[i][j];
+    or_chol_solve4(l, row, sol);
+    for (int j = 0; j < 4; ++j) k[i][j] = sol[j];
+  }
+  double y[4];
+  for (int i = 0; i < 4; ++i) y[i] = z[i] - f->x[i];
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 4; ++j) {
+      const volatile double pr = k[i][j] * y[j];
+      f->x[i] = f->x[i] + pr;
+    }
+  double ikh[6][6], tmp[6][6];
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) ikh[i][j] = (i == j ? 1.0 : 0.0) - (j < 4 ? k[i][j] : 0.0);
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) {
+      volatile double acc = 0.0;
+      for (int m = 0; m < 6; ++m) {
+        const volatile double pr = ikh[i][m] * f->p[m][j];
+        acc = acc + pr;
+      }
+      tmp[i][j] = acc;
+    }
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) {
+      volatile double acc = 0.0;
+      for (int m = 0; m < 6; ++m) {
+        const volatile double pr = tmp[i][m] * ikh[j][m];
+        acc = acc + pr;
+      }
+      for (int m = 0; m < 4; ++m) {
+        const volatile double a = k[i][m] * f->mn;
+        const volatile double pr = a * k[j][m];
+        acc = acc + pr;
+      }
+      f->p[i][j] = acc;
+    }
+  return 0;
+}
+
+int or_track_faces(const int64_t* ts, const int64_t* frame_index, const int* has_face, const double* faces,
+                   int64_t n, uint64_t seed, double process_noise, double measurement_noise,
+                   double initial_variance, double* out4, double* vel2) {
+  or_kf f;
+  memset(&f, 0, sizeof f);
+  f.pn = process_noise;
+  f.mn = measurement_noise;
+  f.iv = initial_variance;
+  int64_t prev = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double z[4];
+    if (has_face[i]) memcpy(z, faces + 4 * i, sizeof z);
+    else or_mock_face_detect(frame_index[i], seed, z);
+    const double dt = f.init ? (double)(ts[i] - prev) / 1000.0 : 0.0;
+    if (or_kf_update(&f, z, dt)) return -1;
+    for (int c = 0; c < 4; ++c) out4[4 * i + c] = f.x[c];
+    vel2[2 * i] = f.x[4];
+    vel2[2 * i + 1] = f.x[5];
+    prev = ts[i];
+  }
+  return 0;
+}
+
+/* bilinear 96x96 crop (our semantics; the reference has no pixels) */
+void or_crop96(const uint8_t* frame, int H, int W, const double* b, uint8_t* out) {
+  const double x0 = b[0] - 0.5 * b[2], y0 = b[1] - 0.5 * b[3];
+  const double sx = b[2] / 96.0, sy = b[3] / 96.0;
+  for (int v = 0; v < 96; ++v)
+    for (int u = 0; u < 96; ++u) {
+      double fx = x0 + (u + 0.5) * sx - 0.5, fy = y0 + (v + 0.5) * sy - 0.5;
+      fx = fx < 0 ? 0 : (fx > W - 1 ? W - 1 : fx);
+      fy = fy < 0 ? 0 : (fy > H - 1 ? H - 1 : fy);
+      const int ix = (int)fx < W - 1 ? (int)fx : W - 2, iy = (int)fy < H - 1 ? (int)fy : H - 2;
+      const double ax = fx - ix, ay = fy - iy;
+      for (int c = 0; c < 3; ++c) {
+        const double p00 = frame[((int64_t)iy * W + ix) * 3 + c], p01 = frame[((int64_t)iy * W + ix + 1) * 3 + c];
+        const double p10 = frame[((int64_t)(iy + 1) * W + ix) * 3 + c];
+        const double p11 = frame[((int64_t)(iy + 1) * W + ix + 1) * 3 + c];
+        const volatile double top = p00 + ax * (p01 - p00);
+        const volatile double bot = p10 + ax * (p11 - p10);
+        const volatile double val = top + ay * (bot - top);
+        out[((int64_t)v * 96 + u) * 3 + c] = (uint8_t)(val + 0.5);
+      }
+    }
+}

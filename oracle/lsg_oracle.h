@@ -123,6 +123,19 @@ int or_motion_envelope(const int64_t* ts, const double* motion, int64_t nf, int6
 int or_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm, int64_t max_lag,
                        or_align_result* r);
 
+/* ------------------------------------------------- face track (row f1)
+ * Restatement of mock_face_detect (visual_mocks.cpp:10-22) and the
+ * detect + KalmanBoxFilter loop (kalman.cpp:58-144, orchestrator.cpp:115-129). */
+void or_mock_face_detect(int64_t frame_index, uint64_t seed, double* box4);
+int or_track_faces(const int64_t* ts, const int64_t* frame_index, const int* has_face, const double* faces,
+                   int64_t n, uint64_t seed, double process_noise, double measurement_noise,
+                   double initial_variance, double* out4, double* vel2);
+/* bilinear crop of box (cx, cy, w, h) of a [H][W][3] u8 frame into
+ * [96][96][3]: source x = cx - w/2 + (u + 0.5) w / 96 - 0.5 (same for y),
+ * clamp-to-edge, round half away from zero (our semantics: the reference
+ * carries no pixels) */
+void or_crop96(const uint8_t* frame, int H, int W, const double* box4, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

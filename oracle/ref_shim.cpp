@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "lipstream/align.hpp"
+#include "lipstream/kalman.hpp"
+#include "lipstream/visual_mocks.hpp"
 #include "lipstream/mel.hpp"
 #include "lipstream/rng.hpp"
 #include "lipstream/segmenter.hpp"
@@ -275,6 +277,49 @@ int ref_motion_envelope(const int64_t* ts, const double* motion, int64_t nf, int
     }
     std::vector<double> e = motion_envelope_ms(fr, t0, span);
     std::memcpy(out, e.data(), e.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// mock_face_detect (visual_mocks.cpp:10-22): out = {cx, cy, w, h}
+void ref_mock_face_detect(int64_t frame_index, uint64_t seed, double* out) {
+  FaceBox b = mock_face_detect(frame_index, seed);
+  out[0] = b.cx;
+  out[1] = b.cy;
+  out[2] = b.w;
+  out[3] = b.h;
+}
+
+// The per-segment detect + smooth loop of orchestrator.cpp:115-129 /
+// runner.cpp:134-141 over n frames: box = the frame's face (has_face[i]) or
+// mock_face_detect(frame_index[i], seed); KalmanBoxFilter::update with
+// dt = (ts - prev) / 1000 after the first.  out[4 i ..] = smoothed box,
+// vel[2 i ..] = (vx, vy).  Returns -1 on a filter exception.
+int ref_track_faces(const int64_t* ts, const int64_t* frame_index, const int* has_face, const double* faces,
+                    int64_t n, uint64_t seed, double pn, double mn, double iv, double* out, double* vel) {
+  try {
+    KalmanConfig cfg;
+    cfg.process_noise = pn;
+    cfg.measurement_noise = mn;
+    cfg.initial_variance = iv;
+    KalmanBoxFilter smoother(cfg);
+    int64_t prev = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      FaceBox box;
+      if (has_face[i]) box = FaceBox{faces[4 * i], faces[4 * i + 1], faces[4 * i + 2], faces[4 * i + 3]};
+      else box = mock_face_detect(frame_index[i], seed);
+      const double dt = smoother.initialized() ? double(ts[i] - prev) / 1000.0 : 0.0;
+      const auto est = smoother.update(box, dt);
+      out[4 * i] = est.box.cx;
+      out[4 * i + 1] = est.box.cy;
+      out[4 * i + 2] = est.box.w;
+      out[4 * i + 3] = est.box.h;
+      vel[2 * i] = est.vx;
+      vel[2 * i + 1] = est.vy;
+      prev = ts[i];
+    }
     return 0;
   } catch (const std::exception&) {
     return -1;

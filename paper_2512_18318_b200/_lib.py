@@ -111,6 +111,10 @@ _SIGS = {
     "lsg_gen_forward": [P, P, P, P, P, P, P, I32, I32],
     "lsg_lipsync_validate": [I64, I64, I64],
     "lsg_align_energy": [P, I32, P, PI64, PI64, I32, P, PI64, PI64],
+    "lsg_kalman_cfg_default": [P],
+    "lsg_face_mock_detect": [I64, C.c_uint64, P],
+    "lsg_face_track": [P, I32, PI64, PI64, P, P, P, P, C.c_uint64, P, P, P, PI32],
+    "lsg_face_crop": [P, I32, P, I32, I32, P, P, P],
     "lsg_align_motion": [P, I32, P, P, PI64, PI64, PI64, PI64, P, PI64],
     "lsg_align_batch": [P, I32, P, PI64, PI64, P, PI64, PI64, I64, P],
     "lsg_pipe_create": [P, C.POINTER(PipeCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), P, PP],

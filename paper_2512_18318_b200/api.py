@@ -583,3 +583,85 @@ def align_batch(pairs, max_lag: int = 50, ctx: Context | None = None) -> list[Al
     finally:
         dev.free()
     return [AlignResult(int(r.offset_ms), float(r.peak_corr), bool(r.low_confidence)) for r in res]
+
+
+# ------------------------------------------------------ face crops (f1)
+@dataclass
+class KalmanConfig:
+    """kalman.hpp:8-12."""
+    process_noise: float = 1e-2
+    measurement_noise: float = 25.0
+    initial_variance: float = 1e6
+
+
+class KalmanCfg(C.Structure):
+    _fields_ = [("process_noise", C.c_double), ("measurement_noise", C.c_double), ("initial_variance", C.c_double)]
+
+
+def mock_face_detect(frame_index: int, seed: int) -> tuple:
+    """visual_mocks.cpp:10-22 -> (cx, cy, w, h)."""
+    b = np.zeros(4, np.float64)
+    lib().call("lsg_face_mock_detect", int(frame_index), C.c_uint64(seed & ((1 << 64) - 1)), _ptr(b))
+    return tuple(float(x) for x in b)
+
+
+def track_faces(segments, seed: int = 0, cfg: KalmanConfig = KalmanConfig(), ctx: Context | None = None):
+    """The detect + smooth loop of orchestrator.cpp:115-129 for many segments
+    in one call.  segments: list of (ts[], frame_index[], faces or None),
+    faces an [n, 4] array with NaN rows for frames without a box.  Returns
+    per segment (boxes [n, 4], velocities [n, 2]); raises RuntimeError where
+    KalmanBoxFilter would throw."""
+    ctx = ctx or default_context()
+    if not segments:
+        return []
+    lens = [len(s[0]) for s in segments]
+    offs = np.cumsum([0] + lens[:-1])
+    F = max(sum(lens), 1)
+    ts = np.zeros(F, np.int64)
+    fi = np.zeros(F, np.int64)
+    has = np.zeros(F, np.int32)
+    faces = np.zeros((F, 4), np.float64)
+    for (t, f, fa), o, n in zip(segments, offs, lens):
+        ts[o:o + n] = t
+        fi[o:o + n] = f
+        if fa is not None:
+            fa = np.asarray(fa, np.float64).reshape(n, 4)
+            ok = ~np.isnan(fa).all(axis=1)
+            has[o:o + n] = ok
+            faces[o:o + n] = np.where(ok[:, None], fa, 0.0)
+    box = np.zeros((F, 4), np.float64)
+    vel = np.zeros((F, 2), np.float64)
+    dev = _DevArrays(ctx, ts, fi, has, faces, box, vel)
+    st = (C.c_int32 * len(segments))()
+    c = KalmanCfg(cfg.process_noise, cfg.measurement_noise, cfg.initial_variance)
+    try:
+        ctx.lib.call("lsg_face_track", ctx.h, len(segments), _i64(offs), _i64(lens), dev.ptrs[0], dev.ptrs[1],
+                     dev.ptrs[2], dev.ptrs[3], C.c_uint64(seed & ((1 << 64) - 1)), C.byref(c), dev.ptrs[4],
+                     dev.ptrs[5], st)
+        ctx.lib.call("lsg_copy", ctx.h, _ptr(box), dev.ptrs[4], box.nbytes)
+        ctx.lib.call("lsg_copy", ctx.h, _ptr(vel), dev.ptrs[5], vel.nbytes)
+        ctx.sync()
+    finally:
+        dev.free()
+    for i, s_ in enumerate(st):
+        if s_:
+            raise RuntimeError(f"kalman: segment {i} diverged or had a bad measurement / time step")
+    return [(box[o:o + n].copy(), vel[o:o + n].copy()) for o, n in zip(offs, lens)]
+
+
+def crop96(frames: np.ndarray, frame_of, boxes, ctx: Context | None = None) -> np.ndarray:
+    """Bilinear 96x96 crops: frames [F, H, W, 3] u8, frame_of [n], boxes [n, 4] -> [n, 96, 96, 3] u8."""
+    ctx = ctx or default_context()
+    frames = np.ascontiguousarray(frames, np.uint8)
+    fo = np.ascontiguousarray(frame_of, np.int64)
+    bx = np.ascontiguousarray(boxes, np.float64).reshape(-1, 4)
+    out = np.zeros((len(fo), 96, 96, 3), np.uint8)
+    dev = _DevArrays(ctx, frames, fo, bx, out)
+    try:
+        ctx.lib.call("lsg_face_crop", ctx.h, len(fo), dev.ptrs[0], frames.shape[1], frames.shape[2], dev.ptrs[1],
+                     dev.ptrs[2], dev.ptrs[3])
+        ctx.lib.call("lsg_copy", ctx.h, _ptr(out), dev.ptrs[3], out.nbytes)
+        ctx.sync()
+    finally:
+        dev.free()
+    return out
