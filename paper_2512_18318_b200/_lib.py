@@ -7,7 +7,7 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblsg.so")
+LIB_PATH = os.environ.get("LSG_LIB", os.path.join(PKG, "liblsg.so"))  # override: A/B builds in tools/
 HEADER = os.path.join(os.path.dirname(PKG), "include", "lsg.h")
 
 LSG_OK, LSG_EINVAL, LSG_ELOGIC, LSG_ERUNTIME, LSG_ECUDA = 0, 1, 2, 3, 4

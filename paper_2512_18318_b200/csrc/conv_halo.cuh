@@ -194,7 +194,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   // SPLIT: both groups take every tile, half the channels each.  Otherwise
   // (BN = 16, or the fused 1x1 output) the groups alternate tiles, group g
   // owning accumulator g.
-  constexpr bool SPLIT = !FUSED_OUT && BN >= 32;
+  // Resident-weight variants have double-buffered staging/residual tiles, so
+  // the groups can own alternate tiles (one accumulator, staging buffer and
+  // residual slot each; 128-thread barriers) and two tiles' epilogues run
+  // concurrently -- the epilogue, not the MMA, bounds these narrow layers in
+  // fp8.  Streamed-weight variants (single staging buffer) split channels.
+  constexpr bool SPLIT = !FUSED_OUT && BN >= 32 && !B_RES;
   constexpr bool EPI_ALT = !SPLIT && NACC == 2;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = tc::smem_u32(smem_raw);
@@ -408,10 +413,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       constexpr int IB = CF::IB;
       const int grp = EPI_ALT ? half : 0;
       const bool leader = (warp == 2 + 4 * grp) && lane == 0;  // issues the group's stores
-      int sb = 0, rs = 0;
-      uint32_t rph = 0;
+      int sb = 0;
       for (int t = blockIdx.x + (int)tl * gridDim.x; t < p.total_tiles; t += step * gridDim.x, tl += step) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
+        // residual ring slot of this tile (the producer fills slots in tile order)
+        const int rs = CF::NRES ? (int)(tl % (uint32_t)(CF::NRES ? CF::NRES : 1)) : 0;
+        const uint32_t rph = CF::NRES ? (tl / (uint32_t)(CF::NRES ? CF::NRES : 1)) & 1u : 0u;
         const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
         const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
         uint8_t* stg = smem + CF::OFF_STG + (EPI_ALT ? grp : sb) * CF::STG_BYTES;
@@ -452,10 +459,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         tc::mbar_arrive(&tempty[a]);
         if constexpr (CF::HAS_RES) {
           tc::mbar_arrive(&rempty[rs]);
-          if (++rs == CF::NRES) {
-            rs = 0;
-            rph ^= 1;
-          }
         }
         tc::fence_proxy_async();  // staging writes -> visible to the TMA (async proxy)
         named_bar(1 + grp, EPI_THREADS);
