@@ -314,7 +314,8 @@ def main():
     launches = ctx.launches() - launches0
     ms_dev = ev0.elapsed_time(ev1) / args.steps
     ms_dev = max_over_ranks(ms_dev)
-    total_frames = n_frames * world
+    from paper_2512_18318_b200.shard import sum_over_ranks
+    total_frames = int(sum_over_ranks(n_frames, dist, device=f"cuda:{local}"))
     value = total_frames / (ms_dev / 1000.0)
     # ------------------------------------------------------------ e2e leg
     for _ in range(2):
@@ -327,7 +328,8 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    e2e = n_e2e * world / (ms_e2e / 1000.0)
+    n_e2e_all = sum_over_ranks(n_e2e, dist, device=f"cuda:{local}")
+    e2e = n_e2e_all / (ms_e2e / 1000.0)
     h2d = sum(p.nbytes for p in pcm) + sum(v.nbytes for v in video) + refs.nbytes
     d2h = n_e2e * CROP
     # ------------------------------------------- config-5 paced (real time)
@@ -352,11 +354,12 @@ def main():
     bf16_b128_ms = measure_generator(eng_bf, torch, torch_stream, local, 128, reps=10)
     eng_bf.close()
     clocks = clk.summary()
+    med = {k: float(np.median([s[k] for s in stats])) for k in stats[0]}
+    unique_all = int(sum_over_ranks(med["unique_frames"], dist, device=f"cuda:{local}"))
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    med = {k: float(np.median([s[k] for s in stats])) for k in stats[0]}
     out = {
         "metric": "lip-sync frames/sec (96x96), full segmenter->mel->generator path",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -364,7 +367,7 @@ def main():
         "dtype": "f16" if prec else "bf16", "data": "synthetic (seeded speech patterns, synthetic face crops, "
                                                     "BN-calibrated random weights)",
         "config": cfg_desc,
-        "frames_per_step": total_frames, "unique_frames_per_step": int(med["unique_frames"]) * world,
+        "frames_per_step": total_frames, "unique_frames_per_step": unique_all,
         "stage_ms_median": {"segment": med["ms_segment"], "mel": med["ms_mel"], "generator": med["ms_generator"],
                             "segments": med["segments"], "mel_frames": med["mel_frames"]},
         "e2e": {"value": e2e, "unit": "frames/s", "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
@@ -684,14 +687,15 @@ def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generat
         frames, _ = step()
     e1.record(stream)
     torch.cuda.synchronize()
-    from paper_2512_18318_b200.shard import max_over_ranks
+    from paper_2512_18318_b200.shard import max_over_ranks, sum_over_ranks
     ms = max_over_ranks(e0.elapsed_time(e1) / 3, dist, device=dev)
+    frames = int(sum_over_ranks(frames, dist, device=dev))
     gms = measure_generator(eng8, torch, stream, local, 128, reps=20)
     burst, sust, src = fp8_peaks()
     tf = FLOPS_PER_FRAME * 128 / (gms / 1e3) / 1e12
     out = {"workload": f"config 4: fp8 generator, {S} streams/GPU x {secs} s, unpaced, batch 128",
-           "dtype": "fp8_e4m3 (f32 accumulate)", "value": frames * world / (ms / 1e3), "unit": "frames/s",
-           "ms_per_step": ms, "frames_per_step": frames * world,
+           "dtype": "fp8_e4m3 (f32 accumulate)", "value": frames / (ms / 1e3), "unit": "frames/s",
+           "ms_per_step": ms, "frames_per_step": frames,
            "generator_b128": {"ms": gms, "frames_per_s": 128 / (gms / 1e3), "achieved_tflops": tf,
                               "peak_tflops": sust, "frac": tf / sust, "frac_vs_burst": tf / burst,
                               "peak_source": src},

@@ -29,6 +29,16 @@ def max_over_ranks(x: float, dist=None, device=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(x: float, dist=None, device=None) -> float:
+    """Work done by all ranks (e.g. frames rendered: ranks own different streams)."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def gather_arrays(arrays: list[np.ndarray], dist=None, world: int = 1) -> list[np.ndarray]:
     """Concatenate per-rank 1-D arrays (e.g. per-segment latencies) over all
     ranks, rank order; every rank receives the result."""

@@ -11,7 +11,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2512_18318_b200.shard import gather_arrays, max_over_ranks, streams_for_rank
+from paper_2512_18318_b200.shard import gather_arrays, max_over_ranks, streams_for_rank, sum_over_ranks
 
 
 def _free_port():
@@ -32,11 +32,12 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(owners, mine)
         step_ms = 10.0 + 5.0 * rank  # rank 1 is the slow one
         slowest = max_over_ranks(step_ms, dist)
+        frames = sum_over_ranks(100 + rank, dist)  # ranks render different frame counts
         rng = np.random.default_rng(100 + rank)
         lat = rng.uniform(100, 900, 50 + 10 * rank)
         dec = lat - 5.0
         all_lat, all_dec = gather_arrays([lat, dec], dist, world)
-        q.put((rank, owners, slowest, all_lat.tolist(), all_dec.tolist()))
+        q.put((rank, owners, slowest, all_lat.tolist(), all_dec.tolist(), frames))
     finally:
         dist.destroy_process_group()
 
@@ -68,6 +69,8 @@ def test_two_rank_gloo():
     assert all(len(o) == 32 for o in owners)
     # the job time is the slowest rank's, on every rank
     assert all(r[2] == 15.0 for r in res)
+    # whole-job work is the sum over ranks
+    assert all(r[5] == 201.0 for r in res)
     # gathered latencies = concatenation in rank order, identical on all ranks
     want = np.concatenate([np.random.default_rng(100 + r).uniform(100, 900, 50 + 10 * r) for r in range(world)])
     for r in res:
