@@ -35,6 +35,24 @@
 namespace lsg {
 namespace gen {
 
+// Phase timestamps (globaltimer, ns) per layer and CTA, only in builds with
+// -DLSG_TRACE (tools/layer_trace.py): where a layer's time goes.
+#ifdef LSG_TRACE
+constexpr int TRACE_EV = 16, TRACE_CTAS = 160, TRACE_LAYERS = 64;
+__device__ unsigned long long g_lsg_trace[TRACE_LAYERS * TRACE_CTAS * TRACE_EV];
+#define LSG_TR(slot, i)                                                                                 \
+  do {                                                                                                  \
+    unsigned long long t_;                                                                              \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                              \
+    if ((slot) >= 0 && blockIdx.x < TRACE_CTAS)                                                         \
+      g_lsg_trace[((size_t)(slot) * TRACE_CTAS + blockIdx.x) * TRACE_EV + (i)] = t_;                    \
+  } while (0)
+#else
+#define LSG_TR(slot, i) \
+  do {                  \
+  } while (0)
+#endif
+
 constexpr int BM = 128;  // UMMA M (TMEM lanes)
 constexpr int BK = 64;   // 16-bit elements per K stage
 constexpr int MAX_TAPS = 49;
@@ -78,6 +96,16 @@ struct alignas(64) ConvParams {
   void* final_out;
   int nphases, ntiles_n, total_tiles;
   int interleave;  // all phases have equal mtiles: t = (mt * nphases + z) * ntiles_n + nt
+  // split-K (grid-starved low-resolution layers): work unit u = t * ksplit + ks
+  // runs kblocks [ks*KB/ksplit, (ks+1)*KB/ksplit) of tile t and adds its fp32
+  // partial into ws[t] (layout [BN/4][BM] float4); the last split of a tile
+  // (counters[t]) runs the epilogue from ws[t] and re-zeroes ws[t] / counters[t]
+  int ksplit, total_units;
+  float* ws;
+  int* counters;
+  int trace_slot;  // layer index (LSG_TRACE builds)
+  int pbn;         // tile width the weights are packed for (a multiple of BN: a
+                   // BN-wide tile is a contiguous, swizzle-aligned slice of it)
   Phase ph[MAX_PHASES];
 };
 
@@ -247,6 +275,15 @@ __device__ __forceinline__ TileId decode_tile(const ConvParams& p, int t) {
   return {z, r - mt * p.ntiles_n, mt};
 }
 
+// Weight tile (nt, kb) of a BN-wide launch over weights packed PBN wide:
+// [PBN tiles][kblocks][PBN rows][64], rows 128 B swizzled in 8-row atoms.
+template <int BN>
+__device__ __forceinline__ const uint16_t* wtile(const ConvParams& p, const Phase& P, int nt, int kb) {
+  const int sub = p.pbn / BN;
+  const int ntp = nt / sub, q = nt - ntp * sub;
+  return P.w + (((size_t)ntp * P.kblocks + kb) * p.pbn + (size_t)q * BN) * BK;
+}
+
 __device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c, int w,
                                               int h, int n, uint16_t off_w, uint16_t off_h) {
   asm volatile(
@@ -285,6 +322,19 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
   uint4 rv[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) rv[i] = rrow ? __ldg(reinterpret_cast<const uint4*>(rrow) + i) : make_uint4(0, 0, 0, 0);
+  // tcgen05.wait::ld orders memory, so per-chunk loads cannot be hoisted past
+  // it: pull this row's bias / scale / residual lines into L1 under the mainloop
+#pragma unroll
+  for (int c = 0; c < HC; c += 32) {
+    tc::prefetch_l1(bias + c);
+    if constexpr (NF::F8) tc::prefetch_l1(oscale + c);
+  }
+  if constexpr (HC > 64) {
+    if (rrow) {
+#pragma unroll
+      for (int c = 128; c < HC / NF::CPU * 2; c += 128) tc::prefetch_l1(reinterpret_cast<const uint8_t*>(rrow) + c);
+    }
+  }
   tc::mbar_wait(tfull_bar, parity);
   tc::tc_fence_after();
 #pragma unroll
@@ -314,6 +364,123 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
   }
 }
 
+// Output pixel of GEMM row m of phase P (m < P.M).
+__device__ __forceinline__ size_t out_pixel(const ConvParams& p, const Phase& P, int m) {
+  const int HW = P.GH * P.GW;
+  const int n = m / HW;
+  const int rem = m - n * HW;
+  const int gy = rem / P.GW, gx = rem - gy * P.GW;
+  return ((size_t)n * p.OH + gy * p.osy + P.oy) * p.OW + gx * p.osx + P.ox;
+}
+
+// Split-K epilogue (all 256 epilogue threads take part).  Each split stores
+// its TMEM partial into its own slot ws[u] ([BN/4][BM] float4: coalesced) and
+// frees the accumulator; the ksplit CTAs of a tile meet at counters[t] (they
+// are co-resident: units <= grid <= SMs, one unit per CTA); then CTA ks sums
+// its 1/ksplit share of the tile's (row, 16-channel) items over the slots in
+// slot order -- deterministic -- and runs the ordinary epilogue math on them.
+template <int BN, int HC, int PR>
+__device__ __forceinline__ void splitk_tile(const ConvParams& p, int u, int t, const TileId& id, int r, int cbeg,
+                                            uint32_t tbase, uint64_t* tfull_bar, uint64_t* tempty_bar,
+                                            uint32_t parity) {
+  using NF = Num<PR>;
+  constexpr int W16 = NF::U4;
+  constexpr int SLOT = BN / 4 * BM;  // float4 per slot
+  const int S = p.ksplit, ks = u - t * S;
+  float4* ws = reinterpret_cast<float4*>(p.ws);
+  {
+    float4* mine = ws + (size_t)u * SLOT + (size_t)(cbeg / 4) * BM + r;
+    tc::mbar_wait(tfull_bar, parity);
+    tc::tc_fence_after();
+    if (threadIdx.x == 64) LSG_TR(p.trace_slot, 6);
+#pragma unroll
+    for (int c0 = 0; c0 < HC; c0 += 16) {
+      uint32_t v[16];
+      tc::tmem_ld16(tbase + c0, v);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        __stcg(mine + (size_t)(c0 / 4 + j) * BM, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                              __uint_as_float(v[4 * j + 2]),
+                                                              __uint_as_float(v[4 * j + 3])));
+    }
+    tc::tc_fence_before();
+    tc::mbar_arrive(tempty_bar);
+  }
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
+  if (threadIdx.x == 64) LSG_TR(p.trace_slot, 7);
+  if (threadIdx.x == 64) {
+    int* c = p.counters + t;
+    atomicAdd(c, 1);
+    int seen;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(c) : "memory");
+      if (seen < S) __nanosleep(32);
+    } while (seen < S);
+    LSG_TR(p.trace_slot, 8);
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
+  __threadfence();
+  const Phase& P = p.ph[id.z];
+  const int n0 = id.nt * BN;
+  constexpr int NI = BM * (BN / 16);
+  const int i0 = ks * NI / S, i1 = (ks + 1) * NI / S;
+  const float4* slots = ws + (size_t)t * S * SLOT;
+#pragma unroll 1
+  for (int i = i0 + (int)threadIdx.x - 64; i < i1; i += 32 * NUM_EPI_WARPS) {
+    const int chunk = i / BM, row = i - chunk * BM;
+    const int m = id.mt * BM + row;
+    if (m >= P.M) continue;
+    float f[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) f[j] = 0.f;
+    // four slots' loads in flight at a time; summed in slot order
+#pragma unroll 1
+    for (int s2 = 0; s2 < S; s2 += 4) {
+      float4 x[4][4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4* q = slots + (size_t)(s2 + k) * SLOT + (size_t)(chunk * 4) * BM + row;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[k][j] = s2 + k < S ? __ldcg(q + (size_t)j * BM) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (s2 + k < S) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            f[4 * j] += x[k][j].x;
+            f[4 * j + 1] += x[k][j].y;
+            f[4 * j + 2] += x[k][j].z;
+            f[4 * j + 3] += x[k][j].w;
+          }
+        }
+      }
+    }
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(f[j]);
+    const size_t pix = out_pixel(p, P, m);
+    const int ch = n0 + chunk * 16;
+    uint4 res[W16], o[W16];
+    if (p.res) {
+      const uint4* rp = reinterpret_cast<const uint4*>(p.res + pix * p.res_pitch + p.res_coff + ch / NF::CPU);
+#pragma unroll
+      for (int w = 0; w < W16; ++w) res[w] = __ldg(rp + w);
+    }
+    epi16<PR>(v, p.bias + ch, p.oscale + (NF::F8 ? ch : 0), p.res ? res : nullptr, p.res_scale, p.relu != 0,
+              p.out_inv, o);
+    uint4* op = reinterpret_cast<uint4*>(p.out + pix * p.out_pitch + p.out_coff + ch / NF::CPU);
+#pragma unroll
+    for (int w = 0; w < W16; ++w) op[w] = o[w];
+  }
+  // second round on the counter: the last CTA out resets it for the next layer
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
+  if (threadIdx.x == 64) LSG_TR(p.trace_slot, 9);
+  if (threadIdx.x == 64 && atomicAdd(p.counters + t, 1) == 2 * S - 1) p.counters[t] = 0;
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -341,6 +508,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) LSG_TR(p.trace_slot, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -361,33 +529,62 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   constexpr int LPS = BK / CC;  // TMA loads per stage
   tc::griddep_launch();
+  if (threadIdx.x == 0) LSG_TR(p.trace_slot, 1);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (whole warp;
     // lane j issues load j of a stage, lane 0 the weights + expect_tx)
-    tc::griddep_wait();  // previous layer's activations complete
     const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
     constexpr uint32_t LOAD_BYTES = BM * CC * 2;
     const int cpt = p.C / CC;  // loads per tap
-    int s = 0;
-    uint32_t ph = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+    // The weights do not depend on the previous layer: the first unit's first
+    // S weight stages are issued (and the rest of its weight range prefetched
+    // into L2) before waiting for the previous layer's activations.
+    int pre = 0;
+    if (blockIdx.x < p.total_units) {
+      const int u = blockIdx.x, t = u / p.ksplit, ks = u - t * p.ksplit;
       const TileId id = decode_tile(p, t);
       const Phase& P = p.ph[id.z];
       const int KB = P.kblocks, NL = P.nloads;
+      const int kb0 = ks * KB / p.ksplit, kb1 = (ks + 1) * KB / p.ksplit;
+      pre = min(S, kb1 - kb0);
+      for (int kb = kb0 + pre + lane; kb < kb1; kb += 32) tc::prefetch_l2(wtile<BN>(p, P, id.nt, kb), CF::B_BYTES);
+      if (lane == 0) {
+        for (int i = 0; i < pre; ++i) {
+          const int kb = kb0 + i;
+          const int nl = min(LPS, NL - kb * LPS);
+          tc::mbar_arrive_expect_tx(&full[i], CF::B_BYTES + nl * LOAD_BYTES);
+          tc::bulk_g2s(sB0 + i * CF::B_BYTES, wtile<BN>(p, P, id.nt, kb), CF::B_BYTES, &full[i]);
+        }
+      }
+      __syncwarp();
+    }
+    tc::griddep_wait();  // previous layer's activations complete
+    if (lane == 0) LSG_TR(p.trace_slot, 2);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+      const int t = u / p.ksplit, ks = u - t * p.ksplit;
+      const TileId id = decode_tile(p, t);
+      const Phase& P = p.ph[id.z];
+      const int KB = P.kblocks, NL = P.nloads;
+      const int kb0 = ks * KB / p.ksplit, kb1 = (ks + 1) * KB / p.ksplit;
       const int m0 = id.mt * BM;
       const int HW = P.GH * P.GW;
       const int n = m0 / HW, rem = m0 - n * HW;
       const int gy = rem / P.GW, gx = rem - gy * P.GW;
       const int w0 = gx * p.sx + p.lower_w, h0 = gy * p.sy + p.lower_h;
-      const uint16_t* wbase = P.w + (size_t)id.nt * KB * BN * BK;
-      for (int kb = 0; kb < KB; ++kb) {
-        tc::mbar_wait(&empty[s], ph ^ 1);
+      for (int kb = kb0; kb < kb1; ++kb) {
         const int l = kb * LPS + lane;
         const int nl = min(LPS, NL - kb * LPS);
-        if (lane == 0) {
-          tc::mbar_arrive_expect_tx(&full[s], CF::B_BYTES + nl * LOAD_BYTES);
-          tc::bulk_g2s(sB0 + s * CF::B_BYTES, wbase + (size_t)kb * BN * BK, CF::B_BYTES, &full[s]);
+        if (pre > 0) {  // weights already in flight (fresh stage: no empty wait)
+          --pre;
+        } else {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          if (lane == 0) {
+            tc::mbar_arrive_expect_tx(&full[s], CF::B_BYTES + nl * LOAD_BYTES);
+            tc::bulk_g2s(sB0 + s * CF::B_BYTES, wtile<BN>(p, P, id.nt, kb), CF::B_BYTES, &full[s]);
+          }
         }
         if (lane < nl) {
           const int tap = l / cpt, ch = (l - tap * cpt) * CC;
@@ -401,6 +598,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
         }
       }
     }
+    if (lane == 0) LSG_TR(p.trace_slot, 3);
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (whole warp
     // runs the loop, one elected lane issues: descriptors stay uniform)
@@ -408,25 +606,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
     const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
     int s = 0;
     uint32_t ph = 0, tl = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ++tl) {
+      const int t = u / p.ksplit, ks = u - t * p.ksplit;
       const TileId id = decode_tile(p, t);
       const int KB = p.ph[id.z].kblocks, NS = p.ph[id.z].nsteps;
+      const int kb0 = ks * KB / p.ksplit, kb1 = (ks + 1) * KB / p.ksplit;
       const uint32_t a = tl & 1, use = tl >> 1;
       tc::mbar_wait(&tempty[a], (use & 1) ^ 1);
       tc::tc_fence_after();
       const uint32_t d = tmem + a * BN;
-      for (int kb = 0; kb < KB; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[s], ph);
         tc::tc_fence_after();
+        if (kb == kb0 && lane == 0) LSG_TR(p.trace_slot, 4);
         const uint64_t da = a_desc_base<CC>(sA0 + s * CF::A_BYTES);
         const uint64_t db = tc::sdesc_sw128(sB0 + s * CF::B_BYTES);
         if (elect_one()) {
           if (kb * 4 + 4 <= NS) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb != kb0) | (k != 0));
           } else {
             const int ns = NS - kb * 4;
-            for (int k = 0; k < ns; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < ns; ++k) NF::mma(d, da + a_koff<CC>(k), db + 2 * k, idesc, (kb != kb0) | (k != 0));
           }
           tc::mma_commit(&empty[s]);
         }
@@ -439,6 +640,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
       if (elect_one()) tc::mma_commit(&tfull[a]);
       __syncwarp();
     }
+    if (lane == 0) LSG_TR(p.trace_slot, 5);
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
     tc::griddep_wait();  // the output / residual buffers are free / complete
@@ -450,7 +652,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
     const bool active = SPLIT || half == 0;
     const int r = q * 32 + lane;
     uint32_t tl = 0;
-    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++tl) {
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ++tl) {
+      const int t = u / p.ksplit;
       const TileId id = decode_tile(p, t);
       const Phase& P = p.ph[id.z];
       const uint32_t a = tl & 1, use = tl >> 1;
@@ -480,6 +683,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
           continue;
         }
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
+        if constexpr (SPLIT) {
+          if (p.ksplit > 1) {
+            splitk_tile<BN, HC, PR>(p, u, t, id, r, cbeg, tbase, &tfull[a], &tempty[a], use & 1);
+            continue;
+          }
+        }
         epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::F8 ? n0 + cbeg : 0), p.res_scale,
                              p.out_inv, p.relu != 0, valid, &tfull[a], use & 1);
       } else {
@@ -528,8 +737,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
       tc::tc_fence_before();
       tc::mbar_arrive(&tempty[a]);
     }
+    if (threadIdx.x == 64) LSG_TR(p.trace_slot, 10);
   }
   __syncthreads();
+  if (threadIdx.x == 0) LSG_TR(p.trace_slot, 11);
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc<CF::TMEM_COLS>(tmem);

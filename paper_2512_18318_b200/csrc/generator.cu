@@ -26,6 +26,7 @@
 //     launch (grid.z = phase), so no zero-insertion work is done.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -357,6 +358,9 @@ struct lsg_gen_s {
   std::vector<float> ascale;                 // fp8: scale per tensor id (1 otherwise)
   DevBuf<float> w1b1;
   DevBuf<uint16_t> act;  // all activation buffers
+  DevBuf<float> splitk_ws;   // split-K partial slots (conv_kernel.cuh ConvParams::ws)
+  DevBuf<int> splitk_cnt;    // split-K arrival counters, zero between uses
+  int splitk_tiles = 0;      // tiles the workspace holds
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
   std::vector<LayerRun> plan;
 };
@@ -382,23 +386,81 @@ static void launch_pdl(void (*kernel)(P), int grid, int block, int smem, cudaStr
 
 // Persistent launch: one CTA per SM walks the tiles round-robin in the
 // L2-friendly order of decode_tile().
+// A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
+// the packed tile width, bit 1 disables split-K.
+static int gen_knobs() {
+  static const int k = [] {
+    const char* e = std::getenv("LSG_GEN_KNOBS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return k;
+}
+
+// Split-K factor of a conv_tc layer: grid-starved layers (fewer than half an
+// SM wave of tiles: the low-resolution encoder / decoder blocks) split their K
+// loop so about one wave of CTAs runs, each split keeping >= 2 kblocks.
+static int splitk_factor(const ConvParams& p, int nphases, int tiles, int bn, bool fused, int sms, int ws_tiles) {
+  if (fused || bn < 32 || tiles * 2 > sms || tiles > ws_tiles || (gen_knobs() & 2)) return 1;
+  int kbmin = 1 << 30, kbmax = 0;
+  for (int z = 0; z < nphases; ++z) {
+    kbmin = std::min(kbmin, p.ph[z].kblocks);
+    kbmax = std::max(kbmax, p.ph[z].kblocks);
+  }
+  // a split costs ~5 us (partial store, meeting, reduce): only mainloops of
+  // >= ~6 us (4 MMAs per kblock at the SS-mode rate, ~1.9 GHz) are split
+  const double mma_cyc = std::max(bn / 2.0, (128.0 + bn) / 4.0);
+  const double main_us = kbmax * 4 * mma_cyc / 1900.0;
+  const int kn = gen_knobs();
+  if (main_us < ((kn & 4) ? 3.0 : (kn & 16) ? 10.0 : 6.0)) return 1;
+  const int s = std::min({sms / tiles, (kn & 8) ? kbmin / 2 : kbmin / 4, 16});
+  return s >= 2 ? s : 1;
+}
+
+// Tiles of a conv_tc layer at batch B and tile width bn.
+static int conv_tiles(const LayerRun& r, int B, int bn) {
+  int tiles = 0;
+  for (int z = 0; z < r.nphases; ++z) tiles += (int)ceil_div((int64_t)B * r.GH[z] * r.GW[z], BM) * (r.ntiles * r.bn / bn);
+  return tiles;
+}
+
+// Launch tile width: the packed width, halved (to slices of the packed tiles)
+// while the layer fills less than half an SM wave and stays within one --
+// grid-starved low-resolution layers get more CTAs, each streaming fewer bytes.
+static int conv_launch_bn(const LayerRun& r, int B, int sms, int ws_tiles) {
+  int bn = r.bn;
+  if (r.fused || (gen_knobs() & 1)) return bn;
+  // a long mainloop is better split along K at full width (narrow tiles
+  // re-stream the A tile once per extra column tile)
+  if (splitk_factor(r.p, r.nphases, conv_tiles(r, B, bn), bn, false, sms, ws_tiles) > 1) return bn;
+  while (bn > 64 && r.bn % (bn / 2) == 0 && (bn / 2) % 64 == 0 && conv_tiles(r, B, bn) * 2 <= sms &&
+         conv_tiles(r, B, bn / 2) <= sms)
+    bn /= 2;
+  return bn;
+}
+
 template <int BN, int CC, bool F, int PR>
-static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st) {
+static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int* cnt, int ws_tiles) {
   ConvParams p = r.p;
+  const int ntiles = r.ntiles * r.bn / BN;
   int tiles = 0;
   for (int z = 0; z < r.nphases; ++z) {
     Phase& P = p.ph[z];
     P.M = B * r.GH[z] * r.GW[z];
     P.mtiles = (int)ceil_div(P.M, BM);
     P.tile0 = tiles;
-    tiles += P.mtiles * r.ntiles;
+    tiles += P.mtiles * ntiles;
   }
+  p.pbn = r.bn;
   p.nphases = r.nphases;
-  p.ntiles_n = r.ntiles;
+  p.ntiles_n = ntiles;
   p.total_tiles = tiles;
   p.interleave = 1;
   for (int z = 1; z < r.nphases; ++z) p.interleave &= p.ph[z].mtiles == p.ph[0].mtiles;
-  const int grid = std::min(tiles, sms);
+  p.ksplit = splitk_factor(p, r.nphases, tiles, BN, F, sms, ws ? ws_tiles : 0);
+  p.total_units = tiles * p.ksplit;
+  p.ws = ws;
+  p.counters = cnt;
+  const int grid = std::min(p.total_units, sms);
   launch_pdl(conv_tc<BN, CC, F, PR>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
 }
 
@@ -472,7 +534,7 @@ static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
 }
 
 template <int PR>
-static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
+static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int* cnt, int ws_tiles) {
   if (r.halo) {
 #define LSG_HALO_DISPATCH(BN, MD, F, R)                                                       \
   if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
@@ -482,8 +544,9 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
     fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / mode " +
                            std::to_string(r.halo_mode) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
+  const int lbn = conv_launch_bn(r, B, sms, ws ? ws_tiles : 0);
 #define LSG_DISPATCH(BN, CC, F) \
-  if (r.bn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st);
+  if (lbn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st, ws, cnt, ws_tiles);
   LSG_CONV_VARIANTS(LSG_DISPATCH)
 #undef LSG_DISPATCH
   fail(LSG_ERUNTIME, "generator: no conv kernel for tile width " + std::to_string(r.bn) + " / channel chunk " +
@@ -491,9 +554,12 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st) {
 }
 
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
-  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st);
-  else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st);
-  else dispatch_t<PR_BF16>(r, B, h->sm_count, st);
+  float* ws = h->splitk_ws.p;
+  int* cnt = h->splitk_cnt.p;
+  const int wt = h->splitk_tiles;
+  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, cnt, wt);
+  else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st, ws, cnt, wt);
+  else dispatch_t<PR_BF16>(r, B, h->sm_count, st, ws, cnt, wt);
 }
 
 // Activation tensors for fp8 scales: 0 face input, 1 mel input, 2..8 the
@@ -575,6 +641,12 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       for (auto& r : reqs) tot += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
       h->act.alloc(tot);
       LSG_CUDA(cudaMemset(h->act.p, 0, h->act.bytes()));
+      // split-K workspace: one 128 x 256 fp32 slot per work unit (units <= SMs),
+      // one counter per tile (tiles <= SMs / 2)
+      h->splitk_tiles = h->sm_count / 2;
+      h->splitk_ws.alloc((size_t)h->sm_count * BM * 256);
+      h->splitk_cnt.alloc((size_t)h->splitk_tiles);
+      LSG_CUDA(cudaMemset(h->splitk_cnt.p, 0, h->splitk_cnt.bytes()));
       size_t off = 0;
       for (auto& r : reqs) {
         *r.v = View{h->act.p + off, r.H, r.W, r.C, 0, r.C};
@@ -1074,6 +1146,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
             encode_box(&hp.tmap_res, in, max_batch, bc, HTW, HTH, 1, 1);
           }
         }
+        r.p.trace_slot = (int)h->plan.size();
         h->plan.push_back(r);
       }
       set_smem_attrs(h->prec);
@@ -1199,6 +1272,26 @@ __global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int
   }
 }
 
+// LSG_TRACE builds: copy the phase timestamps out ([64 layers][160 CTAs][16], ns).
+extern "C" lsg_status lsgdbg_trace_read(unsigned long long* out, int64_t n) {
+  return guard([&] {
+#ifdef LSG_TRACE
+    if (n == 0) {  // clear
+      void* a = nullptr;
+      LSG_CUDA(cudaGetSymbolAddress(&a, g_lsg_trace));
+      LSG_CUDA(cudaMemset(a, 0, sizeof(unsigned long long) * TRACE_LAYERS * TRACE_CTAS * TRACE_EV));
+      return;
+    }
+    const size_t cnt = std::min<size_t>((size_t)n, (size_t)TRACE_LAYERS * TRACE_CTAS * TRACE_EV);
+    LSG_CUDA(cudaMemcpyFromSymbol(out, g_lsg_trace, cnt * sizeof(unsigned long long)));
+#else
+    (void)out;
+    (void)n;
+    invalid("lsgdbg_trace_read: library built without LSG_TRACE");
+#endif
+  });
+}
+
 extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
                                         const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
                                         int32_t B, int32_t stop_layer, int32_t which, float* out_dev,
@@ -1210,6 +1303,7 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
     if (stop_layer < 0 || stop_layer >= (int)h->plan.size() - 1) invalid("lsgdbg_run_until: bad layer");
     for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
+    if (!out_dev) return;  // timing a prefix of the layer chain
     const LayerRun& r = h->plan[stop_layer];
     const ConvParams& p = r.p;
     const LayerSpec& L = kLayers[stop_layer];
