@@ -300,6 +300,57 @@ lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_
                         lsg_frame_rec* recs, void* frames, int64_t cap, int64_t* n_out,
                         lsg_pipe_stats* stats);
 
+/* ------------------------------------------ zero-copy stage hand-off
+ * SURVEY.md §8 f3.  A registry of device buffers keyed by (segment uuid,
+ * kind) lets stages exchange mel, PCM and frames as references instead of
+ * payload bytes: the reference's wire codecs (stage.cpp:176-301) copy every
+ * sample into the message, and AlignedPairMsg (stage.hpp:81-93) carries
+ * only counts because the pixels never existed.  A reference (lsg_devref)
+ * is valid in the process that owns the registry; it encodes to 48 bytes
+ * (lsg_devref_encode) so a wire message can carry it.
+ *
+ * Memory: one device arena per registry, sized at create (no cudaMalloc in
+ * the hot path).  put copies into the arena (async, context stream);
+ * put_view adopts a caller-owned device range (no copy; the caller keeps it
+ * alive until the entry is released); alloc hands out arena space for a
+ * producer to write into (e.g. lsg_mel_compute_batch's output).  release at
+ * refcount 0 makes the space reusable once the work queued on the context
+ * stream so far has completed (stream-ordered reuse).
+ * Errors: duplicate (uuid, kind) -> ELOGIC; unknown or stale reference ->
+ * ELOGIC; arena exhausted -> ERUNTIME. */
+#define LSG_BUF_AUDIO 1  /* int16 PCM of a segment        */
+#define LSG_BUF_MEL 2    /* f32 [frames][80]               */
+#define LSG_BUF_FRAMES 3 /* u8 [n][96][96][3] face crops   */
+#define LSG_BUF_RENDER 4 /* rendered frames                */
+typedef struct {
+  uint8_t uuid[16];   /* Uuid::bytes (uuid.hpp)                         */
+  int32_t kind;       /* LSG_BUF_*                                      */
+  int32_t device;     /* CUDA ordinal of the registry                   */
+  uint64_t generation;/* unique per put: stale references are rejected  */
+  int64_t offset;     /* arena offset, or -1 for an adopted view        */
+  int64_t bytes;
+} lsg_devref;
+#define LSG_DEVREF_WIRE_BYTES 48
+typedef struct lsg_reg_s* lsg_reg;
+lsg_status lsg_reg_create(lsg_ctx ctx, int64_t arena_bytes, lsg_reg* out);
+lsg_status lsg_reg_destroy(lsg_reg r);
+lsg_status lsg_reg_put(lsg_reg r, const uint8_t* uuid16, int32_t kind, const void* src /*[host|device]*/,
+                       int64_t bytes, lsg_devref* ref);
+lsg_status lsg_reg_put_view(lsg_reg r, const uint8_t* uuid16, int32_t kind, const void* dev_ptr,
+                            int64_t bytes, lsg_devref* ref);
+lsg_status lsg_reg_alloc(lsg_reg r, const uint8_t* uuid16, int32_t kind, int64_t bytes, void** dev_ptr,
+                         lsg_devref* ref);
+/* device pointer of a live reference */
+lsg_status lsg_reg_resolve(lsg_reg r, const lsg_devref* ref, void** dev_ptr, int64_t* bytes);
+lsg_status lsg_reg_find(lsg_reg r, const uint8_t* uuid16, int32_t kind, lsg_devref* ref);
+lsg_status lsg_reg_retain(lsg_reg r, const lsg_devref* ref);
+lsg_status lsg_reg_release(lsg_reg r, const lsg_devref* ref);
+/* bytes in use (arena, 256-byte granules), live entries, peak bytes */
+lsg_status lsg_reg_stats(lsg_reg r, int64_t* used, int64_t* entries, int64_t* peak);
+/* little-endian wire form (stage.cpp WireWriter conventions), 48 bytes */
+lsg_status lsg_devref_encode(const lsg_devref* ref, uint8_t* out48);
+lsg_status lsg_devref_decode(const uint8_t* in48, lsg_devref* ref);
+
 /* ------------------------------------------------------- synthetic input
  * render_pattern (synth.cpp:46-65) for workload generation: tone bursts on
  * a silence floor, phase restarting per burst.  Host-only. */

@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -392,6 +393,129 @@ struct LipsyncRender {
 // way mock_lipsync does (visual_mocks.cpp:40-51), then renders.
 inline void validate_lipsync(DurationMs audio_span_ms, DurationMs frame_span_ms, std::int64_t n_frames) {
   check(lsg_lipsync_validate(audio_span_ms, frame_span_ms, n_frames));
+}
+
+// ---------------------------------------------- zero-copy stage hand-off
+// device buffers keyed by (segment uuid, kind); stages pass
+// 48-byte references instead of the payload bytes the reference's codecs copy
+// (stage.cpp:176-301).  Errors: duplicate key / stale reference ->
+// std::logic_error, arena exhausted -> std::runtime_error.
+using DevRef = lsg_devref;
+
+class DeviceRegistry {
+ public:
+  DeviceRegistry(std::int64_t arena_bytes, Context& ctx = Context::default_context()) {
+    check(lsg_reg_create(ctx.handle(), arena_bytes, &h_));
+  }
+  ~DeviceRegistry() { lsg_reg_destroy(h_); }
+  DeviceRegistry(const DeviceRegistry&) = delete;
+  DeviceRegistry& operator=(const DeviceRegistry&) = delete;
+  DevRef put(const std::uint8_t* uuid16, int kind, const void* src, std::int64_t bytes) {
+    DevRef r{};
+    check(lsg_reg_put(h_, uuid16, kind, src, bytes, &r));
+    return r;
+  }
+  DevRef put_view(const std::uint8_t* uuid16, int kind, const void* dev_ptr, std::int64_t bytes) {
+    DevRef r{};
+    check(lsg_reg_put_view(h_, uuid16, kind, dev_ptr, bytes, &r));
+    return r;
+  }
+  DevRef alloc(const std::uint8_t* uuid16, int kind, std::int64_t bytes, void** dev_ptr) {
+    DevRef r{};
+    check(lsg_reg_alloc(h_, uuid16, kind, bytes, dev_ptr, &r));
+    return r;
+  }
+  void* resolve(const DevRef& r, std::int64_t* bytes = nullptr) const {
+    void* p = nullptr;
+    check(lsg_reg_resolve(h_, &r, &p, bytes));
+    return p;
+  }
+  void retain(const DevRef& r) { check(lsg_reg_retain(h_, &r)); }
+  void release(const DevRef& r) { check(lsg_reg_release(h_, &r)); }
+
+ private:
+  lsg_reg h_ = nullptr;
+};
+
+// AlignedPairMsg (stage.hpp:81-93) with its mel rows / face crops as device
+// references; wire layout = encode_aligned_pair's (stage.cpp:243-257) under
+// tag 0x105, then u32 count + 48-byte references.
+inline constexpr std::uint32_t kTagAlignedPairRef = 0x105;
+
+struct AlignedPairRefMsg {
+  std::uint8_t uuid[16] = {};
+  Timestamp birth = 0, begin = 0, end = 0;
+  DurationMs source_duration_ms = 0, offset_ms = 0;
+  bool low_confidence = false;
+  std::int64_t n_frames = 0;
+  Timestamp first_frame_ts = 0, last_frame_ts = 0;
+  std::int64_t mel_frames = 0;
+  std::vector<DevRef> refs;
+};
+
+inline std::vector<std::uint8_t> encode_aligned_pair_ref(const AlignedPairRefMsg& m) {
+  std::vector<std::uint8_t> b;
+  auto u32 = [&](std::uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back(std::uint8_t(v >> (8 * i)));
+  };
+  auto i64 = [&](std::int64_t v) {
+    for (int i = 0; i < 8; ++i) b.push_back(std::uint8_t(std::uint64_t(v) >> (8 * i)));
+  };
+  u32(kTagAlignedPairRef);
+  b.insert(b.end(), m.uuid, m.uuid + 16);
+  i64(m.birth), i64(m.begin), i64(m.end), i64(m.source_duration_ms), i64(m.offset_ms);
+  b.push_back(m.low_confidence ? 1 : 0);
+  i64(m.n_frames), i64(m.first_frame_ts), i64(m.last_frame_ts), i64(m.mel_frames);
+  u32(std::uint32_t(m.refs.size()));
+  for (const DevRef& r : m.refs) {
+    std::uint8_t w[LSG_DEVREF_WIRE_BYTES];
+    check(lsg_devref_encode(&r, w));
+    b.insert(b.end(), w, w + LSG_DEVREF_WIRE_BYTES);
+  }
+  return b;
+}
+
+inline AlignedPairRefMsg decode_aligned_pair_ref(const std::vector<std::uint8_t>& b) {
+  std::size_t pos = 0;
+  auto need = [&](std::size_t n) {
+    if (pos + n > b.size()) throw std::runtime_error("wire: truncated");
+  };
+  auto u32 = [&] {
+    need(4);
+    std::uint32_t v = 0;
+    for (int i = 0; i < 4; ++i) v |= std::uint32_t(b[pos + i]) << (8 * i);
+    pos += 4;
+    return v;
+  };
+  auto i64 = [&] {
+    need(8);
+    std::uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= std::uint64_t(b[pos + i]) << (8 * i);
+    pos += 8;
+    return std::int64_t(v);
+  };
+  const std::uint32_t tag = u32();
+  if (tag != kTagAlignedPairRef)
+    throw std::runtime_error("wire: expected tag " + std::to_string(kTagAlignedPairRef) + ", got " +
+                             std::to_string(tag));
+  AlignedPairRefMsg m;
+  need(16);
+  std::copy(b.begin() + std::ptrdiff_t(pos), b.begin() + std::ptrdiff_t(pos + 16), m.uuid);
+  pos += 16;
+  m.birth = i64(), m.begin = i64(), m.end = i64(), m.source_duration_ms = i64(), m.offset_ms = i64();
+  need(1);
+  m.low_confidence = b[pos++] != 0;
+  m.n_frames = i64(), m.first_frame_ts = i64(), m.last_frame_ts = i64(), m.mel_frames = i64();
+  const std::uint32_t n = u32();
+  for (std::uint32_t i = 0; i < n; ++i) {
+    need(LSG_DEVREF_WIRE_BYTES);
+    DevRef r{};
+    check(lsg_devref_decode(b.data() + pos, &r));
+    pos += LSG_DEVREF_WIRE_BYTES;
+    m.refs.push_back(r);
+  }
+  if (pos != b.size()) throw std::runtime_error("wire: trailing bytes");
+  return m;
 }
 
 }  // namespace lipstream_b200

@@ -18,6 +18,7 @@
 #include "lipstream/mel.hpp"
 #include "lipstream/rng.hpp"
 #include "lipstream/segmenter.hpp"
+#include "lipstream/stage.hpp"
 #include "lipstream/synth.hpp"
 #include "lipstream/vad.hpp"
 
@@ -334,6 +335,106 @@ int ref_align_envelopes(const double* e, int64_t ne, const double* m, int64_t nm
     *offset = r.offset_ms;
     *corr = r.peak_corr;
     *low = r.low_confidence ? 1 : 0;
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// Wire codecs of the path's stage messages (stage.cpp:176-301): encode into
+// out (cap bytes, *n = size); decode back to fields.  -1 = the reference threw
+// (wire: truncated / expected tag / trailing bytes), -2 = out too small.
+static int copy_out(const WireBytes& b, uint8_t* out, int64_t cap, int64_t* n) {
+  *n = (int64_t)b->size();
+  if (*n > cap) return -2;
+  std::memcpy(out, b->data(), b->size());
+  return 0;
+}
+static Uuid to_uuid(const uint8_t* u) {
+  Uuid x;
+  std::memcpy(x.bytes.data(), u, 16);
+  return x;
+}
+
+int ref_encode_segment(const uint8_t* uuid, int64_t birth, int64_t begin, int64_t end, double conf, int32_t rate,
+                       const int16_t* s, int64_t ns, uint8_t* out, int64_t cap, int64_t* n) {
+  SegmentMsg m;
+  m.uuid = to_uuid(uuid);
+  m.birth = birth;
+  m.begin = begin;
+  m.end = end;
+  m.confidence = conf;
+  m.audio.sample_rate = rate;
+  m.audio.samples.assign(s, s + ns);
+  return copy_out(encode_segment(m), out, cap, n);
+}
+
+int ref_decode_segment(const uint8_t* in, int64_t nin, int64_t* f3, double* conf, int32_t* rate, int16_t* s,
+                       int64_t cap, int64_t* ns) {
+  try {
+    SegmentMsg m = decode_segment(std::vector<uint8_t>(in, in + nin));
+    f3[0] = m.birth;
+    f3[1] = m.begin;
+    f3[2] = m.end;
+    *conf = m.confidence;
+    *rate = m.audio.sample_rate;
+    *ns = (int64_t)m.audio.samples.size();
+    if (*ns > cap) return -2;
+    std::copy(m.audio.samples.begin(), m.audio.samples.end(), s);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// f9 = birth, begin, end, source_duration_ms, offset_ms, n_frames, first_frame_ts, last_frame_ts, mel_frames
+int ref_encode_aligned_pair(const uint8_t* uuid, const int64_t* f9, int32_t low, uint8_t* out, int64_t cap,
+                            int64_t* n) {
+  AlignedPairMsg m;
+  m.uuid = to_uuid(uuid);
+  m.birth = f9[0];
+  m.begin = f9[1];
+  m.end = f9[2];
+  m.source_duration_ms = f9[3];
+  m.offset_ms = f9[4];
+  m.low_confidence = low != 0;
+  m.n_frames = f9[5];
+  m.first_frame_ts = f9[6];
+  m.last_frame_ts = f9[7];
+  m.mel_frames = f9[8];
+  return copy_out(encode_aligned_pair(m), out, cap, n);
+}
+
+int ref_decode_aligned_pair(const uint8_t* in, int64_t nin, uint8_t* uuid, int64_t* f9, int32_t* low) {
+  try {
+    AlignedPairMsg m = decode_aligned_pair(std::vector<uint8_t>(in, in + nin));
+    std::memcpy(uuid, m.uuid.bytes.data(), 16);
+    const int64_t v[9] = {m.birth, m.begin, m.end, m.source_duration_ms, m.offset_ms,
+                          m.n_frames, m.first_frame_ts, m.last_frame_ts, m.mel_frames};
+    std::copy(v, v + 9, f9);
+    *low = m.low_confidence ? 1 : 0;
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// f6 = birth, begin, end, source_duration_ms, frames_rendered, offset_ms
+int ref_encode_final(const uint8_t* uuid, const int64_t* f6, uint8_t* out, int64_t cap, int64_t* n) {
+  FinalMsg m;
+  m.uuid = to_uuid(uuid);
+  m.birth = f6[0];
+  m.begin = f6[1];
+  m.end = f6[2];
+  m.source_duration_ms = f6[3];
+  m.frames_rendered = f6[4];
+  m.offset_ms = f6[5];
+  return copy_out(encode_final(m), out, cap, n);
+}
+
+int ref_wire_tag(const uint8_t* in, int64_t nin, uint32_t* tag) {
+  try {
+    *tag = wire_tag(std::vector<uint8_t>(in, in + nin));
     return 0;
   } catch (const std::exception&) {
     return -1;

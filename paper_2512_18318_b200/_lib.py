@@ -60,6 +60,12 @@ class FrameRec(C.Structure):
                 ("mel_row", C.c_int32), ("pad", C.c_int32)]
 
 
+class DevRef(C.Structure):
+    """lsg_devref: a registry reference (uuid, kind, device, generation, offset, bytes)."""
+    _fields_ = [("uuid", C.c_uint8 * 16), ("kind", C.c_int32), ("device", C.c_int32), ("generation", C.c_uint64),
+                ("offset", C.c_int64), ("bytes", C.c_int64)]
+
+
 class PipeStats(C.Structure):
     _fields_ = [("segments", C.c_int64), ("mel_frames", C.c_int64), ("frames_rendered", C.c_int64),
                 ("unique_frames", C.c_int64), ("ms_segment", C.c_double), ("ms_mel", C.c_double),
@@ -121,6 +127,18 @@ _SIGS = {
     "lsg_pipe_destroy": [P],
     "lsg_pipe_run": [P, PP, PI64, PP, PI64, P, C.POINTER(FrameRec), P, I64, PI64, C.POINTER(PipeStats)],
     "lsg_synth_pattern": [I64, I32, PI64, PI64, F64, F64, I64, I32, P, I64, PI64],
+    "lsg_reg_create": [P, I64, PP],
+    "lsg_reg_destroy": [P],
+    "lsg_reg_put": [P, P, I32, P, I64, C.POINTER(DevRef)],
+    "lsg_reg_put_view": [P, P, I32, P, I64, C.POINTER(DevRef)],
+    "lsg_reg_alloc": [P, P, I32, I64, PP, C.POINTER(DevRef)],
+    "lsg_reg_resolve": [P, C.POINTER(DevRef), PP, PI64],
+    "lsg_reg_find": [P, P, I32, C.POINTER(DevRef)],
+    "lsg_reg_retain": [P, C.POINTER(DevRef)],
+    "lsg_reg_release": [P, C.POINTER(DevRef)],
+    "lsg_reg_stats": [P, PI64, PI64, PI64],
+    "lsg_devref_encode": [C.POINTER(DevRef), P],
+    "lsg_devref_decode": [P, C.POINTER(DevRef)],
 }
 _RESTYPE = {"lsg_abi_version": C.c_int32, "lsg_last_error": C.c_char_p}
 

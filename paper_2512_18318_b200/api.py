@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (Cut, InvalidArgument, LogicError, MelCfg, SegCfg, SegMetrics, lib)
+from ._lib import (Cut, DevRef, InvalidArgument, LogicError, MelCfg, SegCfg, SegMetrics, lib)
 
 
 class SegmenterMode(enum.IntEnum):
@@ -665,3 +665,120 @@ def crop96(frames: np.ndarray, frame_of, boxes, ctx: Context | None = None) -> n
     finally:
         dev.free()
     return out
+
+
+# ------------------------------------------------ zero-copy stage hand-off
+class DeviceRegistry:
+    """Device buffers keyed by (segment uuid, kind) -- SURVEY.md §8 f3.
+    Stages exchange `wire.Ref`s (48 bytes on the wire, wire.*_ref codecs)
+    instead of the payload bytes the reference's codecs copy
+    (stage.cpp:176-301).  Errors: duplicate key / stale reference ->
+    LogicError; arena exhausted -> LsgError (ERUNTIME)."""
+
+    def __init__(self, arena_bytes: int, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        h = C.c_void_p()
+        self.lib.call("lsg_reg_create", self.ctx.h, int(arena_bytes), C.byref(h))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lsg_reg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _uuid(u) -> C.Array:
+        b = bytes(u)
+        if len(b) != 16:
+            raise ValueError("uuid must be 16 bytes")
+        return (C.c_uint8 * 16).from_buffer_copy(b)
+
+    @staticmethod
+    def _to_py(r: DevRef):
+        from .wire import Ref
+        return Ref(bytes(r.uuid), r.kind, r.device, r.generation, r.offset, r.bytes)
+
+    @staticmethod
+    def _to_c(ref) -> DevRef:
+        r = DevRef()
+        C.memmove(r.uuid, bytes(ref.uuid), 16)
+        r.kind, r.device, r.generation, r.offset, r.bytes = ref.kind, ref.device, ref.generation, ref.offset, ref.bytes
+        return r
+
+    def put(self, uuid, kind: int, src, nbytes: int | None = None):
+        """Copy a host array / device pointer into the arena (async on the
+        context stream); returns the Ref."""
+        if isinstance(src, np.ndarray):
+            src = np.ascontiguousarray(src)
+            ptr, n = src.ctypes.data, src.nbytes if nbytes is None else nbytes
+            keep = src
+        else:
+            ptr, n, keep = int(src), int(nbytes), None
+        r = DevRef()
+        self.lib.call("lsg_reg_put", self.h, self._uuid(uuid), kind, C.c_void_p(ptr), n, C.byref(r))
+        if keep is not None:  # host source: the async copy must finish before the array may go
+            self.ctx.sync()
+        return self._to_py(r)
+
+    def put_view(self, uuid, kind: int, dev_ptr: int, nbytes: int):
+        """Adopt a caller-owned device range (no copy)."""
+        r = DevRef()
+        self.lib.call("lsg_reg_put_view", self.h, self._uuid(uuid), kind, C.c_void_p(dev_ptr), int(nbytes), C.byref(r))
+        return self._to_py(r)
+
+    def alloc(self, uuid, kind: int, nbytes: int):
+        """Arena space for a producer to write into: (device pointer, Ref)."""
+        r, p = DevRef(), C.c_void_p()
+        self.lib.call("lsg_reg_alloc", self.h, self._uuid(uuid), kind, int(nbytes), C.byref(p), C.byref(r))
+        return p.value or 0, self._to_py(r)
+
+    def resolve(self, ref) -> tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int64()
+        self.lib.call("lsg_reg_resolve", self.h, C.byref(self._to_c(ref)), C.byref(p), C.byref(n))
+        return p.value or 0, n.value
+
+    def find(self, uuid, kind: int):
+        r = DevRef()
+        self.lib.call("lsg_reg_find", self.h, self._uuid(uuid), kind, C.byref(r))
+        return self._to_py(r)
+
+    def retain(self, ref):
+        self.lib.call("lsg_reg_retain", self.h, C.byref(self._to_c(ref)))
+
+    def release(self, ref):
+        self.lib.call("lsg_reg_release", self.h, C.byref(self._to_c(ref)))
+
+    def read(self, ref) -> bytes:
+        """D2H copy of a buffer (for consumers that really need host bytes)."""
+        p, n = self.resolve(ref)
+        out = np.empty(n, np.uint8)
+        if n:
+            self.lib.call("lsg_copy", self.ctx.h, C.c_void_p(out.ctypes.data), C.c_void_p(p), n)
+            self.ctx.sync()
+        return out.tobytes()
+
+    def stats(self) -> dict:
+        u, e, pk = C.c_int64(), C.c_int64(), C.c_int64()
+        self.lib.call("lsg_reg_stats", self.h, C.byref(u), C.byref(e), C.byref(pk))
+        return {"used": u.value, "entries": e.value, "peak": pk.value}
+
+
+def devref_encode(ref) -> bytes:
+    """lsg_devref_encode through the library (the wire.Ref.to_bytes layout)."""
+    out = (C.c_uint8 * 48)()
+    lib().call("lsg_devref_encode", C.byref(DeviceRegistry._to_c(ref)), out)
+    return bytes(out)
+
+
+def devref_decode(b: bytes):
+    r = DevRef()
+    buf = (C.c_uint8 * 48).from_buffer_copy(bytes(b))
+    lib().call("lsg_devref_decode", buf, C.byref(r))
+    return DeviceRegistry._to_py(r)

@@ -201,6 +201,38 @@ int main(int argc, char** argv) {
   CHECK(throws<std::invalid_argument>([] { validate_lipsync(2000, 2020, 1); }));
   CHECK(throws<std::invalid_argument>([] { validate_lipsync(2000, 2400, 61); }));
   validate_lipsync(2000, 2020, 61);
+  // zero-copy hand-off: mel into registry space, the pair
+  // message carries the reference, the consumer resolves the same buffer
+  {
+    DeviceRegistry reg(1 << 20);
+    std::uint8_t u[16];
+    for (int i = 0; i < 16; ++i) u[i] = std::uint8_t(i * 7);
+    void* mel_dev = nullptr;
+    const std::int64_t bytes = mel.n_frames * 80 * 4;
+    DevRef rm = reg.alloc(u, LSG_BUF_MEL, bytes, &mel_dev);
+    CHECK(mel_dev != nullptr && rm.bytes == bytes && rm.kind == LSG_BUF_MEL);
+    AlignedPairRefMsg m;
+    std::copy(u, u + 16, m.uuid);
+    m.end = 1000, m.n_frames = 25, m.mel_frames = mel.n_frames;
+    m.refs.push_back(rm);
+    const auto wire_bytes = encode_aligned_pair_ref(m);
+    CHECK(wire_bytes.size() == 4 + 16 + 8 * 5 + 1 + 8 * 4 + 4 + LSG_DEVREF_WIRE_BYTES);
+    const AlignedPairRefMsg back = decode_aligned_pair_ref(wire_bytes);
+    std::int64_t nb = 0;
+    CHECK(reg.resolve(back.refs.at(0), &nb) == mel_dev && nb == bytes && back.mel_frames == mel.n_frames);
+    CHECK(throws<std::runtime_error>([&] {
+      auto t = wire_bytes;
+      t.pop_back();
+      decode_aligned_pair_ref(t);
+    }));
+    CHECK(throws<std::logic_error>([&] { reg.put(u, LSG_BUF_MEL, mel.data.data(), 64); }));  // duplicate key
+    reg.release(rm);
+    CHECK(throws<std::logic_error>([&] { reg.resolve(rm); }));  // stale
+    CHECK(throws<std::runtime_error>([&] {
+      void* p = nullptr;
+      reg.alloc(u, LSG_BUF_MEL, 2 << 20, &p);  // exhausted
+    }));
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "all drop-in checks passed", g_fail);
   return g_fail ? 1 : 0;
 }
