@@ -106,6 +106,9 @@ struct alignas(64) ConvParams {
   int trace_slot;  // layer index (LSG_TRACE builds)
   int pbn;         // tile width the weights are packed for (a multiple of BN: a
                    // BN-wide tile is a contiguous, swizzle-aligned slice of it)
+  CUtensorMap wmap;  // the layer's packed weights as 2-D [rows][64] (no swizzle:
+                     // the bytes are pre-swizzled), for CTA-pair TMA loads
+  int wrow0[MAX_PHASES];  // first weight row of each phase in wmap
   Phase ph[MAX_PHASES];
 };
 

@@ -36,6 +36,7 @@
 
 #include "conv_halo.cuh"
 #include "conv_kernel.cuh"
+#include "conv_pair.cuh"
 #include "gen_internal.h"
 #include "lsg_common.cuh"
 #include "tc.cuh"
@@ -209,6 +210,7 @@ struct LayerRun {
   bool halo = false;                   // routed to conv_halo
   bool halo_bres = false;              // weights resident in shared memory
   int halo_mode = 0;                   // HaloMode of a conv_halo layer
+  bool pair_ok = false;                // conv_tc layer with a weight map for CTA-pair launches
   HaloParams hp;
 };
 
@@ -464,6 +466,56 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st, floa
   launch_pdl(conv_tc<BN, CC, F, PR>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
 }
 
+// CTA-pair launch (conv_pair.cuh): tiles are pairs of m-tiles, one cluster of
+// two CTAs per pair, grid = an even number of SMs.
+template <int BN, int CC, int PR>
+static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
+  ConvParams p = r.p;
+  const int ntiles = r.ntiles * r.bn / BN;
+  int tiles = 0;
+  for (int z = 0; z < r.nphases; ++z) {
+    Phase& P = p.ph[z];
+    P.M = B * r.GH[z] * r.GW[z];
+    P.mtiles = (int)ceil_div(ceil_div(P.M, BM), 2);
+    P.tile0 = tiles;
+    tiles += P.mtiles * ntiles;
+  }
+  p.pbn = r.bn;
+  p.nphases = r.nphases;
+  p.ntiles_n = ntiles;
+  p.total_tiles = tiles;
+  p.interleave = 1;
+  for (int z = 1; z < r.nphases; ++z) p.interleave &= p.ph[z].mtiles == p.ph[0].mtiles;
+  p.ksplit = 1;
+  p.total_units = tiles;
+  p.ws = nullptr;
+  p.counters = nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::min(2 * tiles, sms & ~1));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = (size_t)Cfg2<BN>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  LSG_CUDA(cudaLaunchKernelEx(&cfg, conv_tc2<BN, CC, PR>, p));
+}
+
+// (tile width, channel chunk) combinations of the pair kernel
+#define LSG_PAIR_VARIANTS(X) \
+  X(128, 64)                 \
+  X(192, 64)                 \
+  X(256, 64)                 \
+  X(128, 32)                 \
+  X(192, 32)                 \
+  X(256, 32)
+
 // (tile width BN, channel chunk CC in 16-bit units, fused output)
 // combinations the Wav2Lip layers use; every combination is compiled for
 // bf16, fp16 and fp8 (fp8 halves the units per channel, hence CC 8/16/32 with
@@ -516,6 +568,10 @@ static void set_smem_attrs_t() {
                                 HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
+#define LSG_SET_PAIR_ATTR(BN, CC) \
+  LSG_CUDA(cudaFuncSetAttribute(conv_tc2<BN, CC, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
+  LSG_PAIR_VARIANTS(LSG_SET_PAIR_ATTR)
+#undef LSG_SET_PAIR_ATTR
 }
 static void set_smem_attrs(int prec) {
   if (prec == PR_FP8) set_smem_attrs_t<PR_FP8>();
@@ -545,6 +601,14 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float
                            std::to_string(r.halo_mode) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
   const int lbn = conv_launch_bn(r, B, sms, ws ? ws_tiles : 0);
+  // wide layers with at least a full wave of tiles: CTA pairs
+  if (r.pair_ok && lbn == r.bn && !(gen_knobs() & 32) && conv_tiles(r, B, r.bn) >= sms &&
+      splitk_factor(r.p, r.nphases, conv_tiles(r, B, r.bn), r.bn, false, sms, ws ? ws_tiles : 0) == 1) {
+#define LSG_PAIR_DISPATCH(BN, CC) \
+  if (r.bn == BN && r.p.cc == CC) return launch_pair<BN, CC, PR>(r, B, sms, st);
+    LSG_PAIR_VARIANTS(LSG_PAIR_DISPATCH)
+#undef LSG_PAIR_DISPATCH
+  }
 #define LSG_DISPATCH(BN, CC, F) \
   if (lbn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st, ws, cnt, ws_tiles);
   LSG_CONV_VARIANTS(LSG_DISPATCH)
@@ -1082,6 +1146,24 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // the tensor map's bounding box must generate exactly the phase grid
           const int gw = (in.W + upper_w - lower_w - 1) / p.sx + 1, gh = (in.H + upper_h - lower_h - 1) / p.sy + 1;
           if (gw != P.GW || gh != P.GH) fail(LSG_ERUNTIME, std::string("generator: im2col grid mismatch at ") + L.name);
+        }
+        // CTA-pair launches load weight half-tiles through a 2-D map over the
+        // layer's packed weights (all phases, rows of 64 units, pre-swizzled)
+        if (!fused && r.bn >= 128) {
+          int64_t rows = 0;
+          for (int z = 0; z < r.nphases; ++z) {
+            p.wrow0[z] = (int)((p.ph[z].w - p.ph[0].w) / BK);
+            rows = std::max<int64_t>(rows, p.wrow0[z] + (int64_t)r.ntiles * p.ph[z].kblocks * r.bn);
+          }
+          const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)rows};
+          const cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
+          const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(r.bn / 2)};
+          const cuuint32_t estr[2] = {1, 1};
+          CUresult cr = tiled_fn()(&p.wmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(p.ph[0].w), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (cr != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled (weights) failed");
+          r.pair_ok = true;
         }
         const HaloGeo& hg = hgeo[l];
         if (hg.mode != HALO_NONE && (hg.mode != HALO_CONV3 || in.W >= 16)) {
