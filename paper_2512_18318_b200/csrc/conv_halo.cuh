@@ -36,7 +36,7 @@ constexpr int MAX_HTAPS = 9;
 // Routing modes and their compile-time tap tables (patch offset in pixels,
 // output phase).  The host builds the same lists from the layer geometry and
 // checks them against these (generator.cu), so packing and issue agree.
-enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3 };
+enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3, HALO_STEM4X = 4 };
 
 template <int MODE>
 struct HaloTaps;
@@ -61,6 +61,18 @@ struct HaloTaps<HALO_STEM7> {  // 7x7 on 8 channels: planes = x shifts, taps = k
   __host__ __device__ static constexpr int aoff(int t) { return t * PW; }
   __host__ __device__ static constexpr int phase(int) { return 0; }
 };
+// The stem on "macro-pixels": a GEMM row is 4 horizontally adjacent output
+// pixels (N = 4 x 16 channels per MMA instead of 16 -- the SS-mode MMA cost
+// is set by the A read, so 4 pixels per row cost 48 instead of 4 x 36
+// cycles).  Plane g (g = 0..9) holds input column 4j + g - 3 for macro
+// column j (a W-strided TMA box), so a K step still reads 2 planes; the
+// 4 pixel offsets are the epilogue's "phases" (element-strided stores).
+template <>
+struct HaloTaps<HALO_STEM4X> {
+  static constexpr int NPH = 4, NT = 7, PW = HTW, PH = HTH + 6;
+  __host__ __device__ static constexpr int aoff(int t) { return t * PW; }
+  __host__ __device__ static constexpr int phase(int) { return 0; }
+};
 
 struct alignas(64) HaloParams {
   CUtensorMap tmap;      // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
@@ -74,6 +86,7 @@ struct alignas(64) HaloParams {
   int ngran;         // planes per tile over all channel blocks (C/8, or 8 shifted copies)
   int ncb;           // channel blocks of <= 8 planes
   int shift_planes;  // planes are x-shifted copies of channels 0..7 (fe0)
+  int xmul;          // input columns per grid column (4 for the macro-pixel stem)
   int ntaps;
   int aoff[MAX_HTAPS];   // tap start offset in the patch, 16-byte units (= pixels)
   int tphase[MAX_HTAPS]; // output phase the tap accumulates into
@@ -110,10 +123,11 @@ struct HaloCfg {
   static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
-  static constexpr int BBLK = BN * BK * 2;  // one (cb, tap) weight block
+  static constexpr int MN = MODE == HALO_STEM4X ? NPH * BN : BN;  // MMA N: every phase at once for macro-pixels
+  static constexpr int BBLK = MN * BK * 2;  // one (cb, tap) weight block
   static constexpr int WG = 3;              // streamed weights: taps per ring slot (one wait + commit each)
   static constexpr int GBLK = WG * BBLK;
-  static constexpr int W_RES_BYTES = 72 * 1024;
+  static constexpr int W_RES_BYTES = MODE == HALO_STEM4X ? 112 * 1024 : 72 * 1024;
   static constexpr int IB = BN * ES < 128 ? BN * ES : 128;  // bytes per position per box
   static constexpr int NCH = BN * ES > 128 ? BN * ES / 128 : 1;  // boxes across the channels
   static constexpr int BOX = 128 * IB;                 // one [128][IB] box
@@ -122,7 +136,11 @@ struct HaloCfg {
   static constexpr int RES_BYTES = HAS_RES ? NCH * BOX : 0;
   static constexpr int NRES = HAS_RES ? (B_RES ? 2 : 1) : 0;
   static constexpr int EPI_BYTES = NSTG * STG_BYTES + NRES * RES_BYTES;
-  static constexpr int HS = (B_RES || 3 * HSTAGE + EPI_BYTES + 2 * GBLK <= 220 * 1024) ? 3 : 2;
+  // patch stages: 3 where the weight ring still gets >= 2 groups; the ConvT's
+  // 4-phase staging leaves room for only 3 weight groups (~0.9 us of MMAs,
+  // less than the L2 round trip), so it trades a patch stage for a 4th group
+  static constexpr int HS =
+      MODE == HALO_CONVT2 ? 2 : ((B_RES || 3 * HSTAGE + EPI_BYTES + 2 * GBLK <= 220 * 1024) ? 3 : 2);
   static constexpr int FIXED = HS * HSTAGE + EPI_BYTES;
   static constexpr int BS_FIT = (220 * 1024 - FIXED) / GBLK;
   static constexpr int BS = B_RES ? 1 : (BS_FIT > 4 ? 4 : BS_FIT);
@@ -270,7 +288,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       const int n = t / p.tiles_per_img, r = t - n * p.tiles_per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
-      const int y0 = ty * HTH + p.oy0, x0 = tx * HTW + p.ox0;
+      const int y0 = ty * HTH + p.oy0, x0 = tx * HTW * p.xmul + p.ox0;
 
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
@@ -279,19 +297,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         __syncwarp();
         if (lane < ng)
           tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * cstep,
-                      x0 + lane * xstep, y0, n);
+                      x0 + (g0 + lane) * xstep, y0, n);
         if (++hs == HS) {
           hs = 0;
           hph ^= 1;
         }
         if constexpr (!B_RES) {  // taps [g*WG, g*WG+WG) of this channel block per ring slot
-          const uint16_t* wb = p.w + (size_t)cb * p.ntaps * BN * BK;
+          const uint16_t* wb = p.w + (size_t)cb * p.ntaps * CF::MN * BK;
           for (int t0 = 0; t0 < p.ntaps; t0 += CF::WG) {
             const uint32_t bytes = (uint32_t)(min(CF::WG, p.ntaps - t0) * CF::BBLK);
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             if (lane == 0) {
               tc::mbar_arrive_expect_tx(&bfull[bs], bytes);
-              tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * BN * BK, bytes, &bfull[bs]);
+              tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * CF::MN * BK, bytes, &bfull[bs]);
             }
             __syncwarp();
             if (++bs == BS) {
@@ -326,7 +344,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     // is a handful of uniform adds per 4 MMAs (profiles/r01: with divisions,
     // parameter reloads and per-tap warp reconvergence it cost more than the
     // MMAs themselves).
-    constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+    constexpr uint32_t idesc = tc::idesc_f16kind(BM, CF::MN, NF::kFmt);
     constexpr int NT = TT::NT;
     constexpr uint64_t PLANE2 = (uint64_t)((2 * ((TT::PW * TT::PH * 16 + 127) / 128 * 128)) >> 4);
     constexpr uint64_t BBLK16 = CF::BBLK >> 4;
@@ -359,7 +377,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
               db = b_desc0 + (uint64_t)bs * (CF::GBLK >> 4) + (uint64_t)(tap % CF::WG) * BBLK16;
             }
             const uint64_t at = ah + (uint64_t)TT::aoff(tap);
-            const uint32_t dd = d + (uint32_t)(TT::phase(tap) * BN);
+            const uint32_t dd = d + (uint32_t)(MODE == HALO_STEM4X ? 0 : TT::phase(tap) * BN);
             bool first = true;  // first tap of its phase (compile time)
 #pragma unroll
             for (int u = 0; u < tap; ++u) first = first && TT::phase(u) != TT::phase(tap);

@@ -214,6 +214,16 @@ struct LayerRun {
   HaloParams hp;
 };
 
+// A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
+// the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem.
+static int gen_knobs() {
+  static const int k = [] {
+    const char* e = std::getenv("LSG_GEN_KNOBS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return k;
+}
+
 // Layers routed to the patch-reuse kernel (conv_halo.cuh); everything else
 // goes to the im2col kernel.
 HaloMode halo_mode(const LayerSpec& L) {
@@ -224,8 +234,8 @@ HaloMode halo_mode(const LayerSpec& L) {
       L.opw == 1 && L.cout <= 64 && L.cin % 16 == 0)
     return HALO_CONVT2;  // fd6.0: 4 output phases share one accumulator set
   if (L.kind == CONV && L.kh == 7 && L.kw == 7 && L.sh == 1 && L.sw == 1 && L.ph == 3 && L.pw == 3 && L.cin <= 8 &&
-      L.cout <= 16)
-    return HALO_STEM7;  // fe0 on the 8-channel face tensor
+      L.cout <= 16)  // fe0 on the 8-channel face tensor: macro-pixels (LSG_GEN_KNOBS bit 64: one pixel per row)
+    return (gen_knobs() & 64) ? HALO_STEM7 : HALO_STEM4X;
   return HALO_NONE;
 }
 
@@ -255,12 +265,13 @@ EncodeTiled tiled_fn() {
 }
 
 // tiled map of an NHWC channel-slice view, box = 8 channels x pw x ph x 1 image
-void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph) {
+// (ex > 1: every ex-th column, pw of them -- the macro-pixel stem's planes)
+void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph, int ex = 1) {
   const cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)n};
   const cuuint64_t strides[3] = {(cuuint64_t)v.pitch * 2, (cuuint64_t)v.W * v.pitch * 2,
                                  (cuuint64_t)v.H * v.W * v.pitch * 2};
-  const cuuint32_t box[4] = {8, (cuuint32_t)pw, (cuuint32_t)ph, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const cuuint32_t box[4] = {8, (cuuint32_t)(pw * ex), (cuuint32_t)ph, 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)ex, 1, 1};
   CUresult r = tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -388,16 +399,6 @@ static void launch_pdl(void (*kernel)(P), int grid, int block, int smem, cudaStr
 
 // Persistent launch: one CTA per SM walks the tiles round-robin in the
 // L2-friendly order of decode_tile().
-// A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
-// the packed tile width, bit 1 disables split-K.
-static int gen_knobs() {
-  static const int k = [] {
-    const char* e = std::getenv("LSG_GEN_KNOBS");
-    return e ? std::atoi(e) : 0;
-  }();
-  return k;
-}
-
 // Split-K factor of a conv_tc layer: grid-starved layers (fewer than half an
 // SM wave of tiles: the low-resolution encoder / decoder blocks) split their K
 // loop so about one wave of CTAs runs, each split keeping >= 2 kblocks.
@@ -540,6 +541,7 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
 // halo kernel variants: (tile width, mode, fused output, weights resident)
 #define LSG_HALO_VARIANTS(X)             \
   X(16, HALO_STEM7, false, true)         \
+  X(16, HALO_STEM4X, false, true)        \
   X(32, HALO_CONV3, false, true)         \
   X(64, HALO_CONV3, false, true)         \
   X(128, HALO_CONV3, false, false)       \
@@ -853,18 +855,25 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                 add_tap(G[z].dy[t] * hg.pw + G[z].dx[t], z, G[z].ky[t], G[z].kx[t]);
               }
             }
-          } else {  // stem: planes = x shifts 0..7, taps = the 7 kernel rows
+          } else {  // stem: planes = x shifts, taps = the 7 kernel rows
             hg.oy0 = hg.ox0 = -3;
             hg.pw = HTW;
             hg.ph = HTH + 6;
+            if (hm == HALO_STEM4X) {  // 4-pixel macro columns: pixel offset z is output phase z
+              hg.nph = 4;
+              for (int z = 0; z < 4; ++z) hg.pox[z] = z;
+            }
             for (int ky = 0; ky < 7; ++ky) add_tap(ky * hg.pw, 0, ky, -1);
           }
           const bool ok = hm == HALO_CONV3    ? taps_match<HALO_CONV3>(hg)
                           : hm == HALO_CONVT2 ? taps_match<HALO_CONVT2>(hg)
+                          : hm == HALO_STEM4X ? taps_match<HALO_STEM4X>(hg)
                                               : taps_match<HALO_STEM7>(hg);
           if (!ok) fail(LSG_ERUNTIME, std::string("generator: halo tap table mismatch at ") + L.name);
-          // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap)
-          const int ncb = hm == HALO_STEM7 ? 1 : (L.cin + KE - 1) / KE, bnh = L.cout;
+          // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap);
+          // macro-pixel stem: rows (pixel offset z, cout), K = (x-shift plane, channel)
+          const bool x4 = hm == HALO_STEM4X;
+          const int ncb = hm == HALO_STEM7 ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE, bnh = x4 ? 4 * L.cout : L.cout;
           hg.off = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)ncb * hg.ntaps * bnh * BK, 0);
           uint16_t* dst = pack.data() + hg.off;
@@ -874,13 +883,17 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
               uint16_t* blk = dst + ((size_t)cb * hg.ntaps + tap) * bnh * BK;
               for (int r = 0; r < bnh; ++r)
                 for (int j = 0; j < KE; ++j) {
+                  const int co = r % L.cout;
                   int c = cb * KE + j, ky = hg.ky[tap], kx = hg.kx[tap];
                   if (hm == HALO_STEM7) {
                     kx = j / gch;
                     c = j % gch;
+                  } else if (x4) {  // plane cb*8 + j/gch reads input column 4*jm + plane - 3
+                    kx = cb * 8 + j / gch - r / L.cout;
+                    c = j % gch;
                   }
-                  const float v = (c < L.cin && kx < L.kw) ? wat(r, c, ky, kx) : 0.f;
-                  store(blk, r, j, v, 1.f / sw[r]);
+                  const float v = (c < L.cin && kx >= 0 && kx < L.kw) ? wat(co, c, ky, kx) : 0.f;
+                  store(blk, r, j, v, 1.f / sw[co]);
                 }
             }
         }
@@ -1174,17 +1187,18 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.W = in.W;
           hp.C = p.C;
           hp.GH = hg.mode == HALO_CONVT2 ? in.H : OH;
-          hp.GW = hg.mode == HALO_CONVT2 ? in.W : OW;
+          hp.GW = hg.mode == HALO_CONVT2 ? in.W : hg.mode == HALO_STEM4X ? (int)ceil_div(OW, 4) : OW;
+          hp.xmul = hg.mode == HALO_STEM4X ? 4 : 1;
           hp.oy0 = hg.oy0;
           hp.ox0 = hg.ox0;
           hp.pw = hg.pw;
           hp.ph = hg.ph;
           hp.plane = (hp.pw * hp.ph * 16 + 127) / 128 * 128;
           if (hp.plane > HaloCfg<32, HALO_CONV3, false, true>::PLANE_MAX) fail(LSG_ERUNTIME, "generator: halo patch too large");
-          hp.shift_planes = hg.mode == HALO_STEM7;
+          hp.shift_planes = hg.mode == HALO_STEM7 || hg.mode == HALO_STEM4X;
           // planes come in pairs per K step; an odd last plane reads channels past the
           // view, which the TMA zero-fills (fp8 out0: 80 channels = 5 planes)
-          hp.ngran = hp.shift_planes ? 8 : ((p.C / 8 + 1) & ~1);
+          hp.ngran = hg.mode == HALO_STEM4X ? 10 : hp.shift_planes ? 8 : ((p.C / 8 + 1) & ~1);
           hp.ncb = (hp.ngran + 7) / 8;
           hp.ntaps = hg.ntaps;
           for (int t = 0; t < MAX_HTAPS; ++t) {
@@ -1192,7 +1206,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
             hp.tphase[t] = hg.tphase[t];
           }
           hp.tfirst = hg.tfirst;
-          hp.osy = hp.osx = hg.mode == HALO_CONVT2 ? 2 : 1;
+          hp.osy = hg.mode == HALO_CONVT2 ? 2 : 1;
+          hp.osx = hg.mode == HALO_CONVT2 ? 2 : hg.mode == HALO_STEM4X ? 4 : 1;
           for (int z = 0; z < 4; ++z) {
             hp.poy[z] = hg.poy[z];
             hp.pox[z] = hg.pox[z];
@@ -1202,7 +1217,9 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
-          r.halo_bres = (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;
+          r.halo_bres = hg.mode == HALO_STEM4X
+                            ? (int64_t)hp.wblocks * 4 * r.bn * BK * 2 <= HaloCfg<16, HALO_STEM4X, false, true>::W_RES_BYTES
+                            : (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;
           if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
           hp.OH = OH;
           hp.OW = OW;
@@ -1220,7 +1237,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.out_mode = p.out_mode;
           hp.w1 = p.w1;
           hp.b1 = p.b1;
-          encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph);
+          encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, hp.xmul);
           const int bc = std::min(r.bn * 2 / cpu, 128) / 2;  // box channels in 16-bit units (128-byte rows max)
           if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
           if (hg.mode == HALO_CONV3 && !fused) {
