@@ -215,7 +215,8 @@ struct LayerRun {
 };
 
 // A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
-// the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem.
+// the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
+// bit 9 (512) the concurrent audio-encoder branch.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -374,6 +375,18 @@ struct lsg_gen_s {
   DevBuf<float> splitk_ws;   // split-K partial slots (conv_kernel.cuh ConvParams::ws)
   DevBuf<int> splitk_cnt;    // split-K arrival counters, zero between uses
   int splitk_tiles = 0;      // tiles the workspace holds
+  // the audio encoder runs on a side stream, concurrently with the face
+  // encoder (disjoint buffers: x_mel/A0/A1 vs x_face/S0/S1/cat), joined
+  // before the decoder; its split-K layers use their own workspace
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DevBuf<float> splitk_ws2;
+  DevBuf<int> splitk_cnt2;
+  ~lsg_gen_s() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
   std::vector<LayerRun> plan;
 };
@@ -619,9 +632,9 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float
                          std::to_string(r.p.cc));
 }
 
-static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st) {
-  float* ws = h->splitk_ws.p;
-  int* cnt = h->splitk_cnt.p;
+static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st, int wset = 0) {
+  float* ws = wset ? h->splitk_ws2.p : h->splitk_ws.p;
+  int* cnt = wset ? h->splitk_cnt2.p : h->splitk_cnt.p;
   const int wt = h->splitk_tiles;
   if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, cnt, wt);
   else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st, ws, cnt, wt);
@@ -713,6 +726,12 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       h->splitk_ws.alloc((size_t)h->sm_count * BM * 256);
       h->splitk_cnt.alloc((size_t)h->splitk_tiles);
       LSG_CUDA(cudaMemset(h->splitk_cnt.p, 0, h->splitk_cnt.bytes()));
+      h->splitk_ws2.alloc((size_t)h->sm_count * BM * 256);
+      h->splitk_cnt2.alloc((size_t)h->splitk_tiles);
+      LSG_CUDA(cudaMemset(h->splitk_cnt2.p, 0, h->splitk_cnt2.bytes()));
+      LSG_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+      LSG_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+      LSG_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
       size_t off = 0;
       for (auto& r : reqs) {
         *r.v = View{h->act.p + off, r.H, r.W, r.C, 0, r.C};
@@ -1441,13 +1460,37 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
   LSG_LAUNCHED(ctx);
   const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
                                                   : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
+  // audio encoder (plan layers whose name starts with "ae") on the side
+  // stream, forked after the input prep and joined before the decoder
+  const bool fork = !(gen_knobs() & 512);
+  if (fork) {
+    LSG_CUDA(cudaEventRecord(h->ev_fork, st));
+    LSG_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  }
+  bool joined = !fork;
   for (auto& r : h->plan) {
     if (r.fused) {
       r.p.out_mode = r.hp.out_mode = mode;
       r.p.final_out = r.hp.final_out = out;
     }
-    dispatch(h, r, B, st);
+    // (both branches launch full-SM grids: capping either branch's SMs measured
+    // slower at B = 128 and 512 -- the concurrency is in the small layers' tails)
+    const bool audio = kLayers[r.layer].name[0] == 'a';
+    if (fork && audio) {
+      dispatch(h, r, B, h->side, 1);
+    } else {
+      if (!joined && kLayers[r.layer].name[0] == 'f' && kLayers[r.layer].name[1] == 'd') {
+        LSG_CUDA(cudaEventRecord(h->ev_join, h->side));
+        LSG_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
+        joined = true;
+      }
+      dispatch(h, r, B, st);
+    }
     LSG_LAUNCHED(ctx);
+  }
+  if (!joined) {  // (a plan without decoder layers)
+    LSG_CUDA(cudaEventRecord(h->ev_join, h->side));
+    LSG_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
 }
 
