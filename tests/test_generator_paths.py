@@ -44,6 +44,8 @@ def test_launch_paths_agree(tmp_path, B, prec):
     ref = _render(tmp_path, B, 1, 0)[0] if prec == 2 else None
     # knobs: 1 no narrow tiles, 2 no split-K, 32 no CTA pairs, 64 one pixel
     # per stem row, 99 none of them
+    # the concurrent audio-encoder branch (knob 512) changes no arithmetic
+    assert np.array_equal(base[0], _render(tmp_path, B, prec, 512)[0])
     for knobs in (1, 2, 32, 64, 99):
         other = _render(tmp_path, B, prec, knobs)[0]
         if prec == 2:
