@@ -23,8 +23,10 @@ def load(path):
     return ks
 
 
-def main(path, B=512):
+def main(path, B=512, last=0):
     ks = load(path)
+    if last:  # only the final `last` launches (e.g. the last forward of a multi-forward capture)
+        ks = OrderedDict(list(ks.items())[-last:])
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))
     try:
@@ -62,4 +64,5 @@ def main(path, B=512):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 512)
+    # launches.py <csv> [B] [last N launches]
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 512, int(sys.argv[3]) if len(sys.argv) > 3 else 0)
