@@ -78,6 +78,7 @@ struct alignas(64) HaloParams {
   CUtensorMap tmap;      // tiled map of the input view (C, W, H, N), box (8, pw, ph, 1)
   CUtensorMap tmap_out;  // output view, box (min(BN,64), 8, 16, 1) output positions (x2 stride for ConvT)
   CUtensorMap tmap_res;  // residual view, box (min(BN,64), 8, 16, 1)
+  CUtensorMap wmap;      // packed weights as 2-D [rows][64 units], box (64, MN/2): CTA-pair loads
   int H, W, C, B;    // input view
   int GH, GW;        // grid (output positions for convs, input positions for ConvT)
   int oy0, ox0;      // patch origin relative to the tile origin (-pad for convs)
@@ -117,14 +118,17 @@ struct alignas(64) HaloParams {
 // barriers.  Staging / residual tiles are [128 positions][IB bytes] boxes in
 // the tensor map's swizzle (IB = 128 -> 128B, 64 -> 64B, 32 -> 32B) so the
 // epilogue's per-position 16-byte accesses are bank-conflict free.
-template <int BN, int MODE, bool FUSED, bool B_RES, int ES = 2>  // ES: bytes per channel (2, or 1 for fp8)
+// PAIR: CTA-pair variant (cta_group::2): each CTA holds half of every weight
+// block (MN / 2 rows), so the same smem carries twice the weight ring.
+template <int BN, int MODE, bool FUSED, bool B_RES, int ES = 2, bool PAIR = false>
 struct HaloCfg {
   static constexpr int NPH = HaloTaps<MODE>::NPH;
   static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
   static constexpr int MN = MODE == HALO_STEM4X ? NPH * BN : BN;  // MMA N: every phase at once for macro-pixels
-  static constexpr int BBLK = MN * BK * 2;  // one (cb, tap) weight block
+  static constexpr int BROWS = PAIR ? MN / 2 : MN;  // weight rows of a block held by one CTA
+  static constexpr int BBLK = BROWS * BK * 2;  // one (cb, tap) weight block (this CTA's rows)
   static constexpr int WG = 3;              // streamed weights: taps per ring slot (one wait + commit each)
   static constexpr int GBLK = WG * BBLK;
   static constexpr int W_RES_BYTES = MODE == HALO_STEM4X ? 112 * 1024 : 72 * 1024;
@@ -195,15 +199,44 @@ __device__ __forceinline__ void tma_tile_4d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// CTA-pair forms: data to this CTA's smem, completion on the even CTA's
+// barrier (cluster address)
+__device__ __forceinline__ void tma_tile_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t mbar, int c, int x,
+                                                 int y, int n) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c), "r"(x), "r"(y), "r"(n)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_pair_h(uint32_t dst, const CUtensorMap* map, uint32_t mbar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(tc::smem_u32(p)));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
 }
 
-template <int BN, int MODE, bool FUSED_OUT, int PR, bool B_RES>
+// PAIR: launched in clusters of two; CTA r of a cluster owns tile
+// blockIdx.x + k * gridDim.x as usual (the pair = two adjacent tiles, the tile
+// count is even), the even CTA issues M = 256 MMAs over both CTAs' patches
+// and weight halves, both CTAs' TMA loads complete on the even CTA's
+// barriers, commits are multicast, and every epilogue warp of the pair
+// releases the accumulator on the even CTA's tempty barrier.
+template <int BN, int MODE, bool FUSED_OUT, int PR, bool B_RES, bool PAIR = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
   using NF = Num<PR>;
-  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::F8 ? 1 : 2>;
+  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::F8 ? 1 : 2, PAIR>;
   using TT = HaloTaps<MODE>;
   constexpr int NPH = TT::NPH;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
@@ -235,6 +268,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
   constexpr int EPI_THREADS = EPI_ALT ? 32 * NUM_EPI_WARPS / 2 : 32 * NUM_EPI_WARPS;  // per tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < HS; ++s) {
@@ -247,7 +281,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], EPI_THREADS);
+      tc::mbar_init(&tempty[a], PAIR ? 2 * (EPI_THREADS / 32) : EPI_THREADS);  // pair: one arrive per warp
       tc::mbar_init(&rfull[a], 1);
       tc::mbar_init(&rempty[a], EPI_THREADS);
     }
@@ -257,10 +291,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_out)) : "memory");
     if constexpr (CF::HAS_RES)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tmap_res)) : "memory");
+    if constexpr (PAIR) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.wmap)) : "memory");
   }
-  if (warp == 1) tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tc::tmem_alloc2<CF::TMEM_COLS>(tmem_slot);
+    else tc::tmem_alloc<CF::TMEM_COLS>(tmem_slot);
+  }
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // both CTAs' barriers exist before cross-CTA signals
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t box_bytes = (uint32_t)(p.pw * p.ph * 16);
@@ -272,10 +311,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     if constexpr (B_RES) {
       if (lane == 0) {  // every weight block of this layer, once per CTA
         const uint32_t bytes = (uint32_t)(p.wblocks * CF::BBLK);
-        tc::mbar_arrive_expect_tx(&bfull[0], bytes);
-        for (uint32_t off = 0; off < bytes; off += 32768) {
-          const uint32_t chunk = bytes - off < 32768 ? bytes - off : 32768;
-          tc::bulk_g2s(sB0 + off, reinterpret_cast<const uint8_t*>(p.w) + off, chunk, &bfull[0]);
+        if constexpr (PAIR) {  // this CTA's half of each block, completing on the even CTA's barrier
+          if (rank == 0) tc::mbar_arrive_expect_tx(&bfull[0], 2 * bytes);
+          const uint32_t fb = leader_addr(&bfull[0]);
+          for (int b = 0; b < p.wblocks; ++b)
+            tma_2d_pair_h(sB0 + b * CF::BBLK, &p.wmap, fb, 0, b * CF::MN + (int)rank * CF::BROWS);
+        } else {
+          tc::mbar_arrive_expect_tx(&bfull[0], bytes);
+          for (uint32_t off = 0; off < bytes; off += 32768) {
+            const uint32_t chunk = bytes - off < 32768 ? bytes - off : 32768;
+            tc::bulk_g2s(sB0 + off, reinterpret_cast<const uint8_t*>(p.w) + off, chunk, &bfull[0]);
+          }
         }
       }
       __syncwarp();
@@ -293,11 +339,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
         tc::mbar_wait(&hempty[hs], hph ^ 1);
-        if (lane == 0) tc::mbar_arrive_expect_tx(&hfull[hs], ng * box_bytes);
+        if (lane == 0 && rank == 0) tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) * ng * box_bytes);
         __syncwarp();
-        if (lane < ng)
-          tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * cstep,
-                      x0 + (g0 + lane) * xstep, y0, n);
+        if (lane < ng) {
+          if constexpr (PAIR)
+            tma_tile_4d_pair(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, leader_addr(&hfull[hs]),
+                             (g0 + lane) * cstep, x0 + (g0 + lane) * xstep, y0, n);
+          else
+            tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (g0 + lane) * cstep,
+                        x0 + (g0 + lane) * xstep, y0, n);
+        }
         if (++hs == HS) {
           hs = 0;
           hph ^= 1;
@@ -308,8 +359,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             const uint32_t bytes = (uint32_t)(min(CF::WG, p.ntaps - t0) * CF::BBLK);
             tc::mbar_wait(&bempty[bs], bph ^ 1);
             if (lane == 0) {
-              tc::mbar_arrive_expect_tx(&bfull[bs], bytes);
-              tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * CF::MN * BK, bytes, &bfull[bs]);
+              if constexpr (PAIR) {
+                if (rank == 0) tc::mbar_arrive_expect_tx(&bfull[bs], 2 * bytes);
+                const uint32_t fb = leader_addr(&bfull[bs]);
+                for (int i = 0; i < min(CF::WG, p.ntaps - t0); ++i)
+                  tma_2d_pair_h(sB0 + bs * CF::GBLK + i * CF::BBLK, &p.wmap, fb, 0,
+                                (cb * p.ntaps + t0 + i) * CF::MN + (int)rank * CF::BROWS);
+              } else {
+                tc::mbar_arrive_expect_tx(&bfull[bs], bytes);
+                tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * CF::MN * BK, bytes, &bfull[bs]);
+              }
             }
             __syncwarp();
             if (++bs == BS) {
@@ -344,12 +403,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     // is a handful of uniform adds per 4 MMAs (profiles/r01: with divisions,
     // parameter reloads and per-tap warp reconvergence it cost more than the
     // MMAs themselves).
-    constexpr uint32_t idesc = tc::idesc_f16kind(BM, CF::MN, NF::kFmt);
+    constexpr uint32_t idesc = tc::idesc_f16kind(PAIR ? 2 * BM : BM, CF::MN, NF::kFmt);
     constexpr int NT = TT::NT;
     constexpr uint64_t PLANE2 = (uint64_t)((2 * ((TT::PW * TT::PH * 16 + 127) / 128 * 128)) >> 4);
     constexpr uint64_t BBLK16 = CF::BBLK >> 4;
     constexpr uint64_t HST16 = CF::HSTAGE >> 4;
-    if (elect_one()) {
+    if ((!PAIR || rank == 0) && elect_one()) {
       const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
       if constexpr (B_RES) tc::mbar_wait_nc(&bfull[0], 0);
       const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)(PLANE2 << 3), (uint32_t)(TT::PW * 16));
@@ -359,7 +418,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       uint32_t hph = 0, bph = 0, tl = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-        tc::mbar_wait_fast(&tempty[a], (use & 1) ^ 1);
+        if constexpr (PAIR) tc::mbar_wait_cluster(&tempty[a], (use & 1) ^ 1);  // both CTAs' epilogues
+        else tc::mbar_wait_fast(&tempty[a], (use & 1) ^ 1);
         tc::tc_fence_after_nc();  // TMEM reuse after the epilogue's reads
         const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < ncb; ++cb) {
@@ -384,10 +444,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             const uint32_t acc0 = (first && cb == 0) ? 0u : 1u;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              if (ks < ksteps) NF::mma_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+              if (ks < ksteps) {
+                if constexpr (PAIR) {
+                  if constexpr (NF::F8) tc::mma2_f8(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+                  else tc::mma2_f16(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+                } else {
+                  NF::mma_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+                }
+              }
             if constexpr (!B_RES) {
               if (tap % CF::WG == CF::WG - 1 || tap == NT - 1) {
-                tc::mma_commit_nc(&bempty[bs]);
+                if constexpr (PAIR) tc::mma_commit2(&bempty[bs]);
+                else tc::mma_commit_nc(&bempty[bs]);
                 if (++bs == BS) {
                   bs = 0;
                   bph ^= 1;
@@ -395,13 +463,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
               }
             }
           }
-          tc::mma_commit_nc(&hempty[hs]);
+          if constexpr (PAIR) tc::mma_commit2(&hempty[hs]);
+          else tc::mma_commit_nc(&hempty[hs]);
           if (++hs == HS) {
             hs = 0;
             hph ^= 1;
           }
         }
-        tc::mma_commit_nc(&tfull[a]);
+        if constexpr (PAIR) tc::mma_commit2(&tfull[a]);
+        else tc::mma_commit_nc(&tfull[a]);
       }
     }
     __syncwarp();
@@ -474,7 +544,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           }
         }
         tc::tc_fence_before();
-        tc::mbar_arrive(&tempty[a]);
+        if constexpr (PAIR) {
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[a], 0);
+        } else {
+          tc::mbar_arrive(&tempty[a]);
+        }
         if constexpr (CF::HAS_RES) {
           tc::mbar_arrive(&rempty[rs]);
         }
@@ -517,7 +592,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           }
         }
         tc::tc_fence_before();
-        tc::mbar_arrive(&tempty[a]);  // accumulator drained: stores below overlap the next tile's MMAs
+        if constexpr (PAIR) {  // accumulator drained: stores below overlap the next tile's MMAs
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_remote(&tempty[a], 0);
+        } else {
+          tc::mbar_arrive(&tempty[a]);
+        }
         if (gvalid) {
           const int HWo = p.OH * p.OW;
           const size_t pp = (size_t)gy * p.OW + gx;
@@ -541,10 +621,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       }
     }
   }
+  tc::tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // the peer's TMEM / smem / barriers stay live until both are done
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
+    if constexpr (PAIR) tc::tmem_dealloc2<CF::TMEM_COLS>(tmem);
+    else tc::tmem_dealloc<CF::TMEM_COLS>(tmem);
   }
 }
 

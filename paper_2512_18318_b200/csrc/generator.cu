@@ -211,12 +211,13 @@ struct LayerRun {
   bool halo_bres = false;              // weights resident in shared memory
   int halo_mode = 0;                   // HaloMode of a conv_halo layer
   bool pair_ok = false;                // conv_tc layer with a weight map for CTA-pair launches
+  bool hp_pair_ok = false;             // halo layer with a weight map (HaloParams::wmap) for CTA pairs
   HaloParams hp;
 };
 
 // A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
-// bit 9 (512) the concurrent audio-encoder branch.
+// bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -561,6 +562,13 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(64, HALO_CONVT2, false, false)       \
   X(32, HALO_CONV3, true, true)
 
+// halo variants that also run as CTA pairs (cta_group::2; HaloCfg PAIR).
+// Measured per layer (B = 512): the streamed-weight 3x3 at N = 128 (fd5.1/5.2,
+// 288 KB of weights per 128-position tile) gains 18% from halving each SM's
+// weight stream; resident-weight layers (fe1/fe2/ae/fd6.1-2, N <= 64) and the
+// streamed ConvT fd6.0 lose 15-35%, the fused output layer is neutral.
+#define LSG_HALO_PAIR_VARIANTS(X) X(128, HALO_CONV3, false, false)
+
 // The host-built tap list of a halo layer must be the kernel's compile-time
 // table (conv_halo.cuh HaloTaps): packing order == issue order.
 template <int MODE>
@@ -583,6 +591,11 @@ static void set_smem_attrs_t() {
                                 HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
+#define LSG_SET_HALO_PAIR_ATTR(BN, MD, F, R)                                                                      \
+  LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, PR, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2, true>::SMEM));
+  LSG_HALO_PAIR_VARIANTS(LSG_SET_HALO_PAIR_ATTR)
+#undef LSG_SET_HALO_PAIR_ATTR
 #define LSG_SET_PAIR_ATTR(BN, CC) \
   LSG_CUDA(cudaFuncSetAttribute(conv_tc2<BN, CC, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
   LSG_PAIR_VARIANTS(LSG_SET_PAIR_ATTR)
@@ -604,9 +617,39 @@ static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
              hp);
 }
 
+// CTA-pair halo launch: clusters of two adjacent tiles (the tile count is even)
+template <int BN, int MD, bool F, int PR, bool R>
+static void launch_halo_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
+  HaloParams hp = r.hp;
+  hp.B = B;
+  hp.total_tiles = B * hp.tiles_per_img;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::min(hp.total_tiles, sms & ~1));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = (size_t)HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2, true>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  LSG_CUDA(cudaLaunchKernelEx(&cfg, conv_halo<BN, MD, F, PR, R, true>, hp));
+}
+
 template <int PR>
 static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int* cnt, int ws_tiles) {
   if (r.halo) {
+    if (!(gen_knobs() & 1024) && r.hp_pair_ok && (B * r.hp.tiles_per_img) % 2 == 0 && B * r.hp.tiles_per_img >= sms) {
+#define LSG_HALO_PAIR_DISPATCH(BN, MD, F, R)                                                  \
+  if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
+    return launch_halo_pair<BN, MD, F, PR, R>(r, B, sms, st);
+      LSG_HALO_PAIR_VARIANTS(LSG_HALO_PAIR_DISPATCH)
+#undef LSG_HALO_PAIR_DISPATCH
+    }
 #define LSG_HALO_DISPATCH(BN, MD, F, R)                                                       \
   if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
     return launch_halo<BN, MD, F, PR, R>(r, B, sms, st);
@@ -1236,6 +1279,17 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
+          if (hg.mode != HALO_STEM4X && hg.mode != HALO_STEM7) {  // CTA pairs: weight half-blocks by TMA
+            const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)hp.wblocks * r.bn};
+            const cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
+            const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(r.bn / 2)};
+            const cuuint32_t estr[2] = {1, 1};
+            CUresult cr = tiled_fn()(&hp.wmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t*>(hp.w), dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled (halo weights) failed");
+            r.hp_pair_ok = true;
+          }
           r.halo_bres = hg.mode == HALO_STEM4X
                             ? (int64_t)hp.wblocks * 4 * r.bn * BK * 2 <= HaloCfg<16, HALO_STEM4X, false, true>::W_RES_BYTES
                             : (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;

@@ -42,11 +42,11 @@ def test_launch_paths_agree(tmp_path, B, prec):
     # decorrelates under any change of summation order, so fp8 paths are
     # compared by their accuracy against the fp16 render of the same batch
     ref = _render(tmp_path, B, 1, 0)[0] if prec == 2 else None
-    # knobs: 1 no narrow tiles, 2 no split-K, 32 no CTA pairs, 64 one pixel
-    # per stem row, 99 none of them
     # the concurrent audio-encoder branch (knob 512) changes no arithmetic
     assert np.array_equal(base[0], _render(tmp_path, B, prec, 512)[0])
-    for knobs in (1, 2, 32, 64, 99):
+    # knobs: 1 no narrow tiles, 2 no split-K, 32 no CTA pairs (im2col), 64 one
+    # pixel per stem row, 1024 no CTA pairs (halo), 1123 none of them
+    for knobs in (1, 2, 32, 64, 1024, 1123):
         other = _render(tmp_path, B, prec, knobs)[0]
         if prec == 2:
             q0, q1 = _psnr(base[0], ref), _psnr(other, ref)
