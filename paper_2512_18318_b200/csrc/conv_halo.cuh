@@ -95,6 +95,7 @@ struct alignas(64) HaloParams {
   int osy, osx;          // output stride of the grid (2 for ConvT phases)
   int poy[4], pox[4];    // per-phase output offset
   int tiles_x, tiles_y, tiles_per_img, total_tiles;
+  int ntn;  // N tiles of BN output channels (streamed weights only); tile t = spatial t / ntn, n tile t % ntn
   const uint16_t* w;  // packed [cb][tap][BN][64] (128 B swizzled rows)
   int wblocks;        // ncb * ntaps
   // epilogue (as ConvParams)
@@ -332,7 +333,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     int hs = 0, bs = 0, rs = 0;
     uint32_t hph = 0, bph = 0, rph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      const int n = t / p.tiles_per_img, r = t - n * p.tiles_per_img;
+      const int ts = t / p.ntn, nt = t - ts * p.ntn;
+      const int n = ts / p.tiles_per_img, r = ts - n * p.tiles_per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
       const int y0 = ty * HTH + p.oy0, x0 = tx * HTW * p.xmul + p.ox0;
 
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           hph ^= 1;
         }
         if constexpr (!B_RES) {  // taps [g*WG, g*WG+WG) of this channel block per ring slot
-          const uint16_t* wb = p.w + (size_t)cb * p.ntaps * CF::MN * BK;
+          const uint16_t* wb = p.w + ((size_t)nt * p.ncb + cb) * p.ntaps * CF::MN * BK;
           for (int t0 = 0; t0 < p.ntaps; t0 += CF::WG) {
             const uint32_t bytes = (uint32_t)(min(CF::WG, p.ntaps - t0) * CF::BBLK);
             tc::mbar_wait(&bempty[bs], bph ^ 1);
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
                 const uint32_t fb = leader_addr(&bfull[bs]);
                 for (int i = 0; i < min(CF::WG, p.ntaps - t0); ++i)
                   tma_2d_pair_h(sB0 + bs * CF::GBLK + i * CF::BBLK, &p.wmap, fb, 0,
-                                (cb * p.ntaps + t0 + i) * CF::MN + (int)rank * CF::BROWS);
+                                ((nt * p.ncb + cb) * p.ntaps + t0 + i) * CF::MN + (int)rank * CF::BROWS);
               } else {
                 tc::mbar_arrive_expect_tx(&bfull[bs], bytes);
                 tc::bulk_g2s(sB0 + bs * CF::GBLK, wb + (size_t)t0 * CF::MN * BK, bytes, &bfull[bs]);
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           const uint32_t dst = tc::smem_u32(smem + CF::OFF_RES + rs * CF::RES_BYTES);
 #pragma unroll
           for (int cc = 0; cc < CF::NCH; ++cc)
-            tma_tile_4d(dst + cc * CF::BOX, &p.tmap_res, &rfull[rs], cc * 64, tx * HTW, ty * HTH, n);
+            tma_tile_4d(dst + cc * CF::BOX, &p.tmap_res, &rfull[rs], nt * (BN / NF::CPU) + cc * 64, tx * HTW, ty * HTH, n);
         }
         __syncwarp();
         if (++rs == CF::NRES) {
@@ -507,7 +509,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         // residual ring slot of this tile (the producer fills slots in tile order)
         const int rs = CF::NRES ? (int)(tl % (uint32_t)(CF::NRES ? CF::NRES : 1)) : 0;
         const uint32_t rph = CF::NRES ? (tl / (uint32_t)(CF::NRES ? CF::NRES : 1)) & 1u : 0u;
-        const int n = t / p.tiles_per_img, rr = t - n * p.tiles_per_img;
+        const int ts = t / p.ntn, nt = t - ts * p.ntn;
+        const int n = ts / p.tiles_per_img, rr = ts - n * p.tiles_per_img;
         const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
         uint8_t* stg = smem + CF::OFF_STG + (EPI_ALT ? grp : sb) * CF::STG_BYTES;
         // the store that last read this staging buffer must have drained
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             }
             tc::tmem_ld_wait();
             uint4 o[W16];
-            epi16<PR>(v, p.bias + cbeg + c0, p.oscale + (NF::F8 ? cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
+            epi16<PR>(v, p.bias + nt * BN + cbeg + c0, p.oscale + (NF::F8 ? nt * BN + cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
                       p.res_scale, p.relu != 0, p.out_inv, o);
 #pragma unroll
             for (int w = 0; w < W16; ++w)
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           for (int z = 0; z < NPH; ++z)
 #pragma unroll
             for (int cc = 0; cc < CF::NCH; ++cc)
-              tma_store_4d(&p.tmap_out, src + (z * CF::NCH + cc) * CF::BOX, cc * 64,
+              tma_store_4d(&p.tmap_out, src + (z * CF::NCH + cc) * CF::BOX, nt * (BN / NF::CPU) + cc * 64,
                            tx * HTW * p.osx + p.pox[z], ty * HTH * p.osy + p.poy[z], n);
           bulk_commit();
         }

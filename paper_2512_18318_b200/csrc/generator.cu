@@ -217,7 +217,8 @@ struct LayerRun {
 
 // A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
-// bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs.
+// bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs, bit 11 (2048)
+// the 128-channel ConvT (fd5.0) on the halo kernel.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -233,8 +234,8 @@ HaloMode halo_mode(const LayerSpec& L) {
       L.cin % 16 == 0)
     return HALO_CONV3;  // 3x3 "same": fe1.x, fe2.x, ae1-5, fd5.x, fd6.x, out0
   if (L.kind != CONV && L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2 && L.ph == 1 && L.pw == 1 && L.oph == 1 &&
-      L.opw == 1 && L.cout <= 64 && L.cin % 16 == 0)
-    return HALO_CONVT2;  // fd6.0: 4 output phases share one accumulator set
+      L.opw == 1 && L.cin % 16 == 0 && (L.cout <= 64 || (L.cout == 128 && !(gen_knobs() & 2048))))
+    return HALO_CONVT2;  // fd6.0, fd5.0 (as two 64-channel N tiles): 4 output phases share one accumulator set
   if (L.kind == CONV && L.kh == 7 && L.kw == 7 && L.sh == 1 && L.sw == 1 && L.ph == 3 && L.pw == 3 && L.cin <= 8 &&
       L.cout <= 16)  // fe0 on the 8-channel face tensor: macro-pixels (LSG_GEN_KNOBS bit 64: one pixel per row)
     return (gen_knobs() & 64) ? HALO_STEM7 : HALO_STEM4X;
@@ -611,7 +612,7 @@ template <int BN, int MD, bool F, int PR, bool R>
 static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   HaloParams hp = r.hp;
   hp.B = B;
-  hp.total_tiles = B * hp.tiles_per_img;
+  hp.total_tiles = B * hp.tiles_per_img * hp.ntn;
   const int grid = std::min(hp.total_tiles, sms);
   launch_pdl(conv_halo<BN, MD, F, PR, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM, st,
              hp);
@@ -622,7 +623,7 @@ template <int BN, int MD, bool F, int PR, bool R>
 static void launch_halo_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
   HaloParams hp = r.hp;
   hp.B = B;
-  hp.total_tiles = B * hp.tiles_per_img;
+  hp.total_tiles = B * hp.tiles_per_img * hp.ntn;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)std::min(hp.total_tiles, sms & ~1));
   cfg.blockDim = dim3(NUM_THREADS);
@@ -935,17 +936,20 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap);
           // macro-pixel stem: rows (pixel offset z, cout), K = (x-shift plane, channel)
           const bool x4 = hm == HALO_STEM4X;
-          const int ncb = hm == HALO_STEM7 ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE, bnh = x4 ? 4 * L.cout : L.cout;
+          // N tiles of 64 channels for the wide ConvT (4 phase accumulators x 64 fill TMEM)
+          const int hbn = hm == HALO_CONVT2 ? std::min(L.cout, 64) : L.cout, hnt = L.cout / hbn;
+          const int ncb = hm == HALO_STEM7 ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE, bnh = x4 ? 4 * L.cout : hbn;
           hg.off = (int64_t)pack.size();
-          pack.resize(pack.size() + (size_t)ncb * hg.ntaps * bnh * BK, 0);
+          pack.resize(pack.size() + (size_t)hnt * ncb * hg.ntaps * bnh * BK, 0);
           uint16_t* dst = pack.data() + hg.off;
           const int gch = 8 * cpu;  // channels per 16-byte granule (stem: one x-shifted plane)
+          for (int nt = 0; nt < hnt; ++nt)
           for (int cb = 0; cb < ncb; ++cb)
             for (int tap = 0; tap < hg.ntaps; ++tap) {
-              uint16_t* blk = dst + ((size_t)cb * hg.ntaps + tap) * bnh * BK;
+              uint16_t* blk = dst + (((size_t)nt * ncb + cb) * hg.ntaps + tap) * bnh * BK;
               for (int r = 0; r < bnh; ++r)
                 for (int j = 0; j < KE; ++j) {
-                  const int co = r % L.cout;
+                  const int co = x4 ? r % L.cout : nt * hbn + r;
                   int c = cb * KE + j, ky = hg.ky[tap], kx = hg.kx[tap];
                   if (hm == HALO_STEM7) {
                     kx = j / gch;
@@ -1277,10 +1281,12 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.tiles_x = (int)ceil_div(hp.GW, HTW);
           hp.tiles_y = (int)ceil_div(hp.GH, HTH);
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
+          if (hg.mode == HALO_CONVT2) r.bn = std::min(L.cout, 64);  // N tiles (packed per tile above)
+          hp.ntn = L.cout / r.bn;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
           if (hg.mode != HALO_STEM4X && hg.mode != HALO_STEM7) {  // CTA pairs: weight half-blocks by TMA
-            const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)hp.wblocks * r.bn};
+            const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)hp.wblocks * r.bn * hp.ntn};
             const cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
             const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)(r.bn / 2)};
             const cuuint32_t estr[2] = {1, 1};
@@ -1293,7 +1299,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           r.halo_bres = hg.mode == HALO_STEM4X
                             ? (int64_t)hp.wblocks * 4 * r.bn * BK * 2 <= HaloCfg<16, HALO_STEM4X, false, true>::W_RES_BYTES
                             : (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;
-          if (r.bn != L.cout) fail(LSG_ERUNTIME, "generator: halo layers need one N tile");
+          if (r.bn * hp.ntn != L.cout || (hp.ntn > 1 && (r.halo_bres || fused || hg.mode != HALO_CONVT2)))
+            fail(LSG_ERUNTIME, "generator: halo N tiling only for streamed-weight ConvT layers");
           hp.OH = OH;
           hp.OW = OW;
           hp.out = p.out;
