@@ -95,7 +95,7 @@ struct alignas(64) HaloParams {
   int osy, osx;          // output stride of the grid (2 for ConvT phases)
   int poy[4], pox[4];    // per-phase output offset
   int tiles_x, tiles_y, tiles_per_img, total_tiles;
-  int ntn;  // N tiles of BN output channels (streamed weights only); tile t = spatial t / ntn, n tile t % ntn
+  int ntn;  // N tiles of BN output channels (streamed weights only); see halo_tile()
   const uint16_t* w;  // packed [cb][tap][BN][64] (128 B swizzled rows)
   int wblocks;        // ncb * ntaps
   // epilogue (as ConvParams)
@@ -223,6 +223,16 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
   return r;
 }
 
+// Tile t -> (spatial tile ts, N tile nt): pairs of adjacent t are two adjacent
+// spatial tiles of the SAME N tile (a CTA pair shares its weights), and
+// consecutive pairs walk the N tiles of one spatial pair (its patches stay in
+// L2).  With one N tile this is the identity.  Needs an even spatial count.
+__device__ __forceinline__ void halo_tile(const HaloParams& p, int t, int& ts, int& nt) {
+  const int g = t >> 1, sp = g / p.ntn;
+  nt = g - sp * p.ntn;
+  ts = 2 * sp + (t & 1);
+}
+
 __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // layout 0: no swizzle
@@ -333,7 +343,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     int hs = 0, bs = 0, rs = 0;
     uint32_t hph = 0, bph = 0, rph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-      const int ts = t / p.ntn, nt = t - ts * p.ntn;
+      int ts, nt;
+      halo_tile(p, t, ts, nt);
       const int n = ts / p.tiles_per_img, r = ts - n * p.tiles_per_img;
       const int ty = r / p.tiles_x, tx = r - ty * p.tiles_x;
       const int y0 = ty * HTH + p.oy0, x0 = tx * HTW * p.xmul + p.ox0;
@@ -509,7 +520,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         // residual ring slot of this tile (the producer fills slots in tile order)
         const int rs = CF::NRES ? (int)(tl % (uint32_t)(CF::NRES ? CF::NRES : 1)) : 0;
         const uint32_t rph = CF::NRES ? (tl / (uint32_t)(CF::NRES ? CF::NRES : 1)) & 1u : 0u;
-        const int ts = t / p.ntn, nt = t - ts * p.ntn;
+        int ts, nt;
+        halo_tile(p, t, ts, nt);
         const int n = ts / p.tiles_per_img, rr = ts - n * p.tiles_per_img;
         const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
         uint8_t* stg = smem + CF::OFF_STG + (EPI_ALT ? grp : sb) * CF::STG_BYTES;

@@ -230,6 +230,8 @@ static int gen_knobs() {
 // Layers routed to the patch-reuse kernel (conv_halo.cuh); everything else
 // goes to the im2col kernel.
 HaloMode halo_mode(const LayerSpec& L) {
+  // (fd4.1/4.2, 256 channels, as two 128-channel N tiles on CTA pairs measured
+  // 1.3% slower end to end than the im2col pair kernel: kept there)
   if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 && L.cout <= 128 &&
       L.cin % 16 == 0)
     return HALO_CONV3;  // 3x3 "same": fe1.x, fe2.x, ae1-5, fd5.x, fd6.x, out0
@@ -937,7 +939,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // macro-pixel stem: rows (pixel offset z, cout), K = (x-shift plane, channel)
           const bool x4 = hm == HALO_STEM4X;
           // N tiles of 64 channels for the wide ConvT (4 phase accumulators x 64 fill TMEM)
-          const int hbn = hm == HALO_CONVT2 ? std::min(L.cout, 64) : L.cout, hnt = L.cout / hbn;
+          const int hbn = hm == HALO_CONVT2 ? std::min(L.cout, 64) : hm == HALO_CONV3 ? std::min(L.cout, 128) : L.cout,
+                    hnt = L.cout / hbn;
           const int ncb = hm == HALO_STEM7 ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE, bnh = x4 ? 4 * L.cout : hbn;
           hg.off = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)hnt * ncb * hg.ntaps * bnh * BK, 0);
@@ -1282,6 +1285,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.tiles_y = (int)ceil_div(hp.GH, HTH);
           hp.tiles_per_img = hp.tiles_x * hp.tiles_y;
           if (hg.mode == HALO_CONVT2) r.bn = std::min(L.cout, 64);  // N tiles (packed per tile above)
+          if (hg.mode == HALO_CONV3) r.bn = std::min(L.cout, 128);
           hp.ntn = L.cout / r.bn;
           hp.w = h->wpack.p + hg.off;
           hp.wblocks = hp.ncb * hg.ntaps;
@@ -1299,8 +1303,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           r.halo_bres = hg.mode == HALO_STEM4X
                             ? (int64_t)hp.wblocks * 4 * r.bn * BK * 2 <= HaloCfg<16, HALO_STEM4X, false, true>::W_RES_BYTES
                             : (int64_t)hp.wblocks * r.bn * BK * 2 <= HaloCfg<32, HALO_CONV3, false, true>::W_RES_BYTES;
-          if (r.bn * hp.ntn != L.cout || (hp.ntn > 1 && (r.halo_bres || fused || hg.mode != HALO_CONVT2)))
-            fail(LSG_ERUNTIME, "generator: halo N tiling only for streamed-weight ConvT layers");
+          if (r.bn * hp.ntn != L.cout || (hp.ntn > 1 && (r.halo_bres || fused || hp.tiles_per_img % 2)))
+            fail(LSG_ERUNTIME, "generator: halo N tiling needs streamed weights and an even tile count");
           hp.OH = OH;
           hp.OW = OW;
           hp.out = p.out;
