@@ -112,6 +112,7 @@ static const LayerSpec kLayers[] = {
     {"out1", CONV, 32, 3, 1, 1, 1, 1, 0, 0, 0, 0, 0},
 };
 constexpr int kNumLayers = sizeof(kLayers) / sizeof(kLayers[0]);
+constexpr int kAe0 = 18;  // plan index of ae0 (checked against the layer table at create)
 static_assert(kNumLayers == 51, "Wav2Lip has 51 conv layers");
 
 // ------------------------------------------------------------ input prep
@@ -168,6 +169,61 @@ __global__ void prep_mel(const float* __restrict__ rows, const int32_t* __restri
   reinterpret_cast<uint4*>(out)[i] = pack_px<PR>(c, inv_scale);
 }
 
+// ae0 (1 -> 32 channels, 3x3, 80x16 mel chunk) on CUDA cores: on the tensor
+// cores its K is 9 taps x 8 padded channels with ONE real one, so the MMAs and
+// im2col loads are ~8x padding (71 us at B = 512 for 0.7 MFLOP/frame).  Same
+// arithmetic as the tensor-core path: the quantized input (channel 0 of
+// x_mel), the quantized weights (w [32][9] as the packed MMA operand holds
+// them), fp32 accumulation, y = acc (* oscale, fp8) + bias, ReLU (* out_inv).
+template <int PR>
+__global__ void audio_stem(const uint16_t* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
+                           const float* __restrict__ oscale, float out_inv, uint16_t* __restrict__ out,
+                           int out_pitch, int out_coff, int B) {
+  using NF = Num<PR>;
+  __shared__ float sw[32 * 9], sb[32], so[32];
+  for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) sw[i] = w[i];
+  if (threadIdx.x < 32) {
+    sb[threadIdx.x] = bias[threadIdx.x];
+    so[threadIdx.x] = NF::F8 ? oscale[threadIdx.x] : 1.f;
+  }
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, h, w) of the 80 x 16 grid
+  if (i >= (int64_t)B * 1280) return;
+  const int b = (int)(i / 1280), hw = (int)(i - (int64_t)b * 1280), h = hw >> 4, wc = hw & 15;
+  float xv[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int hh = h + t / 3 - 1, ww = wc + t % 3 - 1;
+    float v = 0.f;
+    if (hh >= 0 && hh < 80 && ww >= 0 && ww < 16) {
+      const uint32_t u = __ldg(x + (((int64_t)b * 80 + hh) * 16 + ww) * 8);  // unit 0 of the 16-byte pixel
+      if constexpr (NF::F8) {
+        const __half_raw hr = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(u & 0xffu), __NV_E4M3);
+        v = __half2float(*reinterpret_cast<const __half*>(&hr));
+      } else {
+        v = NF::unpack(u).x;
+      }
+    }
+    xv[t] = v;
+  }
+  uint16_t* o = out + i * out_pitch + out_coff;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float f[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int co = half * 16 + j;
+      float acc = 0.f;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) acc = fmaf(xv[t], sw[co * 9 + t], acc);
+      float y = fmaxf(acc * so[co] + sb[co], 0.f);
+      if constexpr (NF::F8) y *= out_inv;
+      f[j] = y;
+    }
+    NF::from_float16(f, reinterpret_cast<uint4*>(o) + half * NF::U4);
+  }
+}
+
 // max |x| over a 16-bit (bf16/fp16) channel-slice view (calibration)
 template <int PR>
 __global__ void absmax_view(const uint16_t* __restrict__ src, int pitch, int coff, int C, int64_t pixels,
@@ -218,7 +274,7 @@ struct LayerRun {
 // A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
 // bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs, bit 11 (2048)
-// the 128-channel ConvT (fd5.0) on the halo kernel.
+// the 128-channel ConvT (fd5.0) on the halo kernel, bit 13 (8192) ae0 on the tensor cores.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -386,6 +442,7 @@ struct lsg_gen_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf<float> splitk_ws2;
   DevBuf<int> splitk_cnt2;
+  DevBuf<float> ae0w;  // ae0 weights [32][9] as quantized for the MMA (audio_stem)
   ~lsg_gen_s() {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -834,6 +891,32 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                 for (int kx = 0; kx < L.kw; ++kx) m = std::max(m, std::fabs(wat(co, ci, ky, kx)));
             sw[co] = m > 0.f ? m / 448.f : 1.f;
           }
+        if (std::string(L.name) == "ae0") {  // audio_stem's copy of the quantized operand
+          if (li != kAe0 || L.cin != 1 || L.cout != 32 || L.kh != 3 || L.kw != 3 || L.sh != 1 || L.ph != 1)
+            fail(LSG_ERUNTIME, "generator: ae0 shape / position");
+          std::vector<float> q(32 * 9);
+          for (int co = 0; co < 32; ++co)
+            for (int t = 0; t < 9; ++t) {
+              const float v = wat(co, 0, t / 3, t % 3);
+              if (f8) {
+                const __nv_fp8_storage_t e = __nv_cvt_float_to_fp8(v / sw[co], __NV_SATFINITE, __NV_E4M3);
+                const __half_raw hr = __nv_cvt_fp8_to_halfraw(e, __NV_E4M3);
+                q[co * 9 + t] = __half2float(__half(hr));
+              } else if (h->prec == PR_FP16) {
+                const uint16_t bits = f2h(v);
+                __half_raw hr;
+                hr.x = bits;
+                q[co * 9 + t] = __half2float(__half(hr));
+              } else {
+                const uint32_t u = (uint32_t)f2bf(v) << 16;
+                float f;
+                std::memcpy(&f, &u, 4);
+                q[co * 9 + t] = f;
+              }
+            }
+          h->ae0w.alloc(q.size());
+          LSG_CUDA(cudaMemcpy(h->ae0w.p, q.data(), q.size() * 4, cudaMemcpyHostToDevice));
+        }
         // phases
         std::vector<PhaseGeo>& G = geo[li];
         if (L.kind == CONV) {
@@ -1541,7 +1624,20 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
     // (both branches launch full-SM grids: capping either branch's SMs measured
     // slower at B = 128 and 512 -- the concurrency is in the small layers' tails)
     const bool audio = kLayers[r.layer].name[0] == 'a';
-    if (fork && audio) {
+    if (audio && r.layer == kAe0 && h->ae0w.p && !(gen_knobs() & 8192)) {  // ae0 on CUDA cores
+      cudaStream_t s2 = fork ? h->side : st;
+      const unsigned grid = (unsigned)ceil_div((int64_t)B * 1280, 256);
+      const ConvParams& p = r.p;
+      if (h->prec == PR_FP8)
+        audio_stem<PR_FP8><<<grid, 256, 0, s2>>>(h->x_mel.p, h->ae0w.p, p.bias, p.oscale, p.out_inv, p.out, p.out_pitch,
+                                                p.out_coff, B);
+      else if (h->prec == PR_FP16)
+        audio_stem<PR_FP16><<<grid, 256, 0, s2>>>(h->x_mel.p, h->ae0w.p, p.bias, p.oscale, p.out_inv, p.out,
+                                                 p.out_pitch, p.out_coff, B);
+      else
+        audio_stem<PR_BF16><<<grid, 256, 0, s2>>>(h->x_mel.p, h->ae0w.p, p.bias, p.oscale, p.out_inv, p.out,
+                                                 p.out_pitch, p.out_coff, B);
+    } else if (fork && audio) {
       dispatch(h, r, B, h->side, 1);
     } else {
       if (!joined && kLayers[r.layer].name[0] == 'f' && kLayers[r.layer].name[1] == 'd') {
