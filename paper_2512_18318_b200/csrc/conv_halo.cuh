@@ -36,7 +36,7 @@ constexpr int MAX_HTAPS = 9;
 // Routing modes and their compile-time tap tables (patch offset in pixels,
 // output phase).  The host builds the same lists from the layer geometry and
 // checks them against these (generator.cu), so packing and issue agree.
-enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3, HALO_STEM4X = 4 };
+enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3, HALO_STEM4X = 4, HALO_CONV3S2 = 5 };
 
 template <int MODE>
 struct HaloTaps;
@@ -67,6 +67,23 @@ struct HaloTaps<HALO_STEM7> {  // 7x7 on 8 channels: planes = x shifts, taps = k
 // cycles).  Plane g (g = 0..9) holds input column 4j + g - 3 for macro
 // column j (a W-strided TMA box), so a K step still reads 2 planes; the
 // 4 pixel offsets are the epilogue's "phases" (element-strided stores).
+// Stride-2 3x3 (fe1.0, fe2.0): the input under a tile is loaded as its 4
+// parity sub-grids (TMA boxes with element stride 2 in H and W), so every
+// tap is a fixed offset into one (16+1) x (8+1) parity patch instead of an
+// im2col row per output pixel.  Output o, tap k reads input 2o + k - 1: k = 1
+// the even grid at o, k = 0 / 2 the odd grid at o - 1 / o; with the patch
+// origin at o0 - 1 the local offset is (k != 0).  A stage holds 8 planes =
+// [parity ey*2+ex][2 channel granules]; a K step reads both granules of one
+// parity (LBO = 1 plane), a tap adds its parity base.
+template <>
+struct HaloTaps<HALO_CONV3S2> {
+  static constexpr int NPH = 1, NT = 9, PW = HTW + 1, PH = HTH + 1;
+  static constexpr int PL16 = ((PW * PH * 16 + 127) / 128 * 128) / 16;  // plane, 16-byte units
+  __host__ __device__ static constexpr int aoff(int t) {
+    return ((t / 3 == 1 ? 0 : 2) + (t % 3 == 1 ? 0 : 1)) * 2 * PL16 + (t / 3 != 0) * PW + (t % 3 != 0);
+  }
+  __host__ __device__ static constexpr int phase(int) { return 0; }
+};
 template <>
 struct HaloTaps<HALO_STEM4X> {
   static constexpr int NPH = 4, NT = 7, PW = HTW, PH = HTH + 6;
@@ -246,6 +263,7 @@ __device__ __forceinline__ uint64_t halo_desc(uint32_t addr, uint32_t lbo, uint3
 // releases the accumulator on the even CTA's tempty barrier.
 template <int BN, int MODE, bool FUSED_OUT, int PR, bool B_RES, bool PAIR = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
+  static_assert(MODE != HALO_CONV3S2 || (B_RES && !PAIR && !FUSED_OUT), "stride-2 halo: resident weights only");
   using NF = Num<PR>;
   using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::F8 ? 1 : 2, PAIR>;
   using TT = HaloTaps<MODE>;
@@ -352,9 +370,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
         tc::mbar_wait(&hempty[hs], hph ^ 1);
-        if (lane == 0 && rank == 0) tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) * ng * box_bytes);
+        if (lane == 0 && rank == 0)
+          tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) * (MODE == HALO_CONV3S2 ? 8 : ng) * box_bytes);
         __syncwarp();
-        if (lane < ng) {
+        if constexpr (MODE == HALO_CONV3S2) {
+          if (lane < 8) {  // plane lane = parity (lane >> 1) x granule (lane & 1) of this channel block
+            const int pp = lane >> 1;
+            tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (cb * 2 + (lane & 1)) * 8,
+                        2 * (tx * HTW - 1) + (pp & 1), 2 * (ty * HTH - 1) + (pp >> 1), n);
+          }
+        } else if (lane < ng) {
           if constexpr (PAIR)
             tma_tile_4d_pair(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, leader_addr(&hfull[hs]),
                              (g0 + lane) * cstep, x0 + (g0 + lane) * xstep, y0, n);
@@ -436,14 +461,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         tc::tc_fence_after_nc();  // TMEM reuse after the epilogue's reads
         const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < ncb; ++cb) {
-          const int ksteps = min(8, ngran - cb * 8) >> 1;
+          const int ksteps = MODE == HALO_CONV3S2 ? 1 : min(8, ngran - cb * 8) >> 1;
           tc::mbar_wait_fast(&hfull[hs], hph);  // TMA data: the mbarrier alone orders it
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
           const uint64_t bcb = b_desc0 + (uint64_t)(cb * NT) * BBLK16;
 #pragma unroll
           for (int tap = 0; tap < NT; ++tap) {
             uint64_t db;
-            if constexpr (B_RES) {
+            if constexpr (MODE == HALO_CONV3S2) {  // one block per tap; channel block cb = K offset 32 * cb bytes
+              db = b_desc0 + (uint64_t)tap * BBLK16 + (uint64_t)(2 * cb);
+            } else if constexpr (B_RES) {
               db = bcb + (uint64_t)tap * BBLK16;
             } else {
               if (tap % CF::WG == 0) tc::mbar_wait_fast(&bfull[bs], bph);

@@ -274,7 +274,8 @@ struct LayerRun {
 // A/B switches for tuning runs (env LSG_GEN_KNOBS, read once): bit 0 keeps
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
 // bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs, bit 11 (2048)
-// the 128-channel ConvT (fd5.0) on the halo kernel, bit 13 (8192) ae0 on the tensor cores.
+// the 128-channel ConvT (fd5.0) on the halo kernel, bit 13 (8192) ae0 on the tensor cores,
+// bit 14 (16384) the stride-2 3x3 convs on the im2col kernel.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -291,6 +292,9 @@ HaloMode halo_mode(const LayerSpec& L) {
   if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 && L.cout <= 128 &&
       L.cin % 16 == 0)
     return HALO_CONV3;  // 3x3 "same": fe1.x, fe2.x, ae1-5, fd5.x, fd6.x, out0
+  if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2 && L.ph == 1 && L.pw == 1 && L.cin % 16 == 0 &&
+      L.cin <= 64 && L.cout <= 64 && !(gen_knobs() & 16384))
+    return HALO_CONV3S2;  // fe1.0, fe2.0: stride-2 3x3 on parity sub-grids
   if (L.kind != CONV && L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2 && L.ph == 1 && L.pw == 1 && L.oph == 1 &&
       L.opw == 1 && L.cin % 16 == 0 && (L.cout <= 64 || (L.cout == 128 && !(gen_knobs() & 2048))))
     return HALO_CONVT2;  // fd6.0, fd5.0 (as two 64-channel N tiles): 4 output phases share one accumulator set
@@ -327,12 +331,12 @@ EncodeTiled tiled_fn() {
 
 // tiled map of an NHWC channel-slice view, box = 8 channels x pw x ph x 1 image
 // (ex > 1: every ex-th column, pw of them -- the macro-pixel stem's planes)
-void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph, int ex = 1) {
+void encode_patch(CUtensorMap* map, const View& v, int n, int pw, int ph, int ex = 1, int ey = 1) {
   const cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)n};
   const cuuint64_t strides[3] = {(cuuint64_t)v.pitch * 2, (cuuint64_t)v.W * v.pitch * 2,
                                  (cuuint64_t)v.H * v.W * v.pitch * 2};
-  const cuuint32_t box[4] = {8, (cuuint32_t)(pw * ex), (cuuint32_t)ph, 1};
-  const cuuint32_t estr[4] = {1, (cuuint32_t)ex, 1, 1};
+  const cuuint32_t box[4] = {8, (cuuint32_t)(pw * ex), (cuuint32_t)(ph * ey), 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)ex, (cuuint32_t)ey, 1};
   CUresult r = tiled_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, v.p + v.coff, dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -616,6 +620,8 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
 #define LSG_HALO_VARIANTS(X)             \
   X(16, HALO_STEM7, false, true)         \
   X(16, HALO_STEM4X, false, true)        \
+  X(32, HALO_CONV3S2, false, true)        \
+  X(64, HALO_CONV3S2, false, true)        \
   X(32, HALO_CONV3, false, true)         \
   X(64, HALO_CONV3, false, true)         \
   X(128, HALO_CONV3, false, false)       \
@@ -1003,6 +1009,13 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                 add_tap(G[z].dy[t] * hg.pw + G[z].dx[t], z, G[z].ky[t], G[z].kx[t]);
               }
             }
+          } else if (hm == HALO_CONV3S2) {  // parity sub-grid patch (tile + 1), taps at parity base + (k != 0)
+            hg.pw = HTW + 1;
+            hg.ph = HTH + 1;
+            const int pl16 = ((hg.pw * hg.ph * 16 + 127) / 128 * 128) / 16;
+            for (int ky = 0; ky < 3; ++ky)
+              for (int kx = 0; kx < 3; ++kx)
+                add_tap(((ky == 1 ? 0 : 2) + (kx == 1 ? 0 : 1)) * 2 * pl16 + (ky != 0) * hg.pw + (kx != 0), 0, ky, kx);
           } else {  // stem: planes = x shifts, taps = the 7 kernel rows
             hg.oy0 = hg.ox0 = -3;
             hg.pw = HTW;
@@ -1016,6 +1029,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           const bool ok = hm == HALO_CONV3    ? taps_match<HALO_CONV3>(hg)
                           : hm == HALO_CONVT2 ? taps_match<HALO_CONVT2>(hg)
                           : hm == HALO_STEM4X ? taps_match<HALO_STEM4X>(hg)
+                          : hm == HALO_CONV3S2 ? taps_match<HALO_CONV3S2>(hg)
                                               : taps_match<HALO_STEM7>(hg);
           if (!ok) fail(LSG_ERUNTIME, std::string("generator: halo tap table mismatch at ") + L.name);
           // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap);
@@ -1024,7 +1038,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // N tiles of 64 channels for the wide ConvT (4 phase accumulators x 64 fill TMEM)
           const int hbn = hm == HALO_CONVT2 ? std::min(L.cout, 64) : hm == HALO_CONV3 ? std::min(L.cout, 128) : L.cout,
                     hnt = L.cout / hbn;
-          const int ncb = hm == HALO_STEM7 ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE, bnh = x4 ? 4 * L.cout : hbn;
+          const int ncb = (hm == HALO_STEM7 || hm == HALO_CONV3S2) ? 1 : x4 ? 2 : (L.cin + KE - 1) / KE,
+                    bnh = x4 ? 4 * L.cout : hbn;
           hg.off = (int64_t)pack.size();
           pack.resize(pack.size() + (size_t)hnt * ncb * hg.ntaps * bnh * BK, 0);
           uint16_t* dst = pack.data() + hg.off;
@@ -1351,7 +1366,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // planes come in pairs per K step; an odd last plane reads channels past the
           // view, which the TMA zero-fills (fp8 out0: 80 channels = 5 planes)
           hp.ngran = hg.mode == HALO_STEM4X ? 10 : hp.shift_planes ? 8 : ((p.C / 8 + 1) & ~1);
-          hp.ncb = (hp.ngran + 7) / 8;
+          hp.ncb = hg.mode == HALO_CONV3S2 ? hp.ngran / 2 : (hp.ngran + 7) / 8;  // S2: 2 granules x 4 parities
           hp.ntaps = hg.ntaps;
           for (int t = 0; t < MAX_HTAPS; ++t) {
             hp.aoff[t] = hg.aoff[t];
@@ -1371,7 +1386,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           if (hg.mode == HALO_CONV3) r.bn = std::min(L.cout, 128);
           hp.ntn = L.cout / r.bn;
           hp.w = h->wpack.p + hg.off;
-          hp.wblocks = hp.ncb * hg.ntaps;
+          hp.wblocks = hg.mode == HALO_CONV3S2 ? hg.ntaps : hp.ncb * hg.ntaps;  // S2: channel blocks share a block
+          if (hg.mode == HALO_CONV3S2 && hp.ncb * 32 > 128) fail(LSG_ERUNTIME, "generator: stride-2 halo needs <= 4 channel blocks");
           if (hg.mode != HALO_STEM4X && hg.mode != HALO_STEM7) {  // CTA pairs: weight half-blocks by TMA
             const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)hp.wblocks * r.bn * hp.ntn};
             const cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
@@ -1404,7 +1420,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.out_mode = p.out_mode;
           hp.w1 = p.w1;
           hp.b1 = p.b1;
-          encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, hp.xmul);
+          if (hg.mode == HALO_CONV3S2) encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, 2, 2);
+          else encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, hp.xmul);
           const int bc = std::min(r.bn * 2 / cpu, 128) / 2;  // box channels in 16-bit units (128-byte rows max)
           if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
           if (hg.mode == HALO_CONV3 && !fused) {

@@ -46,8 +46,9 @@ def test_launch_paths_agree(tmp_path, B, prec):
     assert np.array_equal(base[0], _render(tmp_path, B, prec, 512)[0])
     # knobs: 1 no narrow tiles, 2 no split-K, 32 no CTA pairs (im2col), 64 one
     # pixel per stem row, 1024 no CTA pairs (halo), 2048 the 128-channel ConvT
-    # on the im2col kernel, 8192 ae0 on the tensor cores, 11363 none of them
-    for knobs in (1, 2, 32, 64, 1024, 2048, 8192, 11363):
+    # on the im2col kernel, 8192 ae0 on the tensor cores, 16384 the stride-2
+    # 3x3 convs on the im2col kernel, 27747 none of them
+    for knobs in (1, 2, 32, 64, 1024, 2048, 8192, 16384, 27747):
         other = _render(tmp_path, B, prec, knobs)[0]
         if prec == 2:
             q0, q1 = _psnr(base[0], ref), _psnr(other, ref)
