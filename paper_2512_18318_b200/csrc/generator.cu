@@ -632,7 +632,9 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
 // Measured per layer (B = 512): the streamed-weight 3x3 at N = 128 (fd5.1/5.2,
 // 288 KB of weights per 128-position tile) gains 18% from halving each SM's
 // weight stream; resident-weight layers (fe1/fe2/ae/fd6.1-2, N <= 64) and the
-// streamed ConvT fd6.0 lose 15-35%, the fused output layer is neutral.
+// streamed ConvT fd6.0 lose 15-35% (and fd5.0's N-tiled ConvT, despite twice
+// the weight stream, about as much as fd5.1/5.2 gain), the fused output layer
+// is neutral.
 #define LSG_HALO_PAIR_VARIANTS(X) X(128, HALO_CONV3, false, false)
 
 // The host-built tap list of a halo layer must be the kernel's compile-time
