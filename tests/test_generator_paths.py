@@ -57,3 +57,12 @@ def test_launch_paths_agree(tmp_path, B, prec):
             # only the fp32 summation order differs; 16-bit activation rounding
             # in between moves pixels by a level or so
             assert _psnr(base[0], other) > 40.0, (knobs, _psnr(base[0], other))
+
+
+@pytest.mark.parametrize("B", [1, 3, 17])
+def test_small_odd_batches(tmp_path, B):
+    """Tiny and odd batches: few / odd tile counts change which launch paths
+    apply (split factors, pair eligibility, grid sizes); all must agree."""
+    base = _render(tmp_path, B, 1, 0)[0]
+    off = _render(tmp_path, B, 1, 27747)[0]
+    assert _psnr(base, off) > 40.0, _psnr(base, off)
