@@ -45,7 +45,7 @@ def main(path, B=512, last=0):
         tot += t
         dram = (m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)) / 1e6
         lname, tf, frac = "", 0.0, 0.0
-        if Ls and ("conv_tc" in name or "conv_halo" in name):
+        if Ls and ("conv_tc" in name or "conv_halo" in name or "audio_stem" in name):
             if li == len(names):  # next forward of a multi-rep capture
                 print(f"subtotal {tot - t:.1f} us")
                 li = 0
