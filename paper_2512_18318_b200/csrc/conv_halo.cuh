@@ -96,6 +96,8 @@ struct alignas(64) HaloParams {
   CUtensorMap tmap_out;  // output view, box (min(BN,64), 8, 16, 1) output positions (x2 stride for ConvT)
   CUtensorMap tmap_res;  // residual view, box (min(BN,64), 8, 16, 1)
   CUtensorMap wmap;      // packed weights as 2-D [rows][64 units], box (64, MN/2): CTA-pair loads
+  CUtensorMap tmap_out2; // second copy of the output (out2): fe0 also writes a dense 16-channel tensor
+                         // for fe1.0 (its concat-buffer slice is 16 of 80 channels)
   int H, W, C, B;    // input view
   int GH, GW;        // grid (output positions for convs, input positions for ConvT)
   int oy0, ox0;      // patch origin relative to the tile origin (-pad for convs)
@@ -105,6 +107,7 @@ struct alignas(64) HaloParams {
   int ncb;           // channel blocks of <= 8 planes
   int shift_planes;  // planes are x-shifted copies of channels 0..7 (fe0)
   int xmul;          // input columns per grid column (4 for the macro-pixel stem)
+  int out2;          // also store every output box through tmap_out2
   int ntaps;
   int aoff[MAX_HTAPS];   // tap start offset in the patch, 16-byte units (= pixels)
   int tphase[MAX_HTAPS]; // output phase the tap accumulates into
@@ -605,6 +608,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             for (int cc = 0; cc < CF::NCH; ++cc)
               tma_store_4d(&p.tmap_out, src + (z * CF::NCH + cc) * CF::BOX, nt * (BN / NF::CPU) + cc * 64,
                            tx * HTW * p.osx + p.pox[z], ty * HTH * p.osy + p.poy[z], n);
+          if (p.out2) {
+#pragma unroll
+            for (int z = 0; z < NPH; ++z)
+#pragma unroll
+              for (int cc = 0; cc < CF::NCH; ++cc)
+                tma_store_4d(&p.tmap_out2, src + (z * CF::NCH + cc) * CF::BOX, cc * 64, tx * HTW * p.osx + p.pox[z],
+                             ty * HTH * p.osy + p.poy[z], n);
+          }
           bulk_commit();
         }
         if (++sb == CF::NSTG) sb = 0;

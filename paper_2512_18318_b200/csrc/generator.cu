@@ -275,7 +275,7 @@ struct LayerRun {
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
 // bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs, bit 11 (2048)
 // the 128-channel ConvT (fd5.0) on the halo kernel, bit 13 (8192) ae0 on the tensor cores,
-// bit 14 (16384) the stride-2 3x3 convs on the im2col kernel.
+// bit 14 (16384) the stride-2 3x3 convs on the im2col kernel, bit 15 (32768) fe1.0 reading the concat slice.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -453,6 +453,7 @@ struct lsg_gen_s {
     if (side) cudaStreamDestroy(side);
   }
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
+  View X16;  // dense copy of fe0's output (fe1.0's input; cat[6] keeps the concat copy)
   std::vector<LayerRun> plan;
 };
 
@@ -823,6 +824,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       reqs.push_back({&h->x_face, 96, 96, 8});  // 16 bytes per pixel in every format
       reqs.push_back({&h->x_mel, 80, 16, 8});
       for (int l = 0; l < 7; ++l) reqs.push_back({&h->cat[l], cat_hw[l], cat_hw[l], cat_c[l] / cpu});
+      reqs.push_back({&h->X16, 96, 96, 16 / cpu});
       reqs.push_back({&h->S0, 96, 96, 64 / cpu});
       reqs.push_back({&h->S1, 96, 96, 64 / cpu});
       reqs.push_back({&h->A0, 80, 16, 32 / cpu});
@@ -1127,7 +1129,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       int li = 0;
       // face encoder
       io[li++] = {h->x_face, slice(cat[6], 64, 16)};
-      io[li++] = {slice(cat[6], 64, 16), resize(S0, 48, 48, 32)};
+      io[li++] = {(gen_knobs() & 32768) ? slice(cat[6], 64, 16) : h->X16, resize(S0, 48, 48, 32)};
       io[li++] = {resize(S0, 48, 48, 32), resize(S1, 48, 48, 32)};
       io[li++] = {resize(S1, 48, 48, 32), slice(cat[5], 128, 32)};
       io[li++] = {slice(cat[5], 128, 32), resize(S0, 24, 24, 64)};
@@ -1186,6 +1188,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
         auto fixed = [&](const View& v) -> int {
           if (v.p == h->x_face.p) return 0;
           if (v.p == h->x_mel.p) return 1;
+          if (v.p == h->X16.p) return 8;  // fe0's output: same values (and fp8 scale) as its cat[6] slice
           for (int k = 0; k < 7; ++k)
             if (v.p == h->cat[k].p) return 2 + k;
           return -1;
@@ -1426,6 +1429,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           else encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, hp.xmul);
           const int bc = std::min(r.bn * 2 / cpu, 128) / 2;  // box channels in 16-bit units (128-byte rows max)
           if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
+          hp.out2 = l == 0 && !(gen_knobs() & 32768);  // fe0: the dense copy fe1.0 reads
+          if (hp.out2) encode_box(&hp.tmap_out2, h->X16, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
           if (hg.mode == HALO_CONV3 && !fused) {
             if (!L.res || in.C != L.cout / cpu) fail(LSG_ERUNTIME, std::string("generator: halo 3x3 block without residual at ") + L.name);
             encode_box(&hp.tmap_res, in, max_batch, bc, HTW, HTH, 1, 1);

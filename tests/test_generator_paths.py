@@ -47,8 +47,9 @@ def test_launch_paths_agree(tmp_path, B, prec):
     # knobs: 1 no narrow tiles, 2 no split-K, 32 no CTA pairs (im2col), 64 one
     # pixel per stem row, 1024 no CTA pairs (halo), 2048 the 128-channel ConvT
     # on the im2col kernel, 8192 ae0 on the tensor cores, 16384 the stride-2
-    # 3x3 convs on the im2col kernel, 27747 none of them
-    for knobs in (1, 2, 32, 64, 1024, 2048, 8192, 16384, 27747):
+    # 3x3 convs on the im2col kernel, 32768 fe1.0 reading the concat slice
+    # instead of fe0's dense copy, 60515 none of them
+    for knobs in (1, 2, 32, 64, 1024, 2048, 8192, 16384, 32768, 60515):
         other = _render(tmp_path, B, prec, knobs)[0]
         if prec == 2:
             q0, q1 = _psnr(base[0], ref), _psnr(other, ref)
@@ -64,5 +65,5 @@ def test_small_odd_batches(tmp_path, B):
     """Tiny and odd batches: few / odd tile counts change which launch paths
     apply (split factors, pair eligibility, grid sizes); all must agree."""
     base = _render(tmp_path, B, 1, 0)[0]
-    off = _render(tmp_path, B, 1, 27747)[0]
+    off = _render(tmp_path, B, 1, 60515)[0]
     assert _psnr(base, off) > 40.0, _psnr(base, off)
