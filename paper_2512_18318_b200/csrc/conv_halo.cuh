@@ -31,12 +31,14 @@ namespace lsg {
 namespace gen {
 
 constexpr int HTH = 16, HTW = 8;  // tile: 16 rows x 8 columns = 128 grid positions
-constexpr int MAX_HTAPS = 9;
+constexpr int MAX_HTAPS = 12;
 
 // Routing modes and their compile-time tap tables (patch offset in pixels,
 // output phase).  The host builds the same lists from the layer geometry and
 // checks them against these (generator.cu), so packing and issue agree.
-enum HaloMode { HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3, HALO_STEM4X = 4, HALO_CONV3S2 = 5 };
+enum HaloMode {
+  HALO_NONE = 0, HALO_CONV3 = 1, HALO_CONVT2 = 2, HALO_STEM7 = 3, HALO_STEM4X = 4, HALO_CONV3S2 = 5, HALO_CONV3X2 = 6
+};
 
 template <int MODE>
 struct HaloTaps;
@@ -81,6 +83,22 @@ struct HaloTaps<HALO_CONV3S2> {
   static constexpr int PL16 = ((PW * PH * 16 + 127) / 128 * 128) / 16;  // plane, 16-byte units
   __host__ __device__ static constexpr int aoff(int t) {
     return ((t / 3 == 1 ? 0 : 2) + (t % 3 == 1 ? 0 : 1)) * 2 * PL16 + (t / 3 != 0) * PW + (t % 3 != 0);
+  }
+  __host__ __device__ static constexpr int phase(int) { return 0; }
+};
+// The output conv (out0, 80 -> 32 channels, fused with out1) on macro-pixels
+// of 2 horizontally adjacent outputs: N = 2 x 32 per MMA and half the tiles
+// (its N = 32 MMAs cost ~45 cycles each plus a per-tile overhead, DESIGN
+// §3.1).  Output 2j + z, column tap kx reads input 2j + d - 1 with d = z + kx
+// in 0..3: the patch is stored as x-parity planes (W-strided TMA boxes,
+// element stride 2), plane parity d & 1 at macro column j + (d >> 1).  A stage
+// holds [parity][4 channel granules]; taps t = (ky, d), 12 of them.
+template <>
+struct HaloTaps<HALO_CONV3X2> {
+  static constexpr int NPH = 2, NT = 12, PW = HTW + 1, PH = HTH + 2;
+  static constexpr int PL16 = ((PW * PH * 16 + 127) / 128 * 128) / 16;  // plane, 16-byte units
+  __host__ __device__ static constexpr int aoff(int t) {
+    return ((t % 4) & 1) * 4 * PL16 + (t / 4) * PW + ((t % 4) >> 1);
   }
   __host__ __device__ static constexpr int phase(int) { return 0; }
 };
@@ -147,12 +165,15 @@ struct HaloCfg {
   static constexpr bool HAS_RES = MODE == HALO_CONV3 && !FUSED;  // every routed 3x3 block is residual
   static constexpr int PLANE_MAX = 2944;  // 18 x 10 x 16 B rounded to 128; also 22 x 8 and 17 x 9
   static constexpr int HSTAGE = 8 * PLANE_MAX;
-  static constexpr int MN = MODE == HALO_STEM4X ? NPH * BN : BN;  // MMA N: every phase at once for macro-pixels
+  static constexpr bool MACRO = MODE == HALO_STEM4X || MODE == HALO_CONV3X2;
+  static constexpr int MN = MACRO ? NPH * BN : BN;  // MMA N: every phase at once for macro-pixels
   static constexpr int BROWS = PAIR ? MN / 2 : MN;  // weight rows of a block held by one CTA
-  static constexpr int BBLK = BROWS * BK * 2;  // one (cb, tap) weight block (this CTA's rows)
+  // one (cb, tap) weight block (this CTA's rows); the macro-pixel output conv
+  // keeps one block per tap: 64 channels SW128 + (16-bit) 16 channels SW32
+  static constexpr int BBLK = MODE == HALO_CONV3X2 ? MN * BK * 2 + (ES == 2 ? MN * 32 : 0) : BROWS * BK * 2;
   static constexpr int WG = 3;              // streamed weights: taps per ring slot (one wait + commit each)
   static constexpr int GBLK = WG * BBLK;
-  static constexpr int W_RES_BYTES = MODE == HALO_STEM4X ? 112 * 1024 : 72 * 1024;
+  static constexpr int W_RES_BYTES = MODE == HALO_STEM4X ? 112 * 1024 : (MODE == HALO_CONV3X2 ? 120 * 1024 : 72 * 1024);
   static constexpr int IB = BN * ES < 128 ? BN * ES : 128;  // bytes per position per box
   static constexpr int NCH = BN * ES > 128 ? BN * ES / 128 : 1;  // boxes across the channels
   static constexpr int BOX = 128 * IB;                 // one [128][IB] box
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   using TT = HaloTaps<MODE>;
   constexpr int NPH = TT::NPH;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
-  static_assert(!FUSED_OUT || NPH == 1, "fused output conv has one phase");
+  static_assert(!FUSED_OUT || NPH == 1 || MODE == HALO_CONV3X2, "fused output conv: one phase, or 2-pixel macro columns");
   // epilogue warps 2-9 = two groups of four (one per TMEM lane quadrant).
   // SPLIT: both groups take every tile, half the channels each.  Otherwise
   // (BN = 16, or the fused 1x1 output) the groups alternate tiles, group g
@@ -374,9 +395,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
         tc::mbar_wait(&hempty[hs], hph ^ 1);
         if (lane == 0 && rank == 0)
-          tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) * (MODE == HALO_CONV3S2 ? 8 : ng) * box_bytes);
+          tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) *
+                                                    (MODE == HALO_CONV3S2   ? 8
+                                                     : MODE == HALO_CONV3X2 ? 2 * min(4, p.ngran - cb * 4)
+                                                                            : ng) *
+                                                    box_bytes);
         __syncwarp();
-        if constexpr (MODE == HALO_CONV3S2) {
+        if constexpr (MODE == HALO_CONV3X2) {
+          const int gs = lane & 3, g = cb * 4 + gs;  // plane lane = parity (lane >> 2) x granule slot
+          if (lane < 8 && g < p.ngran)
+            tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], g * 8,
+                        2 * (tx * HTW) - 1 + (lane >> 2), ty * HTH - 1, n);
+        } else if constexpr (MODE == HALO_CONV3S2) {
           if (lane < 8) {  // plane lane = parity (lane >> 1) x granule (lane & 1) of this channel block
             const int pp = lane >> 1;
             tma_tile_4d(sH0 + hs * CF::HSTAGE + lane * p.plane, &p.tmap, &hfull[hs], (cb * 2 + (lane & 1)) * 8,
@@ -464,14 +494,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         tc::tc_fence_after_nc();  // TMEM reuse after the epilogue's reads
         const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < ncb; ++cb) {
-          const int ksteps = MODE == HALO_CONV3S2 ? 1 : min(8, ngran - cb * 8) >> 1;
+          const int ksteps = MODE == HALO_CONV3S2   ? 1
+                             : MODE == HALO_CONV3X2 ? min(4, ngran - cb * 4) >> 1
+                                                    : min(8, ngran - cb * 8) >> 1;
           tc::mbar_wait_fast(&hfull[hs], hph);  // TMA data: the mbarrier alone orders it
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
           const uint64_t bcb = b_desc0 + (uint64_t)(cb * NT) * BBLK16;
 #pragma unroll
           for (int tap = 0; tap < NT; ++tap) {
             uint64_t db;
-            if constexpr (MODE == HALO_CONV3S2) {  // one block per tap; channel block cb = K offset 32 * cb bytes
+            if constexpr (MODE == HALO_CONV3X2) {  // one block per tap; K step cb*2+ks (B below)
+              db = b_desc0 + (uint64_t)tap * BBLK16;
+            } else if constexpr (MODE == HALO_CONV3S2) {  // one block per tap; channel block cb = K offset 32 * cb bytes
               db = b_desc0 + (uint64_t)tap * BBLK16 + (uint64_t)(2 * cb);
             } else if constexpr (B_RES) {
               db = bcb + (uint64_t)tap * BBLK16;
@@ -487,7 +521,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             const uint32_t acc0 = (first && cb == 0) ? 0u : 1u;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              if (ks < ksteps) {
+              if constexpr (MODE == HALO_CONV3X2) {
+                if (ks < ksteps) {
+                  const int kg = cb * 2 + ks;  // global K step: 0-3 in the SW128 part, 4 in the SW32 part
+                  uint64_t bk;
+                  if (kg < 4) {
+                    bk = db + (uint64_t)(2 * kg);
+                  } else {
+                    const uint32_t a32 = sB0 + (uint32_t)(tap * CF::BBLK + CF::MN * BK * 2);
+                    bk = (uint64_t)((a32 >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+                         (1ull << 46) | (6ull << 61);  // K-major, 32-byte swizzle, 8-row groups 256 B apart
+                  }
+                  NF::mma_nc(dd, at + ks * PLANE2, bk, idesc, (ks || cb || tap) ? 1u : 0u);
+                }
+              } else if (ks < ksteps) {
                 if constexpr (PAIR) {
                   if constexpr (NF::F8) tc::mma2_f8(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
                   else tc::mma2_f16(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
@@ -630,18 +677,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         tc::mbar_wait(&tfull[a], use & 1);
         tc::tc_fence_after();
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS;
-        float o[3] = {__ldg(p.b1 + 0), __ldg(p.b1 + 1), __ldg(p.b1 + 2)};
+        float oz[NPH][3];
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          uint32_t v[16];
-          tc::tmem_ld16(tbase + c0, v);
-          tc::tmem_ld_wait();
+        for (int z = 0; z < NPH; ++z) {  // macro-pixels: phase z = output column 2 gx + z
+          float* o = oz[z];
+          o[0] = __ldg(p.b1 + 0);
+          o[1] = __ldg(p.b1 + 1);
+          o[2] = __ldg(p.b1 + 2);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
-            const float xx = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tbase + z * BN + c0, v);
+            tc::tmem_ld_wait();
 #pragma unroll
-            for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
+            for (int j = 0; j < 16; ++j) {
+              const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
+              const float xx = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
+#pragma unroll
+              for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);
+            }
           }
         }
         tc::tc_fence_before();
@@ -651,9 +705,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         } else {
           tc::mbar_arrive(&tempty[a]);
         }
+#pragma unroll
+        for (int z = 0; z < NPH; ++z) {
+        const float* o = oz[z];
         if (gvalid) {
           const int HWo = p.OH * p.OW;
-          const size_t pp = (size_t)gy * p.OW + gx;
+          const size_t pp = (size_t)gy * p.OW + gx * p.osx + p.pox[z];
           if (p.out_mode == OUT_F32_LOGITS) {
             float* out = reinterpret_cast<float*>(p.final_out);
 #pragma unroll
@@ -670,6 +727,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
               out[o3] = (uint8_t)__float2int_rn(fminf(fmaxf(s * 255.f, 0.f), 255.f));
             }
           }
+        }
         }
       }
     }

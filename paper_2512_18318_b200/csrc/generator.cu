@@ -275,7 +275,8 @@ struct LayerRun {
 // the packed tile width, bit 1 disables split-K, bit 5 (32) CTA pairs, bit 6 (64) the macro-pixel stem,
 // bit 9 (512) the concurrent audio-encoder branch, bit 10 (1024) halo CTA pairs, bit 11 (2048)
 // the 128-channel ConvT (fd5.0) on the halo kernel, bit 13 (8192) ae0 on the tensor cores,
-// bit 14 (16384) the stride-2 3x3 convs on the im2col kernel, bit 15 (32768) fe1.0 reading the concat slice.
+// bit 14 (16384) the stride-2 3x3 convs on the im2col kernel, bit 15 (32768) fe1.0 reading the concat slice,
+// bit 16 (65536) out0 on one pixel per GEMM row.
 static int gen_knobs() {
   static const int k = [] {
     const char* e = std::getenv("LSG_GEN_KNOBS");
@@ -289,6 +290,8 @@ static int gen_knobs() {
 HaloMode halo_mode(const LayerSpec& L) {
   // (fd4.1/4.2, 256 channels, as two 128-channel N tiles on CTA pairs measured
   // 1.3% slower end to end than the im2col pair kernel: kept there)
+  if (std::string(L.name) == "out0" && L.cout == 32 && L.cin == 80 && !(gen_knobs() & 65536))
+    return HALO_CONV3X2;  // the fused output conv on 2-pixel macro columns
   if (L.kind == CONV && L.kh == 3 && L.kw == 3 && L.sh == 1 && L.sw == 1 && L.ph == 1 && L.pw == 1 && L.cout <= 128 &&
       L.cin % 16 == 0)
     return HALO_CONV3;  // 3x3 "same": fe1.x, fe2.x, ae1-5, fd5.x, fd6.x, out0
@@ -627,7 +630,8 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
   X(64, HALO_CONV3, false, true)         \
   X(128, HALO_CONV3, false, false)       \
   X(64, HALO_CONVT2, false, false)       \
-  X(32, HALO_CONV3, true, true)
+  X(32, HALO_CONV3, true, true)          \
+  X(32, HALO_CONV3X2, true, true)
 
 // halo variants that also run as CTA pairs (cta_group::2; HaloCfg PAIR).
 // Measured per layer (B = 512): the streamed-weight 3x3 at N = 128 (fd5.1/5.2,
@@ -1013,6 +1017,14 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                 add_tap(G[z].dy[t] * hg.pw + G[z].dx[t], z, G[z].ky[t], G[z].kx[t]);
               }
             }
+          } else if (hm == HALO_CONV3X2) {  // x-parity planes, 12 taps (ky, d = z + kx)
+            hg.pw = HTW + 1;
+            hg.ph = HTH + 2;
+            hg.nph = 2;
+            hg.pox[1] = 1;
+            const int pl16 = ((hg.pw * hg.ph * 16 + 127) / 128 * 128) / 16;
+            for (int ky = 0; ky < 3; ++ky)
+              for (int d = 0; d < 4; ++d) add_tap((d & 1) * 4 * pl16 + ky * hg.pw + (d >> 1), 0, ky, d);
           } else if (hm == HALO_CONV3S2) {  // parity sub-grid patch (tile + 1), taps at parity base + (k != 0)
             hg.pw = HTW + 1;
             hg.ph = HTH + 1;
@@ -1034,8 +1046,33 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                           : hm == HALO_CONVT2 ? taps_match<HALO_CONVT2>(hg)
                           : hm == HALO_STEM4X ? taps_match<HALO_STEM4X>(hg)
                           : hm == HALO_CONV3S2 ? taps_match<HALO_CONV3S2>(hg)
+                          : hm == HALO_CONV3X2 ? taps_match<HALO_CONV3X2>(hg)
                                               : taps_match<HALO_STEM7>(hg);
           if (!ok) fail(LSG_ERUNTIME, std::string("generator: halo tap table mismatch at ") + L.name);
+          if (hm == HALO_CONV3X2) {
+            // per tap: rows (z, co) x K = input channel; 16-bit: a SW128 block of
+            // channels 0..63 then a SW32 block of channels 64..79; fp8: one SW128 block
+            const int rows = 2 * L.cout;
+            const int64_t blk_units = (int64_t)rows * BK + (f8 ? 0 : rows * 16);
+            hg.off = (int64_t)pack.size();
+            pack.resize(pack.size() + (size_t)hg.ntaps * blk_units, 0);
+            for (int tap = 0; tap < hg.ntaps; ++tap) {
+              uint16_t* blk = pack.data() + hg.off + tap * blk_units;
+              for (int r = 0; r < rows; ++r) {
+                const int z = r / L.cout, co = r % L.cout, kx = hg.kx[tap] - z, ky = hg.ky[tap];
+                for (int c = 0; c < L.cin; ++c) {
+                  const float v = (kx >= 0 && kx < 3) ? wat(co, c, ky, kx) : 0.f;
+                  if (f8 || c < 64) {
+                    store(blk, r, c, v, 1.f / sw[co]);
+                  } else {  // SW32: 32-byte rows, 16-byte chunk ^= (row >> 2) & 1
+                    const int j = c - 64;
+                    uint16_t* b32 = blk + rows * BK;
+                    b32[r * 16 + (((j >> 3) ^ ((r >> 2) & 1)) << 3) + (j & 7)] = h->prec == PR_FP16 ? f2h(v) : f2bf(v);
+                  }
+                }
+              }
+            }
+          } else {
           // [cb][tap][cout][KE]: one K block per (channel block of KE channels, tap);
           // macro-pixel stem: rows (pixel offset z, cout), K = (x-shift plane, channel)
           const bool x4 = hm == HALO_STEM4X;
@@ -1067,6 +1104,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                   store(blk, r, j, v, 1.f / sw[co]);
                 }
             }
+          }
         }
         // input channels padded to whole 16-byte granules (8 units)
         const int cin_pad = (L.cin + 8 * cpu - 1) / (8 * cpu) * (8 * cpu);
@@ -1359,7 +1397,10 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.W = in.W;
           hp.C = p.C;
           hp.GH = hg.mode == HALO_CONVT2 ? in.H : OH;
-          hp.GW = hg.mode == HALO_CONVT2 ? in.W : hg.mode == HALO_STEM4X ? (int)ceil_div(OW, 4) : OW;
+          hp.GW = hg.mode == HALO_CONVT2   ? in.W
+                  : hg.mode == HALO_STEM4X ? (int)ceil_div(OW, 4)
+                  : hg.mode == HALO_CONV3X2 ? (int)ceil_div(OW, 2)
+                                            : OW;
           hp.xmul = hg.mode == HALO_STEM4X ? 4 : 1;
           hp.oy0 = hg.oy0;
           hp.ox0 = hg.ox0;
@@ -1371,7 +1412,9 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           // planes come in pairs per K step; an odd last plane reads channels past the
           // view, which the TMA zero-fills (fp8 out0: 80 channels = 5 planes)
           hp.ngran = hg.mode == HALO_STEM4X ? 10 : hp.shift_planes ? 8 : ((p.C / 8 + 1) & ~1);
-          hp.ncb = hg.mode == HALO_CONV3S2 ? hp.ngran / 2 : (hp.ngran + 7) / 8;  // S2: 2 granules x 4 parities
+          hp.ncb = hg.mode == HALO_CONV3S2   ? hp.ngran / 2         // S2: 2 granules x 4 parities
+                   : hg.mode == HALO_CONV3X2 ? (hp.ngran + 3) / 4  // X2: 4 granules x 2 parities
+                                             : (hp.ngran + 7) / 8;
           hp.ntaps = hg.ntaps;
           for (int t = 0; t < MAX_HTAPS; ++t) {
             hp.aoff[t] = hg.aoff[t];
@@ -1379,7 +1422,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           }
           hp.tfirst = hg.tfirst;
           hp.osy = hg.mode == HALO_CONVT2 ? 2 : 1;
-          hp.osx = hg.mode == HALO_CONVT2 ? 2 : hg.mode == HALO_STEM4X ? 4 : 1;
+          hp.osx = hg.mode == HALO_CONVT2 || hg.mode == HALO_CONV3X2 ? 2 : hg.mode == HALO_STEM4X ? 4 : 1;
           for (int z = 0; z < 4; ++z) {
             hp.poy[z] = hg.poy[z];
             hp.pox[z] = hg.pox[z];
@@ -1391,7 +1434,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           if (hg.mode == HALO_CONV3) r.bn = std::min(L.cout, 128);
           hp.ntn = L.cout / r.bn;
           hp.w = h->wpack.p + hg.off;
-          hp.wblocks = hg.mode == HALO_CONV3S2 ? hg.ntaps : hp.ncb * hg.ntaps;  // S2: channel blocks share a block
+          hp.wblocks = (hg.mode == HALO_CONV3S2 || hg.mode == HALO_CONV3X2) ? hg.ntaps  // one block per tap
+                                                                            : hp.ncb * hg.ntaps;
           if (hg.mode == HALO_CONV3S2 && hp.ncb * 32 > 128) fail(LSG_ERUNTIME, "generator: stride-2 halo needs <= 4 channel blocks");
           if (hg.mode != HALO_STEM4X && hg.mode != HALO_STEM7) {  // CTA pairs: weight half-blocks by TMA
             const cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)hp.wblocks * r.bn * hp.ntn};
@@ -1426,6 +1470,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           hp.w1 = p.w1;
           hp.b1 = p.b1;
           if (hg.mode == HALO_CONV3S2) encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, 2, 2);
+          else if (hg.mode == HALO_CONV3X2) encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, 2, 1);
           else encode_patch(&hp.tmap, in, max_batch, hp.pw, hp.ph, hp.xmul);
           const int bc = std::min(r.bn * 2 / cpu, 128) / 2;  // box channels in 16-bit units (128-byte rows max)
           if (!fused) encode_box(&hp.tmap_out, ov, max_batch, bc, HTW * hp.osx, HTH * hp.osy, hp.osx, hp.osy);
