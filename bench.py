@@ -506,7 +506,8 @@ def scaled_leg(args, local, torch, ctx, stream, api):
     chunks = [(base + s * n * 2, n) for s in range(S)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    seg_ms, mel_ms, cuts = [], [], []
+    import ctypes as Cc
+    seg_ms, mel_ms, cuts, k1_ms = [], [], [], []
     with torch.cuda.stream(stream):
         ctx.set_stream(stream.cuda_stream)
         for rep in range(4):
@@ -521,6 +522,9 @@ def scaled_leg(args, local, torch, ctx, stream, api):
             cuts = seg.take_all_cuts()
             if rep:
                 seg_ms.append(e0.elapsed_time(e1))
+                k1 = Cc.c_float()
+                ctx.lib.check(ctx.lib.dll.lsgdbg_seg_k1_ms(seg.h, Cc.byref(k1)))
+                k1_ms.append(k1.value)
         N, hop = 1024, 256
         offs = [c.stream * n + c.sample_off for c in cuts]
         lens = [c.sample_len for c in cuts]
@@ -617,7 +621,15 @@ def scaled_leg(args, local, torch, ctx, stream, api):
                       "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
                       "frac": nbytes / (t_seg / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0), "segments": len(cuts),
                       "timed": "lsg_seg_push + lsg_seg_finish over all streams (device events, includes the cut "
-                               "readback sync)"},
+                               "readback sync)",
+                      # K1 alone: the HBM-streaming pass (2 B/sample in, 16 B per 20 ms frame out); the
+                      # rest of the call is the per-stream sequential decaying-peak scan (K2) and cut collection
+                      "frame_stats_kernel": ({"ms": float(np.median(k1_ms)),
+                                              "achieved": (nbytes + nbytes // 640 * 16) / (float(np.median(k1_ms)) / 1e3) / 1e9,
+                                              "frac": (nbytes + nbytes // 640 * 16) / (float(np.median(k1_ms)) / 1e3) / 1e9
+                                              / peaks.get("hbm_gbs", 6650.0),
+                                              "timed": "CUDA events around the K1 launch inside lsg_seg_push"}
+                                             if k1_ms else None)},
         "align": {"energy_envelope": {"bound": "hbm", "ms": float(np.median(en_ms)),
                                       "bytes": nbytes + S * secs * 1000 * 8,
                                       "achieved": (nbytes + S * secs * 1000 * 8) / (float(np.median(en_ms)) / 1e3) / 1e9,

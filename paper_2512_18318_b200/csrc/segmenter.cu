@@ -77,7 +77,8 @@ struct alignas(16) FrameStat {
 
 // ---------------------------------------------------------------- K1 -----
 constexpr int K1_WARPS = 8;
-constexpr int K1_FPW = 2;  // frames per warp per block
+constexpr int K1_FPW = 4;  // frames per warp per block
+constexpr int K1_MAXV = 2;  // int4 per lane per frame held in registers (frames up to 512 samples)
 
 // 8 samples: squares summed pairwise in uint32 (each pair <= 2^31, exact),
 // one 64-bit add per pair; max |s| from packed int16 max/min (exact for
@@ -112,8 +113,32 @@ seg_frame_stats(const Chunk* __restrict__ chunks, const int16_t* __restrict__ ca
   int mx[K1_FPW];
 #pragma unroll
   for (int j = 0; j < K1_FPW; ++j) { ss[j] = 0; mx[j] = 0; }
-  if (vec) {
-    const int nv = fs >> 3;  // int4 per frame
+  const int nv = fs >> 3;  // int4 per frame
+  if (vec && nv <= 32 * K1_MAXV) {
+    // every load of the warp's frames in flight before any is consumed (a
+    // 320-sample frame is 40 int4: lanes 0-7 take two); zero padding adds
+    // nothing to the sum of squares or to |max|
+    int4 buf[K1_FPW][K1_MAXV];
+#pragma unroll
+    for (int j = 0; j < K1_FPW; ++j) {
+      const int4* p = reinterpret_cast<const int4*>(c.pcm + (f0 + j) * fs);
+      const bool live = f0 + j < c.nframes;
+#pragma unroll
+      for (int k = 0; k < K1_MAXV; ++k) {
+        const int q = lane + 32 * k;
+        buf[j][k] = (live && q < nv) ? __ldg(p + q) : make_int4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K1_FPW; ++j) {
+      unsigned long long s2 = 0;
+      unsigned pmax = 0x80008000u, pmin = 0x7fff7fffu;
+#pragma unroll
+      for (int k = 0; k < K1_MAXV; ++k) acc8(buf[j][k], s2, pmax, pmin);
+      ss[j] = (long long)s2;
+      mx[j] = absmax_packed(pmax, pmin);
+    }
+  } else if (vec) {
     // issue every load of the warp's frames before reducing (memory-level parallelism)
 #pragma unroll
     for (int j = 0; j < K1_FPW; ++j) {
@@ -651,7 +676,13 @@ struct lsg_seg_s {
   lsg_cut* h_cuts = nullptr;
   uint32_t* h_flags = nullptr;
   int64_t h_cut_cap = 0;
+  // device time of the last push's K1 (the HBM-streaming pass), for the
+  // benchmark's per-kernel roofline (lsgdbg_seg_k1_ms)
+  cudaEvent_t k1a = nullptr, k1b = nullptr;
+  bool k1_recorded = false;
   ~lsg_seg_s() {
+    if (k1a) cudaEventDestroy(k1a);
+    if (k1b) cudaEventDestroy(k1b);
     if (h_state) cudaFreeHost(h_state);
     if (h_off) cudaFreeHost(h_off);
     if (h_cuts) cudaFreeHost(h_cuts);
@@ -800,6 +831,17 @@ lsg_status lsg_seg_reset(lsg_seg h) {
   });
 }
 
+// Device time (ms) of the last push's frame-statistics kernel (K1).
+lsg_status lsgdbg_seg_k1_ms(lsg_seg h, float* ms) {
+  return guard([&] {
+    if (!h || !ms) invalid("lsgdbg_seg_k1_ms: null argument");
+    if (!h->k1_recorded) logic("lsgdbg_seg_k1_ms: no push with frames yet");
+    DeviceGuard g(h->ctx);
+    LSG_CUDA(cudaEventSynchronize(h->k1b));
+    LSG_CUDA(cudaEventElapsedTime(ms, h->k1a, h->k1b));
+  });
+}
+
 lsg_status lsg_seg_destroy(lsg_seg h) {
   return guard([&] {
     if (!h) return;
@@ -882,9 +924,16 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
                              cudaMemcpyHostToDevice, ctx->stream));
     if (max_frames > 0) {
       dim3 grid((unsigned)ceil_div(max_frames, K1_WARPS * K1_FPW), (unsigned)nc);
+      if (!h->k1a) {
+        LSG_CUDA(cudaEventCreate(&h->k1a));
+        LSG_CUDA(cudaEventCreate(&h->k1b));
+      }
+      LSG_CUDA(cudaEventRecord(h->k1a, ctx->stream));
       seg_frame_stats<<<grid, K1_WARPS * 32, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, P.fs,
                                                                h->stats.p);
       LSG_LAUNCHED(ctx);
+      LSG_CUDA(cudaEventRecord(h->k1b, ctx->stream));
+      h->k1_recorded = true;
     }
     seg_scan<<<nc, K2_THREADS, 0, ctx->stream>>>(h->chunks_dev.p, h->stats.p, h->st.p, h->cuts.p,
                                                  h->flags.p, P);
