@@ -1,6 +1,6 @@
-# Round-1 final record: tests, smoke, bench, launch lists, full captures of the top layers.
+# Round-1 final record (r01f: + faster segmenter K1): tests, smoke, bench, launch lists, full captures of the top layers.
 set -x
-O=gpurun_out/r01e
+O=gpurun_out/r01f
 mkdir -p $O
 timeout 1300 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
