@@ -50,25 +50,35 @@ constexpr int S_STRIDE = 33;                       // padded row (complex) for t
 constexpr int S_CPLX = 16 * S_STRIDE;              // 528 complex per warp (the power spectrum aliases it)
 constexpr size_t SMEM_PER_WARP = S_CPLX * 16;
 
+// Filterbank schedule entry: the 80 triangles are dealt to the 32 lanes by
+// longest-band-first balancing, so a warp runs max(lane load) ~ 37 steps
+// instead of one pass per 32 mels at the widest band of each pass (~67).
+// code = bin | mel << 16 | end-of-band << 31.  Weights and codes are kept
+// as separate planes (3 shared-memory wavefronts per step instead of 4).
+struct FbEntry {
+  double w;
+  int32_t code;
+};
+
 // Block-shared tables of the 1024 fast path (staged once per CTA, so the
 // per-frame loop never reads tables through L1 with divergent addresses).
 struct FastTables {
   const double* window;   // [1024]
   const cplx* tw;         // [512] W512^j
   const cplx* tw_half;    // [513] W1024^k
-  const int32_t* band_lo; // [M]
-  const int32_t* band_n;  // [M]
-  const double* fbq;      // [maxnb][M]: weight q of band m (0 past the band)
-  int maxnb;
+  const double* fb_w;     // [nsteps][32] per-lane filterbank schedule: weights
+  const int32_t* fb_code; // [nsteps][32] codes
+  int nsteps;
 };
-__host__ __device__ constexpr size_t fast_table_bytes(int M, int maxnb) {
+__host__ __device__ constexpr size_t fast_table_bytes(int nsteps) {
   return 1024 * 8                 // window
          + 16 * 32 * 16           // step-1 twiddles per (k1, lane)
          + 32 * 16                // W512^(16 c), c < 32 (W32^c; W16^e = W32^(2e))
          + 264 * 16               // real-split twiddles k <= 256
-         + (size_t)maxnb * M * 8  // filterbank, q-major
-         + (size_t)M * 8;         // band lo | n
+         + (size_t)nsteps * 32 * 12;
 }
+constexpr int ACC_OFF = 520;  // band sums live past P[0..512] in the warp's buffer
+constexpr int FAST_MAX_MELS = 2 * S_CPLX - ACC_OFF;
 
 struct Batch {
   const int16_t* pcm;
@@ -133,17 +143,17 @@ __global__ void __launch_bounds__(MEL_WARPS * 32, 1)
 mel1024_kernel(Batch B, FastTables T) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = B.n_mels, maxnb = T.maxnb;
+  const int M = B.n_mels, nsteps = T.nsteps;
   // ---- block tables
   double* s_win = reinterpret_cast<double*>(smem);
   cplx* s_tw1 = reinterpret_cast<cplx*>(s_win + 1024);   // [16][32]
   cplx* s_w32 = s_tw1 + 16 * 32;                         // [32]
   cplx* s_twh = s_w32 + 32;                              // [264]
-  double* s_fbq = reinterpret_cast<double*>(s_twh + 264);  // [maxnb][M]
-  int32_t* s_blo = reinterpret_cast<int32_t*>(s_fbq + (size_t)maxnb * M);
-  int32_t* s_bn = s_blo + M;
-  cplx* S = reinterpret_cast<cplx*>(smem + fast_table_bytes(M, maxnb)) + warp * S_CPLX;
+  double* s_fbw = reinterpret_cast<double*>(s_twh + 264);  // [nsteps][32]
+  int32_t* s_fbc = reinterpret_cast<int32_t*>(s_fbw + nsteps * 32);
+  cplx* S = reinterpret_cast<cplx*>(smem + fast_table_bytes(nsteps)) + warp * S_CPLX;
   double* P = reinterpret_cast<double*>(S);  // |X|^2 after the spectrum has been read
+  double* s_acc = P + ACC_OFF;               // [M] band sums
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_win[i] = __ldg(T.window + i);
   for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {
     const int k1 = i >> 5, l = i & 31;
@@ -158,10 +168,9 @@ mel1024_kernel(Batch B, FastTables T) {
     const double2 d = __ldg(reinterpret_cast<const double2*>(T.tw_half) + i);
     s_twh[i] = {d.x, d.y};
   }
-  for (int i = threadIdx.x; i < maxnb * M; i += blockDim.x) s_fbq[i] = __ldg(T.fbq + i);
-  for (int i = threadIdx.x; i < M; i += blockDim.x) {
-    s_blo[i] = __ldg(T.band_lo + i);
-    s_bn[i] = __ldg(T.band_n + i);
+  for (int i = threadIdx.x; i < nsteps * 32; i += blockDim.x) {
+    s_fbw[i] = __ldg(T.fb_w + i);
+    s_fbc[i] = __ldg(T.fb_code + i);
   }
   __syncthreads();
   // Each warp takes a contiguous run of frames: one binary search for the
@@ -182,12 +191,22 @@ mel1024_kernel(Batch B, FastTables T) {
     const int16_t* x = B.pcm + __ldg(B.seg_pcm_off + s) + j * B.hop;
     // ---- step 1: lane m2 = lane; z[32*m1 + m2] = (x[64 m1 + 2 m2], x[64 m1 + 2 m2 + 1])
     cplx v[16];
+    const bool al4 = (reinterpret_cast<uintptr_t>(x) & 3) == 0;  // warp-uniform: one 4 B load per pair
 #pragma unroll
     for (int m1 = 0; m1 < 16; ++m1) {
       const int i0 = 64 * m1 + 2 * lane;
-      const double s0 = (double)__ldg(x + i0), s1 = (double)__ldg(x + i0 + 1);
-      v[m1].x = __dmul_rn(s0 * (1.0 / 32768.0), s_win[i0]);
-      v[m1].y = __dmul_rn(s1 * (1.0 / 32768.0), s_win[i0 + 1]);
+      double s0, s1;
+      if (al4) {
+        const int pr = __ldg(reinterpret_cast<const int*>(x + i0));
+        s0 = (double)(int16_t)(pr & 0xffff);
+        s1 = (double)(pr >> 16);
+      } else {
+        s0 = (double)__ldg(x + i0);
+        s1 = (double)__ldg(x + i0 + 1);
+      }
+      const double2 wp = *reinterpret_cast<const double2*>(s_win + i0);
+      v[m1].x = __dmul_rn(s0 * (1.0 / 32768.0), wp.x);
+      v[m1].y = __dmul_rn(s1 * (1.0 / 32768.0), wp.y);
     }
     dft16s(v, s_w32);
     {
@@ -253,12 +272,26 @@ mel1024_kernel(Batch B, FastTables T) {
       }
     }
     __syncwarp();
-    // ---- step 4: sparse filterbank + log (mel.cpp:119-124), bin order, unfused
+    // ---- step 4: sparse filterbank (mel.cpp:119-122), each band summed in
+    // bin order with unfused mul/add from 0.0 (the reference's own summation;
+    // the zero weights it also adds contribute +0.0 exactly); bands dealt
+    // across lanes by the host schedule, sums parked in shared memory
+    {
+      double acc = 0.0;
+      for (int t = 0; t < nsteps; ++t) {
+        const int code = s_fbc[t * 32 + lane];
+        acc = __dadd_rn(acc, __dmul_rn(s_fbw[t * 32 + lane], P[code & 0xffff]));
+        if (code < 0) {
+          s_acc[(code >> 16) & 0x7fff] = acc;
+          acc = 0.0;
+        }
+      }
+    }
+    __syncwarp();
+    // (float)ln(max(acc, 1e-10)) (mel.cpp:123), coalesced row store
     float* orow = B.out + (__ldg(B.seg_out_row + s) + j) * M;
     for (int m = lane; m < M; m += 32) {
-      const int lo = s_blo[m], nb = s_bn[m];
-      double acc = 0.0;
-      for (int q = 0; q < nb; ++q) acc = __dadd_rn(acc, __dmul_rn(s_fbq[q * M + m], P[lo + q]));
+      const double acc = s_acc[m];
       orow[m] = (float)log(acc > 1e-10 ? acc : 1e-10);
     }
     __syncwarp();
@@ -357,7 +390,8 @@ struct lsg_mel_s {
   DevBuf<float> out_stage;
   Tables T{};
   // fast path (fft 1024): q-major filterbank + block-shared tables
-  DevBuf<double> fbq;
+  DevBuf<double> fb_w;
+  DevBuf<int32_t> fb_code;
   FastTables FT{};
   bool fast = false;
   size_t fast_smem = 0;
@@ -456,12 +490,32 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
           for (int b = first; b <= last; ++b) wts.push_back(row[b]);
         }
       }
-      // fast path (fft 1024): q-major filterbank [maxnb][M]; its block tables
-      // + per-warp buffers must fit in shared memory, else the generic kernel
-      int maxnb = 0;
-      for (int m = 0; m < M; ++m) maxnb = std::max(maxnb, bn[m]);
-      h->fast_smem = fast_table_bytes(M, maxnb) + MEL_WARPS * SMEM_PER_WARP;
-      h->fast = N == 1024 && h->fast_smem <= 227 * 1024;
+      // fast path (fft 1024): per-lane filterbank schedule (longest band
+      // first onto the least-loaded lane; an empty band is one w = 0 entry
+      // so it still ends at +0.0 -> ln(1e-10)); its block tables + per-warp
+      // buffers must fit in shared memory, else the generic kernel
+      std::vector<std::vector<FbEntry>> lanes(32);
+      {
+        std::vector<int> order(M);
+        for (int m = 0; m < M; ++m) order[m] = m;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bn[a] > bn[b]; });
+        for (int m : order) {
+          size_t best = 0;
+          for (size_t l = 1; l < lanes.size(); ++l)
+            if (lanes[l].size() < lanes[best].size()) best = l;
+          const int n = std::max(bn[m], 1);
+          for (int q = 0; q < n; ++q) {
+            FbEntry e{};
+            e.w = bn[m] ? wts[(size_t)boff[m] + q] : 0.0;
+            e.code = (bn[m] ? blo[m] + q : 0) | (m << 16) | (q == n - 1 ? int32_t(0x80000000u) : 0);
+            lanes[best].push_back(e);
+          }
+        }
+      }
+      int nsteps = 0;
+      for (auto& l : lanes) nsteps = std::max(nsteps, (int)l.size());
+      h->fast_smem = fast_table_bytes(nsteps) + MEL_WARPS * SMEM_PER_WARP;
+      h->fast = N == 1024 && M <= FAST_MAX_MELS && h->fast_smem <= 227 * 1024;
       // twiddles: fast path W512^j, generic path W_N^j; real split W_N^k
       const int half = N / 2;
       std::vector<cplx> tw, twh(half + 1);
@@ -501,12 +555,20 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
       h->pcm_stage.alloc((size_t)max_samples);
       h->out_stage.alloc((size_t)max_frames * M);
       if (h->fast) {
-        std::vector<double> fbq((size_t)std::max(maxnb, 1) * M, 0.0);
-        for (int m = 0; m < M; ++m)
-          for (int q = 0; q < bn[m]; ++q) fbq[(size_t)q * M + m] = wts[(size_t)boff[m] + q];
-        h->fbq.alloc(fbq.size());
-        LSG_CUDA(cudaMemcpy(h->fbq.p, fbq.data(), fbq.size() * 8, cudaMemcpyHostToDevice));
-        h->FT = {h->window.p, h->tw.p, h->tw_half.p, h->band.p, h->band.p + M, h->fbq.p, maxnb};
+        // [nsteps][32]; a lane's tail past its last band is w = 0 padding
+        const size_t ns = (size_t)std::max(nsteps, 1) * 32;
+        std::vector<double> fw(ns, 0.0);
+        std::vector<int32_t> fc(ns, 0);
+        for (int l = 0; l < 32; ++l)
+          for (size_t t = 0; t < lanes[l].size(); ++t) {
+            fw[t * 32 + l] = lanes[l][t].w;
+            fc[t * 32 + l] = lanes[l][t].code;
+          }
+        h->fb_w.alloc(ns);
+        h->fb_code.alloc(ns);
+        LSG_CUDA(cudaMemcpy(h->fb_w.p, fw.data(), ns * 8, cudaMemcpyHostToDevice));
+        LSG_CUDA(cudaMemcpy(h->fb_code.p, fc.data(), ns * 4, cudaMemcpyHostToDevice));
+        h->FT = {h->window.p, h->tw.p, h->tw_half.p, h->fb_w.p, h->fb_code.p, nsteps};
         LSG_CUDA(cudaFuncSetAttribute(mel1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)h->fast_smem));
       } else {

@@ -76,8 +76,14 @@ struct alignas(16) FrameStat {
 };
 
 // ---------------------------------------------------------------- K1 -----
-constexpr int K1_WARPS = 8;
-constexpr int K1_FPW = 4;  // frames per warp per block
+#ifndef LSG_K1_WARPS
+#define LSG_K1_WARPS 8
+#endif
+#ifndef LSG_K1_FPW
+#define LSG_K1_FPW 4
+#endif
+constexpr int K1_WARPS = LSG_K1_WARPS;
+constexpr int K1_FPW = LSG_K1_FPW;  // frames per warp per block
 constexpr int K1_MAXV = 2;  // int4 per lane per frame held in registers (frames up to 512 samples)
 
 // 8 samples: squares summed pairwise in uint32 (each pair <= 2^31, exact),
