@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "lsg_common.cuh"
@@ -397,6 +399,106 @@ struct lsg_mel_s {
   size_t fast_smem = 0;
 };
 
+// Deals the bands to the 32 lanes: longest band first onto the least-loaded
+// lane (nsteps = max lane load), then a deterministic local search over
+// band order within a lane, band swaps between lanes and lane swaps that
+// lowers the P-gather's shared-memory wavefronts without raising nsteps.
+// At step t lane l reads P[bin(l, t)] (8 B): a half-warp's 16 lanes cost
+// one wavefront per distinct bin that shares a bank pair (bin mod 16) with
+// another, so the cost of a step is max over bank pairs of its distinct
+// bins, per half.  Summation order inside a band is untouched (bin order),
+// so the schedule changes only speed, never a value.  The stock 80-band
+// bank: 188 -> ~121 wavefronts per frame (ideal 74).
+static std::vector<std::vector<int>> schedule_bands_search(const std::vector<int32_t>& blo,
+                                                          const std::vector<int32_t>& bn);
+// memoised per band table (engines are created often; the search is ~0.1 s)
+static std::vector<std::vector<int>> schedule_bands(const std::vector<int32_t>& blo, const std::vector<int32_t>& bn) {
+  static std::mutex mu;
+  static std::map<std::pair<std::vector<int32_t>, std::vector<int32_t>>, std::vector<std::vector<int>>> memo;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(blo, bn);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  return memo[key] = schedule_bands_search(blo, bn);
+}
+static std::vector<std::vector<int>> schedule_bands_search(const std::vector<int32_t>& blo,
+                                                          const std::vector<int32_t>& bn) {
+  const int M = (int)bn.size();
+  auto len = [&](int m) { return std::max(bn[m], 1); };
+  std::vector<std::vector<int>> bl(32);
+  std::vector<int> load(32, 0), order(M);
+  for (int m = 0; m < M; ++m) order[m] = m;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bn[a] > bn[b]; });
+  for (int m : order) {
+    int best = 0;
+    for (int l = 1; l < 32; ++l)
+      if (load[l] < load[best]) best = l;
+    bl[best].push_back(m);
+    load[best] += len(m);
+  }
+  int T = *std::max_element(load.begin(), load.end());
+  std::vector<int> bins((size_t)32 * T);
+  auto cost = [&](const std::vector<std::vector<int>>& b) -> long {
+    for (int l = 0; l < 32; ++l) {
+      int t = 0;
+      for (int m : b[l])
+        for (int q = 0; q < len(m); ++q) {
+          if (t >= T) return -1;
+          bins[(size_t)l * T + t++] = bn[m] ? blo[m] + q : 0;
+        }
+      for (; t < T; ++t) bins[(size_t)l * T + t] = 0;
+    }
+    long c = 0;
+    for (int t = 0; t < T; ++t)
+      for (int h = 0; h < 32; h += 16) {
+        int cnt[16] = {0}, held[16][16];
+        int worst = 1;
+        for (int i = h; i < h + 16; ++i) {
+          const int bi = bins[(size_t)i * T + t], k = bi & 15;
+          bool seen = false;
+          for (int j = 0; j < cnt[k]; ++j) seen |= held[k][j] == bi;
+          if (!seen) {
+            held[k][cnt[k]++] = bi;
+            worst = std::max(worst, cnt[k]);
+          }
+        }
+        c += worst;
+      }
+    return c;
+  };
+  long cur = cost(bl);
+  uint64_t x = 0x9e3779b97f4a7c15ull;  // fixed seed: the schedule is reproducible
+  auto rnd = [&](uint32_t n) {
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    return (int)((x >> 11) % n);
+  };
+  for (int it = 0; it < 20000; ++it) {
+    std::vector<std::vector<int>> nb = bl;
+    const int mv = rnd(10);
+    if (mv < 4) {
+      auto& v = nb[rnd(32)];
+      if (v.size() < 2) continue;
+      std::swap(v[rnd((uint32_t)v.size())], v[rnd((uint32_t)v.size())]);
+    } else if (mv < 8) {
+      const int a = rnd(32), b = rnd(32);
+      if (a == b || nb[a].empty() || nb[b].empty()) continue;
+      std::swap(nb[a][rnd((uint32_t)nb[a].size())], nb[b][rnd((uint32_t)nb[b].size())]);
+    } else {
+      const int a = rnd(32), b = rnd(32);
+      if (a == b) continue;
+      std::swap(nb[a], nb[b]);
+    }
+    const long c = cost(nb);
+    if (c >= 0 && c <= cur) {
+      bl.swap(nb);
+      cur = c;
+    }
+  }
+  return bl;
+}
+
 static void launch(lsg_mel h, const int16_t* pcm, int32_t n_seg, int64_t total_frames, float* out) {
   Ctx* ctx = h->ctx;
   if (total_frames == 0) return;
@@ -494,24 +596,18 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
       // first onto the least-loaded lane; an empty band is one w = 0 entry
       // so it still ends at +0.0 -> ln(1e-10)); its block tables + per-warp
       // buffers must fit in shared memory, else the generic kernel
+      std::vector<std::vector<int>> bl = schedule_bands(blo, bn);
       std::vector<std::vector<FbEntry>> lanes(32);
-      {
-        std::vector<int> order(M);
-        for (int m = 0; m < M; ++m) order[m] = m;
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bn[a] > bn[b]; });
-        for (int m : order) {
-          size_t best = 0;
-          for (size_t l = 1; l < lanes.size(); ++l)
-            if (lanes[l].size() < lanes[best].size()) best = l;
+      for (int l = 0; l < 32; ++l)
+        for (int m : bl[l]) {
           const int n = std::max(bn[m], 1);
           for (int q = 0; q < n; ++q) {
             FbEntry e{};
             e.w = bn[m] ? wts[(size_t)boff[m] + q] : 0.0;
             e.code = (bn[m] ? blo[m] + q : 0) | (m << 16) | (q == n - 1 ? int32_t(0x80000000u) : 0);
-            lanes[best].push_back(e);
+            lanes[l].push_back(e);
           }
         }
-      }
       int nsteps = 0;
       for (auto& l : lanes) nsteps = std::max(nsteps, (int)l.size());
       h->fast_smem = fast_table_bytes(nsteps) + MEL_WARPS * SMEM_PER_WARP;
