@@ -58,7 +58,10 @@ def test_short_and_silent():
 
 
 @pytest.mark.parametrize("fft,hop,n_mels,fmax", [(512, 128, 40, 8000.0), (2048, 256, 80, 7600.0),
-                                                 (1024, 160, 64, 4000.0)])
+                                                 (1024, 160, 64, 4000.0),
+                                                 # fast path, band schedules with 1-2 bin and
+                                                 # empty bands (-> ln 1e-10) and a single band
+                                                 (1024, 256, 512, 8000.0), (1024, 256, 1, 8000.0)])
 def test_other_configs(reference, fft, hop, n_mels, fmax):
     cfg = api.MelConfig(16000, fft, hop, n_mels, 0.0, fmax)
     pcm = reference.render_pattern(Pattern(), 3000)
