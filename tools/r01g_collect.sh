@@ -1,6 +1,6 @@
 # Round-1 record r01g (+ scheduled mel filterbank): tests, smoke, bench (both arms), bench launch list.
 set -x
-O=gpurun_out/r01g
+O=${O:-gpurun_out/r01g}
 mkdir -p $O
 timeout 1300 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
