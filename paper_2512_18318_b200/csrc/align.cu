@@ -68,14 +68,27 @@ __global__ void __launch_bounds__(EW * 32) energy_kernel(const int16_t* __restri
   if ((((uintptr_t)(x + s_begin)) & 15) == 0 && (hop_samples & 7) == 0) {
     const int4* src = reinterpret_cast<const int4*>(x + s_begin);
     const int nv = (int)(cnt >> 3), per_row = hop_samples >> 3;
-    for (int q = lane; q < nv; q += 32) {
-      const int4 v = __ldg(src + q);
-      const int r = q / per_row, c = (q - r * per_row) * 8;
-      uint32_t* d = reinterpret_cast<uint32_t*>(buf + r * row + c);  // 4-byte aligned (row is even)
-      d[0] = (uint32_t)v.x;
-      d[1] = (uint32_t)v.y;
-      d[2] = (uint32_t)v.z;
-      d[3] = (uint32_t)v.w;
+    // 8 loads per lane in flight before any store (a load-store loop
+    // serialised one DRAM round trip per 512 B of the warp's 10 KB)
+    for (int q0 = 0; q0 < nv; q0 += 32 * 8) {
+      int4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + lane + 32 * u;
+        if (q < nv) v[u] = __ldg(src + q);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = q0 + lane + 32 * u;
+        if (q < nv) {
+          const int r = q / per_row, c = (q - r * per_row) * 8;
+          uint32_t* d = reinterpret_cast<uint32_t*>(buf + r * row + c);  // 4-byte aligned (row is even)
+          d[0] = (uint32_t)v[u].x;
+          d[1] = (uint32_t)v[u].y;
+          d[2] = (uint32_t)v[u].z;
+          d[3] = (uint32_t)v[u].w;
+        }
+      }
     }
     for (int64_t i = (int64_t)nv * 8 + lane; i < cnt; i += 32) buf[(i / hop_samples) * row + i % hop_samples] = __ldg(x + s_begin + i);
   } else {
