@@ -213,13 +213,12 @@ using namespace lsg::align;
 namespace {
 
 // stream-ordered scratch for the per-call tables (pooled by the driver)
+// The context's grow-only scratch, held (mutex) until the call has
+// synchronised its stream and returns.
 struct Scratch {
+  std::unique_lock<std::mutex> lk;
   void* p = nullptr;
-  cudaStream_t st;
-  Scratch(size_t bytes, cudaStream_t s) : st(s) { LSG_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s)); }
-  ~Scratch() {
-    if (p) cudaFreeAsync(p, st);
-  }
+  Scratch(Ctx* c, size_t bytes) : lk(c->scratch_mu) { p = c->scratch_get(std::max<size_t>(bytes, 16)); }
 };
 
 }  // namespace
@@ -251,7 +250,7 @@ lsg_status lsg_align_energy(lsg_ctx ctx, int32_t n, const int16_t* pcm_base, con
     tab[5 * (size_t)n] = chunks;
     if (chunks == 0) return;
     DeviceGuard g(ctx);
-    Scratch sc(tab.size() * 8, ctx->stream);
+    Scratch sc(ctx, tab.size() * 8);
     LSG_CUDA(cudaMemcpyAsync(sc.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
     const size_t smem = (size_t)EW * 32 * (hop + 2) * sizeof(int16_t);
     if (smem > 48 * 1024)
@@ -284,7 +283,7 @@ lsg_status lsg_align_motion(lsg_ctx ctx, int32_t n, const int64_t* ts_base, cons
     tab[6 * (size_t)n] = ms;
     if (ms == 0) return;
     DeviceGuard g(ctx);
-    Scratch sc(tab.size() * 8, ctx->stream);
+    Scratch sc(ctx, tab.size() * 8);
     LSG_CUDA(cudaMemcpyAsync(sc.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
     motion_kernel<<<(unsigned)ceil_div(ms, 256), 256, 0, ctx->stream>>>(ts_base, motion_base,
                                                                         static_cast<int64_t*>(sc.p), n, ms, out_base);
@@ -309,7 +308,7 @@ lsg_status lsg_align_batch(lsg_ctx ctx, int32_t n, const double* energy_base, co
       tab[3 * n + i] = m_len[i];
     }
     DeviceGuard g(ctx);
-    Scratch sc(tab.size() * 8 + (size_t)n * sizeof(lsg_align_result), ctx->stream);
+    Scratch sc(ctx, tab.size() * 8 + (size_t)n * sizeof(lsg_align_result));
     int64_t* dtab = static_cast<int64_t*>(sc.p);
     lsg_align_result* dres = reinterpret_cast<lsg_align_result*>(dtab + tab.size());
     LSG_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, ctx->stream));

@@ -68,6 +68,7 @@ lsg_status lsg_ctx_destroy(lsg_ctx ctx) {
     {
       DeviceGuard g(ctx);
       cudaStreamSynchronize(ctx->stream);
+      if (ctx->scratch) cudaFree(ctx->scratch);
       if (ctx->own) cudaStreamDestroy(ctx->own);
     }
     delete ctx;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -45,6 +46,24 @@ struct Ctx {
   std::atomic<int64_t> launches{0};
   void note_launch() { launches.fetch_add(1, std::memory_order_relaxed); }
   void sync() { LSG_CUDA(cudaStreamSynchronize(stream)); }
+  // grow-only device scratch for calls that stage a per-call table and
+  // synchronise before returning (align.cu): no allocation per call
+  std::mutex scratch_mu;
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* scratch_get(size_t bytes) {
+    if (bytes > scratch_bytes) {
+      if (scratch) {
+        sync();
+        LSG_CUDA(cudaFree(scratch));
+        scratch = nullptr;
+        scratch_bytes = 0;
+      }
+      LSG_CUDA(cudaMalloc(&scratch, bytes));
+      scratch_bytes = bytes;
+    }
+    return scratch;
+  }
 };
 
 // Makes the context's device current for the calling host thread.
