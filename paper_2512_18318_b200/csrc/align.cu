@@ -44,7 +44,7 @@ __device__ __forceinline__ int find_seg(const int64_t* __restrict__ first, int n
 // One warp per 32 consecutive hops of one segment: the warp stages the
 // chunk's PCM into shared memory with coalesced loads (16-byte vectors when
 // aligned), then each lane sums its own hop in the reference's order.
-constexpr int EW = 8;  // warps per CTA
+constexpr int EW = 4;  // warps per CTA (41 KB staged: 5 CTAs = 20 warps per SM)
 __global__ void __launch_bounds__(EW * 32) energy_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ tab,
                                                          int n, int64_t total_chunks, int hop_samples,
                                                          double* __restrict__ out) {
@@ -68,17 +68,17 @@ __global__ void __launch_bounds__(EW * 32) energy_kernel(const int16_t* __restri
   if ((((uintptr_t)(x + s_begin)) & 15) == 0 && (hop_samples & 7) == 0) {
     const int4* src = reinterpret_cast<const int4*>(x + s_begin);
     const int nv = (int)(cnt >> 3), per_row = hop_samples >> 3;
-    // 8 loads per lane in flight before any store (a load-store loop
+    // 16 loads per lane in flight before any store (a load-store loop
     // serialised one DRAM round trip per 512 B of the warp's 10 KB)
-    for (int q0 = 0; q0 < nv; q0 += 32 * 8) {
-      int4 v[8];
+    for (int q0 = 0; q0 < nv; q0 += 32 * 16) {
+      int4 v[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const int q = q0 + lane + 32 * u;
         if (q < nv) v[u] = __ldg(src + q);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         const int q = q0 + lane + 32 * u;
         if (q < nv) {
           const int r = q / per_row, c = (q - r * per_row) * 8;
