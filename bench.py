@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: lip-sync frames/sec of the full GPU hot path (BASELINE.json
-metric; config 5 "full queue-decoupled pipeline (segmenter->mel->generator)",
-unpaced).
+metric; config 5 "full queue-decoupled pipeline (segmenter->mel->generator),
+256 streams at 25 fps, scaling at 1/2/4/8 GPUs with p50/p99 segment latency").
 
 One step = lsg_pipe_run over this rank's streams: segment every stream,
 log-mel every segment, gather each segment's 25 fps face crops with the
@@ -10,11 +10,19 @@ log-mel every segment, gather each segment's 25 fps face crops with the
          frames left on the device), device time with CUDA events;
   e2e    the same call with pinned HOST inputs and the rendered u8 frames
          copied back to host inside the timed region.
-Multi-GPU: one process per GPU, streams sharded (weak scaling: the per-GPU
-stream count is fixed), no data-path collective; the step time is the max
-over ranks (NCCL all-reduce of the timing only).
+Multi-GPU: one process per GPU; the job's --streams (default 256, config 5)
+are sharded s mod N (strong scaling: total work fixed), no data-path
+collective; the step time is the max over ranks (NCCL all-reduce of the
+timing only).  `--gpus N` without a torchrun environment re-launches itself
+under torch.distributed.run with N ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+The reference arm (--impl reference) imports nothing from the product
+package: it times the reference's own Segmenter + compute_mel (oracle/_ref,
+compiled unmodified from /root/reference's sources) and the fp32 CPU
+restatement of the generator (oracle/generator_ref.py; the reference itself
+only has a cost model) on the host's cores.
 """
 from __future__ import annotations
 
@@ -33,6 +41,8 @@ sys.path.insert(0, ROOT)
 
 M64 = (1 << 64) - 1
 FLOPS_PER_FRAME = 7.933968384e9  # generator.flops_per_frame(), SURVEY §0.6
+# BASELINE.json "metric", printed verbatim by both arms
+METRIC = "lip-sync frames/sec at 1/2/4/8 B200 (96\u00d796); p50 per-segment latency ms"
 
 
 def splitmix64(st):
@@ -62,7 +72,8 @@ def stream_pattern(seed: int):
 def make_workload(rank: int, n_streams: int, seconds: int, fps: float, api, generator, world: int = 1,
                   seed_base: int = 0):
     """Host inputs of one rank: PCM, per-frame face crops, reference crops of
-    the streams it owns (global stream s lives on GPU s mod world)."""
+    the streams it owns out of the job's n_streams (global stream s lives on
+    GPU s mod world)."""
     from paper_2512_18318_b200.shard import streams_for_rank
     pcm, video, refs = [], [], []
     for sid in streams_for_rank(n_streams, rank, world):
@@ -137,26 +148,29 @@ def measured_peaks():
 
 
 def cpu_reference_step(n_streams: int, seconds: int, gen_frames: int, threads: int):
-    """The reference's CPU path on a bounded sample: the reference's own
-    Segmenter + compute_mel (oracle/_ref, compiled from /root/reference's
-    sources) on `n_streams` x `seconds` streams, one stream per thread, and
-    the fp32 CPU restatement of the generator (oracle/generator_ref.py; the
-    reference only has a cost model) on `gen_frames` frames with all host
-    threads.  Returns (frames/s, details)."""
+    """The reference's CPU path on a bounded sample, importing nothing from
+    the product package: the reference's own render_pattern, Segmenter and
+    compute_mel (oracle/_ref, compiled unmodified from /root/reference's
+    sources) on `n_streams` x `seconds` streams of the bench's stream
+    patterns, one stream per thread; and the fp32 CPU restatement of the
+    generator (oracle/generator_ref.py; the reference only has a cost model)
+    on `gen_frames` frames with all host threads, He-normal weights (the
+    CPU time does not depend on their values).  frames/s = frames the
+    segments gather / (seg+mel time + frames x generator time per frame).
+    Returns (frames/s, details)."""
     import concurrent.futures as cf
+    import importlib.util
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from _oracle import Reference
-    import importlib.util
+    from _oracle import Pattern, Reference
     spec = importlib.util.spec_from_file_location("generator_ref", os.path.join(ROOT, "oracle", "generator_ref.py"))
     gref = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(gref)
-    from paper_2512_18318_b200 import api, generator
     ref = Reference()
     streams = []
     for i in range(n_streams):
         lead, bursts, hz, amp = stream_pattern(i + 1)
-        streams.append(api.synth_pattern(lead, bursts, hz, amp, seconds * 1000))
+        streams.append(ref.render_pattern(Pattern(lead, bursts, hz, amp), seconds * 1000))
 
     def segmel(pcm):
         cuts, _, _ = ref.segment(pcm)
@@ -173,17 +187,37 @@ def cpu_reference_step(n_streams: int, seconds: int, gen_frames: int, threads: i
         frames = sum(ex.map(segmel, streams))
     t_segmel = time.perf_counter() - t0
     torch.set_num_threads(threads)
-    w = generator.synthetic_weights(0)
+    w = gref.he_weights(0)
     rng = np.random.default_rng(0)
     mel = rng.normal(-5.0, 2.5, (gen_frames, 1, 80, 16)).astype(np.float32)
-    faces = np.stack([generator.face_input(generator.synthetic_face(i), generator.synthetic_face(i + 1))
-                      for i in range(gen_frames)])
-    gref.forward(w, mel[:1], faces[:1])  # warm
+    faces = rng.random((gen_frames, 6, 96, 96), dtype=np.float32)
+    gref.forward(w, mel[:2], faces[:2])  # warm
     t0 = time.perf_counter()
-    gref.forward(w, mel, faces)
+    for b0 in range(0, gen_frames, 16):  # config 1's generator batch
+        gref.forward(w, mel[b0:b0 + 16], faces[b0:b0 + 16])
     t_gen = (time.perf_counter() - t0) / gen_frames
     total = t_segmel + frames * t_gen
     return frames / total, {"t_segmel_s": t_segmel, "gen_s_per_frame": t_gen, "frames": frames}
+
+
+def ref_sample_desc(n_streams, seconds, gen_frames, threads):
+    return (f"reference render_pattern+Segmenter+compute_mel (oracle/_ref, compiled from /root/reference sources) on "
+            f"{n_streams} x {seconds} s streams of the bench's patterns, one per thread on {threads} threads, + the "
+            f"fp32 CPU generator restatement (oracle/generator_ref.py, torch CPU, {threads} threads) timed on "
+            f"{gen_frames} frames in batches of 16; frames/s = gathered frames / (seg+mel time + frames x generator "
+            f"time per frame)")
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`--gpus N` with no torchrun environment: run this script as N ranks."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -192,45 +226,60 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=32, help="streams per GPU")
-    ap.add_argument("--seconds", type=int, default=30, help="seconds of audio/video per stream")
+    ap.add_argument("--streams", type=int, default=256, help="streams of the whole job (config 5: 256), s mod N")
+    ap.add_argument("--seconds", type=int, default=20, help="seconds of audio/video per stream")
     ap.add_argument("--batch", type=int, default=512, help="generator frames per launch sequence")
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--paced-seconds", type=int, default=20, help="config-5 paced leg length (0: skip)")
     ap.add_argument("--paced-streams", type=int, default=256, help="config-5 paced streams over all GPUs")
     ap.add_argument("--scaled-streams", type=int, default=512, help="segmenter/mel roofline set: streams x 60 s")
-    ap.add_argument("--config4-streams", type=int, default=8, help="fp8 leg (config 4): streams per GPU (0: skip)")
+    ap.add_argument("--config4-streams", type=int, default=64,
+                    help="fp8 leg (config 4): streams of the whole job, s mod N (0: skip)")
+    ap.add_argument("--ref-streams", type=int, default=0, help="reference arm sample: streams (0: host threads)")
+    ap.add_argument("--ref-seconds", type=int, default=20, help="reference arm sample: seconds per stream")
+    ap.add_argument("--ref-gen-frames", type=int, default=64, help="reference arm sample: generator frames")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     fps = 25.0
-    cfg_desc = {"workload": f"config5-unpaced: {args.streams} streams/GPU x {args.seconds} s 16 kHz synthetic speech "
-                            f"+ 25 fps 96x96 face crops; segmenter -> 80-bin log-mel -> Wav2Lip generator",
-                "streams_per_gpu": args.streams, "seconds_per_stream": args.seconds, "fps": fps,
-                "generator_batch": args.batch, "parallelism": f"streams sharded over {args.gpus} GPU(s), no collective",
+    cfg_desc = {"workload": f"config 5 unpaced: {args.streams} streams x {args.seconds} s of 16 kHz synthetic speech "
+                            f"+ 25 fps 96x96 face crops, sharded s mod {world} over {world} GPU(s); segmenter -> "
+                            f"80-bin log-mel -> Wav2Lip generator (batch {args.batch})",
+                "streams": args.streams, "seconds_per_stream": args.seconds, "fps": fps,
+                "generator_batch": args.batch, "parallelism": f"streams sharded s mod {world}, no collective",
                 "l2": "inputs (PCM + face crops) and activations are larger than the 126 MB L2"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         threads = os.cpu_count() or 1
-        vals = []
-        for _ in range(max(args.warmup, 0) and 1):
-            pass
+        rs = args.ref_streams or threads
+        for _ in range(min(args.warmup, 1)):
+            cpu_reference_step(n_streams=min(rs, threads), seconds=2, gen_frames=2, threads=threads)
+        vals, dets = [], []
         for _ in range(args.steps):
-            v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
+            v, det = cpu_reference_step(n_streams=rs, seconds=args.ref_seconds, gen_frames=args.ref_gen_frames,
+                                        threads=threads)
             vals.append(v)
+            dets.append(det)
         value = float(np.median(vals))
-        sample = (f"reference Segmenter+compute_mel (oracle/_ref, /root/reference sources) on {min(threads, 8)} x 10 s "
-                  f"streams, one per thread, + fp32 CPU generator restatement (oracle/generator_ref.py) on 8 frames, "
-                  f"extrapolated per frame")
-        print(json.dumps({"impl": "reference", "metric": "lip-sync frames/sec (96x96)", "value": value,
+        # the reference arm runs none of the product's code
+        assert not any(m.startswith("paper_2512_18318_b200") for m in sys.modules), "reference arm imported ours"
+        sample = ref_sample_desc(rs, args.ref_seconds, args.ref_gen_frames, threads)
+        ref_cfg = dict(cfg_desc, workload=cfg_desc["workload"] + " -- timed on the bounded sample in cpu_baseline",
+                       reference_sample=sample)
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": value,
                           "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                          "higher_is_better": True, "dtype": "f64 (seg/mel) + f32 (generator)", "data": "synthetic",
-                          "config": cfg_desc,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "f64 (seg/mel) + f32 (generator)", "data": "synthetic",
+                          "config": ref_cfg, "per_step": vals, "details_last": dets[-1],
                           "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "reference",
                                            "sample": sample},
                           "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -254,9 +303,8 @@ def main():
     prec = 1 if args.precision == "fp16" else 0
     weights = generator.synthetic_weights(0)
     eng = generator.LipsyncEngine(weights, max_batch=args.batch, ctx=ctx, precision=prec)
-    pipe = Pipeline(PipelineConfig(args.streams, args.seconds * 1000, fps, 50, args.batch, True), eng, ctx=ctx)
-
     pcm, video, refs = make_workload(rank, args.streams, args.seconds, fps, api, generator, world)
+    pipe = Pipeline(PipelineConfig(len(pcm), args.seconds * 1000, fps, 50, args.batch, True), eng, ctx=ctx)
     # pinned host copies (e2e leg) and device-resident copies (value leg)
     lib = ctx.lib
     import ctypes as C
@@ -347,7 +395,8 @@ def main():
     gen_ms = measure_generator(eng, torch, torch_stream, local, B, reps=10)
     peaks = measured_peaks()
     achieved = FLOPS_PER_FRAME * B / (gen_ms / 1000.0) / 1e12
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+    peak = peaks.get("bf16_tflops", 1590.0)  # burst: the forward is timed alone (10 back-to-back launches)
+    peak_sus = peaks.get("bf16_tflops_sustained", peak)
     gen_b128_ms = measure_generator(eng, torch, torch_stream, local, 128, reps=10) if B >= 128 else None
     # config 3 as BASELINE.json states it: bf16, batch 128
     eng_bf = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_BF16)
@@ -361,9 +410,9 @@ def main():
             dist.destroy_process_group()
         return
     out = {
-        "metric": "lip-sync frames/sec (96x96), full segmenter->mel->generator path",
+        "metric": METRIC,
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-        "ms_per_step": ms_dev, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_dev, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16" if prec else "bf16", "data": "synthetic (seeded speech patterns, synthetic face crops, "
                                                     "BN-calibrated random weights)",
         "config": cfg_desc,
@@ -374,9 +423,13 @@ def main():
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "tensor", "kernel": f"generator forward (51 tcgen05 conv launches, batch {B})",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (the forward runs back to back "
-                                    "inside a long step; dense fp16 == bf16 rate)",
-                     "frac_vs_burst_peak": achieved / peaks.get("bf16_tflops", 1590.0),
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: the forward is timed alone, 10 "
+                                    "back-to-back launches; dense fp16 == bf16 rate)",
+                     "in_step": {"achieved": FLOPS_PER_FRAME * total_frames / world / (med["ms_generator"] / 1e3) / 1e12,
+                                 "peak": peak_sus, "frac": FLOPS_PER_FRAME * total_frames / world
+                                 / (med["ms_generator"] / 1e3) / 1e12 / peak_sus,
+                                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                                 "timed": "the pipeline's generator stage inside the step (device events), rank 0"},
                      "ms_per_launch_sequence": gen_ms, "flops_per_frame": FLOPS_PER_FRAME,
                      "traffic": generator_traffic(B),
                      "traffic_source": "profiles/r01_gen512_launches.csv: sum of dram__bytes_read+write over the "
@@ -386,7 +439,8 @@ def main():
                            if gen_b128_ms else None),
         "config3_bf16_b128": {"ms": bf16_b128_ms, "frames_per_s": 128 / (bf16_b128_ms / 1000.0),
                               "achieved_tflops": FLOPS_PER_FRAME * 128 / (bf16_b128_ms / 1000.0) / 1e12,
-                              "frac": FLOPS_PER_FRAME * 128 / (bf16_b128_ms / 1000.0) / 1e12 / peak},
+                              "frac": FLOPS_PER_FRAME * 128 / (bf16_b128_ms / 1000.0) / 1e12 / peak,
+                              "peak": peak, "peak_source": "bf16_tflops (burst)"},
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -400,11 +454,12 @@ def main():
         out["config4_fp8"] = cfg4
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        v, det = cpu_reference_step(n_streams=min(threads, 8), seconds=10, gen_frames=8, threads=threads)
+        rs = args.ref_streams or threads
+        v, det = cpu_reference_step(n_streams=rs, seconds=args.ref_seconds, gen_frames=args.ref_gen_frames,
+                                    threads=threads)
         out["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
-                               "sample": f"reference Segmenter+compute_mel (oracle/_ref) on {min(threads, 8)} x 10 s "
-                                         f"streams + fp32 CPU generator restatement on 8 frames, per-frame "
-                                         f"extrapolation; {det}"}
+                               "sample": ref_sample_desc(rs, args.ref_seconds, args.ref_gen_frames, threads) +
+                               f"; {det}"}
     print(json.dumps(out))
     if dist:
         dist.destroy_process_group()
@@ -451,9 +506,9 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
     time; p50/p99 of (segment's last frame rendered - media time of its cut)
     over all ranks' segments (paper_2512_18318_b200/paced.py)."""
     from paper_2512_18318_b200.paced import PacedRunner, summarize
-    per = max(1, args.paced_streams // world)
     secs = args.paced_seconds
-    pcm, video, refs = make_workload(rank, per, secs + 1, fps, api, generator, world, seed_base=1000)
+    pcm, video, refs = make_workload(rank, args.paced_streams, secs + 1, fps, api, generator, world, seed_base=1000)
+    per = len(pcm)
     dev = f"cuda:{local}"
     ms = max(len(p) for p in pcm)
     pcm_dev = torch.zeros((per, ms), dtype=torch.int16, device=dev)
@@ -479,7 +534,7 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
             [res.latencies_ms, res.decision_ms, res.render_ms, [res.frames], [res.late_ticks]], dist, world)
         res.frames, res.late_ticks = int(fr.sum()), int(lt.max())
         res.segments = len(res.latencies_ms)
-    out = summarize(res, per * world, secs)
+    out = summarize(res, args.paced_streams, secs)
     out["streams_per_gpu"] = per
     out["definition"] = ("latency = wall time the segment's last frame is rendered on the device - wall time media "
                          "time reached the segment end (audio and 25 fps video released in real time, 40 ms "
@@ -678,8 +733,8 @@ def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generat
     from paper_2512_18318_b200.pipeline import Pipeline, PipelineConfig
     S, secs = args.config4_streams, 30
     eng8 = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
-    pipe = Pipeline(PipelineConfig(S, secs * 1000, fps, 50, 128, True), eng8, ctx=ctx)
     pcm, video, refs = make_workload(rank, S, secs, fps, api, generator, world, seed_base=2000)
+    pipe = Pipeline(PipelineConfig(len(pcm), secs * 1000, fps, 50, 128, True), eng8, ctx=ctx)
     dev = f"cuda:{local}"
     d_pcm = [torch.from_numpy(p).to(dev) for p in pcm]
     d_vid = [torch.from_numpy(v).to(dev) for v in video]
@@ -707,7 +762,7 @@ def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generat
     gms = measure_generator(eng8, torch, stream, local, 128, reps=20)
     burst, sust, src = fp8_peaks()
     tf = FLOPS_PER_FRAME * 128 / (gms / 1e3) / 1e12
-    out = {"workload": f"config 4: fp8 generator, {S} streams/GPU x {secs} s, unpaced, batch 128",
+    out = {"workload": f"config 4: fp8 generator, {S} streams x {secs} s sharded s mod {world}, unpaced, batch 128",
            "dtype": "fp8_e4m3 (f32 accumulate)", "value": frames / (ms / 1e3), "unit": "frames/s",
            "ms_per_step": ms, "frames_per_step": frames,
            "generator_b128": {"ms": gms, "frames_per_s": 128 / (gms / 1e3), "achieved_tflops": tf,

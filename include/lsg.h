@@ -15,7 +15,9 @@
  *    visual_mocks.cpp:43-46); LSG_ECUDA is a device failure.  The message of
  *    the last failure on the calling thread is lsg_last_error().
  *  - Handles own every device workspace, sized at create time; the compute
- *    calls do not allocate.  A handle is externally synchronised (one host
+ *    calls do not allocate.  (One exception: lsg_align_* / lsg_face_track
+ *    stage a per-call table in the context's scratch, 1 MiB at create time;
+ *    a call needing more grows it once, synchronising the context's stream.)  A handle is externally synchronised (one host
  *    thread at a time), like one reference Segmenter per stream
  *    (SPEC.md:258-259).
  *  - Pointers marked [dev] are device pointers on the context's device,

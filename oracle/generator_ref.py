@@ -130,3 +130,16 @@ def face_input(target_u8: np.ndarray, ref_u8: np.ndarray) -> np.ndarray:
 def psnr(a: np.ndarray, b: np.ndarray) -> float:
     mse = float(np.mean((np.asarray(a, np.float64) - np.asarray(b, np.float64)) ** 2))
     return float("inf") if mse == 0 else 10.0 * np.log10(1.0 / mse)
+
+
+def he_weights(seed: int = 0) -> np.ndarray:
+    """He-normal weight blob in layer order, zero biases: for TIMING the CPU
+    restatement (bench.py's reference arm), where values do not matter; the
+    parity tests use the library's BN-calibrated synthetic weights."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for kind, cin, cout, k, s, p, op, res in layer_table():
+        fan_in = cin * k * k / (s[0] * s[1] if kind == T_ else 1)
+        parts.append(rng.normal(0.0, np.sqrt(2.0 / fan_in), cin * cout * k * k).astype(np.float32))
+        parts.append(np.zeros(cout, np.float32))
+    return np.concatenate(parts)

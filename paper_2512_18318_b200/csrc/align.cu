@@ -212,14 +212,7 @@ using namespace lsg::align;
 
 namespace {
 
-// stream-ordered scratch for the per-call tables (pooled by the driver)
-// The context's grow-only scratch, held (mutex) until the call has
-// synchronised its stream and returns.
-struct Scratch {
-  std::unique_lock<std::mutex> lk;
-  void* p = nullptr;
-  Scratch(Ctx* c, size_t bytes) : lk(c->scratch_mu) { p = c->scratch_get(std::max<size_t>(bytes, 16)); }
-};
+using Scratch = ScratchLease;
 
 }  // namespace
 
@@ -233,7 +226,10 @@ lsg_status lsg_align_energy(lsg_ctx ctx, int32_t n, const int16_t* pcm_base, con
     if (sample_rate <= 0) invalid("AudioBuffer: bad sample rate");
     const int hop = (int)((int64_t)sample_rate * 10 / 1000);
     if (hop <= 0) invalid("align: rate too low");  // align.cpp:18
-    if (hop > 2048) invalid("lsg_align_energy: sample rate above 204.8 kHz");
+    // the energy kernel stages EW warps x 32 hops of PCM in shared memory
+    if ((size_t)EW * 32 * (hop + 2) * sizeof(int16_t) > (size_t)ctx->smem_optin)
+      invalid("lsg_align_energy: sample rate too high for the shared-memory staging (max hop " +
+              std::to_string(ctx->smem_optin / (EW * 32 * 2) - 2) + " samples)");
     std::vector<int64_t> tab(5 * (size_t)n + 1);
     int64_t chunks = 0;
     for (int i = 0; i < n; ++i) {

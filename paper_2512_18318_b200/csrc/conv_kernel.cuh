@@ -97,12 +97,14 @@ struct alignas(64) ConvParams {
   int nphases, ntiles_n, total_tiles;
   int interleave;  // all phases have equal mtiles: t = (mt * nphases + z) * ntiles_n + nt
   // split-K (grid-starved low-resolution layers): work unit u = t * ksplit + ks
-  // runs kblocks [ks*KB/ksplit, (ks+1)*KB/ksplit) of tile t and adds its fp32
-  // partial into ws[t] (layout [BN/4][BM] float4); the last split of a tile
-  // (counters[t]) runs the epilogue from ws[t] and re-zeroes ws[t] / counters[t]
+  // runs kblocks [ks*KB/ksplit, (ks+1)*KB/ksplit) of tile t and stores its fp32
+  // partial into slot ws[u] (layout [BN/4][BM] float4).  The ksplit CTAs of a
+  // tile are ONE thread-block cluster (launched with clusterDim.x = ksplit), so
+  // the hardware co-schedules them and they meet at a cluster barrier -- never
+  // a spin on CTAs that might not be resident (a concurrent kernel on another
+  // stream can hold the other SMs); then each reduces 1/ksplit of the tile.
   int ksplit, total_units;
   float* ws;
-  int* counters;
   int trace_slot;  // layer index (LSG_TRACE builds)
   int pbn;         // tile width the weights are packed for (a multiple of BN: a
                    // BN-wide tile is a contiguous, swizzle-aligned slice of it)
@@ -378,8 +380,8 @@ __device__ __forceinline__ size_t out_pixel(const ConvParams& p, const Phase& P,
 
 // Split-K epilogue (all 256 epilogue threads take part).  Each split stores
 // its TMEM partial into its own slot ws[u] ([BN/4][BM] float4: coalesced) and
-// frees the accumulator; the ksplit CTAs of a tile meet at counters[t] (they
-// are co-resident: units <= grid <= SMs, one unit per CTA); then CTA ks sums
+// frees the accumulator; the ksplit CTAs of a tile (one cluster, one unit per
+// CTA) meet at the cluster barrier; then CTA ks sums
 // its 1/ksplit share of the tile's (row, 16-channel) items over the slots in
 // slot order -- deterministic -- and runs the ordinary epilogue math on them.
 template <int BN, int HC, int PR>
@@ -410,21 +412,12 @@ __device__ __forceinline__ void splitk_tile(const ConvParams& p, int u, int t, c
     tc::tc_fence_before();
     tc::mbar_arrive(tempty_bar);
   }
+  // every thread of the cluster arrives once (the producer / MMA warps after
+  // their loops, see conv_tc): release the slot stores, acquire the siblings'
   __threadfence();
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
   if (threadIdx.x == 64) LSG_TR(p.trace_slot, 7);
-  if (threadIdx.x == 64) {
-    int* c = p.counters + t;
-    atomicAdd(c, 1);
-    int seen;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(c) : "memory");
-      if (seen < S) __nanosleep(32);
-    } while (seen < S);
-    LSG_TR(p.trace_slot, 8);
-  }
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
-  __threadfence();
+  tc::cluster_arrive_wait();
+  if (threadIdx.x == 64) LSG_TR(p.trace_slot, 8);
   const Phase& P = p.ph[id.z];
   const int n0 = id.nt * BN;
   constexpr int NI = BM * (BN / 16);
@@ -478,10 +471,7 @@ __device__ __forceinline__ void splitk_tile(const ConvParams& p, int u, int t, c
 #pragma unroll
     for (int w = 0; w < W16; ++w) op[w] = o[w];
   }
-  // second round on the counter: the last CTA out resets it for the next layer
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * NUM_EPI_WARPS) : "memory");
   if (threadIdx.x == 64) LSG_TR(p.trace_slot, 9);
-  if (threadIdx.x == 64 && atomicAdd(p.counters + t, 1) == 2 * S - 1) p.counters[t] = 0;
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -602,6 +592,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
       }
     }
     if (lane == 0) LSG_TR(p.trace_slot, 3);
+    if (p.ksplit > 1) tc::cluster_arrive_wait();  // splitk_tile's meeting
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (whole warp
     // runs the loop, one elected lane issues: descriptors stay uniform)
@@ -644,6 +635,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
       __syncwarp();
     }
     if (lane == 0) LSG_TR(p.trace_slot, 5);
+    if (p.ksplit > 1) tc::cluster_arrive_wait();  // splitk_tile's meeting
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
     tc::griddep_wait();  // the output / residual buffers are free / complete

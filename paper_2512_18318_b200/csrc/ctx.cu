@@ -58,6 +58,8 @@ lsg_status lsg_ctx_create(int32_t device, lsg_ctx* out) {
     DeviceGuard g(c);
     LSG_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
     c->stream = c->own;
+    c->smem_optin = (int)prop.sharedMemPerBlockOptin;
+    c->scratch_get(Ctx::kScratchInit);  // pre-sized: the compute calls do not allocate
     *out = c;
   });
 }

@@ -256,16 +256,14 @@ lsg_status lsg_face_track(lsg_ctx ctx, int32_t n, const int64_t* seg_off, const 
       tab[n + i] = seg_len[i];
     }
     DeviceGuard g(ctx);
-    void* d = nullptr;
-    LSG_CUDA(cudaMallocAsync(&d, tab.size() * 8 + (size_t)n * 4, ctx->stream));
-    int64_t* dtab = static_cast<int64_t*>(d);
+    ScratchLease sc(ctx, tab.size() * 8 + (size_t)n * 4);
+    int64_t* dtab = static_cast<int64_t*>(sc.p);
     int32_t* dst = reinterpret_cast<int32_t*>(dtab + tab.size());
     LSG_CUDA(cudaMemcpyAsync(dtab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
     face::track_kernel<<<(unsigned)ceil_div(n, 64), 64, 0, ctx->stream>>>(dtab, n, ts, frame_index, has_face, faces,
                                                                           seed, *cfg, out_box, out_vel, dst);
     LSG_LAUNCHED(ctx);
     LSG_CUDA(cudaMemcpyAsync(status, dst, (size_t)n * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    LSG_CUDA(cudaFreeAsync(d, ctx->stream));
     ctx->sync();
   });
 }

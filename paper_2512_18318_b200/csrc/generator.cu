@@ -440,7 +440,6 @@ struct lsg_gen_s {
   DevBuf<float> w1b1;
   DevBuf<uint16_t> act;  // all activation buffers
   DevBuf<float> splitk_ws;   // split-K partial slots (conv_kernel.cuh ConvParams::ws)
-  DevBuf<int> splitk_cnt;    // split-K arrival counters, zero between uses
   int splitk_tiles = 0;      // tiles the workspace holds
   // the audio encoder runs on a side stream, concurrently with the face
   // encoder (disjoint buffers: x_mel/A0/A1 vs x_face/S0/S1/cat), joined
@@ -448,7 +447,6 @@ struct lsg_gen_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevBuf<float> splitk_ws2;
-  DevBuf<int> splitk_cnt2;
   DevBuf<float> ae0w;  // ae0 weights [32][9] as quantized for the MMA (audio_stem)
   ~lsg_gen_s() {
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -497,7 +495,8 @@ static int splitk_factor(const ConvParams& p, int nphases, int tiles, int bn, bo
   const double main_us = kbmax * 4 * mma_cyc / 1900.0;
   const int kn = gen_knobs();
   if (main_us < ((kn & 4) ? 3.0 : (kn & 16) ? 10.0 : 6.0)) return 1;
-  const int s = std::min({sms / tiles, (kn & 8) ? kbmin / 2 : kbmin / 4, 16});
+  // <= 8: the splits of a tile form one (portable-size) cluster
+  const int s = std::min({sms / tiles, (kn & 8) ? kbmin / 2 : kbmin / 4, 8});
   return s >= 2 ? s : 1;
 }
 
@@ -524,7 +523,7 @@ static int conv_launch_bn(const LayerRun& r, int B, int sms, int ws_tiles) {
 }
 
 template <int BN, int CC, bool F, int PR>
-static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int* cnt, int ws_tiles) {
+static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int ws_tiles) {
   ConvParams p = r.p;
   const int ntiles = r.ntiles * r.bn / BN;
   int tiles = 0;
@@ -544,9 +543,28 @@ static void launch_conv(const LayerRun& r, int B, int sms, cudaStream_t st, floa
   p.ksplit = splitk_factor(p, r.nphases, tiles, BN, F, sms, ws ? ws_tiles : 0);
   p.total_units = tiles * p.ksplit;
   p.ws = ws;
-  p.counters = cnt;
-  const int grid = std::min(p.total_units, sms);
-  launch_pdl(conv_tc<BN, CC, F, PR>, grid, NUM_THREADS, Cfg<BN>::SMEM, st, p);
+  if (p.ksplit == 1) {
+    launch_pdl(conv_tc<BN, CC, F, PR>, std::min(p.total_units, sms), NUM_THREADS, Cfg<BN>::SMEM, st, p);
+    return;
+  }
+  // split-K: the ksplit CTAs of a tile are one cluster (co-scheduled by the
+  // hardware, so their meeting in splitk_tile cannot wait on a CTA that is
+  // not resident); grid = tiles * ksplit <= SMs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)p.total_units);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = (size_t)Cfg<BN>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)p.ksplit;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  LSG_CUDA(cudaLaunchKernelEx(&cfg, conv_tc<BN, CC, F, PR>, p));
 }
 
 // CTA-pair launch (conv_pair.cuh): tiles are pairs of m-tiles, one cluster of
@@ -572,7 +590,6 @@ static void launch_pair(const LayerRun& r, int B, int sms, cudaStream_t st) {
   p.ksplit = 1;
   p.total_units = tiles;
   p.ws = nullptr;
-  p.counters = nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)std::min(2 * tiles, sms & ~1));
   cfg.blockDim = dim3(NUM_THREADS);
@@ -713,16 +730,54 @@ static void launch_halo_pair(const LayerRun& r, int B, int sms, cudaStream_t st)
   LSG_CUDA(cudaLaunchKernelEx(&cfg, conv_halo<BN, MD, F, PR, R, true>, hp));
 }
 
-template <int PR>
-static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int* cnt, int ws_tiles) {
+// Kernel route of a plan layer at batch B: decided here ONCE, used by the
+// launch and reported by lsgdbg_gen_routes (tests assert which kernel paths
+// a benchmarked batch size exercises).
+enum Route : int { RT_HALO = 1, RT_HALO_PAIR = 2, RT_CONV = 3, RT_CONV_SPLITK = 4, RT_CONV_NARROW = 5,
+                   RT_PAIR = 6, RT_STEM = 7 };
+struct RouteInfo {
+  int route, bn, ksplit;
+};
+static bool has_halo_pair_variant(const LayerRun& r) {
+#define LSG_HAS_HP(BN, MD, F, R) \
+  if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R) return true;
+  LSG_HALO_PAIR_VARIANTS(LSG_HAS_HP)
+#undef LSG_HAS_HP
+  return false;
+}
+static bool has_pair_variant(const LayerRun& r) {
+#define LSG_HAS_P(BN, CC) \
+  if (r.bn == BN && r.p.cc == CC) return true;
+  LSG_PAIR_VARIANTS(LSG_HAS_P)
+#undef LSG_HAS_P
+  return false;
+}
+static RouteInfo route_of(const LayerRun& r, int B, int sms, int ws_tiles) {
   if (r.halo) {
-    if (!(gen_knobs() & 1024) && r.hp_pair_ok && (B * r.hp.tiles_per_img) % 2 == 0 && B * r.hp.tiles_per_img >= sms) {
+    const bool pair = !(gen_knobs() & 1024) && r.hp_pair_ok && (B * r.hp.tiles_per_img) % 2 == 0 &&
+                      B * r.hp.tiles_per_img >= sms && has_halo_pair_variant(r);
+    return {pair ? RT_HALO_PAIR : RT_HALO, r.bn, 1};
+  }
+  const int lbn = conv_launch_bn(r, B, sms, ws_tiles);
+  const int ks = splitk_factor(r.p, r.nphases, conv_tiles(r, B, lbn), lbn, r.fused, sms, ws_tiles);
+  // wide layers with at least a full wave of tiles: CTA pairs
+  if (r.pair_ok && lbn == r.bn && !(gen_knobs() & 32) && conv_tiles(r, B, r.bn) >= sms && ks == 1 &&
+      has_pair_variant(r))
+    return {RT_PAIR, r.bn, 1};
+  return {ks > 1 ? RT_CONV_SPLITK : (lbn < r.bn ? RT_CONV_NARROW : RT_CONV), lbn, ks};
+}
+
+template <int PR>
+static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float* ws, int ws_tiles) {
+  const RouteInfo ri = route_of(r, B, sms, ws ? ws_tiles : 0);
+  if (ri.route == RT_HALO_PAIR) {
 #define LSG_HALO_PAIR_DISPATCH(BN, MD, F, R)                                                  \
   if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
     return launch_halo_pair<BN, MD, F, PR, R>(r, B, sms, st);
-      LSG_HALO_PAIR_VARIANTS(LSG_HALO_PAIR_DISPATCH)
+    LSG_HALO_PAIR_VARIANTS(LSG_HALO_PAIR_DISPATCH)
 #undef LSG_HALO_PAIR_DISPATCH
-    }
+  }
+  if (ri.route == RT_HALO || ri.route == RT_HALO_PAIR) {
 #define LSG_HALO_DISPATCH(BN, MD, F, R)                                                       \
   if (r.bn == BN && r.halo_mode == MD && r.fused == F && r.halo_bres == R)                    \
     return launch_halo<BN, MD, F, PR, R>(r, B, sms, st);
@@ -731,17 +786,15 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float
     fail(LSG_ERUNTIME, "generator: no halo kernel for tile width " + std::to_string(r.bn) + " / mode " +
                            std::to_string(r.halo_mode) + (r.halo_bres ? " / resident weights" : " / streamed weights"));
   }
-  const int lbn = conv_launch_bn(r, B, sms, ws ? ws_tiles : 0);
-  // wide layers with at least a full wave of tiles: CTA pairs
-  if (r.pair_ok && lbn == r.bn && !(gen_knobs() & 32) && conv_tiles(r, B, r.bn) >= sms &&
-      splitk_factor(r.p, r.nphases, conv_tiles(r, B, r.bn), r.bn, false, sms, ws ? ws_tiles : 0) == 1) {
+  if (ri.route == RT_PAIR) {
 #define LSG_PAIR_DISPATCH(BN, CC) \
   if (r.bn == BN && r.p.cc == CC) return launch_pair<BN, CC, PR>(r, B, sms, st);
     LSG_PAIR_VARIANTS(LSG_PAIR_DISPATCH)
 #undef LSG_PAIR_DISPATCH
   }
+  const int lbn = ri.bn;
 #define LSG_DISPATCH(BN, CC, F) \
-  if (lbn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st, ws, cnt, ws_tiles);
+  if (lbn == BN && r.p.cc == CC && r.fused == F) return launch_conv<BN, CC, F, PR>(r, B, sms, st, ws, ws_tiles);
   LSG_CONV_VARIANTS(LSG_DISPATCH)
 #undef LSG_DISPATCH
   fail(LSG_ERUNTIME, "generator: no conv kernel for tile width " + std::to_string(r.bn) + " / channel chunk " +
@@ -750,11 +803,10 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float
 
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st, int wset = 0) {
   float* ws = wset ? h->splitk_ws2.p : h->splitk_ws.p;
-  int* cnt = wset ? h->splitk_cnt2.p : h->splitk_cnt.p;
   const int wt = h->splitk_tiles;
-  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, cnt, wt);
-  else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st, ws, cnt, wt);
-  else dispatch_t<PR_BF16>(r, B, h->sm_count, st, ws, cnt, wt);
+  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, wt);
+  else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st, ws, wt);
+  else dispatch_t<PR_BF16>(r, B, h->sm_count, st, ws, wt);
 }
 
 // Activation tensors for fp8 scales: 0 face input, 1 mel input, 2..8 the
@@ -837,15 +889,11 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       for (auto& r : reqs) tot += ((size_t)B * r.H * r.W * r.C + 127) & ~size_t(127);
       h->act.alloc(tot);
       LSG_CUDA(cudaMemset(h->act.p, 0, h->act.bytes()));
-      // split-K workspace: one 128 x 256 fp32 slot per work unit (units <= SMs),
-      // one counter per tile (tiles <= SMs / 2)
+      // split-K workspace: one 128 x 256 fp32 slot per work unit (units <= SMs,
+      // tiles <= SMs / 2)
       h->splitk_tiles = h->sm_count / 2;
       h->splitk_ws.alloc((size_t)h->sm_count * BM * 256);
-      h->splitk_cnt.alloc((size_t)h->splitk_tiles);
-      LSG_CUDA(cudaMemset(h->splitk_cnt.p, 0, h->splitk_cnt.bytes()));
       h->splitk_ws2.alloc((size_t)h->sm_count * BM * 256);
-      h->splitk_cnt2.alloc((size_t)h->splitk_tiles);
-      LSG_CUDA(cudaMemset(h->splitk_cnt2.p, 0, h->splitk_cnt2.bytes()));
       LSG_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
       LSG_CUDA(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
       LSG_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
@@ -1624,6 +1672,27 @@ extern "C" lsg_status lsgdbg_trace_read(unsigned long long* out, int64_t n) {
     (void)n;
     invalid("lsgdbg_trace_read: library built without LSG_TRACE");
 #endif
+  });
+}
+
+// Per plan layer at batch B: {layer index, Route, launch tile width, split-K
+// factor} -- the decisions forward() takes (route_of), for the tests.
+extern "C" lsg_status lsgdbg_gen_routes(lsg_gen h, int32_t B, int32_t* out, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    if (!h || !n_out) invalid("lsgdbg_gen_routes: null argument");
+    if (B < 1 || B > h->max_batch) invalid("lsgdbg_gen_routes: bad batch");
+    const int n = (int)h->plan.size();
+    *n_out = n;
+    if (!out) return;
+    for (int i = 0; i < n && i < cap; ++i) {
+      const LayerRun& r = h->plan[i];
+      RouteInfo ri = route_of(r, B, h->sm_count, h->splitk_tiles);
+      if (r.layer == kAe0 && h->ae0w.p && !(gen_knobs() & 8192)) ri = {RT_STEM, 0, 1};
+      out[4 * i] = r.layer;
+      out[4 * i + 1] = ri.route;
+      out[4 * i + 2] = ri.bn;
+      out[4 * i + 3] = ri.ksplit;
+    }
   });
 }
 

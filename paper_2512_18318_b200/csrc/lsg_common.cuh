@@ -46,8 +46,13 @@ struct Ctx {
   std::atomic<int64_t> launches{0};
   void note_launch() { launches.fetch_add(1, std::memory_order_relaxed); }
   void sync() { LSG_CUDA(cudaStreamSynchronize(stream)); }
-  // grow-only device scratch for calls that stage a per-call table and
-  // synchronise before returning (align.cu): no allocation per call
+  int smem_optin = 0;  // sharedMemPerBlockOptin
+  // device scratch for calls that stage a per-call table and synchronise
+  // before returning (align.cu, face.cu): allocated at context creation
+  // (kScratchInit covers ~25k segments per call); a larger call grows it once
+  // (synchronising) -- the one exception to "compute calls do not allocate",
+  // documented in lsg.h
+  static constexpr size_t kScratchInit = 1 << 20;
   std::mutex scratch_mu;
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -64,6 +69,14 @@ struct Ctx {
     }
     return scratch;
   }
+};
+
+// The context's scratch, held (mutex) until the call has synchronised its
+// stream and returns.
+struct ScratchLease {
+  std::unique_lock<std::mutex> lk;
+  void* p = nullptr;
+  ScratchLease(Ctx* c, size_t bytes) : lk(c->scratch_mu) { p = c->scratch_get(bytes < 16 ? 16 : bytes); }
 };
 
 // Makes the context's device current for the calling host thread.

@@ -308,7 +308,9 @@ lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_
     LSG_CUDA(cudaEventRecord(h->ev[4], st));
     LSG_CUDA(cudaStreamSynchronize(h->d2h));
     ctx->sync();
-    for (int64_t j = 0; j < n_copy && recs; ++j)
+    // records are filled up to cap whether or not frames are copied back
+    const int64_t n_recs = recs ? std::min<int64_t>(J, cap) : 0;
+    for (int64_t j = 0; j < n_recs; ++j)
       recs[j] = {jobs[j].stream, jobs[j].seg, jobs[j].frame, jobs[j].ts, jobs[j].k, 0};
     *n_out = J;
     if (stats) {

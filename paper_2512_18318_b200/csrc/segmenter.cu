@@ -868,7 +868,9 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->flags.alloc((size_t)n_streams * P.flag_words);
       h->stats.alloc((size_t)n_streams * h->max_frames_push);
       h->chunks_dev.alloc(n_streams);
-      h->staging.alloc((size_t)n_streams * max_push_samples + 64);
+      // each staged chunk starts 64-sample (128 B) aligned: <= one chunk per
+      // stream per push, each rounded up to 64 samples
+      h->staging.alloc((size_t)n_streams * (size_t)((max_push_samples + 63) & ~int64_t(63)) + 64);
       h->streams_dev.alloc(n_streams);
       h->totals_dev.alloc(n_streams);
       h->chunks_host.alloc(n_streams);
@@ -961,6 +963,7 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       const int16_t* src = pcm[i];
       if (!pcm_on_device && !is_device_ptr(src)) {
         int16_t* dst = h->staging.p + stage_off;
+        if (stage_off + n_samples[i] > (int64_t)h->staging.n) fail(LSG_ERUNTIME, "lsg_seg_push: staging overflow");
         LSG_CUDA(cudaMemcpyAsync(dst, src, n_samples[i] * 2, cudaMemcpyHostToDevice, ctx->stream));
         src = dst;
         stage_off += (n_samples[i] + 63) & ~int64_t(63);  // keep 128 B alignment

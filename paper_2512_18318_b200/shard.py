@@ -11,12 +11,13 @@ from __future__ import annotations
 import numpy as np
 
 
-def streams_for_rank(n_per_gpu: int, rank: int, world: int) -> list[int]:
-    """Global stream ids owned by `rank`: s mod world == rank (weak scaling:
-    n_per_gpu streams per GPU, n_per_gpu * world in total)."""
-    if world < 1 or not 0 <= rank < world:
-        raise ValueError("streams_for_rank: bad rank/world")
-    return [s for s in range(n_per_gpu * world) if s % world == rank]
+def streams_for_rank(n_total: int, rank: int, world: int) -> list[int]:
+    """Global stream ids owned by `rank` out of n_total streams: s mod world
+    == rank (strong scaling: the job's stream count is fixed, each of the
+    `world` GPUs owns ~n_total / world of them)."""
+    if world < 1 or not 0 <= rank < world or n_total < 0:
+        raise ValueError("streams_for_rank: bad rank/world/count")
+    return [s for s in range(n_total) if s % world == rank]
 
 
 def max_over_ranks(x: float, dist=None, device=None) -> float:

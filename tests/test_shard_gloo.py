@@ -27,7 +27,7 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        mine = streams_for_rank(32, rank, world)
+        mine = streams_for_rank(64, rank, world)
         owners = [None] * world
         dist.all_gather_object(owners, mine)
         step_ms = 10.0 + 5.0 * rank  # rank 1 is the slow one
@@ -44,7 +44,12 @@ def _worker(rank, world, port, q):
 
 def test_streams_for_rank_single():
     assert streams_for_rank(4, 0, 1) == [0, 1, 2, 3]
-    assert streams_for_rank(3, 1, 2) == [1, 3, 5]
+    assert streams_for_rank(6, 1, 2) == [1, 3, 5]
+    assert streams_for_rank(7, 0, 2) == [0, 2, 4, 6]
+    # 256 streams over 1/2/4/8 GPUs: every stream owned exactly once
+    for g in (1, 2, 4, 8):
+        owned = sorted(s for r in range(g) for s in streams_for_rank(256, r, g))
+        assert owned == list(range(256))
     with pytest.raises(ValueError):
         streams_for_rank(3, 2, 2)
 
@@ -62,7 +67,7 @@ def test_two_rank_gloo():
         assert p.exitcode == 0
     res.sort()
     owners = res[0][1]
-    # every stream owned by exactly one rank, s mod G, 32 per rank
+    # 64 streams in total: every stream owned by exactly one rank, s mod G, 32 per rank
     flat = sorted(s for o in owners for s in o)
     assert flat == list(range(64))
     assert all(s % world == r for r, o in enumerate(owners) for s in o)
