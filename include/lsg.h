@@ -148,6 +148,11 @@ lsg_status lsg_mel_frames(int64_t n_samples, const lsg_mel_cfg* cfg, int64_t* fr
 /* Builds window, filterbank (host fp64, exactly mel.cpp:83-110) and FFT
  * tables once.  max_frames bounds one compute call. */
 lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frames, lsg_mel* out);
+/* fft_radix2 (mel.cpp:46-70, mel.hpp:42), in place, bit-identical to the
+ * reference: `count` transforms of n complex doubles, data [any] interleaved
+ * (re, im), transform i at data + 2*n*i.  n a power of two <= 8192, else
+ * EINVAL ("fft: size must be a power of two", mel.cpp:48-49).  Synchronises. */
+lsg_status lsg_fft_radix2(lsg_ctx ctx, double* data, int64_t n, int32_t count);
 lsg_status lsg_mel_destroy(lsg_mel h);
 /* compute_mel of one buffer: pcm [any] (n samples) -> out [any]
  * [frames][n_mels] f32, row major like MelSpectrogram::data. */

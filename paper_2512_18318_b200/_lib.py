@@ -108,6 +108,7 @@ _SIGS = {
     "lsg_mel_destroy": [P],
     "lsg_mel_compute": [P, P, I64, P, PI64],
     "lsg_mel_compute_batch": [P, I32, P, PI64, PI64, P, PI64],
+    "lsg_fft_radix2": [P, P, I64, I32],
     "lsg_gen_param_count": [PI64],
     "lsg_gen_layer_info": [PI32, I32, PI32],
     "lsg_gen_create": [P, P, I64, I32, I32, PP],

@@ -454,6 +454,16 @@ def compute_mel(audio: AudioBuffer, cfg: MelConfig = MelConfig()) -> MelSpectrog
     return ext(audio)
 
 
+def fft_radix2(buf: np.ndarray) -> None:
+    """Drop-in for fft_radix2 (mel.hpp:42, mel.cpp:46-70): in-place radix-2
+    FFT of a complex128 array on the GPU, bit-identical to the reference;
+    InvalidArgument unless len(buf) is a power of two (<= 8192)."""
+    if buf.dtype != np.complex128 or not buf.flags.c_contiguous:
+        raise TypeError("fft_radix2: needs a C-contiguous complex128 array (std::vector<std::complex<double>>)")
+    ctx = default_context()
+    ctx.lib.call("lsg_fft_radix2", ctx.h, _ptr(buf), len(buf), 1)
+
+
 def synth_pattern(lead_silence_ms: int, bursts, tone_hz: float, amplitude: float, total_ms: int,
                   sample_rate: int = 16000) -> np.ndarray:
     """render_pattern restated in liblsg (workload generation)."""
