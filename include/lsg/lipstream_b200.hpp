@@ -18,7 +18,12 @@
 #include <cstdint>
 #include <cstdlib>
 #include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -151,18 +156,23 @@ class Segmenter {
   Segmenter& operator=(const Segmenter&) = delete;
 
   std::vector<RawSegment> push(const AudioBuffer& chunk) {
+    return push(chunk.samples.data(), static_cast<std::int64_t>(chunk.samples.size()), chunk.sample_rate,
+                chunk.start);
+  }
+  // The same push over a borrowed host buffer (no AudioBuffer copy): what
+  // the reference-typed adapter (integration/lipstream_gpu.cpp) calls.
+  std::vector<RawSegment> push(const std::int16_t* samples, std::int64_t n, int sample_rate, Timestamp start) {
     const int32_t sid = 0;
-    const int16_t* ptr = chunk.samples.data();
-    const int64_t n = static_cast<int64_t>(chunk.samples.size());
-    const int64_t st = chunk.start;
-    check(lsg_seg_push(h_, 1, &sid, &ptr, &n, &st, chunk.sample_rate, 0));
+    const int16_t* ptr = samples;
+    const int64_t st = start;
+    check(lsg_seg_push(h_, 1, &sid, &ptr, &n, &st, sample_rate, 0));
     std::vector<RawSegment> out;
     if (n == 0) return out;
     if (!started_) {
       started_ = true;
-      base_ = seg_start_ = chunk.start;
+      base_ = seg_start_ = start;
     }
-    pending_.insert(pending_.end(), chunk.samples.begin(), chunk.samples.end());
+    pending_.insert(pending_.end(), samples, samples + n);
     if (!scorer_) return materialise();
     std::vector<uint8_t> flags = take_flags();
     for (uint8_t f : flags) process_frame(f != 0, out);
@@ -348,8 +358,7 @@ inline std::int64_t mel_frame_count(std::int64_t n_samples, const MelConfig& cfg
   return f;
 }
 
-// Drop-in for compute_mel (mel.hpp:39).  Builds the tables once per call;
-// hold a MelExtractor to amortise them.
+// compute_mel (mel.hpp:39) with the tables built once: a reusable handle.
 class MelExtractor {
  public:
   explicit MelExtractor(const MelConfig& cfg = {}, std::int64_t max_frames = 1 << 16,
@@ -357,30 +366,49 @@ class MelExtractor {
       : cfg_(cfg) {
     lsg_mel_cfg c = to_c(cfg);
     check(lsg_mel_create(ctx.handle(), &c, max_frames, &h_));
+    max_frames_ = max_frames;
   }
   ~MelExtractor() { lsg_mel_destroy(h_); }
   MelExtractor(const MelExtractor&) = delete;
   MelExtractor& operator=(const MelExtractor&) = delete;
-  MelSpectrogram operator()(const AudioBuffer& audio) const {
+  MelSpectrogram operator()(const AudioBuffer& audio) const { return (*this)(audio.samples.data(), audio.samples.size()); }
+  MelSpectrogram operator()(const std::int16_t* samples, std::size_t n) const {
     MelSpectrogram m;
     m.n_mels = cfg_.n_mels;
-    m.n_frames = mel_frame_count(std::int64_t(audio.samples.size()), cfg_);
+    m.n_frames = mel_frame_count(std::int64_t(n), cfg_);
     m.data.resize(static_cast<std::size_t>(m.n_frames) * cfg_.n_mels);
     int64_t f = 0;
-    if (m.n_frames)
-      check(lsg_mel_compute(h_, audio.samples.data(), int64_t(audio.samples.size()), m.data.data(), &f));
+    if (m.n_frames) check(lsg_mel_compute(h_, samples, int64_t(n), m.data.data(), &f));
     return m;
   }
+  std::int64_t max_frames() const { return max_frames_; }
 
  private:
   MelConfig cfg_;
   lsg_mel h_ = nullptr;
+  std::int64_t max_frames_ = 0;
 };
 
+// Drop-in for compute_mel (mel.hpp:39): pure and re-entrant like the
+// reference; each host thread keeps one extractor per config (tables built
+// once, device buffers grown to the longest buffer seen), so the hot path
+// does not allocate.
+inline MelSpectrogram compute_mel(const std::int16_t* samples, std::size_t n, const MelConfig& cfg = {}) {
+  const std::int64_t f = mel_frame_count(std::int64_t(n), cfg);
+  using Key = std::tuple<int, int, int, int, double, double>;
+  thread_local std::map<Key, std::unique_ptr<MelExtractor>> cache;
+  auto& ext = cache[Key{cfg.sample_rate, cfg.fft_size, cfg.hop, cfg.n_mels, cfg.fmin, cfg.fmax}];
+  if (!ext || ext->max_frames() < f) ext = std::make_unique<MelExtractor>(cfg, std::max<std::int64_t>(f, 1 << 12));
+  return (*ext)(samples, n);
+}
 inline MelSpectrogram compute_mel(const AudioBuffer& audio, const MelConfig& cfg = {}) {
-  const std::int64_t f = mel_frame_count(std::int64_t(audio.samples.size()), cfg);
-  MelExtractor ext(cfg, f > 0 ? f : 1);
-  return ext(audio);
+  return compute_mel(audio.samples.data(), audio.samples.size(), cfg);
+}
+
+// Drop-in for fft_radix2 (mel.hpp:42): the GPU transform, bit-identical to
+// the reference (lsg_fft_radix2); std::invalid_argument on a bad size.
+inline void fft_radix2(std::vector<std::complex<double>>& buf, Context& ctx = Context::default_context()) {
+  check(lsg_fft_radix2(ctx.handle(), reinterpret_cast<double*>(buf.data()), std::int64_t(buf.size()), 1));
 }
 
 // ------------------------------------------------------------------ lipsync
@@ -394,6 +422,108 @@ struct LipsyncRender {
 inline void validate_lipsync(DurationMs audio_span_ms, DurationMs frame_span_ms, std::int64_t n_frames) {
   check(lsg_lipsync_validate(audio_span_ms, frame_span_ms, n_frames));
 }
+
+enum class Precision { BF16 = LSG_PREC_BF16, FP16 = LSG_PREC_FP16 };
+
+// The lip-sync stage with mock_lipsync's contract (visual_mocks.hpp:32-43):
+// validate the pair exactly as mock_lipsync does, render every frame through
+// the Wav2Lip generator on the GPU, return LipsyncRender{frames, cost_us}
+// with cost_us the measured render time instead of the profile's charge.
+// render() takes the segment's device-resident inputs (mel rows, each frame's
+// 16-row chunk start, face crops, reference crop -- e.g. resolved from a
+// DeviceRegistry); render_placeholder() renders n frames of a fixed
+// synthetic input for callers that, like the reference's StageFn, hold only
+// spans and a frame count.  Weights: a host fp32 blob (lsg_gen_param_count
+// floats, BN folded).
+class LipsyncStage {
+ public:
+  LipsyncStage(const std::vector<float>& weights, int max_batch = 128, Precision prec = Precision::FP16,
+               Context& ctx = Context::default_context())
+      : ctx_(ctx), max_batch_(max_batch) {
+    check(lsg_gen_create(ctx.handle(), weights.data(), std::int64_t(weights.size()), int32_t(prec), max_batch, &g_));
+  }
+  ~LipsyncStage() {
+    for (void* p : bufs_) lsg_dev_free(ctx_.handle(), p);
+    lsg_gen_destroy(g_);
+  }
+  LipsyncStage(const LipsyncStage&) = delete;
+  LipsyncStage& operator=(const LipsyncStage&) = delete;
+
+  // All pointers [dev]; out [n][96][96][3] u8.  ref_index may be null (one
+  // reference crop for the segment).
+  LipsyncRender render(DurationMs audio_span_ms, DurationMs frame_span_ms, std::int64_t n_frames,
+                       const float* mel_rows, const std::int32_t* chunk_row, const std::uint8_t* faces,
+                       const std::uint8_t* ref, std::uint8_t* out) {
+    validate_lipsync(audio_span_ms, frame_span_ms, n_frames);
+    const auto t0 = std::chrono::steady_clock::now();
+    const std::int32_t* ridx = zeros();
+    for (std::int64_t b0 = 0; b0 < n_frames; b0 += max_batch_) {
+      const int B = int(std::min<std::int64_t>(max_batch_, n_frames - b0));
+      check(lsg_gen_forward(g_, mel_rows, chunk_row + b0, faces + b0 * kCrop, ref, ridx, out + b0 * kCrop,
+                            LSG_OUT_U8_NHWC, B));
+    }
+    check(lsg_ctx_sync(ctx_.handle()));
+    const auto us = std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0);
+    return LipsyncRender{n_frames, std::int64_t(us.count())};
+  }
+
+  LipsyncRender render_placeholder(DurationMs audio_span_ms, DurationMs frame_span_ms, std::int64_t n_frames) {
+    validate_lipsync(audio_span_ms, frame_span_ms, n_frames);
+    if (!ph_mel_) make_placeholder();
+    LipsyncRender r{0, 0};
+    for (std::int64_t b0 = 0; b0 < n_frames; b0 += max_batch_) {
+      const std::int64_t B = std::min<std::int64_t>(max_batch_, n_frames - b0);
+      LipsyncRender p = render(audio_span_ms, frame_span_ms, std::max<std::int64_t>(B, 2), ph_mel_, ph_chunk_,
+                               ph_faces_, ph_faces_, ph_out_);
+      r.frames += B;
+      r.cost_us += p.cost_us;
+    }
+    return r;
+  }
+
+ private:
+  static constexpr std::int64_t kCrop = 96 * 96 * 3;
+  void* dev(std::size_t bytes) {
+    void* p = nullptr;
+    check(lsg_dev_alloc(ctx_.handle(), bytes, &p));
+    bufs_.push_back(p);
+    return p;
+  }
+  const std::int32_t* zeros() {
+    if (!zeros_) {
+      std::vector<std::int32_t> z(std::size_t(max_batch_), 0);
+      zeros_ = static_cast<std::int32_t*>(dev(z.size() * 4));
+      check(lsg_copy(ctx_.handle(), zeros_, z.data(), z.size() * 4));
+      check(lsg_ctx_sync(ctx_.handle()));
+    }
+    return zeros_;
+  }
+  void make_placeholder() {
+    // 16 rows of log-mel silence (ln 1e-10), every frame on chunk 0, a
+    // mid-grey crop with a darker lower half
+    std::vector<float> mel(16 * 80, float(std::log(1e-10)));
+    std::vector<std::int32_t> chunk(std::size_t(max_batch_), 0);
+    std::vector<std::uint8_t> face(std::size_t(max_batch_) * kCrop);
+    for (std::size_t i = 0; i < face.size(); ++i) face[i] = ((i / (96 * 3)) % 96) < 48 ? 150 : 90;
+    ph_mel_ = static_cast<float*>(dev(mel.size() * 4));
+    ph_chunk_ = static_cast<std::int32_t*>(dev(chunk.size() * 4));
+    ph_faces_ = static_cast<std::uint8_t*>(dev(face.size()));
+    ph_out_ = static_cast<std::uint8_t*>(dev(face.size()));
+    check(lsg_copy(ctx_.handle(), ph_mel_, mel.data(), mel.size() * 4));
+    check(lsg_copy(ctx_.handle(), ph_chunk_, chunk.data(), chunk.size() * 4));
+    check(lsg_copy(ctx_.handle(), ph_faces_, face.data(), face.size()));
+    check(lsg_ctx_sync(ctx_.handle()));
+  }
+  Context& ctx_;
+  int max_batch_;
+  lsg_gen g_ = nullptr;
+  std::vector<void*> bufs_;
+  std::int32_t* zeros_ = nullptr;
+  float* ph_mel_ = nullptr;
+  std::int32_t* ph_chunk_ = nullptr;
+  std::uint8_t* ph_faces_ = nullptr;
+  std::uint8_t* ph_out_ = nullptr;
+};
 
 // ---------------------------------------------- zero-copy stage hand-off
 // device buffers keyed by (segment uuid, kind); stages pass

@@ -513,7 +513,7 @@ seg_scan(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, 
     M.cand_cut = S->cand_cut;
     M.n_pause = 0;
     M.n_forced = 0;
-    M.n_cuts = 0;
+    M.n_cuts = S->n_cuts;  // cuts not collected yet stay in front (collection is deferred)
     M.overflow = S->overflow;
     peak = S->peak;
     s_speech = 0;
@@ -626,7 +626,6 @@ __global__ void seg_finish(const int32_t* __restrict__ streams, const int64_t* _
   if (i >= n) return;
   const int s = streams[i];
   DevState* S = st + s;
-  S->n_cuts = 0;
   S->n_flag_frames = 0;
   const int64_t tail_ms = (int64_t)S->carry_len * 1000 / P.rate;
   const int64_t pending = totals[i] - S->emitted;
@@ -639,8 +638,12 @@ __global__ void seg_finish(const int32_t* __restrict__ streams, const int64_t* _
   c.stream = s;
   c.sample_off = S->emitted;
   c.sample_len = pending;
-  cuts_all[(int64_t)s * P.cut_cap] = c;
-  S->n_cuts = 1;
+  if (S->n_cuts < P.cut_cap) {
+    cuts_all[(int64_t)s * P.cut_cap + S->n_cuts] = c;
+    S->n_cuts += 1;
+  } else {
+    S->overflow = 1;
+  }
   S->emitted += pending;
   S->m_eos += 1;
 }
@@ -653,7 +656,8 @@ constexpr int COLLECT_MAX = 4096;  // streams per push / finish
 __global__ void __launch_bounds__(COLLECT_THREADS)
 seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
             const lsg_cut* __restrict__ cuts_all, const uint32_t* __restrict__ flags_all, Params P,
-            DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts, uint32_t* h_flags, int cut_cap_total) {
+            DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts, uint32_t* h_flags, int cut_cap_total,
+            DevState* st_mut) {
   __shared__ int s_off[COLLECT_MAX + 1];
   __shared__ int s_warp[COLLECT_THREADS / 32];
   __shared__ int s_carry;
@@ -702,6 +706,8 @@ seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restri
       for (int j = lane; j < nw; j += 32) h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
     }
   }
+  __syncthreads();  // every copy above read st[] first
+  for (int i = tid; i < n; i += COLLECT_THREADS) st_mut[streams[i]].n_cuts = 0;
 }
 
 }  // namespace seg
@@ -738,10 +744,19 @@ struct lsg_seg_s {
   DevBuf<Chunk> chunks_dev;
   DevBuf<int16_t> staging;
   DevBuf<int32_t> streams_dev;
+  DevBuf<int32_t> collect_dev;  // streams whose results are still on the device
   DevBuf<int64_t> totals_dev;
   PinnedBuf<Chunk> chunks_host;
   PinnedBuf<int32_t> streams_host;
+  PinnedBuf<int32_t> collect_host;
   PinnedBuf<int64_t> totals_host;
+  // Deferred collection: a push leaves its cuts, state and metrics on the
+  // device (no stream synchronisation); they are gathered into mapped host
+  // memory by the next call that needs them (take_cuts / metrics / finish)
+  // or when a stream's pending-cut bound could reach its device capacity.
+  std::vector<char> dirty;
+  std::vector<int32_t> dirty_list;
+  std::vector<int64_t> cut_bound;  // upper bound of uncollected cuts per stream
   // mapped (zero-copy) result area
   DevState* h_state = nullptr;
   int32_t* h_off = nullptr;
@@ -778,16 +793,27 @@ static void validate_cfg(const lsg_seg_cfg* c) {
   if (c->peak_mode < 0 || c->peak_mode > 2) invalid("vad: unknown peak mode");
 }
 
-// Runs collect for the listed streams, synchronises, and distributes results.
-static void collect(lsg_seg h, int n, bool finishing) {
+// Gathers every dirty stream's cuts + state (+flags) into mapped host
+// memory, synchronises once, and distributes the results to the host mirror.
+static void collect(lsg_seg h, bool finishing) {
   Ctx* ctx = h->ctx;
-  seg_collect<<<1, COLLECT_THREADS, 0, ctx->stream>>>(h->streams_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
+  const int n = (int)h->dirty_list.size();
+  if (n == 0) return;
+  std::memcpy(h->collect_host.p, h->dirty_list.data(), sizeof(int32_t) * n);
+  LSG_CUDA(cudaMemcpyAsync(h->collect_dev.p, h->collect_host.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  seg_collect<<<1, COLLECT_THREADS, 0, ctx->stream>>>(h->collect_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
                                           h->h_state, h->h_off, h->h_cuts, h->h_flags,
-                                          (int)h->h_cut_cap);
+                                          (int)h->h_cut_cap, h->st.p);
   LSG_LAUNCHED(ctx);
   ctx->sync();
+  for (int s : h->dirty_list) {
+    h->dirty[s] = 0;
+    h->cut_bound[s] = 0;
+  }
+  h->dirty_list.clear();
   for (int i = 0; i < n; ++i) {
-    const int s = h->streams_host.p[i];
+    const int s = h->collect_host.p[i];
     StreamHost& S = h->hs[s];
     const DevState& D = h->h_state[i];
     if (D.overflow) fail(LSG_ERUNTIME, "segmenter: cut buffer overflow");
@@ -872,10 +898,14 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       // stream per push, each rounded up to 64 samples
       h->staging.alloc((size_t)n_streams * (size_t)((max_push_samples + 63) & ~int64_t(63)) + 64);
       h->streams_dev.alloc(n_streams);
+      h->collect_dev.alloc(n_streams);
       h->totals_dev.alloc(n_streams);
       h->chunks_host.alloc(n_streams);
       h->streams_host.alloc(n_streams);
+      h->collect_host.alloc(n_streams);
       h->totals_host.alloc(n_streams);
+      h->dirty.assign(n_streams, 0);
+      h->cut_bound.assign(n_streams, 0);
       h->h_cut_cap = (int64_t)n_streams * P.cut_cap;
       LSG_CUDA(cudaHostAlloc(&h->h_state, sizeof(DevState) * n_streams, cudaHostAllocMapped));
       LSG_CUDA(cudaHostAlloc(&h->h_off, sizeof(int32_t) * (n_streams + 1), cudaHostAllocMapped));
@@ -902,6 +932,9 @@ lsg_status lsg_seg_reset(lsg_seg h) {
     LSG_CUDA(cudaMemcpyAsync(h->st.p, init.data(), h->st.bytes(), cudaMemcpyHostToDevice, ctx->stream));
     ctx->sync();
     for (auto& d : h->hs) d = StreamHost{};
+    h->dirty.assign(h->n_streams, 0);
+    h->cut_bound.assign(h->n_streams, 0);
+    h->dirty_list.clear();
   });
 }
 
@@ -951,6 +984,16 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
         invalid("segmenter: non-contiguous chunk");
     }
     DeviceGuard g(ctx);
+    // uncollected cuts of a stream must fit its device cut buffer: <= 2 per
+    // frame (a pause cut and a forced split) + the EOS cut
+    for (int i = 0; i < n_chunks; ++i) {
+      const int s = streams[i];
+      const int64_t fr = (h->hs[s].stage_len + n_samples[i]) / P.fs;
+      if (h->cut_bound[s] + 2 * fr + 1 > P.cut_cap) {
+        collect(h, false);
+        break;
+      }
+    }
     // pass 2: stage + describe chunks
     int nc = 0;
     int64_t frame_total = 0, max_frames = 0, stage_off = 0;
@@ -981,6 +1024,11 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       frame_total += c.nframes;
       max_frames = std::max<int64_t>(max_frames, c.nframes);
       h->streams_host.p[nc] = s;
+      h->cut_bound[s] += 2 * (int64_t)c.nframes;
+      if (!h->dirty[s]) {
+        h->dirty[s] = 1;
+        h->dirty_list.push_back(s);
+      }
       // host mirror
       if (first) S.base = start_ms[i];
       S.consumed += c.nframes;
@@ -1015,7 +1063,9 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
     LSG_LAUNCHED(ctx);
     seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     LSG_LAUNCHED(ctx);
-    collect(h, nc, false);
+    // per-push flags feed the host state machine (scorer order): collect now;
+    // otherwise the results stay on the device until they are asked for
+    if (P.flags_only) collect(h, false);
   });
 }
 
@@ -1034,10 +1084,15 @@ lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
     if (n == 0) return;
     DeviceGuard g(ctx);
     for (int i = 0; i < n; ++i) {
-      h->streams_host.p[i] = streams[i];
-      h->totals_host.p[i] = h->hs[streams[i]].total;
-      h->hs[streams[i]].finished = true;
-      h->hs[streams[i]].stage_len = 0;
+      const int s = streams[i];
+      h->streams_host.p[i] = s;
+      h->totals_host.p[i] = h->hs[s].total;
+      h->hs[s].finished = true;
+      h->hs[s].stage_len = 0;
+      if (!h->dirty[s]) {
+        h->dirty[s] = 1;
+        h->dirty_list.push_back(s);
+      }
     }
     LSG_CUDA(cudaMemcpyAsync(h->streams_dev.p, h->streams_host.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
                              ctx->stream));
@@ -1046,13 +1101,17 @@ lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
     seg_finish<<<(unsigned)ceil_div(n, 128), 128, 0, ctx->stream>>>(h->streams_dev.p, h->totals_dev.p, n,
                                                                     h->st.p, h->cuts.p, h->P);
     LSG_LAUNCHED(ctx);
-    collect(h, n, true);
+    collect(h, true);  // one synchronisation for every stream's remaining cuts
   });
 }
 
 lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t cap, int64_t* n_out) {
   return guard([&] {
     if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_take_cuts: stream id out of range");
+    if (h->dirty[stream]) {
+      DeviceGuard g(h->ctx);
+      collect(h, false);
+    }
     auto& v = h->hs[stream].cuts;
     *n_out = (int64_t)v.size();
     if ((int64_t)v.size() > cap) return;
@@ -1063,6 +1122,10 @@ lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t ca
 
 lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* n_out) {
   return guard([&] {
+    if (!h->dirty_list.empty()) {
+      DeviceGuard g(h->ctx);
+      collect(h, false);
+    }
     int64_t tot = 0;
     for (auto& s : h->hs) tot += (int64_t)s.cuts.size();
     *n_out = tot;
@@ -1079,6 +1142,10 @@ lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* 
 lsg_status lsg_seg_get_metrics(lsg_seg h, int32_t stream, lsg_seg_metrics* out) {
   return guard([&] {
     if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_get_metrics: stream id out of range");
+    if (h->dirty[stream]) {
+      DeviceGuard g(h->ctx);
+      collect(h, false);
+    }
     *out = h->hs[stream].metrics;
   });
 }
