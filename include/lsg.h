@@ -174,6 +174,9 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
 #define LSG_PREC_FP16 1         /* fp16 weights/activations, f32 accumulate (same tcgen05 rate) */
 #define LSG_PREC_FP8 2          /* e4m3 weights (per output channel scale) and activations (per tensor
                                    scale from lsg_gen_calibrate), f32 accumulate */
+#define LSG_PREC_FP8_TAIL 3     /* fp16 up to fd5.2, e4m3 (as LSG_PREC_FP8) for fd6.0-out0 (28% of the
+                                   FLOPs): the fp8 split that keeps >= 30 dB vs the fp32 oracle on the
+                                   synthetic network; needs act_absmax like LSG_PREC_FP8 */
 #define LSG_OUT_F32_NCHW 0      /* [B][3][96][96] f32 in [0,1] */
 #define LSG_OUT_U8_NHWC 1       /* [B][96][96][3] u8, round(255*x) */
 #define LSG_OUT_F32_LOGITS 2    /* [B][3][96][96] f32 pre-sigmoid (parity checks) */

@@ -192,6 +192,23 @@ class MultiStreamSegmenter:
         except Exception:
             pass
 
+    def push_args(self, streams, chunks, starts, sample_rate=None):
+        """Prebuilt lsg_seg_push arguments for device-resident chunks
+        ((ptr, n) pairs): time the C-ABI call, not the ctypes marshalling."""
+        n = len(streams)
+        ids = (C.c_int32 * max(n, 1))(*streams)
+        ptrs = (C.c_void_p * max(n, 1))(*[p for p, _ in chunks])
+        lens = (C.c_int64 * max(n, 1))(*[ln for _, ln in chunks])
+        st = (C.c_int64 * max(n, 1))(*starts)
+        rate = self.cfg.sample_rate if sample_rate is None else sample_rate
+        return (self.h, n, ids, ptrs, lens, st, rate, 1), (self.h, n, ids)
+
+    def push_finish_prepared(self, args):
+        """lsg_seg_push + lsg_seg_finish with push_args()'s arguments."""
+        push, fin = args
+        self.lib.call("lsg_seg_push", *push)
+        self.lib.call("lsg_seg_finish", *fin)
+
     def push(self, streams, chunks, starts, sample_rate=None, on_device=False):
         """chunks: list of int16 numpy arrays (host) or raw device pointers + lengths."""
         n = len(streams)

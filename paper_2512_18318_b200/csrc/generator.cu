@@ -449,6 +449,7 @@ struct lsg_gen_s {
   DevBuf<float> splitk_ws2;
   DevBuf<float> ae0w;  // ae0 weights [32][9] as quantized for the MMA (audio_stem)
   ~lsg_gen_s() {
+    delete head;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -456,6 +457,12 @@ struct lsg_gen_s {
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
   View X16;  // dense copy of fe0's output (fe1.0's input; cat[6] keeps the concat copy)
   std::vector<LayerRun> plan;
+  // LSG_PREC_FP8_TAIL: this fp8 engine runs plan layers [tail0, end); the
+  // 16-bit engine `head` runs [0, tail0) and its tensors that the tail reads
+  // (cat[5] whole, cat[6]'s encoder slice) are requantised into this
+  // engine's buffers in between
+  lsg_gen_s* head = nullptr;
+  int tail0 = 0;
 };
 
 static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
@@ -850,9 +857,10 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
     lsg_gen_param_count(&want);
     if (n_floats != want) invalid("lsg_gen_create: weight blob has " + std::to_string(n_floats) + " floats, expected " +
                                   std::to_string(want));
-    if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16 && precision != LSG_PREC_FP8)
+    if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16 && precision != LSG_PREC_FP8 &&
+        precision != LSG_PREC_FP8_TAIL)
       invalid("lsg_gen_create: unsupported precision");
-    if (precision == LSG_PREC_FP8 && (!act_absmax || n_act != kTensors))
+    if ((precision == LSG_PREC_FP8 || precision == LSG_PREC_FP8_TAIL) && (!act_absmax || n_act != kTensors))
       invalid("lsg_gen_create: fp8 needs the calibrated activation ranges (lsg_gen_calibrate)");
     if (max_batch <= 0 || max_batch > 4096) invalid("lsg_gen_create: max_batch out of range");
     DeviceGuard g(ctx);
@@ -860,7 +868,9 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
     try {
       h->ctx = ctx;
       h->max_batch = max_batch;
-      h->prec = precision == LSG_PREC_FP8 ? PR_FP8 : (precision == LSG_PREC_FP16 ? PR_FP16 : PR_BF16);
+      h->prec = (precision == LSG_PREC_FP8 || precision == LSG_PREC_FP8_TAIL)
+                    ? PR_FP8
+                    : (precision == LSG_PREC_FP16 ? PR_FP16 : PR_BF16);
       const bool f8 = h->prec == PR_FP8;
       const int cpu = h->cpu = f8 ? 2 : 1;
       h->sm_count = ctx->sm_count;
@@ -1533,6 +1543,18 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
         h->plan.push_back(r);
       }
       set_smem_attrs(h->prec);
+      if (precision == LSG_PREC_FP8_TAIL) {
+        // fp8 on the decoder's last block + the output conv only (fd6.0 ..
+        // out0: 28% of the FLOPs), the 16-bit engine before it -- the split
+        // a sensitivity sweep picks for a >= 30 dB floor on this network
+        // (tools/precision_sweep.py)
+        for (int l = 0; l < kNumLayers; ++l)
+          if (std::strcmp(kLayers[l].name, "fd6.0") == 0) h->tail0 = l;
+        lsg_gen hd = nullptr;
+        if (lsg_gen_create_q(ctx, weights, n_floats, LSG_PREC_FP16, nullptr, 0, max_batch, &hd) != LSG_OK)
+          fail(LSG_ERUNTIME, std::string("lsg_gen_create: fp16 head: ") + lsg_last_error());
+        h->head = hd;
+      }
     } catch (...) {
       delete h;
       throw;
@@ -1685,9 +1707,10 @@ extern "C" lsg_status lsgdbg_gen_routes(lsg_gen h, int32_t B, int32_t* out, int3
     *n_out = n;
     if (!out) return;
     for (int i = 0; i < n && i < cap; ++i) {
-      const LayerRun& r = h->plan[i];
-      RouteInfo ri = route_of(r, B, h->sm_count, h->splitk_tiles);
-      if (r.layer == kAe0 && h->ae0w.p && !(gen_knobs() & 8192)) ri = {RT_STEM, 0, 1};
+      const lsg_gen_s* e = (h->head && i < h->tail0) ? h->head : h;  // fp8 tail: head's layers
+      const LayerRun& r = e->plan[i];
+      RouteInfo ri = route_of(r, B, e->sm_count, e->splitk_tiles);
+      if (r.layer == kAe0 && e->ae0w.p && !(gen_knobs() & 8192)) ri = {RT_STEM, 0, 1};
       out[4 * i] = r.layer;
       out[4 * i + 1] = ri.route;
       out[4 * i + 2] = ri.bn;
@@ -1704,6 +1727,7 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     cudaStream_t st = ctx->stream;
+    if (h->head) invalid("lsgdbg_run_until: not on an fp8-tail engine (check its fp8 / fp16 parts separately)");
     prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
     if (stop_layer < 0 || stop_layer >= (int)h->plan.size() - 1) invalid("lsgdbg_run_until: bad layer");
     for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
@@ -1734,27 +1758,22 @@ namespace gen {
 
 int32_t max_batch(lsg_gen h) { return h->max_batch; }
 
-void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target_base,
-                    const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, void* out,
-                    int32_t out_format, int32_t B) {
-  if (B <= 0 || B > h->max_batch) invalid("lsg_gen_forward: batch out of range");
-  if (out_format < 0 || out_format > 2) invalid("lsg_gen_forward: unknown output format");
+// Launches plan layers [l0, l1) on st (the audio encoder, when in range, on
+// the side stream, joined before the first decoder layer).
+static void run_plan(lsg_gen h, int l0, int l1, int mode, void* out, int B, cudaStream_t st) {
   Ctx* ctx = h->ctx;
-  cudaStream_t st = ctx->stream;
-  prep_inputs(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
-  LSG_LAUNCHED(ctx);
-  LSG_LAUNCHED(ctx);
-  const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
-                                                  : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
+  bool any_audio = false;
+  for (int l = l0; l < l1; ++l) any_audio |= kLayers[h->plan[l].layer].name[0] == 'a';
   // audio encoder (plan layers whose name starts with "ae") on the side
   // stream, forked after the input prep and joined before the decoder
-  const bool fork = !(gen_knobs() & 512);
+  const bool fork = any_audio && !(gen_knobs() & 512);
   if (fork) {
     LSG_CUDA(cudaEventRecord(h->ev_fork, st));
     LSG_CUDA(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   }
   bool joined = !fork;
-  for (auto& r : h->plan) {
+  for (int l = l0; l < l1; ++l) {
+    LayerRun& r = h->plan[l];
     if (r.fused) {
       r.p.out_mode = r.hp.out_mode = mode;
       r.p.final_out = r.hp.final_out = out;
@@ -1787,10 +1806,81 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
     }
     LSG_LAUNCHED(ctx);
   }
-  if (!joined) {  // (a plan without decoder layers)
+  if (!joined) {  // (a range without decoder layers)
     LSG_CUDA(cudaEventRecord(h->ev_join, h->side));
     LSG_CUDA(cudaStreamWaitEvent(st, h->ev_join, 0));
   }
+}
+
+// 16-bit tensor -> this fp8 engine's e4m3 buffer (x / scale, RN, satfinite:
+// the epilogues' own conversion): 8 channels per thread.
+template <int PRS>
+__global__ void requant_fp8(const uint16_t* __restrict__ src, int spitch, int scoff, uint16_t* __restrict__ dst,
+                            int dpitch, int dcoff, int C, int64_t pixels, float inv) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int G = C / 8;
+  if (i >= pixels * G) return;
+  const int64_t px = i / G;
+  const int g = (int)(i - px * G);
+  const uint4 v = *reinterpret_cast<const uint4*>(src + px * spitch + scoff + 8 * g);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t o[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    float f[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t u = w[2 * k + j];
+      const uint16_t lo = (uint16_t)(u & 0xffff), hi = (uint16_t)(u >> 16);
+      f[2 * j] = (PRS == PR_FP16 ? __half2float(__ushort_as_half(lo)) : __bfloat162float(__ushort_as_bfloat16(lo))) * inv;
+      f[2 * j + 1] = (PRS == PR_FP16 ? __half2float(__ushort_as_half(hi)) : __bfloat162float(__ushort_as_bfloat16(hi))) * inv;
+    }
+    const uint32_t a = __nv_cvt_float2_to_fp8x2(make_float2(f[0], f[1]), __NV_SATFINITE, __NV_E4M3);
+    const uint32_t b = __nv_cvt_float2_to_fp8x2(make_float2(f[2], f[3]), __NV_SATFINITE, __NV_E4M3);
+    o[k] = a | (b << 16);
+  }
+  *reinterpret_cast<uint2*>(dst + px * dpitch + dcoff + 4 * g) = make_uint2(o[0], o[1]);
+}
+
+// channels [c0, c0 + C) of concat buffer k: head's 16-bit copy -> h's fp8 copy
+static void requant_cat(lsg_gen h, int k, int c0, int C, int B, cudaStream_t st) {
+  const View& s = h->head->cat[k];
+  const View& d = h->cat[k];
+  const int64_t pixels = (int64_t)B * s.H * s.W;
+  const unsigned grid = (unsigned)ceil_div(pixels * (C / 8), 256);
+  requant_fp8<PR_FP16><<<grid, 256, 0, st>>>(s.p, s.pitch, s.coff + c0, d.p, d.pitch, d.coff + c0 / 2, C, pixels,
+                                             1.f / h->ascale[2 + k]);
+  LSG_LAUNCHED(h->ctx);
+}
+
+void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target_base,
+                    const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, void* out,
+                    int32_t out_format, int32_t B) {
+  if (B <= 0 || B > h->max_batch) invalid("lsg_gen_forward: batch out of range");
+  if (out_format < 0 || out_format > 2) invalid("lsg_gen_forward: unknown output format");
+  Ctx* ctx = h->ctx;
+  cudaStream_t st = ctx->stream;
+  const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
+                                                  : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
+  const int n = (int)h->plan.size();
+  if (h->head) {
+    // fp8 tail: the 16-bit head up to fd5.2, then the tail's inputs
+    // requantised -- cat[5] (fd5.2's 128 + fe1's 32 channels) and cat[6]'s
+    // fe0 slice (channels 64-79; fd6.2 writes 0-63 in fp8 itself)
+    lsg_gen hd = h->head;
+    prep_inputs(hd, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
+    LSG_LAUNCHED(ctx);
+    LSG_LAUNCHED(ctx);
+    run_plan(hd, 0, h->tail0, mode, out, B, st);
+    requant_cat(h, 5, 0, 160, B, st);
+    requant_cat(h, 6, 64, 16, B, st);
+    run_plan(h, h->tail0, n, mode, out, B, st);
+    return;
+  }
+  prep_inputs(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
+  LSG_LAUNCHED(ctx);
+  LSG_LAUNCHED(ctx);
+  run_plan(h, 0, n, mode, out, B, st);
 }
 
 }  // namespace gen

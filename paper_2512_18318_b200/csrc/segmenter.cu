@@ -42,6 +42,11 @@ struct Params {
   int32_t mode, peak_mode;
   double decay;  // exp2(-frame_ms / half_life), host libm
   double thr;
+  // rms/peak outside [x_lo, x_hi] decides without a logarithm: x_lo / x_hi
+  // are 10^(thr/20) -/+ 1e-9 relative, so 20 log10(x) is 8.7e-9 dB or more
+  // from thr there -- ~10^6 ulps, far beyond log10's error (0 / inf: always
+  // take the logarithm, e.g. thr <= -120 where the -120 clamp decides)
+  double x_lo, x_hi;
   int64_t frame_ms, min_sil, min_seg, max_seg;
   int32_t rate, fs;
   int32_t flags_only, cut_cap;
@@ -331,11 +336,14 @@ __device__ double log10_dd(double x) {
 }
 
 // VadTracker::update's decision (vad.cpp:47-52) from exact frame stats.
-__device__ __forceinline__ bool vad_decide(long long sumsq, double peak, int n, double thr) {
+__device__ __forceinline__ bool vad_decide(long long sumsq, double peak, int n, double thr, double x_lo,
+                                           double x_hi) {
   double rms = __dsqrt_rn(__ddiv_rn((double)sumsq, (double)n));
   double db = -120.0;
   if (rms > 0.0 && peak > 0.0) {
     double x = __ddiv_rn(rms, peak);
+    if (x < x_lo) return false;  // db = max(20 log10 x, -120) < thr
+    if (x > x_hi) return true;
     double d = __dmul_rn(20.0, log10(x));
     if (fabs(d - thr) < 1e-9 * fmax(1.0, fabs(thr))) d = __dmul_rn(20.0, log10_dd(x));
     db = d > -120.0 ? d : -120.0;
@@ -565,7 +573,7 @@ seg_scan(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, 
     for (int i0 = 0; i0 < n; i0 += K2_THREADS) {
       const int i = i0 + tid;
       bool sp = false;
-      if (i < n) sp = vad_decide(fst[t0 + i].sumsq, s_peak[i], P.fs, P.thr);
+      if (i < n) sp = vad_decide(fst[t0 + i].sumsq, s_peak[i], P.fs, P.thr, P.x_lo, P.x_hi);
       const unsigned bal = __ballot_sync(0xffffffffu, sp);
       if ((tid & 31) == 0 && i < n) s_bits[i >> 5] = bal;
       my_speech += sp;
@@ -865,6 +873,14 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       P.peak_mode = cfg->peak_mode;
       P.decay = std::exp2(-double(cfg->frame_ms) / cfg->peak_half_life_ms);  // vad.cpp:37
       P.thr = cfg->speech_threshold_db;
+      if (P.thr > -119.0 && P.thr < 300.0) {
+        const double xs = std::pow(10.0, P.thr / 20.0);
+        P.x_lo = xs * (1.0 - 1e-9);
+        P.x_hi = xs * (1.0 + 1e-9);
+      } else {
+        P.x_lo = 0.0;
+        P.x_hi = INFINITY;
+      }
       P.frame_ms = cfg->frame_ms;
       P.min_sil = cfg->min_silence_ms;
       P.min_seg = cfg->min_segment_ms;

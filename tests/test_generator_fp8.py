@@ -172,3 +172,94 @@ def test_fp8_forward_tracks_fp8_rounding_model(weights, gref):
     assert np.abs(u8.cpu().numpy().astype(int) - np.round(got.transpose(0, 2, 3, 1) * 255).astype(int)).max() <= 1
     eng.close()
     ctx.set_stream(None)
+
+
+TAIL0 = 46  # fd6.0: first layer of the fp8 tail (LSG_PREC_FP8_TAIL)
+
+
+def fp8_tail_rounding_model(gref, blob, mel, faces, absmax, tail0=TAIL0):
+    """LSG_PREC_FP8_TAIL's quantisation points: the fp16 rounding model up to
+    layer tail0 - 1, then cat[5] (whole) and cat[6]'s encoder slice
+    requantised to e4m3 with their calibrated scales, e4m3 weights and e4m3
+    stored outputs for the tail layers, out0 + out1 in f32."""
+    import torch
+    import torch.nn.functional as F
+    scale = np.maximum(absmax, 1e-6) * 1.1 / 448.0
+    h16 = lambda t: t.to(torch.float16).float()  # noqa: E731
+
+    def q8(t, s):
+        return (t / s).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).float() * s
+    layers = list(zip(gref.layer_table(), gref.split_blob(blob)))
+    li = [0]
+
+    def conv(x, fp8):
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        wq = _wq(torch, w, kind) if fp8 else h16(torch.from_numpy(np.ascontiguousarray(w)))
+        b = torch.from_numpy(np.ascontiguousarray(b))
+        y = F.conv2d(x, wq, b, s_, p) if kind == 0 else F.conv_transpose2d(x, wq, b, s_, p, op)
+        if res:
+            y = y + x
+        li[0] += 1
+        return torch.relu(y)
+    with torch.no_grad():
+        x = h16(torch.from_numpy(faces))
+        feats = []
+        for blk in gref.FACE:
+            for _ in blk:
+                x = h16(conv(x, False))
+            feats.append(x)
+        a = h16(torch.from_numpy(mel))
+        for _ in gref.AUDIO:
+            a = h16(conv(a, False))
+        x = a
+        for j, blk in enumerate(gref.DECODER):
+            for n, _ in enumerate(blk):
+                if li[0] < tail0:
+                    x = h16(conv(x, False))
+                else:
+                    tid = 2 + j if n == len(blk) - 1 else 9 + li[0]
+                    x = q8(conv(x, True), scale[tid])
+            x = torch.cat([x, feats.pop()], 1)
+            if j == 5:  # cat[5] -> e4m3 (the tail's input)
+                x = q8(x, scale[7])
+        # cat[6]: fd6.2's output is already e4m3 (scale 8); the fe0 slice is requantised
+        x = torch.cat([x[:, :64], q8(x[:, 64:], scale[8])], 1)
+        x = conv(x, True)  # out0: kept in f32 by the fused epilogue
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        y = F.conv2d(x, torch.from_numpy(np.ascontiguousarray(w)), torch.from_numpy(np.ascontiguousarray(b)))
+        return torch.sigmoid(y).numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [16, 128])
+def test_fp8_tail_meets_30db_floor(weights, gref, B):
+    """LSG_PREC_FP8_TAIL (config 4's fp8 generator): PSNR >= 30 dB vs the fp32
+    oracle on the [0,1] frames and on the u8 frames -- the stated fp8 floor
+    -- and within 1.5 dB of its CPU rounding model; at B=128 on a seeded
+    subset of one full launch."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8_TAIL)
+    rows, chunk_row, target, refs, ref_index = _inputs(B, 300 + B)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    out = torch.empty(B, 3, 96, 96, dtype=torch.float32, device="cuda")
+    u8 = torch.empty(B, 96, 96, 3, dtype=torch.uint8, device="cuda")
+    eng.forward_device(*[t.data_ptr() for t in d], out.data_ptr(), 0, B)
+    eng.forward_device(*[t.data_ptr() for t in d], u8.data_ptr(), 1, B)
+    torch.cuda.synchronize()
+    idx = list(range(B)) if B <= 16 else sorted({0, 1, 63, 64, 126, 127, 17, 90})
+    mel = np.stack([gref.mel_chunk(rows, int(chunk_row[b]))[None] for b in idx])
+    faces = np.stack([gref.face_input(target[b], refs[ref_index[b]]) for b in idx])
+    want = gref.forward(weights, mel, faces)
+    got = out.cpu().numpy()[idx]
+    p = gref.psnr(got, want)
+    pu8 = gref.psnr(u8.cpu().numpy()[idx].astype(np.float64) / 255.0, want.transpose(0, 2, 3, 1))
+    pm = gref.psnr(fp8_tail_rounding_model(gref, weights, mel, faces, eng.act_absmax), want)
+    print(f"fp8-tail B={B}: GPU {p:.2f} dB (u8 {pu8:.2f}), CPU rounding model {pm:.2f} dB")
+    assert p >= 30.0 and pu8 >= 30.0, (p, pu8)
+    assert p >= pm - 1.5, (p, pm)
+    eng.close()
+    ctx.set_stream(None)
