@@ -8,13 +8,15 @@
 //                       integer squares) and max|s|; 16-byte vector loads,
 //                       warp-shuffle reductions.  2 B/sample read, 16 B/frame
 //                       written (2.5% of the input).
-//   K2 seg_scan         one CTA per stream: the decaying-peak recurrence
-//                       (sequential by definition, one DMUL+DMAX per frame),
-//                       per-frame dB decisions in parallel (ballot-packed),
-//                       then the integer-millisecond state machine, which
-//                       fast-forwards over runs of frames that cannot raise
-//                       an event and steps event frames exactly like
-//                       process_frame (segmenter.cpp:51-99).
+//   K2a seg_peaks       the decaying-peak recurrence (sequential by
+//                       definition, one DMUL + compare per frame), one LANE
+//                       per stream;
+//   K2b seg_decide      per-frame dB decisions, thread per frame,
+//                       ballot-packed bit rows;
+//   K2c seg_machine     the integer-millisecond state machine, lane per
+//                       stream, fast-forwarding over runs of frames that
+//                       cannot raise an event and stepping event frames
+//                       exactly like process_frame (segmenter.cpp:51-99).
 //   K3 seg_carry        keeps each stream's sub-frame tail (stage_,
 //                       segmenter.cpp:40-48) on the device.
 //   K4 seg_collect      compacts cuts/flags/state into mapped pinned memory,
@@ -352,9 +354,6 @@ __device__ __forceinline__ bool vad_decide(long long sumsq, double peak, int n, 
 }
 
 // ---------------------------------------------------------------- K2 -----
-constexpr int K2_THREADS = 256;
-constexpr int K2_TILE = 2048;
-
 struct Machine {
   int64_t base, seg_start, pause_start, silence_run, consumed, emitted;
   double conf;
@@ -490,125 +489,126 @@ __device__ void run_machine(Machine& M, const Params& P, lsg_cut* cuts, int stre
   }
 }
 
-__global__ void __launch_bounds__(K2_THREADS)
-seg_scan(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, DevState* st,
-         lsg_cut* __restrict__ cuts_all, uint32_t* __restrict__ flags_all, Params P) {
-  __shared__ double s_peak[K2_TILE];
-  __shared__ uint32_t s_bits[K2_TILE / 32];
-  __shared__ int s_speech;
-  const Chunk c = chunks[blockIdx.x];
-  DevState* S = st + c.stream;
-  lsg_cut* cuts = cuts_all + (int64_t)c.stream * P.cut_cap;
-  uint32_t* flags = flags_all + (int64_t)c.stream * P.flag_words;
-  const int tid = threadIdx.x;
+// K2 runs as three launches so that only the two inherently sequential
+// recurrences are sequential, and those run ONE LANE PER STREAM (a warp
+// carries 32 streams' recurrences in one instruction stream):
+//   K2a seg_peaks    the decaying peak (vad.cpp:35-45): p = max(RN(p*c), m),
+//                    one DMUL + compare per frame and stream; peaks -> HBM;
+//   K2b seg_decide   every frame's decision in parallel (thread per frame),
+//                    ballot-packed into the stream's bit row;
+//   K2c seg_machine  the state machine over the bits (segmenter.cpp:51-99),
+//                    lane per stream, fast-forwarding event-free runs.
+constexpr int K2_LANES = 128;  // streams per K2a / K2c block
 
-  Machine M;
-  double peak;
-  if (tid == 0) {
-    if (c.first) {
-      S->base = c.start_ms;
-      S->seg_start = c.start_ms;
-    }
-    M.base = S->base;
-    M.seg_start = S->seg_start;
-    M.pause_start = S->pause_start;
-    M.silence_run = S->silence_run;
-    M.consumed = S->consumed;
-    M.emitted = S->emitted;
-    M.conf = S->cand_conf;
-    M.speech_seen = S->speech_seen;
-    M.cand_open = S->cand_open;
-    M.cand_cut = S->cand_cut;
-    M.n_pause = 0;
-    M.n_forced = 0;
-    M.n_cuts = S->n_cuts;  // cuts not collected yet stay in front (collection is deferred)
-    M.overflow = S->overflow;
-    peak = S->peak;
-    s_speech = 0;
-  }
+__global__ void __launch_bounds__(K2_LANES)
+seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict__ stats, DevState* st,
+          double* __restrict__ peaks, Params P) {
+  const int i = blockIdx.x * K2_LANES + threadIdx.x;
+  if (i >= nc) return;
+  const Chunk c = chunks[i];
+  DevState* S = st + c.stream;
   const FrameStat* fst = stats + c.frame_off;
-  for (int t0 = 0; t0 < c.nframes; t0 += K2_TILE) {
-    const int n = min(K2_TILE, c.nframes - t0);
-    // phase A: decaying peak (vad.cpp:35-45), sequential
-    for (int i = tid; i < n; i += K2_THREADS) s_peak[i] = (double)fst[t0 + i].fmax;
-    __syncthreads();
-    if (tid == 0) {
-      if (P.peak_mode == 0) {
-        // the chain is DMUL -> max per frame; frame maxima come in 8 at a
-        // time so shared-memory latency stays off it (n is a multiple of 8
-        // except in the last tile)
-        int i = 0;
-        for (; i + 8 <= n; i += 8) {
-          double m[8];
+  double* pk = peaks + c.frame_off;
+  double peak = S->peak;
+  const int n = c.nframes;
+  if (P.peak_mode == 0) {
+    const double decay = P.decay;
+    int f = 0;
+    // frame maxima are loaded 8 ahead of the chain (they do not depend on it)
+    for (; f + 8 <= n; f += 8) {
+      double m[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) m[k] = s_peak[i + k];
+      for (int k = 0; k < 8; ++k) m[k] = (double)__ldg(&fst[f + k].fmax);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            peak = __dmul_rn(peak, P.decay);
-            peak = m[k] > peak ? m[k] : peak;
-            m[k] = peak;
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) s_peak[i + k] = m[k];
-        }
-        for (; i < n; ++i) {
-          peak = __dmul_rn(peak, P.decay);
-          const double fm = s_peak[i];
-          peak = fm > peak ? fm : peak;
-          s_peak[i] = peak;
-        }
-      } else if (P.peak_mode == 1) {
-        for (int i = 0; i < n; ++i) {
-          const double fm = s_peak[i];
-          peak = fm > peak ? fm : peak;
-          s_peak[i] = peak;
-        }
-      } else {
-        for (int i = 0; i < n; ++i) s_peak[i] = peak;
+      for (int k = 0; k < 8; ++k) {
+        peak = __dmul_rn(peak, decay);
+        peak = m[k] > peak ? m[k] : peak;
+        pk[f + k] = peak;
       }
     }
-    __syncthreads();
-    // phase B: per-frame decisions in parallel, ballot-packed
-    int my_speech = 0;
-    for (int i0 = 0; i0 < n; i0 += K2_THREADS) {
-      const int i = i0 + tid;
-      bool sp = false;
-      if (i < n) sp = vad_decide(fst[t0 + i].sumsq, s_peak[i], P.fs, P.thr, P.x_lo, P.x_hi);
-      const unsigned bal = __ballot_sync(0xffffffffu, sp);
-      if ((tid & 31) == 0 && i < n) s_bits[i >> 5] = bal;
-      my_speech += sp;
+    for (; f < n; ++f) {
+      peak = __dmul_rn(peak, decay);
+      const double m = (double)__ldg(&fst[f].fmax);
+      peak = m > peak ? m : peak;
+      pk[f] = peak;
     }
-    atomicAdd(&s_speech, my_speech);
-    __syncthreads();
-    // phase C: state machine or flag export
-    if (P.flags_only) {
-      const int nw = (n + 31) >> 5;
-      for (int w = tid; w < nw; w += K2_THREADS) flags[(t0 >> 5) + w] = s_bits[w];
-    } else if (tid == 0) {
-      run_machine(M, P, cuts, c.stream, s_bits, n);
+  } else if (P.peak_mode == 1) {
+    for (int f = 0; f < n; ++f) {
+      const double m = (double)__ldg(&fst[f].fmax);
+      peak = m > peak ? m : peak;
+      pk[f] = peak;
     }
-    __syncthreads();
+  } else {
+    for (int f = 0; f < n; ++f) pk[f] = peak;
   }
-  if (tid == 0) {
-    if (P.flags_only) M.consumed += c.nframes;
-    S->peak = peak;
-    S->seg_start = M.seg_start;
-    S->pause_start = M.pause_start;
-    S->silence_run = M.silence_run;
-    S->consumed = M.consumed;
-    S->emitted = M.emitted;
-    S->cand_conf = M.conf;
-    S->speech_seen = M.speech_seen;
-    S->cand_open = M.cand_open;
-    S->cand_cut = M.cand_cut;
-    S->n_cuts = M.n_cuts;
-    S->overflow = M.overflow;
+  S->peak = peak;
+}
+
+__global__ void __launch_bounds__(256)
+seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, const double* __restrict__ peaks,
+           DevState* st, uint32_t* __restrict__ bits_all, Params P) {
+  const Chunk c = chunks[blockIdx.y];
+  const int f = blockIdx.x * 256 + threadIdx.x;
+  if (blockIdx.x * 256 >= c.nframes) return;  // whole block past the chunk (uniform)
+  bool sp = false;
+  if (f < c.nframes)
+    sp = vad_decide(stats[c.frame_off + f].sumsq, peaks[c.frame_off + f], P.fs, P.thr, P.x_lo, P.x_hi);
+  const unsigned bal = __ballot_sync(0xffffffffu, sp);
+  if ((threadIdx.x & 31) == 0) {
+    if (f < c.nframes) bits_all[(int64_t)c.stream * P.flag_words + (f >> 5)] = bal;
+    if (bal) atomicAdd(reinterpret_cast<unsigned long long*>(&st[c.stream].m_speech), (unsigned long long)__popc(bal));
+  }
+}
+
+__global__ void __launch_bounds__(K2_LANES)
+seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __restrict__ cuts_all,
+            const uint32_t* __restrict__ bits_all, Params P) {
+  const int i = blockIdx.x * K2_LANES + threadIdx.x;
+  if (i >= nc) return;
+  const Chunk c = chunks[i];
+  DevState* S = st + c.stream;
+  if (c.first) {
+    S->base = c.start_ms;
+    S->seg_start = c.start_ms;
+  }
+  if (P.flags_only) {  // the host runs the machine (scorer order): bits are the output
+    S->consumed += c.nframes;
     S->n_flag_frames = c.nframes;
     S->m_frames += c.nframes;
-    S->m_speech += s_speech;
-    S->m_pause += M.n_pause;
-    S->m_forced += M.n_forced;
+    return;
   }
+  Machine M;
+  M.base = S->base;
+  M.seg_start = S->seg_start;
+  M.pause_start = S->pause_start;
+  M.silence_run = S->silence_run;
+  M.consumed = S->consumed;
+  M.emitted = S->emitted;
+  M.conf = S->cand_conf;
+  M.speech_seen = S->speech_seen;
+  M.cand_open = S->cand_open;
+  M.cand_cut = S->cand_cut;
+  M.n_pause = 0;
+  M.n_forced = 0;
+  M.n_cuts = S->n_cuts;  // cuts not collected yet stay in front (collection is deferred)
+  M.overflow = S->overflow;
+  run_machine(M, P, cuts_all + (int64_t)c.stream * P.cut_cap, c.stream,
+              bits_all + (int64_t)c.stream * P.flag_words, c.nframes);
+  S->seg_start = M.seg_start;
+  S->pause_start = M.pause_start;
+  S->silence_run = M.silence_run;
+  S->consumed = M.consumed;
+  S->emitted = M.emitted;
+  S->cand_conf = M.conf;
+  S->speech_seen = M.speech_seen;
+  S->cand_open = M.cand_open;
+  S->cand_cut = M.cand_cut;
+  S->n_cuts = M.n_cuts;
+  S->overflow = M.overflow;
+  S->n_flag_frames = c.nframes;
+  S->m_frames += c.nframes;
+  S->m_pause += M.n_pause;
+  S->m_forced += M.n_forced;
 }
 
 // ---------------------------------------------------------------- K3 -----
@@ -749,6 +749,7 @@ struct lsg_seg_s {
   DevBuf<lsg_cut> cuts;
   DevBuf<uint32_t> flags;
   DevBuf<FrameStat> stats;
+  DevBuf<double> peaks;  // K2a -> K2b: every frame's decayed peak
   DevBuf<Chunk> chunks_dev;
   DevBuf<int16_t> staging;
   DevBuf<int32_t> streams_dev;
@@ -909,6 +910,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->cuts.alloc((size_t)n_streams * P.cut_cap);
       h->flags.alloc((size_t)n_streams * P.flag_words);
       h->stats.alloc((size_t)n_streams * h->max_frames_push);
+      h->peaks.alloc((size_t)n_streams * h->max_frames_push);
       h->chunks_dev.alloc(n_streams);
       // each staged chunk starts 64-sample (128 B) aligned: <= one chunk per
       // stream per push, each rounded up to 64 samples
@@ -1074,8 +1076,15 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       LSG_CUDA(cudaEventRecord(h->k1b, ctx->stream));
       h->k1_recorded = true;
     }
-    seg_scan<<<nc, K2_THREADS, 0, ctx->stream>>>(h->chunks_dev.p, h->stats.p, h->st.p, h->cuts.p,
-                                                 h->flags.p, P);
+    const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
+    seg_peaks<<<g2, K2_LANES, 0, ctx->stream>>>(h->chunks_dev.p, nc, h->stats.p, h->st.p, h->peaks.p, P);
+    LSG_LAUNCHED(ctx);
+    if (max_frames > 0) {
+      seg_decide<<<dim3((unsigned)ceil_div(max_frames, 256), (unsigned)nc), 256, 0, ctx->stream>>>(
+          h->chunks_dev.p, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P);
+      LSG_LAUNCHED(ctx);
+    }
+    seg_machine<<<g2, K2_LANES, 0, ctx->stream>>>(h->chunks_dev.p, nc, h->st.p, h->cuts.p, h->flags.p, P);
     LSG_LAUNCHED(ctx);
     seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     LSG_LAUNCHED(ctx);
