@@ -452,6 +452,8 @@ def main():
         out["stage_rooflines"] = scaled
     if cfg4:
         out["config4_fp8"] = cfg4
+    if world == 1 and not args.no_cpu_baseline:
+        out.update(config12_leg(args, local, torch, ctx, torch_stream, api, eng, weights))
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
         rs = args.ref_streams or threads
@@ -714,6 +716,124 @@ def scaled_leg(args, local, torch, ctx, stream, api):
     }
 
 
+def config12_leg(args, local, torch, ctx, stream, api, eng, weights):
+    """Configs 1 and 2 as BASELINE.json states them, next to the reference's
+    CPU path on this host (rank 0, N = 1).
+      config 2: segmenter + 80-bin log-mel over 8 x 60 s streams (the
+        bench's stream patterns), device-resident PCM, one push + finish for
+        all 8 streams and one mel launch for all their segments (device
+        events; the 15 MB fit in L2 -- the scaled set in stage_rooflines is
+        the roofline measurement); the reference's Segmenter + compute_mel
+        (oracle/_ref) on the same streams, one per host thread.
+      config 1: the stock 10 s stream's 258 frames (tests/golden/gen_config1:
+        reference-built inputs), generator batches of 16: the fp32 CPU
+        oracle (oracle/generator_ref.py, all host threads) vs our fp16
+        lsg_gen_forward on the same batches."""
+    import concurrent.futures as cf
+    import importlib.util
+    from paper_2512_18318_b200.api import MelConfig, MelExtractor, MultiStreamSegmenter, SegmenterConfig
+    dev = f"cuda:{local}"
+    S, n = 8, 60 * 16000
+    pcm = [api.synth_pattern(*stream_pattern(i + 1), 60_000)[:n] for i in range(S)]
+    pcm_dev = torch.from_numpy(np.stack(pcm)).to(dev)
+    seg = MultiStreamSegmenter(SegmenterConfig(), S, n, ctx=ctx)
+    mel = MelExtractor(MelConfig(), max_frames=1 << 16, ctx=ctx)
+    base = pcm_dev.data_ptr()
+    seg_args = seg.push_args(list(range(S)), [(base + s * n * 2, n) for s in range(S)], [0] * S)
+    rows = torch.empty((S * 3800, 80), dtype=torch.float32, device=dev)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    t_seg, t_mel = [], []
+    with torch.cuda.stream(stream):
+        ctx.set_stream(stream.cuda_stream)
+        for rep in range(5):
+            ctx.lib.call("lsg_seg_reset", seg.h)
+            e0.record(stream)
+            seg.push_finish_prepared(seg_args)
+            e1.record(stream)
+            cuts = seg.take_all_cuts()
+            offs = [c.stream * n + c.sample_off for c in cuts]
+            lens = [c.sample_len for c in cuts]
+            fr = [0 if ln < 1024 else 1 + (ln - 1024) // 256 for ln in lens]
+            r0 = list(np.cumsum([0] + fr[:-1]))
+            e1b = torch.cuda.Event(enable_timing=True)
+            e1b.record(stream)
+            mel.batch_device(base, offs, lens, rows.data_ptr(), r0)
+            e2.record(stream)
+            stream.synchronize()
+            if rep:
+                t_seg.append(e0.elapsed_time(e1))
+                t_mel.append(e1b.elapsed_time(e2))
+    gpu2 = {"segments": len(cuts), "mel_frames": int(sum(fr)), "segmenter_ms": float(np.median(t_seg)),
+            "mel_ms": float(np.median(t_mel)), "total_ms": float(np.median(t_seg) + np.median(t_mel))}
+    # reference CPU path on the same 8 streams
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _oracle import Reference
+    ref = Reference()
+
+    def segmel(p):
+        cs, _, _ = ref.segment(p)
+        for c in cs:
+            ref.compute_mel(p[c["sample_off"]:c["sample_off"] + c["sample_len"]])
+        return len(cs)
+    with cf.ThreadPoolExecutor(max_workers=S) as ex:
+        list(ex.map(segmel, pcm))  # warm
+        t0 = time.perf_counter()
+        nseg_ref = sum(ex.map(segmel, pcm))
+        t_cpu2 = (time.perf_counter() - t0) * 1e3
+    out = {"config2": {"workload": "8 x 60 s 16 kHz streams: segmenter + 80-bin log-mel", "gpu": gpu2,
+                       "cpu_reference_ms": t_cpu2, "cpu_threads": S, "cpu_segments": nseg_ref,
+                       "speedup": t_cpu2 / gpu2["total_ms"]}}
+    # ---- config 1
+    gpath = os.path.join(ROOT, "tests", "golden", "gen_config1.npz")
+    if not os.path.exists(gpath):
+        return out
+    g = np.load(gpath)
+    recs, mel_rows, face = g["records"], g["mel_rows"], g["ref_face"]
+    from paper_2512_18318_b200 import generator
+    J = len(recs)
+    tgt = np.stack([generator.jitter_face(face, int(r[1]), 1) for r in recs])
+    spec = importlib.util.spec_from_file_location("generator_ref", os.path.join(ROOT, "oracle", "generator_ref.py"))
+    gref = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gref)
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    melc = np.stack([gref.mel_chunk(mel_rows, int(r[4] + r[3]))[None] for r in recs])
+    faces = np.stack([gref.face_input(tgt[b], face) for b in range(J)])
+    gref.forward(weights, melc[:2], faces[:2])
+    t0 = time.perf_counter()
+    for b0 in range(0, J, 16):
+        gref.forward(weights, melc[b0:b0 + 16], faces[b0:b0 + 16])
+    t_cpu1 = time.perf_counter() - t0
+    d_rows = torch.from_numpy(np.ascontiguousarray(mel_rows)).to(dev)
+    d_chunk = torch.from_numpy((recs[:, 4] + recs[:, 3]).astype(np.int32)).to(dev)
+    d_tgt = torch.from_numpy(tgt).to(dev)
+    d_ref = torch.from_numpy(face[None].copy()).to(dev)
+    d_ridx = torch.zeros(16, dtype=torch.int32, device=dev)
+    d_out = torch.empty((J, 96, 96, 3), dtype=torch.uint8, device=dev)
+    eng16 = generator.LipsyncEngine(weights, max_batch=16, ctx=ctx, precision=1)
+
+    def gpu_run():
+        for b0 in range(0, J, 16):
+            B = min(16, J - b0)
+            eng16.forward_device(d_rows.data_ptr(), d_chunk[b0:].data_ptr(), d_tgt[b0:].data_ptr(), d_ref.data_ptr(),
+                                 d_ridx.data_ptr(), d_out[b0:].data_ptr(), 1, B)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            gpu_run()
+        e0.record(stream)
+        for _ in range(5):
+            gpu_run()
+        e1.record(stream)
+        stream.synchronize()
+    ms1 = e0.elapsed_time(e1) / 5
+    eng16.close()
+    out["config1"] = {"workload": "stock 10 s stream, 258 frames, generator batches of 16 (tests/golden/gen_config1)",
+                      "cpu_oracle_s": t_cpu1, "cpu_oracle_fps": J / t_cpu1, "cpu_threads": threads,
+                      "cpu_kind": "fp32 CPU restatement (oracle/generator_ref.py; the reference has no generator)",
+                      "gpu_ms": ms1, "gpu_fps": J / (ms1 / 1e3), "gpu_dtype": "fp16, batches of 16 (17 launches)"}
+    return out
+
+
 def fp8_peaks():
     path = os.path.join(ROOT, "profiles", "r01_fp8_peak.json")
     try:
@@ -732,7 +852,9 @@ def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generat
     against the measured fp8 tensor peak."""
     from paper_2512_18318_b200.pipeline import Pipeline, PipelineConfig
     S, secs = args.config4_streams, 30
-    eng8 = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
+    # the fp8 engine at the stated floor (>= 30 dB vs the fp32 oracle): fp16 up
+    # to fd5.2, e4m3 for fd6.0..out0 (DESIGN.md §4, BASELINE.md §6)
+    eng8 = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8_TAIL)
     pcm, video, refs = make_workload(rank, S, secs, fps, api, generator, world, seed_base=2000)
     pipe = Pipeline(PipelineConfig(len(pcm), secs * 1000, fps, 50, 128, True), eng8, ctx=ctx)
     dev = f"cuda:{local}"
@@ -762,14 +884,21 @@ def config4_leg(args, rank, world, local, dist, torch, ctx, stream, api, generat
     gms = measure_generator(eng8, torch, stream, local, 128, reps=20)
     burst, sust, src = fp8_peaks()
     tf = FLOPS_PER_FRAME * 128 / (gms / 1e3) / 1e12
+    # all-fp8 engine for reference (no usable accuracy floor on this network)
+    eng_all8 = generator.LipsyncEngine(weights, max_batch=128, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8)
+    all8_ms = measure_generator(eng_all8, torch, stream, local, 128, reps=20)
+    eng_all8.close()
     out = {"workload": f"config 4: fp8 generator, {S} streams x {secs} s sharded s mod {world}, unpaced, batch 128",
-           "dtype": "fp8_e4m3 (f32 accumulate)", "value": frames / (ms / 1e3), "unit": "frames/s",
+           "dtype": "fp16 head + fp8_e4m3 tail fd6.0..out0 (f32 accumulate; LSG_PREC_FP8_TAIL)",
+           "value": frames / (ms / 1e3), "unit": "frames/s",
            "ms_per_step": ms, "frames_per_step": frames,
            "generator_b128": {"ms": gms, "frames_per_s": 128 / (gms / 1e3), "achieved_tflops": tf,
                               "peak_tflops": sust, "frac": tf / sust, "frac_vs_burst": tf / burst,
                               "peak_source": src},
-           "quality": "per-layer exact up to e4m3 output rounding; end to end tracks the CPU fp8 rounding model "
-                      "(tests/test_generator_fp8.py)"}
+           "quality": ">= 30 dB PSNR vs the fp32 oracle (30.8 dB at B=128), tracks its CPU rounding model "
+                      "(tests/test_generator_fp8.py::test_fp8_tail_meets_30db_floor)",
+           "all_fp8_b128": {"ms": all8_ms, "frames_per_s": 128 / (all8_ms / 1e3),
+                            "note": "e4m3 in every layer: ~16 dB vs fp32 on this network, no usable floor"}}
     pipe.close()
     eng8.close()
     return out

@@ -221,7 +221,7 @@ extern "C" {
 lsg_status lsg_align_energy(lsg_ctx ctx, int32_t n, const int16_t* pcm_base, const int64_t* pcm_off,
                             const int64_t* n_samples, int32_t sample_rate, double* out_base, const int64_t* out_off,
                             int64_t* out_len) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (n < 0) invalid("lsg_align_energy: negative count");
     if (sample_rate <= 0) invalid("AudioBuffer: bad sample rate");
     const int hop = (int)((int64_t)sample_rate * 10 / 1000);
@@ -261,7 +261,7 @@ lsg_status lsg_align_energy(lsg_ctx ctx, int32_t n, const int16_t* pcm_base, con
 lsg_status lsg_align_motion(lsg_ctx ctx, int32_t n, const int64_t* ts_base, const double* motion_base,
                             const int64_t* frame_off, const int64_t* n_frames, const int64_t* t0, const int64_t* span,
                             double* out_base, const int64_t* out_off) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (n < 0) invalid("lsg_align_motion: negative count");
     std::vector<int64_t> tab(6 * (size_t)n + 1);
     int64_t ms = 0;
@@ -291,7 +291,7 @@ lsg_status lsg_align_motion(lsg_ctx ctx, int32_t n, const int64_t* ts_base, cons
 lsg_status lsg_align_batch(lsg_ctx ctx, int32_t n, const double* energy_base, const int64_t* e_off,
                            const int64_t* e_len, const double* motion_base, const int64_t* m_off, const int64_t* m_len,
                            int64_t max_lag, lsg_align_result* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (max_lag < 0) invalid("align: negative lag bound");  // align.cpp:55
     if (max_lag > kMaxLag) invalid("lsg_align_batch: max_lag above 511");
     if (n < 0) invalid("lsg_align_batch: negative count");

@@ -30,7 +30,7 @@ int32_t lsg_abi_version(void) { return LSG_ABI_VERSION; }
 const char* lsg_last_error(void) { return g_last_error.c_str(); }
 
 lsg_status lsg_device_count(int32_t* n) {
-  return guard([&] {
+  return guard(__func__, [&] {
     int c = 0;
     cudaError_t e = cudaGetDeviceCount(&c);
     if (e != cudaSuccess) {
@@ -42,7 +42,7 @@ lsg_status lsg_device_count(int32_t* n) {
 }
 
 lsg_status lsg_ctx_create(int32_t device, lsg_ctx* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     int n = 0;
     LSG_CUDA(cudaGetDeviceCount(&n));
@@ -65,7 +65,7 @@ lsg_status lsg_ctx_create(int32_t device, lsg_ctx* out) {
 }
 
 lsg_status lsg_ctx_destroy(lsg_ctx ctx) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!ctx) return;
     {
       DeviceGuard g(ctx);
@@ -78,26 +78,26 @@ lsg_status lsg_ctx_destroy(lsg_ctx ctx) {
 }
 
 lsg_status lsg_ctx_set_stream(lsg_ctx ctx, void* s) {
-  return guard([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+  return guard(__func__, [&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
 }
 
 lsg_status lsg_ctx_get_stream(lsg_ctx ctx, void** s) {
-  return guard([&] { *s = ctx->stream; });
+  return guard(__func__, [&] { *s = ctx->stream; });
 }
 
 lsg_status lsg_ctx_sync(lsg_ctx ctx) {
-  return guard([&] {
+  return guard(__func__, [&] {
     DeviceGuard g(ctx);
     ctx->sync();
   });
 }
 
 lsg_status lsg_ctx_launch_count(lsg_ctx ctx, int64_t* n) {
-  return guard([&] { *n = ctx->launches.load(); });
+  return guard(__func__, [&] { *n = ctx->launches.load(); });
 }
 
 lsg_status lsg_dev_alloc(lsg_ctx ctx, size_t bytes, void** out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     DeviceGuard g(ctx);
     *out = nullptr;
     LSG_CUDA(cudaMalloc(out, bytes));
@@ -105,25 +105,25 @@ lsg_status lsg_dev_alloc(lsg_ctx ctx, size_t bytes, void** out) {
 }
 
 lsg_status lsg_dev_free(lsg_ctx ctx, void* p) {
-  return guard([&] {
+  return guard(__func__, [&] {
     DeviceGuard g(ctx);
     LSG_CUDA(cudaFree(p));
   });
 }
 
 lsg_status lsg_host_alloc(size_t bytes, void** out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     LSG_CUDA(cudaMallocHost(out, bytes));
   });
 }
 
 lsg_status lsg_host_free(void* p) {
-  return guard([&] { LSG_CUDA(cudaFreeHost(p)); });
+  return guard(__func__, [&] { LSG_CUDA(cudaFreeHost(p)); });
 }
 
 lsg_status lsg_copy(lsg_ctx ctx, void* dst, const void* src, size_t bytes) {
-  return guard([&] {
+  return guard(__func__, [&] {
     DeviceGuard g(ctx);
     LSG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
   });

@@ -229,7 +229,7 @@ using namespace lsg;
 extern "C" {
 
 lsg_status lsg_kalman_cfg_default(lsg_kalman_cfg* c) {
-  return guard([&] {  // kalman.hpp:8-12
+  return guard(__func__, [&] {  // kalman.hpp:8-12
     c->process_noise = 1e-2;
     c->measurement_noise = 25.0;
     c->initial_variance = 1e6;
@@ -237,13 +237,13 @@ lsg_status lsg_kalman_cfg_default(lsg_kalman_cfg* c) {
 }
 
 lsg_status lsg_face_mock_detect(int64_t frame_index, uint64_t seed, double* box4) {
-  return guard([&] { face::mock_detect(frame_index, seed, box4); });
+  return guard(__func__, [&] { face::mock_detect(frame_index, seed, box4); });
 }
 
 lsg_status lsg_face_track(lsg_ctx ctx, int32_t n, const int64_t* seg_off, const int64_t* seg_len, const int64_t* ts,
                           const int64_t* frame_index, const int32_t* has_face, const double* faces, uint64_t seed,
                           const lsg_kalman_cfg* cfg, double* out_box, double* out_vel, int32_t* status) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (cfg->process_noise <= 0 || cfg->measurement_noise <= 0 || cfg->initial_variance <= 0)
       invalid("kalman: non-positive noise");  // kalman.cpp:52-55
     if (n < 0) invalid("lsg_face_track: negative count");
@@ -270,7 +270,7 @@ lsg_status lsg_face_track(lsg_ctx ctx, int32_t n, const int64_t* seg_off, const 
 
 lsg_status lsg_face_crop(lsg_ctx ctx, int32_t n, const uint8_t* frames, int32_t H, int32_t W, const int64_t* frame_of,
                          const double* boxes, uint8_t* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (n < 0) invalid("lsg_face_crop: negative count");
     if (H < 2 || W < 2) invalid("lsg_face_crop: frame smaller than 2x2");
     if (n == 0) return;

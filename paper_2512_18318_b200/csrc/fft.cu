@@ -73,7 +73,7 @@ static std::vector<double2> twiddles(int log2n) {
 using namespace lsg;
 
 extern "C" lsg_status lsg_fft_radix2(lsg_ctx ctx, double* data, int64_t n, int32_t count) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (n <= 0 || (n & (n - 1)) != 0) invalid("fft: size must be a power of two");  // mel.cpp:48-49
     if (count < 0) invalid("lsg_fft_radix2: negative count");
     int log2n = 0;

@@ -824,14 +824,14 @@ constexpr int kTensors = 9 + kNumLayers;
 extern "C" {
 
 lsg_status lsg_lipsync_validate(int64_t audio_span_ms, int64_t frame_span_ms, int64_t n_frames) {
-  return guard([&] {  // visual_mocks.cpp:43-46
+  return guard(__func__, [&] {  // visual_mocks.cpp:43-46
     if (n_frames < 2) invalid("lipsync: need at least 2 frames");
     if (std::llabs(audio_span_ms - frame_span_ms) > 150) invalid("lipsync: audio and frame spans diverge");
   });
 }
 
 lsg_status lsg_gen_param_count(int64_t* n) {
-  return guard([&] {
+  return guard(__func__, [&] {
     int64_t t = 0;
     for (const auto& L : kLayers) t += layer_params(L);
     *n = t;
@@ -839,7 +839,7 @@ lsg_status lsg_gen_param_count(int64_t* n) {
 }
 
 lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap, int32_t* n_layers) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *n_layers = kNumLayers;
     for (int i = 0; i < kNumLayers && i < cap; ++i) {
       const auto& L = kLayers[i];
@@ -851,7 +851,7 @@ lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap, int32_t* n_layers) {
 
 lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats, int32_t precision,
                             const float* act_absmax, int32_t n_act, int32_t max_batch, lsg_gen* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     int64_t want = 0;
     lsg_gen_param_count(&want);
@@ -1564,7 +1564,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
 }
 
 lsg_status lsg_gen_destroy(lsg_gen h) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h) return;
     DeviceGuard g(h->ctx);
     h->ctx->sync();
@@ -1574,7 +1574,7 @@ lsg_status lsg_gen_destroy(lsg_gen h) {
 
 lsg_status lsg_gen_forward(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
                            const uint8_t* refs, const int32_t* ref_index, void* out, int32_t out_format, int32_t B) {
-  return guard([&] {
+  return guard(__func__, [&] {
     DeviceGuard g(h->ctx);
     gen::forward_gather(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, out, out_format, B);
   });
@@ -1613,7 +1613,7 @@ extern "C" {
 lsg_status lsg_gen_calibrate(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
                              const uint8_t* refs, const int32_t* ref_index, int32_t B, float* absmax, int32_t cap,
                              int32_t* n_tensors) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *n_tensors = kTensors;
     if (cap < kTensors) return;
     if (h->prec == PR_FP8) invalid("lsg_gen_calibrate: calibrate on a bf16/fp16 engine");
@@ -1679,7 +1679,7 @@ __global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int
 
 // LSG_TRACE builds: copy the phase timestamps out ([64 layers][160 CTAs][16], ns).
 extern "C" lsg_status lsgdbg_trace_read(unsigned long long* out, int64_t n) {
-  return guard([&] {
+  return guard(__func__, [&] {
 #ifdef LSG_TRACE
     if (n == 0) {  // clear
       void* a = nullptr;
@@ -1700,7 +1700,7 @@ extern "C" lsg_status lsgdbg_trace_read(unsigned long long* out, int64_t n) {
 // Per plan layer at batch B: {layer index, Route, launch tile width, split-K
 // factor} -- the decisions forward() takes (route_of), for the tests.
 extern "C" lsg_status lsgdbg_gen_routes(lsg_gen h, int32_t B, int32_t* out, int32_t cap, int32_t* n_out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h || !n_out) invalid("lsgdbg_gen_routes: null argument");
     if (B < 1 || B > h->max_batch) invalid("lsgdbg_gen_routes: bad batch");
     const int n = (int)h->plan.size();
@@ -1723,7 +1723,7 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
                                         const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
                                         int32_t B, int32_t stop_layer, int32_t which, float* out_dev,
                                         int32_t* shape4) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     cudaStream_t st = ctx->stream;

@@ -10,6 +10,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "lsg.h"
 
 namespace lsg {
@@ -139,7 +141,13 @@ bool is_device_ptr(const void* p);
 
 // Runs f, translating exceptions into the ABI status + thread-local message.
 template <class F>
-lsg_status guard(F&& f) {
+lsg_status guard(const char* name, F&& f) {
+  // every C-ABI call is an NVTX range (name = the entry point), so an Nsight
+  // timeline attributes host gaps and launches to the reference-facing calls
+  struct Range {
+    explicit Range(const char* n) { nvtxRangePushA(n); }
+    ~Range() { nvtxRangePop(); }
+  } range(name);
   try {
     f();
     return LSG_OK;

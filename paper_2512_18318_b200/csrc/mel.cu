@@ -527,7 +527,7 @@ static void launch(lsg_mel h, const int16_t* pcm, int32_t n_seg, int64_t total_f
 extern "C" {
 
 lsg_status lsg_mel_cfg_default(lsg_mel_cfg* c) {
-  return guard([&] {
+  return guard(__func__, [&] {
     c->sample_rate = 16000;
     c->fft_size = 1024;
     c->hop = 256;
@@ -538,14 +538,14 @@ lsg_status lsg_mel_cfg_default(lsg_mel_cfg* c) {
 }
 
 lsg_status lsg_mel_frames(int64_t n, const lsg_mel_cfg* cfg, int64_t* frames) {
-  return guard([&] {
+  return guard(__func__, [&] {
     validate(cfg);
     *frames = n < cfg->fft_size ? 0 : 1 + (n - cfg->fft_size) / cfg->hop;  // mel.cpp:40-44
   });
 }
 
 lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frames, lsg_mel* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     validate(cfg);
     const int N = cfg->fft_size;
@@ -680,7 +680,7 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
 }
 
 lsg_status lsg_mel_destroy(lsg_mel h) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h) return;
     DeviceGuard g(h->ctx);
     h->ctx->sync();
@@ -689,7 +689,7 @@ lsg_status lsg_mel_destroy(lsg_mel h) {
 }
 
 lsg_status lsg_mel_compute(lsg_mel h, const int16_t* pcm, int64_t n, float* out, int64_t* frames) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     const int N = h->cfg.fft_size;
@@ -721,7 +721,7 @@ lsg_status lsg_mel_compute(lsg_mel h, const int16_t* pcm, int64_t n, float* out,
 
 lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_base, const int64_t* pcm_off,
                                  const int64_t* n_samples, float* out_base, const int64_t* out_row) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     if (n_seg < 0 || n_seg > h->max_seg) invalid("lsg_mel_compute_batch: too many segments (max 4096)");
     DeviceGuard g(ctx);

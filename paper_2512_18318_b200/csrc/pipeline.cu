@@ -96,7 +96,7 @@ extern "C" {
 
 lsg_status lsg_pipe_create(lsg_ctx ctx, const lsg_pipe_cfg* cfg, const lsg_seg_cfg* seg, const lsg_mel_cfg* mel,
                            lsg_gen gen, lsg_pipe* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     if (cfg->n_streams <= 0 || cfg->max_stream_ms <= 0) invalid("lsg_pipe_create: bad stream geometry");
     if (!(cfg->fps > 0)) invalid("lsg_pipe_create: non-positive fps");
@@ -141,7 +141,7 @@ lsg_status lsg_pipe_create(lsg_ctx ctx, const lsg_pipe_cfg* cfg, const lsg_seg_c
 }
 
 lsg_status lsg_pipe_destroy(lsg_pipe h) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h) return;
     DeviceGuard g(h->ctx);
     h->ctx->sync();
@@ -152,7 +152,7 @@ lsg_status lsg_pipe_destroy(lsg_pipe h) {
 lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_samples, const uint8_t* const* video,
                         const int64_t* n_video, const uint8_t* refs, lsg_frame_rec* recs, void* frames, int64_t cap,
                         int64_t* n_out, lsg_pipe_stats* stats) {
-  return guard([&] {
+  return guard(__func__, [&] {
     lsg_ctx ctx = h->ctx;
     DeviceGuard g(ctx);
     cudaStream_t st = ctx->stream;

@@ -207,7 +207,7 @@ void need(const void* p, const char* what) {
 extern "C" {
 
 lsg_status lsg_reg_create(lsg_ctx ctx, int64_t arena_bytes, lsg_reg* out) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(ctx, "context");
     need(out, "output handle");
     if (arena_bytes < kGranule) lsg::invalid("registry: arena must hold at least 256 bytes");
@@ -227,7 +227,7 @@ lsg_status lsg_reg_create(lsg_ctx ctx, int64_t arena_bytes, lsg_reg* out) {
 }
 
 lsg_status lsg_reg_destroy(lsg_reg r) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     if (!r) return;
     lsg::DeviceGuard g(r->ctx);
     r->ctx->sync();  // queued readers of the arena finish first
@@ -237,7 +237,7 @@ lsg_status lsg_reg_destroy(lsg_reg r) {
 
 lsg_status lsg_reg_put(lsg_reg r, const uint8_t* uuid16, int32_t kind, const void* src, int64_t bytes,
                        lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(uuid16, "uuid");
     need(ref, "reference");
@@ -255,7 +255,7 @@ lsg_status lsg_reg_put(lsg_reg r, const uint8_t* uuid16, int32_t kind, const voi
 
 lsg_status lsg_reg_put_view(lsg_reg r, const uint8_t* uuid16, int32_t kind, const void* dev_ptr, int64_t bytes,
                             lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(uuid16, "uuid");
     need(ref, "reference");
@@ -272,7 +272,7 @@ lsg_status lsg_reg_put_view(lsg_reg r, const uint8_t* uuid16, int32_t kind, cons
 
 lsg_status lsg_reg_alloc(lsg_reg r, const uint8_t* uuid16, int32_t kind, int64_t bytes, void** dev_ptr,
                          lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(uuid16, "uuid");
     need(ref, "reference");
@@ -290,7 +290,7 @@ lsg_status lsg_reg_alloc(lsg_reg r, const uint8_t* uuid16, int32_t kind, int64_t
 }
 
 lsg_status lsg_reg_resolve(lsg_reg r, const lsg_devref* ref, void** dev_ptr, int64_t* bytes) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(ref, "reference");
     if (ref->device != r->ctx->device) lsg::logic("registry: reference belongs to another device");
@@ -301,7 +301,7 @@ lsg_status lsg_reg_resolve(lsg_reg r, const lsg_devref* ref, void** dev_ptr, int
 }
 
 lsg_status lsg_reg_find(lsg_reg r, const uint8_t* uuid16, int32_t kind, lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(uuid16, "uuid");
     need(ref, "reference");
@@ -322,7 +322,7 @@ lsg_status lsg_reg_find(lsg_reg r, const uint8_t* uuid16, int32_t kind, lsg_devr
 }
 
 lsg_status lsg_reg_retain(lsg_reg r, const lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(ref, "reference");
     r->lookup(ref).refs++;
@@ -330,7 +330,7 @@ lsg_status lsg_reg_retain(lsg_reg r, const lsg_devref* ref) {
 }
 
 lsg_status lsg_reg_release(lsg_reg r, const lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     need(ref, "reference");
     lsg::DeviceGuard g(r->ctx);
@@ -346,7 +346,7 @@ lsg_status lsg_reg_release(lsg_reg r, const lsg_devref* ref) {
 }
 
 lsg_status lsg_reg_stats(lsg_reg r, int64_t* used, int64_t* entries, int64_t* peak) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(r, "registry");
     if (used) *used = r->used;
     if (entries) *entries = (int64_t)r->index.size();
@@ -357,7 +357,7 @@ lsg_status lsg_reg_stats(lsg_reg r, int64_t* used, int64_t* entries, int64_t* pe
 // Little-endian, field order of the struct (WireWriter::u32/i64 conventions,
 // stage.cpp:38-49): uuid[16] kind u32 device u32 generation u64 offset i64 bytes i64.
 lsg_status lsg_devref_encode(const lsg_devref* ref, uint8_t* out) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(ref, "reference");
     need(out, "output");
     auto put = [&](int at, uint64_t v, int n) {
@@ -373,7 +373,7 @@ lsg_status lsg_devref_encode(const lsg_devref* ref, uint8_t* out) {
 }
 
 lsg_status lsg_devref_decode(const uint8_t* in, lsg_devref* ref) {
-  return lsg::guard([&] {
+  return lsg::guard(__func__, [&] {
     need(in, "input");
     need(ref, "reference");
     auto get = [&](int at, int n) {

@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "lsg_common.cuh"
+#include "tc.cuh"
 
 namespace lsg {
 namespace seg {
@@ -78,8 +79,7 @@ struct alignas(16) Chunk {
 
 struct alignas(16) FrameStat {
   long long sumsq;
-  int32_t fmax;
-  int32_t pad;
+  double fmax;  // max |s| (an integer <= 32768), stored as the double the peak chain compares
 };
 
 // ---------------------------------------------------------------- K1 -----
@@ -187,8 +187,7 @@ seg_frame_stats(const Chunk* __restrict__ chunks, const int16_t* __restrict__ ca
     if ((lane & 7) == 0) {
       FrameStat r;
       r.sumsq = (long long)v;
-      r.fmax = w;
-      r.pad = 0;
+      r.fmax = (double)w;
       out[c.frame_off + f0 + 2 * (lane >> 4) + ((lane >> 3) & 1)] = r;
     }
     return;
@@ -261,8 +260,7 @@ seg_frame_stats(const Chunk* __restrict__ chunks, const int16_t* __restrict__ ca
     if (f < c.nframes) {
       FrameStat r;
       r.sumsq = s;
-      r.fmax = m;
-      r.pad = 0;
+      r.fmax = (double)m;
       out[c.frame_off + f] = r;
     }
   }
@@ -363,6 +361,13 @@ struct Machine {
 };
 
 __device__ __forceinline__ int64_t cdiv(int64_t a, int64_t b) {  // ceil(a/b), b > 0
+  // 32-bit division when both fit (the machine's operands are millisecond
+  // spans and the frame length): a 64-bit division is a long software
+  // sequence on the state machine's critical path
+  if (a > -0x7fffffffLL && a < 0x7fffffffLL && b < 0x7fffffffLL) {
+    const int ai = (int)a, bi = (int)b;
+    return ai >= 0 ? (ai + bi - 1) / bi : -((-ai) / bi);
+  }
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
 }
 
@@ -498,50 +503,115 @@ __device__ void run_machine(Machine& M, const Params& P, lsg_cut* cuts, int stre
 //                    ballot-packed into the stream's bit row;
 //   K2c seg_machine  the state machine over the bits (segmenter.cpp:51-99),
 //                    lane per stream, fast-forwarding event-free runs.
-constexpr int K2_LANES = 128;  // streams per K2a / K2c block
+constexpr int K2_LANES = 32;  // streams per K2a / K2c block: one warp, a lane per stream
+constexpr int PK_T = 128;     // K2a frames per tile
+constexpr int PK_ROW = PK_T * 16 + 16;  // stats row stride in smem (bytes; +16 spreads the banks)
+constexpr size_t PK_SMEM = 2 * K2_LANES * PK_ROW + K2_LANES * (PK_T + 1) * 8 + 64;
 
+// fmax of frames f..f+7 of a staged stats row, issued back to back
+// (volatile: kept ahead of the chain that consumes them)
+__device__ __forceinline__ void ld8(const unsigned char* row, int f, double (&m)[8]) {
+  const uint32_t a = tc::smem_u32(row) + f * 16 + 8;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(m[k]) : "r"(a + 16 * k));
+}
+
+// K2a: each lane's stream is brought in by the TMA engine, tile by tile and
+// double-buffered (a 2 KB bulk copy per stream and tile), so the chain --
+// one DMUL and a compare per frame -- never waits on memory; the warp then
+// writes the tile's peaks out coalesced (a stream's 32 frames per store).
 __global__ void __launch_bounds__(K2_LANES)
 seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict__ stats, DevState* st,
           double* __restrict__ peaks, Params P) {
-  const int i = blockIdx.x * K2_LANES + threadIdx.x;
-  if (i >= nc) return;
-  const Chunk c = chunks[i];
-  DevState* S = st + c.stream;
-  const FrameStat* fst = stats + c.frame_off;
-  double* pk = peaks + c.frame_off;
-  double peak = S->peak;
-  const int n = c.nframes;
-  if (P.peak_mode == 0) {
-    const double decay = P.decay;
-    int f = 0;
-    // frame maxima are loaded 8 ahead of the chain (they do not depend on it)
-    for (; f + 8 <= n; f += 8) {
-      double m[8];
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned char* buf = sm;                                            // [2][32][PK_ROW]
+  double* sp = reinterpret_cast<double*>(sm + 2 * K2_LANES * PK_ROW);  // [32][PK_T + 1]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sp + K2_LANES * (PK_T + 1));
+  const int lane = threadIdx.x;
+  const int i = blockIdx.x * K2_LANES + lane;
+  const bool live = i < nc;
+  Chunk c{};
+  if (live) c = chunks[i];
+  const int n = live ? c.nframes : 0;
+  int tiles = (n + PK_T - 1) / PK_T;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) m[k] = (double)__ldg(&fst[f + k].fmax);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        peak = __dmul_rn(peak, decay);
-        peak = m[k] > peak ? m[k] : peak;
-        pk[f + k] = peak;
-      }
-    }
-    for (; f < n; ++f) {
-      peak = __dmul_rn(peak, decay);
-      const double m = (double)__ldg(&fst[f].fmax);
-      peak = m > peak ? m : peak;
-      pk[f] = peak;
-    }
-  } else if (P.peak_mode == 1) {
-    for (int f = 0; f < n; ++f) {
-      const double m = (double)__ldg(&fst[f].fmax);
-      peak = m > peak ? m : peak;
-      pk[f] = peak;
-    }
-  } else {
-    for (int f = 0; f < n; ++f) pk[f] = peak;
+  for (int o = 16; o; o >>= 1) tiles = max(tiles, __shfl_xor_sync(0xffffffffu, tiles, o));
+  if (lane == 0) {
+    tc::mbar_init(&full[0], K2_LANES);
+    tc::mbar_init(&full[1], K2_LANES);
+    tc::fence_mbar_init();
   }
-  S->peak = peak;
+  __syncwarp();
+  const FrameStat* fst = stats + c.frame_off;
+  auto issue = [&](int t) {  // tile t of this lane's stream into buffer t & 1
+    const int f0 = t * PK_T, nf = max(0, min(PK_T, n - f0));
+    tc::mbar_arrive_expect_tx(&full[t & 1], (uint32_t)nf * 16);
+    if (nf) tc::bulk_g2s(tc::smem_u32(buf + ((t & 1) * K2_LANES + lane) * PK_ROW), fst + f0, (uint32_t)nf * 16,
+                         &full[t & 1]);
+  };
+  if (tiles > 0) issue(0);
+  if (tiles > 1) issue(1);
+  double peak = live ? st[c.stream].peak : 0.0;
+  const double decay = P.decay;
+  for (int t = 0; t < tiles; ++t) {
+    tc::mbar_wait(&full[t & 1], (t >> 1) & 1);
+    const unsigned char* row = buf + ((t & 1) * K2_LANES + lane) * PK_ROW;
+    double* prow = sp + lane * (PK_T + 1);
+    const int nf = max(0, min(PK_T, n - t * PK_T));
+    if (P.peak_mode == 0) {
+      int f = 0;
+      for (; f + 8 <= nf; f += 8) {
+        // the 8 frame maxima are loaded before the chain uses any of them (the
+        // compiler would otherwise put each load's latency on the chain)
+        double m[8];
+        ld8(row, f, m);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          peak = __dmul_rn(peak, decay);
+          peak = m[k] > peak ? m[k] : peak;
+          prow[f + k] = peak;
+        }
+      }
+      for (; f < nf; ++f) {
+        peak = __dmul_rn(peak, decay);
+        const double m = reinterpret_cast<const FrameStat*>(row)[f].fmax;
+        peak = m > peak ? m : peak;
+        prow[f] = peak;
+      }
+    } else if (P.peak_mode == 1) {
+      int f = 0;
+      for (; f + 8 <= nf; f += 8) {
+        double m[8];
+        ld8(row, f, m);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          peak = m[k] > peak ? m[k] : peak;
+          prow[f + k] = peak;
+        }
+      }
+      for (; f < nf; ++f) {
+        const double m = reinterpret_cast<const FrameStat*>(row)[f].fmax;
+        peak = m > peak ? m : peak;
+        prow[f] = peak;
+      }
+    } else {
+      for (int f = 0; f < nf; ++f) prow[f] = peak;
+    }
+    __syncwarp();
+    // coalesced write-out: stream j's frames [t*PK_T, t*PK_T + nf_j)
+    for (int j = 0; j < K2_LANES; ++j) {
+      const int nj = __shfl_sync(0xffffffffu, n, j);
+      const long long off = __shfl_sync(0xffffffffu, (long long)c.frame_off, j);
+      const int nfj = max(0, min(PK_T, nj - t * PK_T));
+      for (int f = lane; f < nfj; f += 32) peaks[off + t * PK_T + f] = sp[j * (PK_T + 1) + f];
+    }
+    __syncwarp();
+    if (t + 2 < tiles) {
+      tc::fence_proxy_async();  // this buffer's generic reads before the TMA overwrites it
+      issue(t + 2);
+    }
+  }
+  if (live) st[c.stream].peak = peak;
 }
 
 __global__ void __launch_bounds__(256)
@@ -560,12 +630,26 @@ seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats
   }
 }
 
+// K2c: the warp first stages its 32 streams' bit rows in shared memory
+// (coalesced), then each lane runs its stream's machine from there.
 __global__ void __launch_bounds__(K2_LANES)
 seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __restrict__ cuts_all,
-            const uint32_t* __restrict__ bits_all, Params P) {
-  const int i = blockIdx.x * K2_LANES + threadIdx.x;
-  if (i >= nc) return;
-  const Chunk c = chunks[i];
+            const uint32_t* __restrict__ bits_all, Params P, int row_words) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint32_t* sb = reinterpret_cast<uint32_t*>(sm);  // [32][row_words] (row_words odd: conflict-free columns)
+  const int lane = threadIdx.x;
+  const int i = blockIdx.x * K2_LANES + lane;
+  const bool live = i < nc;
+  Chunk c{};
+  if (live) c = chunks[i];
+  const int nw = live ? (c.nframes + 31) >> 5 : 0;
+  for (int j = 0; j < K2_LANES; ++j) {
+    const int nwj = __shfl_sync(0xffffffffu, nw, j);
+    const int sj = __shfl_sync(0xffffffffu, c.stream, j);
+    for (int w = lane; w < nwj; w += 32) sb[j * row_words + w] = bits_all[(int64_t)sj * P.flag_words + w];
+  }
+  __syncwarp();
+  if (!live) return;
   DevState* S = st + c.stream;
   if (c.first) {
     S->base = c.start_ms;
@@ -592,8 +676,7 @@ seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __r
   M.n_forced = 0;
   M.n_cuts = S->n_cuts;  // cuts not collected yet stay in front (collection is deferred)
   M.overflow = S->overflow;
-  run_machine(M, P, cuts_all + (int64_t)c.stream * P.cut_cap, c.stream,
-              bits_all + (int64_t)c.stream * P.flag_words, c.nframes);
+  run_machine(M, P, cuts_all + (int64_t)c.stream * P.cut_cap, c.stream, sb + lane * row_words, c.nframes);
   S->seg_start = M.seg_start;
   S->pause_start = M.pause_start;
   S->silence_run = M.silence_run;
@@ -750,6 +833,7 @@ struct lsg_seg_s {
   DevBuf<uint32_t> flags;
   DevBuf<FrameStat> stats;
   DevBuf<double> peaks;  // K2a -> K2b: every frame's decayed peak
+  bool attrs_set = false;
   DevBuf<Chunk> chunks_dev;
   DevBuf<int16_t> staging;
   DevBuf<int32_t> streams_dev;
@@ -844,7 +928,7 @@ static void collect(lsg_seg h, bool finishing) {
 extern "C" {
 
 lsg_status lsg_seg_cfg_default(lsg_seg_cfg* c) {
-  return guard([&] {
+  return guard(__func__, [&] {
     c->mode = 1;
     c->peak_mode = 0;
     c->peak_half_life_ms = 10000.0;
@@ -860,7 +944,7 @@ lsg_status lsg_seg_cfg_default(lsg_seg_cfg* c) {
 
 lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams,
                           int64_t max_push_samples, lsg_seg* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     *out = nullptr;
     validate_cfg(cfg);
     if (n_streams <= 0 || n_streams > kMaxCollect) invalid("lsg_seg_create: n_streams out of range");
@@ -940,7 +1024,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
 }
 
 lsg_status lsg_seg_reset(lsg_seg h) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     std::vector<DevState> init(h->n_streams);
@@ -958,7 +1042,7 @@ lsg_status lsg_seg_reset(lsg_seg h) {
 
 // Device time (ms) of the last push's frame-statistics kernel (K1).
 lsg_status lsgdbg_seg_k1_ms(lsg_seg h, float* ms) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h || !ms) invalid("lsgdbg_seg_k1_ms: null argument");
     if (!h->k1_recorded) logic("lsgdbg_seg_k1_ms: no push with frames yet");
     DeviceGuard g(h->ctx);
@@ -968,7 +1052,7 @@ lsg_status lsgdbg_seg_k1_ms(lsg_seg h, float* ms) {
 }
 
 lsg_status lsg_seg_destroy(lsg_seg h) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h) return;
     DeviceGuard g(h->ctx);
     h->ctx->sync();
@@ -979,7 +1063,7 @@ lsg_status lsg_seg_destroy(lsg_seg h) {
 lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, const int16_t* const* pcm,
                         const int64_t* n_samples, const int64_t* start_ms, int32_t sample_rate,
                         int32_t pcm_on_device) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     const Params& P = h->P;
     if (n_chunks < 0 || n_chunks > h->n_streams) invalid("lsg_seg_push: bad chunk count");
@@ -1077,14 +1161,22 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       h->k1_recorded = true;
     }
     const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
-    seg_peaks<<<g2, K2_LANES, 0, ctx->stream>>>(h->chunks_dev.p, nc, h->stats.p, h->st.p, h->peaks.p, P);
+    if (!h->attrs_set) {  // per handle: kernel attributes are per device
+      LSG_CUDA(cudaFuncSetAttribute(seg_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM));
+      LSG_CUDA(cudaFuncSetAttribute(seg_machine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      h->attrs_set = true;
+    }
+    seg_peaks<<<g2, K2_LANES, PK_SMEM, ctx->stream>>>(h->chunks_dev.p, nc, h->stats.p, h->st.p, h->peaks.p, P);
     LSG_LAUNCHED(ctx);
     if (max_frames > 0) {
       seg_decide<<<dim3((unsigned)ceil_div(max_frames, 256), (unsigned)nc), 256, 0, ctx->stream>>>(
           h->chunks_dev.p, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P);
       LSG_LAUNCHED(ctx);
     }
-    seg_machine<<<g2, K2_LANES, 0, ctx->stream>>>(h->chunks_dev.p, nc, h->st.p, h->cuts.p, h->flags.p, P);
+    const int row_words = (int)((max_frames + 31) / 32) | 1;
+    if ((size_t)K2_LANES * row_words * 4 > 200 * 1024) fail(LSG_ERUNTIME, "lsg_seg_push: push too long for K2c");
+    seg_machine<<<g2, K2_LANES, (size_t)K2_LANES * row_words * 4, ctx->stream>>>(h->chunks_dev.p, nc, h->st.p,
+                                                                               h->cuts.p, h->flags.p, P, row_words);
     LSG_LAUNCHED(ctx);
     seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     LSG_LAUNCHED(ctx);
@@ -1095,7 +1187,7 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
 }
 
 lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
-  return guard([&] {
+  return guard(__func__, [&] {
     Ctx* ctx = h->ctx;
     if (n < 0 || n > h->n_streams) invalid("lsg_seg_finish: bad stream count");
     std::vector<char> seen(h->n_streams, 0);
@@ -1131,7 +1223,7 @@ lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
 }
 
 lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t cap, int64_t* n_out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_take_cuts: stream id out of range");
     if (h->dirty[stream]) {
       DeviceGuard g(h->ctx);
@@ -1146,7 +1238,7 @@ lsg_status lsg_seg_take_cuts(lsg_seg h, int32_t stream, lsg_cut* out, int64_t ca
 }
 
 lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* n_out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (!h->dirty_list.empty()) {
       DeviceGuard g(h->ctx);
       collect(h, false);
@@ -1165,7 +1257,7 @@ lsg_status lsg_seg_take_all_cuts(lsg_seg h, lsg_cut* out, int64_t cap, int64_t* 
 }
 
 lsg_status lsg_seg_get_metrics(lsg_seg h, int32_t stream, lsg_seg_metrics* out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_get_metrics: stream id out of range");
     if (h->dirty[stream]) {
       DeviceGuard g(h->ctx);
@@ -1176,7 +1268,7 @@ lsg_status lsg_seg_get_metrics(lsg_seg h, int32_t stream, lsg_seg_metrics* out) 
 }
 
 lsg_status lsg_seg_take_flags(lsg_seg h, int32_t stream, uint8_t* speech, int64_t cap, int64_t* n_out) {
-  return guard([&] {
+  return guard(__func__, [&] {
     if (stream < 0 || stream >= h->n_streams) invalid("lsg_seg_take_flags: stream id out of range");
     if (!h->P.flags_only) logic("lsg_seg_take_flags: handle was not created with flags_only");
     auto& v = h->hs[stream].flags;
