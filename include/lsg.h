@@ -310,6 +310,28 @@ lsg_status lsg_pipe_run(lsg_pipe h, const int16_t* const* pcm, const int64_t* n_
                         lsg_frame_rec* recs, void* frames, int64_t cap, int64_t* n_out,
                         lsg_pipe_stats* stats);
 
+/* ------------------------------------------------ multi-GPU pipeline
+ * SURVEY.md §8 e: one lsg_pipe per device of `devices` (a context, its
+ * CUDA streams and a generator engine each), driven by one host thread per
+ * device -- the B200 counterpart of the reference's StageWorker threads
+ * (worker.cpp:19-36).  Stream s belongs to device devices[s % n_dev]; there
+ * is no collective.  cfg->n_streams is the total; weights / precision /
+ * act_absmax as lsg_gen_create_q.  The same device may be listed twice
+ * (independent contexts). */
+typedef struct lsg_mpipe_s* lsg_mpipe;
+lsg_status lsg_mpipe_create(const int32_t* devices, int32_t n_dev, const lsg_pipe_cfg* cfg,
+                            const lsg_seg_cfg* seg, const lsg_mel_cfg* mel, const float* weights,
+                            int64_t n_floats, int32_t precision, const float* act_absmax, int32_t n_act,
+                            lsg_mpipe* out);
+lsg_status lsg_mpipe_destroy(lsg_mpipe h);
+/* lsg_pipe_run over all streams on all devices concurrently; [host] inputs
+ * and outputs as lsg_pipe_run, records / frames in global stream order (the
+ * order one lsg_pipe over every stream returns); dev_stats [n_dev] or NULL. */
+lsg_status lsg_mpipe_run(lsg_mpipe h, const int16_t* const* pcm, const int64_t* n_samples,
+                         const uint8_t* const* video, const int64_t* n_video, const uint8_t* refs,
+                         lsg_frame_rec* recs, void* frames, int64_t cap, int64_t* n_out,
+                         lsg_pipe_stats* dev_stats);
+
 /* ------------------------------------------ zero-copy stage hand-off
  * SURVEY.md §8 f3.  A registry of device buffers keyed by (segment uuid,
  * kind) lets stages exchange mel, PCM and frames as references instead of

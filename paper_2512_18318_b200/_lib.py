@@ -127,6 +127,10 @@ _SIGS = {
     "lsg_pipe_create": [P, C.POINTER(PipeCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), P, PP],
     "lsg_pipe_destroy": [P],
     "lsg_pipe_run": [P, PP, PI64, PP, PI64, P, C.POINTER(FrameRec), P, I64, PI64, C.POINTER(PipeStats)],
+    "lsg_mpipe_create": [PI32, I32, C.POINTER(PipeCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), P, I64, I32, P, I32,
+                         PP],
+    "lsg_mpipe_destroy": [P],
+    "lsg_mpipe_run": [P, PP, PI64, PP, PI64, P, C.POINTER(FrameRec), P, I64, PI64, C.POINTER(PipeStats)],
     "lsg_synth_pattern": [I64, I32, PI64, PI64, F64, F64, I64, I32, P, I64, PI64],
     "lsg_reg_create": [P, I64, PP],
     "lsg_reg_destroy": [P],

@@ -13,8 +13,9 @@
 //                       per stream;
 //   K2b seg_decide      per-frame dB decisions, thread per frame,
 //                       ballot-packed bit rows;
-//   K2c seg_machine     the integer-millisecond state machine, lane per
-//                       stream, fast-forwarding over runs of frames that
+//   K2c seg_machine     the integer-millisecond state machine, a warp per
+//                       stream (bits staged by the warp, run by lane 0),
+//                       fast-forwarding over runs of frames that
 //                       cannot raise an event and stepping event frames
 //                       exactly like process_frame (segmenter.cpp:51-99).
 //   K3 seg_carry        keeps each stream's sub-frame tail (stage_,
@@ -54,6 +55,7 @@ struct Params {
   int32_t rate, fs;
   int32_t flags_only, cut_cap;
   int32_t flag_words;  // per stream, per push
+  int32_t pk_stride;   // K2a -> K2b peaks: doubles per stream row (even: 16-byte aligned rows)
 };
 
 struct alignas(16) DevState {
@@ -502,11 +504,12 @@ __device__ void run_machine(Machine& M, const Params& P, lsg_cut* cuts, int stre
 //   K2b seg_decide   every frame's decision in parallel (thread per frame),
 //                    ballot-packed into the stream's bit row;
 //   K2c seg_machine  the state machine over the bits (segmenter.cpp:51-99),
-//                    lane per stream, fast-forwarding event-free runs.
+//                    warp per stream, fast-forwarding event-free runs.
 constexpr int K2_LANES = 32;  // streams per K2a / K2c block: one warp, a lane per stream
 constexpr int PK_T = 128;     // K2a frames per tile
 constexpr int PK_ROW = PK_T * 16 + 16;  // stats row stride in smem (bytes; +16 spreads the banks)
-constexpr size_t PK_SMEM = 2 * K2_LANES * PK_ROW + K2_LANES * (PK_T + 1) * 8 + 64;
+constexpr int PK_PROW = PK_T * 8 + 16;  // peaks row stride in smem (bytes)
+constexpr size_t PK_SMEM = 2 * K2_LANES * PK_ROW + 2 * K2_LANES * PK_PROW + 64;
 
 // fmax of frames f..f+7 of a staged stats row, issued back to back
 // (volatile: kept ahead of the chain that consumes them)
@@ -518,15 +521,15 @@ __device__ __forceinline__ void ld8(const unsigned char* row, int f, double (&m)
 
 // K2a: each lane's stream is brought in by the TMA engine, tile by tile and
 // double-buffered (a 2 KB bulk copy per stream and tile), so the chain --
-// one DMUL and a compare per frame -- never waits on memory; the warp then
-// writes the tile's peaks out coalesced (a stream's 32 frames per store).
+// one DMUL and a compare per frame -- never waits on memory; each tile's
+// peaks leave the same way (one bulk store per stream, double-buffered).
 __global__ void __launch_bounds__(K2_LANES)
 seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict__ stats, DevState* st,
           double* __restrict__ peaks, Params P) {
   extern __shared__ __align__(16) unsigned char sm[];
-  unsigned char* buf = sm;                                            // [2][32][PK_ROW]
-  double* sp = reinterpret_cast<double*>(sm + 2 * K2_LANES * PK_ROW);  // [32][PK_T + 1]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sp + K2_LANES * (PK_T + 1));
+  unsigned char* buf = sm;                                // [2][32][PK_ROW] stats tiles
+  unsigned char* pbuf = sm + 2 * K2_LANES * PK_ROW;       // [2][32][PK_PROW] peak tiles
+  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + 2 * K2_LANES * PK_PROW);
   const int lane = threadIdx.x;
   const int i = blockIdx.x * K2_LANES + lane;
   const bool live = i < nc;
@@ -556,7 +559,9 @@ seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict_
   for (int t = 0; t < tiles; ++t) {
     tc::mbar_wait(&full[t & 1], (t >> 1) & 1);
     const unsigned char* row = buf + ((t & 1) * K2_LANES + lane) * PK_ROW;
-    double* prow = sp + lane * (PK_T + 1);
+    double* prow = reinterpret_cast<double*>(pbuf + ((t & 1) * K2_LANES + lane) * PK_PROW);
+    // the bulk store that read this peak buffer two tiles ago has finished
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     const int nf = max(0, min(PK_T, n - t * PK_T));
     if (P.peak_mode == 0) {
       int f = 0;
@@ -597,20 +602,23 @@ seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict_
     } else {
       for (int f = 0; f < nf; ++f) prow[f] = peak;
     }
-    __syncwarp();
-    // coalesced write-out: stream j's frames [t*PK_T, t*PK_T + nf_j)
-    for (int j = 0; j < K2_LANES; ++j) {
-      const int nj = __shfl_sync(0xffffffffu, n, j);
-      const long long off = __shfl_sync(0xffffffffu, (long long)c.frame_off, j);
-      const int nfj = max(0, min(PK_T, nj - t * PK_T));
-      for (int f = lane; f < nfj; f += 32) peaks[off + t * PK_T + f] = sp[j * (PK_T + 1) + f];
+    // the tile's peaks go out on the TMA engine: one bulk store per stream
+    if (nf) {
+      tc::fence_proxy_async();  // generic smem writes -> visible to the async proxy
+      // stream rows are 16-byte aligned; an odd tail carries one spare double
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                       peaks + (int64_t)c.stream * P.pk_stride + t * PK_T),
+                   "r"(tc::smem_u32(prow)), "r"(((nf + 1) & ~1) * 8)
+                   : "memory");
     }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     __syncwarp();
     if (t + 2 < tiles) {
       tc::fence_proxy_async();  // this buffer's generic reads before the TMA overwrites it
       issue(t + 2);
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before the kernel ends
   if (live) st[c.stream].peak = peak;
 }
 
@@ -622,7 +630,8 @@ seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats
   if (blockIdx.x * 256 >= c.nframes) return;  // whole block past the chunk (uniform)
   bool sp = false;
   if (f < c.nframes)
-    sp = vad_decide(stats[c.frame_off + f].sumsq, peaks[c.frame_off + f], P.fs, P.thr, P.x_lo, P.x_hi);
+    sp = vad_decide(stats[c.frame_off + f].sumsq, peaks[(int64_t)c.stream * P.pk_stride + f], P.fs, P.thr, P.x_lo,
+                    P.x_hi);
   const unsigned bal = __ballot_sync(0xffffffffu, sp);
   if ((threadIdx.x & 31) == 0) {
     if (f < c.nframes) bits_all[(int64_t)c.stream * P.flag_words + (f >> 5)] = bal;
@@ -630,26 +639,24 @@ seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats
   }
 }
 
-// K2c: the warp first stages its 32 streams' bit rows in shared memory
-// (coalesced), then each lane runs its stream's machine from there.
-__global__ void __launch_bounds__(K2_LANES)
+// K2c: one warp per stream -- the lanes stage the stream's bit row in shared
+// memory, then lane 0 runs the machine (warp-uniform control flow: no
+// divergence between streams; 512 streams are 512 concurrent warps).
+constexpr int MC_WARPS = 4;
+__global__ void __launch_bounds__(MC_WARPS * 32)
 seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __restrict__ cuts_all,
             const uint32_t* __restrict__ bits_all, Params P, int row_words) {
   extern __shared__ __align__(16) unsigned char sm[];
-  uint32_t* sb = reinterpret_cast<uint32_t*>(sm);  // [32][row_words] (row_words odd: conflict-free columns)
-  const int lane = threadIdx.x;
-  const int i = blockIdx.x * K2_LANES + lane;
-  const bool live = i < nc;
-  Chunk c{};
-  if (live) c = chunks[i];
-  const int nw = live ? (c.nframes + 31) >> 5 : 0;
-  for (int j = 0; j < K2_LANES; ++j) {
-    const int nwj = __shfl_sync(0xffffffffu, nw, j);
-    const int sj = __shfl_sync(0xffffffffu, c.stream, j);
-    for (int w = lane; w < nwj; w += 32) sb[j * row_words + w] = bits_all[(int64_t)sj * P.flag_words + w];
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * MC_WARPS + warp;
+  if (i >= nc) return;
+  uint32_t* sb = reinterpret_cast<uint32_t*>(sm) + warp * row_words;
+  const Chunk c = chunks[i];
+  const int nw = (c.nframes + 31) >> 5;
+  const uint32_t* src = bits_all + (int64_t)c.stream * P.flag_words;
+  for (int w = lane; w < nw; w += 32) sb[w] = src[w];
   __syncwarp();
-  if (!live) return;
+  if (lane != 0) return;
   DevState* S = st + c.stream;
   if (c.first) {
     S->base = c.start_ms;
@@ -676,7 +683,7 @@ seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __r
   M.n_forced = 0;
   M.n_cuts = S->n_cuts;  // cuts not collected yet stay in front (collection is deferred)
   M.overflow = S->overflow;
-  run_machine(M, P, cuts_all + (int64_t)c.stream * P.cut_cap, c.stream, sb + lane * row_words, c.nframes);
+  run_machine(M, P, cuts_all + (int64_t)c.stream * P.cut_cap, c.stream, sb, c.nframes);
   S->seg_start = M.seg_start;
   S->pause_start = M.pause_start;
   S->silence_run = M.silence_run;
@@ -980,6 +987,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->max_frames_push = (max_push_samples + fs) / fs + 1;
       P.cut_cap = (int32_t)std::min<int64_t>(2 * h->max_frames_push + 2, INT32_MAX);  // <= 2 cuts/frame
       P.flag_words = (int32_t)((h->max_frames_push + 31) / 32);
+      P.pk_stride = (int32_t)((h->max_frames_push + 2) & ~int64_t(1));
       h->hs.resize(n_streams);
       h->st.alloc(n_streams);
       LSG_CUDA(cudaMemsetAsync(h->st.p, 0, h->st.bytes(), ctx->stream));
@@ -994,7 +1002,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->cuts.alloc((size_t)n_streams * P.cut_cap);
       h->flags.alloc((size_t)n_streams * P.flag_words);
       h->stats.alloc((size_t)n_streams * h->max_frames_push);
-      h->peaks.alloc((size_t)n_streams * h->max_frames_push);
+      h->peaks.alloc((size_t)n_streams * P.pk_stride);
       h->chunks_dev.alloc(n_streams);
       // each staged chunk starts 64-sample (128 B) aligned: <= one chunk per
       // stream per push, each rounded up to 64 samples
@@ -1174,9 +1182,9 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       LSG_LAUNCHED(ctx);
     }
     const int row_words = (int)((max_frames + 31) / 32) | 1;
-    if ((size_t)K2_LANES * row_words * 4 > 200 * 1024) fail(LSG_ERUNTIME, "lsg_seg_push: push too long for K2c");
-    seg_machine<<<g2, K2_LANES, (size_t)K2_LANES * row_words * 4, ctx->stream>>>(h->chunks_dev.p, nc, h->st.p,
-                                                                               h->cuts.p, h->flags.p, P, row_words);
+    if ((size_t)MC_WARPS * row_words * 4 > 200 * 1024) fail(LSG_ERUNTIME, "lsg_seg_push: push too long for K2c");
+    seg_machine<<<(unsigned)ceil_div(nc, MC_WARPS), MC_WARPS * 32, (size_t)MC_WARPS * row_words * 4, ctx->stream>>>(
+        h->chunks_dev.p, nc, h->st.p, h->cuts.p, h->flags.p, P, row_words);
     LSG_LAUNCHED(ctx);
     seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     LSG_LAUNCHED(ctx);

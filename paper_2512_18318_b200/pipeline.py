@@ -80,3 +80,64 @@ class Pipeline:
         frames = out[: k * px].view(np.uint8 if self.cfg.out_u8 else np.float32)
         frames = frames.reshape(k, 96, 96, 3) if self.cfg.out_u8 else frames.reshape(k, 3, 96, 96)
         return rec, frames, st
+
+
+class MultiPipeline:
+    """lsg_mpipe: the pipeline over several GPUs of ONE process, one host
+    thread + context + generator per device, stream s on devices[s % G]
+    (SURVEY.md §8 e, no collective).  Same run() contract as Pipeline; the
+    records and frames come back in global stream order."""
+
+    def __init__(self, cfg: PipelineConfig, weights: np.ndarray, devices, precision: int = 1,
+                 seg: SegmenterConfig | None = None, mel: MelConfig | None = None, act_absmax=None):
+        from ._lib import lib
+        self.lib = lib()
+        self.cfg = cfg
+        self.devices = list(devices)
+        pc = PipeCfg(cfg.n_streams, cfg.max_stream_ms, cfg.fps, cfg.gather_margin_ms, cfg.max_batch,
+                     1 if cfg.out_u8 else 0)
+        sc: SegCfg = (seg or SegmenterConfig()).to_c()
+        mc: MelCfg = (mel or MelConfig()).to_c()
+        w = np.ascontiguousarray(weights, np.float32)
+        a = None if act_absmax is None else np.ascontiguousarray(act_absmax, np.float32)
+        devs = (C.c_int32 * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        self.lib.call("lsg_mpipe_create", devs, len(self.devices), C.byref(pc), C.byref(sc), C.byref(mc),
+                      C.c_void_p(w.ctypes.data), w.size, precision,
+                      None if a is None else C.c_void_p(a.ctypes.data), 0 if a is None else a.size, C.byref(h))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_mpipe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, pcm: list[np.ndarray], video: list[np.ndarray], refs: np.ndarray, cap: int | None = None):
+        """Host numpy arrays; returns (records, frames, per-device stats)."""
+        S = self.cfg.n_streams
+        pcm = [np.ascontiguousarray(p, np.int16) for p in pcm]
+        video = [np.ascontiguousarray(v, np.uint8) for v in video]
+        refs = np.ascontiguousarray(refs, np.uint8)
+        if cap is None:
+            cap = sum(len(v) for v in video) * 2 + 64
+        px = CROP if self.cfg.out_u8 else CROP * 4
+        out = np.zeros(cap * px, np.uint8)
+        recs = (FrameRec * max(cap, 1))()
+        st = (PipeStats * len(self.devices))()
+        n = C.c_int64()
+        self.lib.call("lsg_mpipe_run", self.h, (C.c_void_p * S)(*[p.ctypes.data for p in pcm]),
+                      (C.c_int64 * S)(*[len(p) for p in pcm]), (C.c_void_p * S)(*[v.ctypes.data for v in video]),
+                      (C.c_int64 * S)(*[len(v) for v in video]), C.c_void_p(refs.ctypes.data), recs,
+                      C.c_void_p(out.ctypes.data), cap, C.byref(n), st)
+        k = min(n.value, cap)
+        rec = [dict(stream=recs[i].stream, segment=recs[i].segment, frame_index=recs[i].frame_index,
+                    ts_ms=recs[i].ts_ms, mel_row=recs[i].mel_row) for i in range(k)]
+        frames = out[: k * px].view(np.uint8 if self.cfg.out_u8 else np.float32)
+        frames = frames.reshape(k, 96, 96, 3) if self.cfg.out_u8 else frames.reshape(k, 3, 96, 96)
+        return rec, frames, [{f: getattr(s, f) for f, _ in PipeStats._fields_} for s in st]

@@ -76,3 +76,36 @@ def test_pipeline_matches_standalone_stages(reference):
     pipe.close()
     eng.close()
     ctx.set_stream(None)
+
+
+def test_multi_device_pipeline_matches_single(reference):
+    """lsg_mpipe (one host thread + context + generator per device, stream s
+    on device s mod G) returns what one lsg_pipe over all streams returns:
+    the same records in global stream order and the same frames up to fp32
+    summation order (each device forms its own generator batches, and the
+    kernel route -- e.g. the split-K factor -- follows the batch size).  One
+    GPU here, so the two 'devices' are two independent contexts on device 0."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import api, generator
+    from paper_2512_18318_b200.pipeline import MultiPipeline, Pipeline, PipelineConfig
+    S, secs, fps = 5, 6, 25.0
+    pcm = [reference.render_pattern(random_scenario_pattern(20 + i), secs * 1000) for i in range(S)]
+    refs = np.stack([generator.synthetic_face(70 + s) for s in range(S)])
+    nvid = [int(np.ceil(len(p) / 16000 * fps)) for p in pcm]
+    video = [np.stack([generator.jitter_face(refs[s], f, s) for f in range(nvid[s])]) for s in range(S)]
+    w = generator.synthetic_weights(0)
+    cfg = PipelineConfig(S, secs * 1000, fps, 50, 32, True)
+    ctx = api.Context(0)
+    eng = generator.LipsyncEngine(w, max_batch=32, ctx=ctx, precision=1)
+    one = Pipeline(cfg, eng, ctx=ctx)
+    r1, f1, _ = one.run(pcm, video, refs)
+    many = MultiPipeline(cfg, w, devices=[0, 0], precision=1)
+    r2, f2, st = many.run(pcm, video, refs)
+    assert len(st) == 2 and sum(s["frames_rendered"] for s in st) == len(r2)
+    assert r1 == r2
+    d = np.abs(f1.astype(int) - f2.astype(int))
+    mse = float(np.mean(d.astype(np.float64) ** 2)) / 255.0 ** 2
+    assert d.max() <= 3 and (mse == 0 or 10 * np.log10(1 / mse) >= 50), (d.max(), mse)
+    many.close()
+    one.close()
+    eng.close()
