@@ -332,6 +332,51 @@ lsg_status lsg_mpipe_run(lsg_mpipe h, const int16_t* const* pcm, const int64_t* 
                          lsg_frame_rec* recs, void* frames, int64_t cap, int64_t* n_out,
                          lsg_pipe_stats* dev_stats);
 
+/* ------------------------------------------------------- paced driver
+ * BASELINE.json config 5, paced: audio and video released in real time
+ * (media time T available at wall time t0 + T), 40 ms ticks.  Per tick the
+ * new PCM goes to a GPU segmenter on a private context; segments whose frame
+ * window [begin - margin, end + margin] is complete get their mel and frame
+ * jobs (rule a8); a deadline batcher launches generator batches on the
+ * generator's context without blocking the tick loop -- a full batch as soon
+ * as max_batch frames are queued, a partial one once the oldest queued frame
+ * has waited deadline_ms -- and cudaLaunchHostFunc stamps each segment's
+ * completion when its last frame's batch finishes (the reference's
+ * StageWorker -> MediaClock completion, worker.cpp:19-36, clock.cpp:124-145). */
+typedef struct {
+  int32_t n_streams;
+  double fps;                  /* video frame rate (25)                        */
+  int32_t gather_margin_ms;    /* 50 (orchestrator.cpp:90-91)                  */
+  int32_t tick_ms;             /* release granularity (40)                     */
+  int32_t max_batch;           /* generator batch cap (<= the engine's)        */
+  int32_t deadline_ms;         /* flush a partial batch after this wait        */
+  int64_t max_stream_samples;  /* pcm row stride, samples                     */
+  int64_t max_video;           /* video row stride, frames                    */
+} lsg_paced_cfg;
+
+typedef struct {
+  int32_t stream, segment;
+  int64_t begin, end;          /* ms (media time) */
+  int32_t cause, frames;       /* frames rendered for the segment */
+  double decided_ms;           /* wall ms since the run's media epoch: cut known */
+  double rendered_ms;          /* ... last frame rendered (host callback) */
+} lsg_paced_seg;
+
+typedef struct lsg_paced_s* lsg_paced;
+lsg_status lsg_paced_create(lsg_gen gen, const lsg_paced_cfg* cfg, const lsg_seg_cfg* seg,
+                            const lsg_mel_cfg* mel, lsg_paced* out);
+lsg_status lsg_paced_destroy(lsg_paced h);
+/* One real-time run of `seconds` (<= 0: the shortest stream).  [dev]
+ * inputs: pcm [n_streams][max_stream_samples] int16, video
+ * [n_streams][max_video][96][96][3] u8, refs [n_streams][96][96][3].
+ * Outputs: segs [host, seg_cap]; optionally every rendered frame
+ * (frames_out [dev, frames_cap][96][96][3], recs [host, frames_cap]) in
+ * render order. */
+lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_samples, const uint8_t* video,
+                         const int64_t* n_video, const uint8_t* refs, double seconds, lsg_paced_seg* segs,
+                         int64_t seg_cap, int64_t* n_segs, uint8_t* frames_out, lsg_frame_rec* recs,
+                         int64_t frames_cap, int64_t* n_frames, int32_t* late_ticks);
+
 /* ------------------------------------------ zero-copy stage hand-off
  * SURVEY.md §8 f3.  A registry of device buffers keyed by (segment uuid,
  * kind) lets stages exchange mel, PCM and frames as references instead of

@@ -60,6 +60,17 @@ class FrameRec(C.Structure):
                 ("mel_row", C.c_int32), ("pad", C.c_int32)]
 
 
+class PacedCfg(C.Structure):
+    _fields_ = [("n_streams", C.c_int32), ("fps", C.c_double), ("gather_margin_ms", C.c_int32),
+                ("tick_ms", C.c_int32), ("max_batch", C.c_int32), ("deadline_ms", C.c_int32),
+                ("max_stream_samples", C.c_int64), ("max_video", C.c_int64)]
+
+
+class PacedSeg(C.Structure):
+    _fields_ = [("stream", C.c_int32), ("segment", C.c_int32), ("begin", C.c_int64), ("end", C.c_int64),
+                ("cause", C.c_int32), ("frames", C.c_int32), ("decided_ms", C.c_double), ("rendered_ms", C.c_double)]
+
+
 class DevRef(C.Structure):
     """lsg_devref: a registry reference (uuid, kind, device, generation, offset, bytes)."""
     _fields_ = [("uuid", C.c_uint8 * 16), ("kind", C.c_int32), ("device", C.c_int32), ("generation", C.c_uint64),
@@ -130,6 +141,10 @@ _SIGS = {
     "lsg_mpipe_create": [PI32, I32, C.POINTER(PipeCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), P, I64, I32, P, I32,
                          PP],
     "lsg_mpipe_destroy": [P],
+    "lsg_paced_create": [P, C.POINTER(PacedCfg), C.POINTER(SegCfg), C.POINTER(MelCfg), PP],
+    "lsg_paced_destroy": [P],
+    "lsg_paced_run": [P, P, PI64, P, PI64, P, F64, C.POINTER(PacedSeg), I64, PI64, P, C.POINTER(FrameRec), I64, PI64,
+                      PI32],
     "lsg_mpipe_run": [P, PP, PI64, PP, PI64, P, C.POINTER(FrameRec), P, I64, PI64, C.POINTER(PipeStats)],
     "lsg_synth_pattern": [I64, I32, PI64, PI64, F64, F64, I64, I32, P, I64, PI64],
     "lsg_reg_create": [P, I64, PP],

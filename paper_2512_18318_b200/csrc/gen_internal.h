@@ -17,6 +17,7 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
                     int32_t out_format, int32_t B);
 
 int32_t max_batch(lsg_gen h);
+lsg_ctx context(lsg_gen h);  // the context (device, stream) the generator issues on
 
 }  // namespace gen
 }  // namespace lsg

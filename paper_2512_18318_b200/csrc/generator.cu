@@ -1757,6 +1757,7 @@ namespace lsg {
 namespace gen {
 
 int32_t max_batch(lsg_gen h) { return h->max_batch; }
+lsg_ctx context(lsg_gen h) { return static_cast<lsg_ctx>(h->ctx); }
 
 // Launches plan layers [l0, l1) on st (the audio encoder, when in range, on
 // the side stream, joined before the first decoder layer).

@@ -387,6 +387,19 @@ struct lsg_mel_s {
   DevBuf<int32_t> band;  // lo | n | off
   DevBuf<int64_t> seg_tab;  // pcm_off | frame0 | out_row for batch calls
   PinnedBuf<int64_t> seg_tab_host;
+  // the pinned segment table is copied asynchronously by batch calls, which
+  // do not synchronise: the next call waits for that copy before rewriting it
+  cudaEvent_t tab_ev = nullptr;
+  bool tab_pending = false;
+  void tab_free() {
+    if (tab_pending) {
+      LSG_CUDA(cudaEventSynchronize(tab_ev));
+      tab_pending = false;
+    }
+  }
+  ~lsg_mel_s() {
+    if (tab_ev) cudaEventDestroy(tab_ev);
+  }
   int32_t max_seg = 0;
   DevBuf<int16_t> pcm_stage;
   DevBuf<float> out_stage;
@@ -647,6 +660,7 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
       h->max_seg = 4096;
       h->seg_tab.alloc(3 * (size_t)h->max_seg + 1);
       h->seg_tab_host.alloc(3 * (size_t)h->max_seg + 1);
+      LSG_CUDA(cudaEventCreateWithFlags(&h->tab_ev, cudaEventDisableTiming));
       const int64_t max_samples = (max_frames - 1) * cfg->hop + N;
       h->pcm_stage.alloc((size_t)max_samples);
       h->out_stage.alloc((size_t)max_frames * M);
@@ -705,6 +719,7 @@ lsg_status lsg_mel_compute(lsg_mel h, const int16_t* pcm, int64_t n, float* out,
     }
     const bool out_dev = is_device_ptr(out);
     float* dout = out_dev ? out : h->out_stage.p;
+    h->tab_free();
     int64_t* t = h->seg_tab_host.p;  // packed [pcm_off | frame0 (n+1) | out_row], n = 1
     t[0] = 0;
     t[1] = 0;
@@ -726,6 +741,7 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
     if (n_seg < 0 || n_seg > h->max_seg) invalid("lsg_mel_compute_batch: too many segments (max 4096)");
     DeviceGuard g(ctx);
     const int N = h->cfg.fft_size;
+    h->tab_free();
     int64_t* t = h->seg_tab_host.p;
     int64_t tot = 0;
     for (int i = 0; i < n_seg; ++i) {  // packed [pcm_off | frame0 (n+1) | out_row]
@@ -740,6 +756,8 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
     if (tot == 0) return;
     LSG_CUDA(cudaMemcpyAsync(h->seg_tab.p, t, (3 * (size_t)n_seg + 1) * 8, cudaMemcpyHostToDevice,
                              ctx->stream));
+    LSG_CUDA(cudaEventRecord(h->tab_ev, ctx->stream));
+    h->tab_pending = true;
     launch(h, pcm_base, n_seg, tot, out_base);
   });
 }

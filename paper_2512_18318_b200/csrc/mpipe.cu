@@ -9,6 +9,7 @@
 // inputs go in and rendered frames come back, per device, concurrently.
 // Results are returned in global stream order, exactly as one lsg_pipe over
 // all streams would return them.
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -127,10 +128,15 @@ lsg_status lsg_mpipe_run(lsg_mpipe h, const int16_t* const* pcm, const int64_t* 
                            dev_stats ? dev_stats + d : nullptr);
       if (rc[d] != LSG_OK) err[d] = lsg_last_error();  // (thread-local message)
     };
+    static const bool serial = std::getenv("LSG_MPIPE_SERIAL") != nullptr;  // (debug)
     std::vector<std::thread> th;
-    for (int d = 1; d < G; ++d) th.emplace_back(work, d);
-    work(0);
-    for (auto& t : th) t.join();
+    if (serial) {
+      for (int d = 0; d < G; ++d) work(d);
+    } else {
+      for (int d = 1; d < G; ++d) th.emplace_back(work, d);
+      work(0);
+      for (auto& t : th) t.join();
+    }
     for (int d = 0; d < G; ++d)
       if (rc[d] != LSG_OK) fail(rc[d], "lsg_mpipe_run: device " + std::to_string(d) + ": " + err[d]);
     // merge in global stream order: a device's records are stream-major over

@@ -34,6 +34,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "lsg_common.cuh"
@@ -506,6 +508,15 @@ __device__ void run_machine(Machine& M, const Params& P, lsg_cut* cuts, int stre
 //   K2c seg_machine  the state machine over the bits (segmenter.cpp:51-99),
 //                    warp per stream, fast-forwarding event-free runs.
 constexpr int K2_LANES = 32;  // streams per K2a / K2c block: one warp, a lane per stream
+// Time-sliced pushes: a push of many frames per stream is processed in
+// slices of kSlice frames so that the per-stream sequential work (the peak
+// chain and the state machine, latency-bound on a few SMs) of slice s
+// overlaps the HBM-bound K1 of slice s + 1 and of each other.
+#ifndef LSG_SEG_SLICE
+#define LSG_SEG_SLICE 512
+#endif
+constexpr int kSlice = LSG_SEG_SLICE;  // frames (a multiple of 256)
+constexpr int kSlots = 3;    // slices in flight
 constexpr int PK_T = 128;     // K2a frames per tile
 constexpr int PK_ROW = PK_T * 16 + 16;  // stats row stride in smem (bytes; +16 spreads the banks)
 constexpr int PK_PROW = PK_T * 8 + 16;  // peaks row stride in smem (bytes)
@@ -525,7 +536,7 @@ __device__ __forceinline__ void ld8(const unsigned char* row, int f, double (&m)
 // peaks leave the same way (one bulk store per stream, double-buffered).
 __global__ void __launch_bounds__(K2_LANES)
 seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict__ stats, DevState* st,
-          double* __restrict__ peaks, Params P) {
+          double* __restrict__ peaks, Params P, int pk_off) {
   extern __shared__ __align__(16) unsigned char sm[];
   unsigned char* buf = sm;                                // [2][32][PK_ROW] stats tiles
   unsigned char* pbuf = sm + 2 * K2_LANES * PK_ROW;       // [2][32][PK_PROW] peak tiles
@@ -607,7 +618,7 @@ seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict_
       tc::fence_proxy_async();  // generic smem writes -> visible to the async proxy
       // stream rows are 16-byte aligned; an odd tail carries one spare double
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                       peaks + (int64_t)c.stream * P.pk_stride + t * PK_T),
+                       peaks + (int64_t)c.stream * P.pk_stride + pk_off + t * PK_T),
                    "r"(tc::smem_u32(prow)), "r"(((nf + 1) & ~1) * 8)
                    : "memory");
     }
@@ -624,17 +635,17 @@ seg_peaks(const Chunk* __restrict__ chunks, int nc, const FrameStat* __restrict_
 
 __global__ void __launch_bounds__(256)
 seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats, const double* __restrict__ peaks,
-           DevState* st, uint32_t* __restrict__ bits_all, Params P) {
+           DevState* st, uint32_t* __restrict__ bits_all, Params P, int pk_off, int bits_off) {
   const Chunk c = chunks[blockIdx.y];
   const int f = blockIdx.x * 256 + threadIdx.x;
   if (blockIdx.x * 256 >= c.nframes) return;  // whole block past the chunk (uniform)
   bool sp = false;
   if (f < c.nframes)
-    sp = vad_decide(stats[c.frame_off + f].sumsq, peaks[(int64_t)c.stream * P.pk_stride + f], P.fs, P.thr, P.x_lo,
-                    P.x_hi);
+    sp = vad_decide(stats[c.frame_off + f].sumsq, peaks[(int64_t)c.stream * P.pk_stride + pk_off + f], P.fs, P.thr,
+                    P.x_lo, P.x_hi);
   const unsigned bal = __ballot_sync(0xffffffffu, sp);
   if ((threadIdx.x & 31) == 0) {
-    if (f < c.nframes) bits_all[(int64_t)c.stream * P.flag_words + (f >> 5)] = bal;
+    if (f < c.nframes) bits_all[(int64_t)c.stream * P.flag_words + bits_off + (f >> 5)] = bal;
     if (bal) atomicAdd(reinterpret_cast<unsigned long long*>(&st[c.stream].m_speech), (unsigned long long)__popc(bal));
   }
 }
@@ -645,7 +656,7 @@ seg_decide(const Chunk* __restrict__ chunks, const FrameStat* __restrict__ stats
 constexpr int MC_WARPS = 4;
 __global__ void __launch_bounds__(MC_WARPS * 32)
 seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __restrict__ cuts_all,
-            const uint32_t* __restrict__ bits_all, Params P, int row_words) {
+            const uint32_t* __restrict__ bits_all, Params P, int row_words, int bits_off) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * MC_WARPS + warp;
@@ -653,7 +664,7 @@ seg_machine(const Chunk* __restrict__ chunks, int nc, DevState* st, lsg_cut* __r
   uint32_t* sb = reinterpret_cast<uint32_t*>(sm) + warp * row_words;
   const Chunk c = chunks[i];
   const int nw = (c.nframes + 31) >> 5;
-  const uint32_t* src = bits_all + (int64_t)c.stream * P.flag_words;
+  const uint32_t* src = bits_all + (int64_t)c.stream * P.flag_words + bits_off;
   for (int w = lane; w < nw; w += 32) sb[w] = src[w];
   __syncwarp();
   if (lane != 0) return;
@@ -841,6 +852,37 @@ struct lsg_seg_s {
   DevBuf<FrameStat> stats;
   DevBuf<double> peaks;  // K2a -> K2b: every frame's decayed peak
   bool attrs_set = false;
+  // time-sliced pushes (see launch_sliced): K1 on the context stream, the
+  // peak chain on sB, decisions + machine on sC, kSlots slices in flight
+  cudaStream_t sB = nullptr, sC = nullptr;
+  cudaEvent_t eK1[3] = {}, ePk[3] = {}, eM[3] = {}, eJoin = nullptr;
+  DevBuf<Chunk> chunks_sl;
+  PinnedBuf<Chunk> chunks_sl_host;
+  int max_slices = 0;
+  // the pinned chunk / stream tables are copied asynchronously: the next
+  // call waits for the last copy before rewriting them (pushes do not
+  // synchronise the stream any more)
+  cudaEvent_t tab_ev = nullptr;
+  bool tab_pending = false;
+  // the sliced launch sequence, captured once per (chunks, slices) shape: the
+  // tables it reads live at fixed device addresses, so a replay is one
+  // cudaGraphLaunch instead of ~9 API calls per slice
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    int kernels = 0;
+  };
+  std::map<std::pair<int, int>, Graph> graphs;
+  bool slicing = true;  // lsgdbg_seg_slicing
+  void tables_free() {
+    if (tab_pending) {
+      LSG_CUDA(cudaEventSynchronize(tab_ev));
+      tab_pending = false;
+    }
+  }
+  void tables_sent(cudaStream_t st) {
+    LSG_CUDA(cudaEventRecord(tab_ev, st));
+    tab_pending = true;
+  }
   DevBuf<Chunk> chunks_dev;
   DevBuf<int16_t> staging;
   DevBuf<int32_t> streams_dev;
@@ -868,6 +910,17 @@ struct lsg_seg_s {
   cudaEvent_t k1a = nullptr, k1b = nullptr;
   bool k1_recorded = false;
   ~lsg_seg_s() {
+    for (int j = 0; j < 3; ++j) {
+      if (eK1[j]) cudaEventDestroy(eK1[j]);
+      if (ePk[j]) cudaEventDestroy(ePk[j]);
+      if (eM[j]) cudaEventDestroy(eM[j]);
+    }
+    if (eJoin) cudaEventDestroy(eJoin);
+    if (tab_ev) cudaEventDestroy(tab_ev);
+    for (auto& g : graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    if (sB) cudaStreamDestroy(sB);
+    if (sC) cudaStreamDestroy(sC);
     if (k1a) cudaEventDestroy(k1a);
     if (k1b) cudaEventDestroy(k1b);
     if (h_state) cudaFreeHost(h_state);
@@ -918,7 +971,7 @@ static void collect(lsg_seg h, bool finishing) {
     const DevState& D = h->h_state[i];
     if (D.overflow) fail(LSG_ERUNTIME, "segmenter: cut buffer overflow");
     const int a = h->h_off[i], b = h->h_off[i + 1];
-    for (int k = a; k < b; ++k) S.cuts.push_back(h->h_cuts[k]);
+    S.cuts.insert(S.cuts.end(), h->h_cuts + a, h->h_cuts + b);
     S.metrics.frames = D.m_frames;
     S.metrics.speech_frames = D.m_speech;
     S.metrics.cuts_pause = D.m_pause;
@@ -930,6 +983,93 @@ static void collect(lsg_seg h, bool finishing) {
       for (int f = 0; f < D.n_flag_frames; ++f) S.flags[f] = (w[f >> 5] >> (f & 31)) & 1;
     }
   }
+}
+
+// Time-sliced push (see kSlice): slice k of every chunk is frames
+// [k*kSlice, (k+1)*kSlice) (the chunk's last slice also holds its sub-frame
+// tail, which seg_carry keeps).  Per slice, on three streams:
+//   ctx stream: K1 (stats of the slice into slot k % kSlots)     -> eK1
+//   sB:         K2a peak chain (in slice order: the peak carries) -> ePk
+//   sC:         K2b decisions + K2c machine (in slice order)      -> eM
+// A slot is reused only after the machine of the slice that last used it
+// (the slot's last reader) has completed.  Bit-identical to one launch: the
+// peak and machine state carry through DevState exactly as across pushes.
+static void launch_sliced(lsg_seg h, int nc, int64_t max_frames) {
+  Ctx* ctx = h->ctx;
+  const Params& P = h->P;
+  cudaStream_t sA = ctx->stream;
+  const int K = (int)((max_frames + kSlice - 1) / kSlice);
+  if (K > h->max_slices) fail(LSG_ERUNTIME, "lsg_seg_push: push longer than the slice tables");
+  // all slices' chunk tables in one copy
+  for (int k = 0; k < K; ++k) {
+    int64_t off = 0;
+    for (int i = 0; i < nc; ++i) {
+      const Chunk& c = h->chunks_host.p[i];
+      Chunk& d = h->chunks_sl_host.p[(size_t)k * nc + i];
+      d = c;
+      const int last = std::max(0, (c.nframes + kSlice - 1) / kSlice - 1);
+      const int64_t s0 = (int64_t)k * kSlice * P.fs;
+      d.pcm = c.pcm + s0;
+      d.n = k < last ? (int64_t)kSlice * P.fs : (k == last ? c.n - s0 : 0);
+      d.nframes = k <= last ? std::min(kSlice, c.nframes - k * kSlice) : 0;
+      if (d.nframes < 0) d.nframes = 0;
+      d.first = k == 0 ? c.first : 0;
+      d.frame_off = (int64_t)(k % kSlots) * nc * kSlice + off;
+      off += d.nframes;
+    }
+  }
+  LSG_CUDA(cudaMemcpyAsync(h->chunks_sl.p, h->chunks_sl_host.p, sizeof(Chunk) * (size_t)K * nc,
+                           cudaMemcpyHostToDevice, sA));
+  h->tables_sent(sA);
+  if (!h->k1a) {
+    LSG_CUDA(cudaEventCreate(&h->k1a));
+    LSG_CUDA(cudaEventCreate(&h->k1b));
+  }
+  auto& g = h->graphs[std::make_pair(nc, K)];
+  if (!g.exec) {
+    // capture: sB / sC fork from the context stream and join back into it
+    LSG_CUDA(cudaStreamBeginCapture(sA, cudaStreamCaptureModeThreadLocal));
+    LSG_CUDA(cudaEventRecord(h->eJoin, sA));
+    LSG_CUDA(cudaStreamWaitEvent(h->sB, h->eJoin, 0));
+    LSG_CUDA(cudaStreamWaitEvent(h->sC, h->eJoin, 0));
+    const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
+    const int row_words = kSlice / 32 + 1;
+    int kernels = 0;
+    for (int k = 0; k < K; ++k) {
+      const int j = k % kSlots;
+      const Chunk* tab = h->chunks_sl.p + (size_t)k * nc;
+      if (k >= kSlots) LSG_CUDA(cudaStreamWaitEvent(sA, h->eM[j], 0));  // slot free
+      dim3 grid((unsigned)ceil_div(kSlice, K1_WARPS * K1_FPW), (unsigned)nc);
+      seg_frame_stats<<<grid, K1_WARPS * 32, 0, sA>>>(tab, h->carry.p, P.fs, h->stats.p);
+      LSG_CUDA(cudaEventRecord(h->eK1[j], sA));
+      LSG_CUDA(cudaStreamWaitEvent(h->sB, h->eK1[j], 0));
+      seg_peaks<<<g2, K2_LANES, PK_SMEM, h->sB>>>(tab, nc, h->stats.p, h->st.p, h->peaks.p, P, j * kSlice);
+      LSG_CUDA(cudaEventRecord(h->ePk[j], h->sB));
+      LSG_CUDA(cudaStreamWaitEvent(h->sC, h->ePk[j], 0));
+      seg_decide<<<dim3((unsigned)(kSlice / 256), (unsigned)nc), 256, 0, h->sC>>>(
+          tab, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P, j * kSlice, j * kSlice / 32);
+      seg_machine<<<(unsigned)ceil_div(nc, MC_WARPS), MC_WARPS * 32, (size_t)MC_WARPS * row_words * 4, h->sC>>>(
+          tab, nc, h->st.p, h->cuts.p, h->flags.p, P, row_words, j * kSlice / 32);
+      LSG_CUDA(cudaEventRecord(h->eM[j], h->sC));
+      kernels += 4;
+    }
+    // join: the context stream continues after the last machine
+    LSG_CUDA(cudaStreamWaitEvent(sA, h->eM[(K - 1) % kSlots], 0));
+    LSG_CUDA(cudaStreamWaitEvent(sA, h->ePk[(K - 1) % kSlots], 0));
+    seg_carry<<<nc, 256, 0, sA>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
+    kernels += 1;
+    cudaGraph_t graph = nullptr;
+    LSG_CUDA(cudaStreamEndCapture(sA, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    LSG_CUDA(e);
+    g.kernels = kernels;
+  }
+  LSG_CUDA(cudaEventRecord(h->k1a, sA));
+  LSG_CUDA(cudaGraphLaunch(g.exec, sA));
+  LSG_CUDA(cudaEventRecord(h->k1b, sA));  // (sliced: K1 overlapped with K2 -- the whole sequence)
+  h->k1_recorded = true;
+  ctx->launches.fetch_add(g.kernels, std::memory_order_relaxed);
 }
 
 extern "C" {
@@ -1016,6 +1156,25 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->totals_host.alloc(n_streams);
       h->dirty.assign(n_streams, 0);
       h->cut_bound.assign(n_streams, 0);
+      LSG_CUDA(cudaEventCreateWithFlags(&h->tab_ev, cudaEventDisableTiming));
+      if (h->max_frames_push >= kSlots * kSlice) {
+        h->max_slices = (int)((h->max_frames_push + kSlice - 1) / kSlice);
+        h->chunks_sl.alloc((size_t)n_streams * h->max_slices);
+        h->chunks_sl_host.alloc((size_t)n_streams * h->max_slices);
+        // the sequential K2 work is latency-bound on a few SMs: its CTAs get
+        // the highest priority so that they are dispatched as soon as a
+        // (short) K1 CTA retires instead of after the whole K1 grid
+        int lo = 0, hi = 0;
+        LSG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LSG_CUDA(cudaStreamCreateWithPriority(&h->sB, cudaStreamNonBlocking, hi));
+        LSG_CUDA(cudaStreamCreateWithPriority(&h->sC, cudaStreamNonBlocking, hi));
+        for (int j = 0; j < kSlots; ++j) {
+          LSG_CUDA(cudaEventCreateWithFlags(&h->eK1[j], cudaEventDisableTiming));
+          LSG_CUDA(cudaEventCreateWithFlags(&h->ePk[j], cudaEventDisableTiming));
+          LSG_CUDA(cudaEventCreateWithFlags(&h->eM[j], cudaEventDisableTiming));
+        }
+        LSG_CUDA(cudaEventCreateWithFlags(&h->eJoin, cudaEventDisableTiming));
+      }
       h->h_cut_cap = (int64_t)n_streams * P.cut_cap;
       LSG_CUDA(cudaHostAlloc(&h->h_state, sizeof(DevState) * n_streams, cudaHostAllocMapped));
       LSG_CUDA(cudaHostAlloc(&h->h_off, sizeof(int32_t) * (n_streams + 1), cudaHostAllocMapped));
@@ -1048,7 +1207,14 @@ lsg_status lsg_seg_reset(lsg_seg h) {
   });
 }
 
-// Device time (ms) of the last push's frame-statistics kernel (K1).
+// Time slicing of long device-resident pushes on (1, default) or off (0):
+// off measures K1 alone (lsgdbg_seg_k1_ms) for the HBM roofline.
+lsg_status lsgdbg_seg_slicing(lsg_seg h, int32_t on) {
+  return guard(__func__, [&] { h->slicing = on != 0; });
+}
+
+// Device time (ms) of the last push's frame-statistics kernel (K1; for a
+// time-sliced push, the whole overlapped K1 + K2 sequence).
 lsg_status lsgdbg_seg_k1_ms(lsg_seg h, float* ms) {
   return guard(__func__, [&] {
     if (!h || !ms) invalid("lsgdbg_seg_k1_ms: null argument");
@@ -1104,6 +1270,19 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
         break;
       }
     }
+    // time-sliced processing (launch_sliced): long device-resident pushes
+    // with no sub-frame carry, outside the scorer (flags) mode
+    bool sliced = h->max_slices > 0 && !P.flags_only && h->slicing;
+    int64_t longest = 0;
+    for (int i = 0; i < n_chunks && sliced; ++i) {
+      const StreamHost& S = h->hs[streams[i]];
+      if (S.stage_len != 0 || !(pcm_on_device || is_device_ptr(pcm[i])) ||
+          (reinterpret_cast<uintptr_t>(pcm[i]) & 15) != 0)
+        sliced = false;
+      longest = std::max<int64_t>(longest, n_samples[i] / P.fs);
+    }
+    sliced = sliced && longest >= 2 * kSlice;
+    h->tables_free();
     // pass 2: stage + describe chunks
     int nc = 0;
     int64_t frame_total = 0, max_frames = 0, stage_off = 0;
@@ -1155,7 +1334,8 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
                              ctx->stream));
     LSG_CUDA(cudaMemcpyAsync(h->streams_dev.p, h->streams_host.p, sizeof(int32_t) * nc,
                              cudaMemcpyHostToDevice, ctx->stream));
-    if (max_frames > 0) {
+    if (!sliced) h->tables_sent(ctx->stream);
+    if (max_frames > 0 && !sliced) {
       dim3 grid((unsigned)ceil_div(max_frames, K1_WARPS * K1_FPW), (unsigned)nc);
       if (!h->k1a) {
         LSG_CUDA(cudaEventCreate(&h->k1a));
@@ -1168,23 +1348,28 @@ lsg_status lsg_seg_push(lsg_seg h, int32_t n_chunks, const int32_t* streams, con
       LSG_CUDA(cudaEventRecord(h->k1b, ctx->stream));
       h->k1_recorded = true;
     }
-    const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
     if (!h->attrs_set) {  // per handle: kernel attributes are per device
       LSG_CUDA(cudaFuncSetAttribute(seg_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM));
       LSG_CUDA(cudaFuncSetAttribute(seg_machine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       h->attrs_set = true;
     }
-    seg_peaks<<<g2, K2_LANES, PK_SMEM, ctx->stream>>>(h->chunks_dev.p, nc, h->stats.p, h->st.p, h->peaks.p, P);
+    if (sliced) {
+      launch_sliced(h, nc, max_frames);
+      if (P.flags_only) collect(h, false);
+      return;
+    }
+    const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
+    seg_peaks<<<g2, K2_LANES, PK_SMEM, ctx->stream>>>(h->chunks_dev.p, nc, h->stats.p, h->st.p, h->peaks.p, P, 0);
     LSG_LAUNCHED(ctx);
     if (max_frames > 0) {
       seg_decide<<<dim3((unsigned)ceil_div(max_frames, 256), (unsigned)nc), 256, 0, ctx->stream>>>(
-          h->chunks_dev.p, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P);
+          h->chunks_dev.p, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P, 0, 0);
       LSG_LAUNCHED(ctx);
     }
     const int row_words = (int)((max_frames + 31) / 32) | 1;
     if ((size_t)MC_WARPS * row_words * 4 > 200 * 1024) fail(LSG_ERUNTIME, "lsg_seg_push: push too long for K2c");
     seg_machine<<<(unsigned)ceil_div(nc, MC_WARPS), MC_WARPS * 32, (size_t)MC_WARPS * row_words * 4, ctx->stream>>>(
-        h->chunks_dev.p, nc, h->st.p, h->cuts.p, h->flags.p, P, row_words);
+        h->chunks_dev.p, nc, h->st.p, h->cuts.p, h->flags.p, P, row_words, 0);
     LSG_LAUNCHED(ctx);
     seg_carry<<<nc, 256, 0, ctx->stream>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     LSG_LAUNCHED(ctx);
@@ -1208,6 +1393,7 @@ lsg_status lsg_seg_finish(lsg_seg h, int32_t n, const int32_t* streams) {
     }
     if (n == 0) return;
     DeviceGuard g(ctx);
+    h->tables_free();
     for (int i = 0; i < n; ++i) {
       const int s = streams[i];
       h->streams_host.p[i] = s;

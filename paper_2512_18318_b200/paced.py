@@ -162,6 +162,72 @@ class PacedRunner:
         return J
 
 
+class LibPacedRunner:
+    """The paced driver in the library (lsg_paced, csrc/paced.cu): the same
+    real-time release as PacedRunner, but the tick loop, the segment-ready
+    rule, the deadline batcher (a generator batch as soon as max_batch
+    frames are queued, or when the oldest has waited deadline_ms) and the
+    completion stamps (cudaLaunchHostFunc) all run in C++; generator batches
+    never block the tick loop, and the segmenter works on its own context."""
+
+    def __init__(self, engine, n_streams: int, max_stream_samples: int, max_video: int, fps: float = 25.0,
+                 margin_ms: int = 50, tick_ms: int = 40, max_batch: int | None = None, deadline_ms: int = 20,
+                 seg_cfg: SegmenterConfig | None = None, mel_cfg: MelConfig | None = None):
+        import ctypes as C
+        from ._lib import PacedCfg, lib
+        self.lib = lib()
+        self.S = n_streams
+        cfg = PacedCfg(n_streams, fps, margin_ms, tick_ms, max_batch or engine.max_batch, deadline_ms,
+                       max_stream_samples, max_video)
+        h = C.c_void_p()
+        self.lib.call("lsg_paced_create", engine.h, C.byref(cfg), C.byref((seg_cfg or SegmenterConfig()).to_c()),
+                      C.byref((mel_cfg or MelConfig()).to_c()), C.byref(h))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.lsg_paced_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, pcm_dev, n_samples, video_dev, n_video, refs_dev, seconds: float = 0.0, frames_out=None,
+            frames_cap: int = 0):
+        """Device tensors as PacedRunner.run; returns (PacedResult, segments
+        [dicts], records [dicts] when frames_out is given)."""
+        import ctypes as C
+        from ._lib import FrameRec, PacedSeg
+        S = self.S
+        cap = S * 4096
+        segs = (PacedSeg * cap)()
+        ns = (C.c_int64 * S)(*n_samples)
+        nv = (C.c_int64 * S)(*n_video)
+        n_seg, n_fr, late = C.c_int64(), C.c_int64(), C.c_int32()
+        recs = (FrameRec * max(frames_cap, 1))() if frames_out is not None else None
+        self.lib.call("lsg_paced_run", self.h, C.c_void_p(pcm_dev.data_ptr()), ns, C.c_void_p(video_dev.data_ptr()),
+                      nv, C.c_void_p(refs_dev.data_ptr()), float(seconds), segs, cap, C.byref(n_seg),
+                      C.c_void_p(frames_out.data_ptr()) if frames_out is not None else None, recs, frames_cap,
+                      C.byref(n_fr), C.byref(late))
+        k = min(n_seg.value, cap)
+        out = [dict(stream=segs[i].stream, segment=segs[i].segment, begin=segs[i].begin, end=segs[i].end,
+                    cause=segs[i].cause, frames=segs[i].frames, decided_ms=segs[i].decided_ms,
+                    rendered_ms=segs[i].rendered_ms) for i in range(k)]
+        lat = np.array([s["rendered_ms"] - s["end"] for s in out])
+        dec = np.array([s["decided_ms"] - s["end"] for s in out])
+        ren = np.array([s["rendered_ms"] - s["decided_ms"] for s in out])
+        total_ms = int(min(n_samples) * 1000 // 16000) if seconds <= 0 else int(seconds * 1000)
+        res = PacedResult(lat, dec, ren, int(n_fr.value), k, total_ms // 40 + 1, int(late.value))
+        rec = None
+        if recs is not None:
+            rec = [dict(stream=recs[i].stream, segment=recs[i].segment, frame_index=recs[i].frame_index,
+                        ts_ms=recs[i].ts_ms, mel_row=recs[i].mel_row) for i in range(min(n_fr.value, frames_cap))]
+        return res, out, rec
+
+
 def summarize(r: PacedResult, streams_total: int, seconds: float) -> dict:
     return {"streams": streams_total, "seconds": seconds, "segments": r.segments, "frames": r.frames,
             "p50_ms": _pct(r.latencies_ms, 50), "p99_ms": _pct(r.latencies_ms, 99),

@@ -197,3 +197,37 @@ def test_scaled_streams_properties_and_oracle(restated, reference):
             assert sum(c["sample_len"] for c in got) == sum(c["sample_len"] for c in want)
             for k in range(1, len(got)):
                 assert got[k]["begin"] == got[k - 1]["end"]
+
+
+def test_device_resident_long_pushes_time_sliced(reference):
+    """Pushes of >= 1024 frames per stream from device memory take the
+    time-sliced path (K1 of slice s+1 overlapping the peak chain and the
+    machine of slice s, segmenter.cu launch_sliced): cuts and metrics stay
+    bit-identical to the reference, in one push and in a push that follows a
+    frame-aligned first push (the peak / machine state carries across)."""
+    torch = pytest.importorskip("torch")
+    streams = config2_streams(reference.render_pattern)
+    state = [4242]
+    for i in range(8):
+        p = random_pattern(state)
+        p.tone_hz = float(160 + 29 * i)
+        streams.append(reference.render_pattern(p, 60000))
+    n, L = len(streams), 60 * 16000
+    dev = torch.from_numpy(np.stack([s[:L] for s in streams])).cuda()
+    base = dev.data_ptr()
+    for split in (0, 320 * 75):  # one push; 1.5 s then the rest (aligned: no carry)
+        ms = api.MultiStreamSegmenter(api.SegmenterConfig(), n, L)
+        if split:
+            ms.push(list(range(n)), [(base + s * L * 2, split) for s in range(n)], [0] * n, on_device=True)
+        ms.push(list(range(n)), [(base + (s * L + split) * 2, L - split) for s in range(n)],
+                [split // 16] * n, on_device=True)
+        torch.cuda.synchronize()
+        ms.finish(list(range(n)))
+        for s in range(n):
+            want, wm, _ = reference.segment(streams[s][:L])
+            got = [dict(begin=c.begin, end=c.end, confidence=c.confidence, cause=c.cause, sample_off=c.sample_off,
+                        sample_len=c.sample_len) for c in ms.take_cuts(s)]
+            assert got == want, (split, s)
+            m = ms.metrics(s)
+            assert (m.frames, m.speech_frames, m.cuts_pause, m.cuts_forced, m.cuts_eos) == \
+                tuple(int(wm[k]) for k in ("frames", "speech_frames", "cuts_pause", "cuts_forced", "cuts_eos"))

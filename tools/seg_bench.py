@@ -39,14 +39,19 @@ def main():
             ctx.lib.call("lsg_seg_reset", seg.h)
             flush.zero_()
             e0.record(st)
-            seg.push_finish_prepared(args)
+            import time
+            th0 = time.perf_counter()
+            ctx.lib.call("lsg_seg_push", *args[0])
+            thp = time.perf_counter()
+            ctx.lib.call("lsg_seg_finish", *args[1])
+            th1 = time.perf_counter()
             e1.record(st)
         st.synchronize()
         cuts = seg.take_all_cuts()
         k1 = C.c_float()
         ctx.lib.check(ctx.lib.dll.lsgdbg_seg_k1_ms(seg.h, C.byref(k1)))
         ms = e0.elapsed_time(e1)
-        print(f"segmenter {S} x {secs} s: call {ms:.3f} ms = {S * n * 2 / ms / 1e6:.0f} GB/s, "
+        print(f"segmenter {S} x {secs} s: host push {1e3 * (thp - th0):.3f} ms (+finish {1e3 * (th1 - thp):.3f}); call {ms:.3f} ms = {S * n * 2 / ms / 1e6:.0f} GB/s, "
               f"K1 {k1.value:.3f} ms = {S * n * 2 / k1.value / 1e6:.0f} GB/s, {len(cuts)} cuts")
 
 
