@@ -505,9 +505,13 @@ def cuda_core_peaks():
 
 def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, fps):
     """Config 5 paced: this rank's share of --paced-streams released in real
-    time; p50/p99 of (segment's last frame rendered - media time of its cut)
-    over all ranks' segments (paper_2512_18318_b200/paced.py)."""
-    from paper_2512_18318_b200.paced import PacedRunner, summarize
+    time through the library's paced driver (lsg_paced: 40 ms ticks, GPU
+    segmenter on its own context, deadline batcher -- a generator batch of up
+    to 128 frames as soon as it is full or when its oldest frame has waited
+    20 ms -- and completion stamps from cudaLaunchHostFunc); p50/p99 of
+    (segment's last frame rendered - media time of its end) over all ranks'
+    segments."""
+    from paper_2512_18318_b200.paced import LibPacedRunner, summarize
     secs = args.paced_seconds
     pcm, video, refs = make_workload(rank, args.paced_streams, secs + 1, fps, api, generator, world, seed_base=1000)
     per = len(pcm)
@@ -522,14 +526,12 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
         vid_dev[s, :len(v)] = torch.from_numpy(v)
     refs_dev = torch.from_numpy(refs).to(dev)
     n_samples = [secs * 16000] * per
-    s_run = torch.cuda.Stream(device=local)
-    with torch.cuda.stream(s_run):
-        ctx.set_stream(s_run.cuda_stream)
-        runner = PacedRunner(eng, ctx, torch, per, fps=fps)
-        runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, dev, seconds=2)  # warm-up
-        if dist:
-            dist.barrier()
-        res = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, dev)
+    runner = LibPacedRunner(eng, per, ms, mv, fps=fps, max_batch=min(128, eng.max_batch), deadline_ms=20)
+    runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, seconds=2)  # warm-up
+    if dist:
+        dist.barrier()
+    res, _, _ = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev)
+    runner.close()
     if dist:
         from paper_2512_18318_b200.shard import gather_arrays
         res.latencies_ms, res.decision_ms, res.render_ms, fr, lt = gather_arrays(
@@ -538,9 +540,11 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
         res.segments = len(res.latencies_ms)
     out = summarize(res, args.paced_streams, secs)
     out["streams_per_gpu"] = per
-    out["definition"] = ("latency = wall time the segment's last frame is rendered on the device - wall time media "
-                         "time reached the segment end (audio and 25 fps video released in real time, 40 ms "
-                         "ticks); decision = when the segmenter emitted the cut; render = decision -> rendered")
+    out["driver"] = "lsg_paced (csrc/paced.cu): generator batches <= 128 frames, 20 ms deadline"
+    out["definition"] = ("latency = wall time the segment's last frame is rendered on the device (cudaLaunchHostFunc "
+                         "stamp) - wall time media time reached the segment end (audio and 25 fps video released in "
+                         "real time, 40 ms ticks); decision = when the segmenter emitted the cut; render = decision "
+                         "-> rendered")
     out["rendered_fps_demand"] = res.frames / secs
     return out
 
