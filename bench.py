@@ -507,7 +507,7 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
     """Config 5 paced: this rank's share of --paced-streams released in real
     time through the library's paced driver (lsg_paced: 40 ms ticks, GPU
     segmenter on its own context, deadline batcher -- a generator batch of up
-    to 128 frames as soon as it is full or when its oldest frame has waited
+    to 512 frames as soon as it is full or when its oldest frame has waited
     20 ms -- and completion stamps from cudaLaunchHostFunc); p50/p99 of
     (segment's last frame rendered - media time of its end) over all ranks'
     segments."""
@@ -525,12 +525,16 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
     for s, v in enumerate(video):
         vid_dev[s, :len(v)] = torch.from_numpy(v)
     refs_dev = torch.from_numpy(refs).to(dev)
-    n_samples = [secs * 16000] * per
-    runner = LibPacedRunner(eng, per, ms, mv, fps=fps, max_batch=min(128, eng.max_batch), deadline_ms=20)
+    # streams end at staggered times (0-3.6 s before the run's end), as live
+    # feeds do: every stream's EOS segment is flushed on its own tick
+    from paper_2512_18318_b200.shard import streams_for_rank
+    gids = streams_for_rank(args.paced_streams, rank, world)
+    n_samples = [(secs * 1000 - (g % 10) * 400) * 16 for g in gids]
+    runner = LibPacedRunner(eng, per, ms, mv, fps=fps, max_batch=min(512, eng.max_batch), deadline_ms=20)
     runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, seconds=2)  # warm-up
     if dist:
         dist.barrier()
-    res, _, _ = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev)
+    res, _, _ = runner.run(pcm_dev, n_samples, vid_dev, [len(v) for v in video], refs_dev, seconds=secs)
     runner.close()
     if dist:
         from paper_2512_18318_b200.shard import gather_arrays
@@ -540,11 +544,11 @@ def paced_leg(args, rank, world, local, dist, torch, ctx, eng, api, generator, f
         res.segments = len(res.latencies_ms)
     out = summarize(res, args.paced_streams, secs)
     out["streams_per_gpu"] = per
-    out["driver"] = "lsg_paced (csrc/paced.cu): generator batches <= 128 frames, 20 ms deadline"
+    out["driver"] = "lsg_paced (csrc/paced.cu): generator batches <= 512 frames, 20 ms deadline"
     out["definition"] = ("latency = wall time the segment's last frame is rendered on the device (cudaLaunchHostFunc "
                          "stamp) - wall time media time reached the segment end (audio and 25 fps video released in "
-                         "real time, 40 ms ticks); decision = when the segmenter emitted the cut; render = decision "
-                         "-> rendered")
+                         "real time, 40 ms ticks; streams end at staggered times over the last 3.6 s); decision = "
+                         "when the segmenter emitted the cut; render = decision -> rendered")
     out["rendered_fps_demand"] = res.frames / secs
     return out
 

@@ -339,8 +339,9 @@ lsg_status lsg_mpipe_run(lsg_mpipe h, const int16_t* const* pcm, const int64_t* 
  * window [begin - margin, end + margin] is complete get their mel and frame
  * jobs (rule a8); a deadline batcher launches generator batches on the
  * generator's context without blocking the tick loop -- a full batch as soon
- * as max_batch frames are queued, a partial one once the oldest queued frame
- * has waited deadline_ms -- and cudaLaunchHostFunc stamps each segment's
+ * as max_batch frames are queued, a partial one when no batch is in flight
+ * or once the oldest queued frame has waited deadline_ms -- and
+ * cudaLaunchHostFunc stamps each segment's
  * completion when its last frame's batch finishes (the reference's
  * StageWorker -> MediaClock completion, worker.cpp:19-36, clock.cpp:124-145). */
 typedef struct {

@@ -386,19 +386,31 @@ struct lsg_mel_s {
   DevBuf<cplx> tw, tw_half;
   DevBuf<int32_t> band;  // lo | n | off
   DevBuf<int64_t> seg_tab;  // pcm_off | frame0 | out_row for batch calls
-  PinnedBuf<int64_t> seg_tab_host;
   // the pinned segment table is copied asynchronously by batch calls, which
-  // do not synchronise: the next call waits for that copy before rewriting it
-  cudaEvent_t tab_ev = nullptr;
-  bool tab_pending = false;
-  void tab_free() {
-    if (tab_pending) {
-      LSG_CUDA(cudaEventSynchronize(tab_ev));
-      tab_pending = false;
+  // do not synchronise: a ring of kRing host tables, each reused only after
+  // its copy (event) has executed -- a caller that queues batches behind
+  // long-running work (the paced driver) is not blocked by the next call
+  static constexpr int kRing = 8;
+  PinnedBuf<int64_t> seg_tab_host[kRing];
+  cudaEvent_t tab_ev[kRing] = {};
+  bool tab_pending[kRing] = {};
+  int tab_next = 0;
+  int64_t* tab_acquire() {  // the next ring table, free for writing
+    const int i = tab_next;
+    if (tab_pending[i]) {
+      LSG_CUDA(cudaEventSynchronize(tab_ev[i]));
+      tab_pending[i] = false;
     }
+    return seg_tab_host[i].p;
+  }
+  void tab_sent(cudaStream_t st) {  // after the copy of the table tab_acquire returned
+    LSG_CUDA(cudaEventRecord(tab_ev[tab_next], st));
+    tab_pending[tab_next] = true;
+    tab_next = (tab_next + 1) % kRing;
   }
   ~lsg_mel_s() {
-    if (tab_ev) cudaEventDestroy(tab_ev);
+    for (auto e : tab_ev)
+      if (e) cudaEventDestroy(e);
   }
   int32_t max_seg = 0;
   DevBuf<int16_t> pcm_stage;
@@ -659,8 +671,10 @@ lsg_status lsg_mel_create(lsg_ctx ctx, const lsg_mel_cfg* cfg, int64_t max_frame
       h->T.weights = h->weights.p;
       h->max_seg = 4096;
       h->seg_tab.alloc(3 * (size_t)h->max_seg + 1);
-      h->seg_tab_host.alloc(3 * (size_t)h->max_seg + 1);
-      LSG_CUDA(cudaEventCreateWithFlags(&h->tab_ev, cudaEventDisableTiming));
+      for (int i = 0; i < lsg_mel_s::kRing; ++i) {
+        h->seg_tab_host[i].alloc(3 * (size_t)h->max_seg + 1);
+        LSG_CUDA(cudaEventCreateWithFlags(&h->tab_ev[i], cudaEventDisableTiming));
+      }
       const int64_t max_samples = (max_frames - 1) * cfg->hop + N;
       h->pcm_stage.alloc((size_t)max_samples);
       h->out_stage.alloc((size_t)max_frames * M);
@@ -719,13 +733,13 @@ lsg_status lsg_mel_compute(lsg_mel h, const int16_t* pcm, int64_t n, float* out,
     }
     const bool out_dev = is_device_ptr(out);
     float* dout = out_dev ? out : h->out_stage.p;
-    h->tab_free();
-    int64_t* t = h->seg_tab_host.p;  // packed [pcm_off | frame0 (n+1) | out_row], n = 1
+    int64_t* t = h->tab_acquire();  // packed [pcm_off | frame0 (n+1) | out_row], n = 1
     t[0] = 0;
     t[1] = 0;
     t[2] = F;
     t[3] = 0;
     LSG_CUDA(cudaMemcpyAsync(h->seg_tab.p, t, 4 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    h->tab_sent(ctx->stream);
     launch(h, dpcm, 1, F, dout);
     if (!out_dev) {
       LSG_CUDA(cudaMemcpyAsync(out, dout, (size_t)F * h->cfg.n_mels * 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -741,8 +755,7 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
     if (n_seg < 0 || n_seg > h->max_seg) invalid("lsg_mel_compute_batch: too many segments (max 4096)");
     DeviceGuard g(ctx);
     const int N = h->cfg.fft_size;
-    h->tab_free();
-    int64_t* t = h->seg_tab_host.p;
+    int64_t* t = h->tab_acquire();
     int64_t tot = 0;
     for (int i = 0; i < n_seg; ++i) {  // packed [pcm_off | frame0 (n+1) | out_row]
       if (n_samples[i] < 0) invalid("lsg_mel_compute_batch: negative length");
@@ -756,8 +769,7 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
     if (tot == 0) return;
     LSG_CUDA(cudaMemcpyAsync(h->seg_tab.p, t, (3 * (size_t)n_seg + 1) * 8, cudaMemcpyHostToDevice,
                              ctx->stream));
-    LSG_CUDA(cudaEventRecord(h->tab_ev, ctx->stream));
-    h->tab_pending = true;
+    h->tab_sent(ctx->stream);
     launch(h, pcm_base, n_seg, tot, out_base);
   });
 }

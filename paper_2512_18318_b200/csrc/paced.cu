@@ -15,13 +15,15 @@
 //   * segments whose frame window is complete get their log-mel in one batch
 //     launch and their frames (rule a8 chunk index) appended to a frame queue;
 //   * a deadline batcher launches generator batches asynchronously: as soon as
-//     max_batch frames are queued, or when the oldest queued frame has waited
-//     deadline_ms (so a lone segment is not held back for a full batch);
+//     max_batch frames are queued, when the GPU has no batch in flight
+//     (continuous batching), or when the oldest queued frame has waited
+//     deadline_ms;
 //   * each batch ends with cudaLaunchHostFunc: the callback stamps the wall
 //     time for every segment whose last frame was in it -- the completion
 //     event the reference's MediaClock would receive.
 // The host loop never blocks on rendering; buffers (mel rows, job tables,
 // rendered frames) are rings reused once their batch's event has completed.
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -81,20 +83,26 @@ struct lsg_paced_s {
   int64_t ring_rows = 0;
   int64_t ring_pos = 0;   // next free row (monotone; position mod ring_rows)
   DevBuf<int64_t> pad_tab;
-  PinnedBuf<int64_t> h_pad_tab;
-  cudaEvent_t pad_ev = nullptr;
-  bool pad_pending = false;
+  // pinned pad tables: a ring, each reused once its copy has executed (the
+  // render stream may hold many queued batches; the tick loop must not wait)
+  static constexpr int kPadRing = 8;
+  PinnedBuf<int64_t> h_pad_tab[kPadRing];
+  cudaEvent_t pad_ev[kPadRing] = {};
+  bool pad_pending[kPadRing] = {};
+  int pad_next = 0;
   Slot slots[kSlots];
   int next_slot = 0;
   DevBuf<uint8_t> scratch_out;  // rendered frames when the caller keeps none
   // per run
   Clock::time_point t0;
+  std::atomic<int> inflight{0};  // generator batches launched and not completed (host callbacks)
   std::vector<double> rendered;  // per segment id, written by host callbacks
   ~lsg_paced_s() {
     if (rctx) cudaStreamSynchronize(rctx->stream);
     for (auto& s : slots)
       if (s.ev) cudaEventDestroy(s.ev);
-    if (pad_ev) cudaEventDestroy(pad_ev);
+    for (auto e : pad_ev)
+      if (e) cudaEventDestroy(e);
     if (seg) lsg_seg_destroy(seg);
     if (mel) lsg_mel_destroy(mel);
     if (sctx) lsg_ctx_destroy(sctx);
@@ -118,6 +126,7 @@ void CUDART_CB on_batch_done(void* p) {
   Slot* s = static_cast<Slot*>(p);
   const double t = ms_since(s->owner->t0);
   for (int32_t id : s->completes) s->owner->rendered[(size_t)id] = t;
+  s->owner->inflight.fetch_sub(1, std::memory_order_release);
 }
 
 }  // namespace
@@ -157,8 +166,10 @@ lsg_status lsg_paced_create(lsg_gen gen, const lsg_paced_cfg* cfg, const lsg_seg
       h->ring_rows = int64_t(1) << 18;
       h->rows.alloc((size_t)h->ring_rows * 80);
       h->pad_tab.alloc(3 * 4096);
-      h->h_pad_tab.alloc(3 * 4096);
-      LSG_CUDA(cudaEventCreateWithFlags(&h->pad_ev, cudaEventDisableTiming));
+      for (int i = 0; i < lsg_paced_s::kPadRing; ++i) {
+        h->h_pad_tab[i].alloc(3 * 4096);
+        LSG_CUDA(cudaEventCreateWithFlags(&h->pad_ev[i], cudaEventDisableTiming));
+      }
       for (auto& s : h->slots) {
         s.h_chunk.alloc((size_t)h->B);
         s.h_ref.alloc((size_t)h->B);
@@ -197,10 +208,18 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
     DeviceGuard g(h->rctx);
     cudaStream_t rs = h->rctx->stream;
     if (lsg_seg_reset(h->seg) != LSG_OK) fail(LSG_ERUNTIME, std::string("lsg_paced_run: ") + lsg_last_error());
-    int64_t total_ms = INT64_MAX;
-    for (int s = 0; s < S; ++s) total_ms = std::min<int64_t>(total_ms, n_samples[s] * 1000 / rate);
-    if (seconds > 0) total_ms = std::min<int64_t>(total_ms, (int64_t)(seconds * 1000.0));
+    // every stream runs to its own end (n_samples[s], capped at `seconds`):
+    // its EOS segment is flushed (lsg_seg_finish) on the tick its audio runs
+    // out, as a live feed would, not all streams at one final tick
+    std::vector<int64_t> end_samples(S);
+    int64_t total_ms = 0;
+    for (int s = 0; s < S; ++s) {
+      end_samples[s] = n_samples[s];
+      if (seconds > 0) end_samples[s] = std::min<int64_t>(end_samples[s], (int64_t)(seconds * rate));
+      total_ms = std::max<int64_t>(total_ms, end_samples[s] * 1000 / rate);
+    }
     const int64_t n_ticks = total_ms / tick;
+    std::vector<char> finished(S, 0);
     const int64_t spt = (int64_t)rate * tick / 1000;
     struct Seg {
       lsg_cut c;
@@ -256,6 +275,7 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
           const int64_t f = j.frame - (int64_t)sg.c.stream * C.max_video;
           recs[frames_done + b] = {sg.c.stream, sg.index, f, (int64_t)std::floor(f * 1000.0 / C.fps + 0.5), j.k, 0};
         }
+      h->inflight.fetch_add(1, std::memory_order_relaxed);
       LSG_CUDA(cudaLaunchHostFunc(rs, on_batch_done, &sl));
       LSG_CUDA(cudaEventRecord(sl.ev, rs));
       sl.busy = true;
@@ -270,18 +290,28 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
       if (wait > 0) std::this_thread::sleep_for(std::chrono::microseconds((int64_t)(wait * 1000.0)));
       else if (i > 0) ++late;
       // ---- this tick's audio -> segmenter (its own stream)
-      const int64_t a = i * spt, b = std::min<int64_t>((i + 1) * spt, total_ms * rate / 1000);
-      if (b > a) {
-        for (int s = 0; s < S; ++s) {
-          ptrs[s] = pcm + (int64_t)s * C.max_stream_samples + a;
-          lens[s] = b - a;
-          starts[s] = a * 1000 / rate;
+      const int64_t a = i * spt, b = (i + 1) * spt;
+      int np = 0;
+      std::vector<int32_t> ending;
+      for (int s = 0; s < S; ++s) {
+        if (finished[s]) continue;
+        const int64_t bs = std::min<int64_t>(b, end_samples[s]);
+        if (bs > a) {
+          ids[np] = s;
+          ptrs[np] = pcm + (int64_t)s * C.max_stream_samples + a;
+          lens[np] = bs - a;
+          starts[np] = a * 1000 / rate;
+          ++np;
         }
-        if (lsg_seg_push(h->seg, S, ids.data(), ptrs.data(), lens.data(), starts.data(), rate, 1) != LSG_OK)
-          fail(LSG_ERUNTIME, std::string("lsg_paced_run: push: ") + lsg_last_error());
+        if (bs >= end_samples[s] || final) ending.push_back(s);
       }
-      if (final && lsg_seg_finish(h->seg, S, ids.data()) != LSG_OK)
-        fail(LSG_ERUNTIME, std::string("lsg_paced_run: finish: ") + lsg_last_error());
+      if (np && lsg_seg_push(h->seg, np, ids.data(), ptrs.data(), lens.data(), starts.data(), rate, 1) != LSG_OK)
+        fail(LSG_ERUNTIME, std::string("lsg_paced_run: push: ") + lsg_last_error());
+      if (!ending.empty()) {
+        if (lsg_seg_finish(h->seg, (int32_t)ending.size(), ending.data()) != LSG_OK)
+          fail(LSG_ERUNTIME, std::string("lsg_paced_run: finish: ") + lsg_last_error());
+        for (int s : ending) finished[s] = 1;
+      }
       int64_t nc = 0;
       if (lsg_seg_take_all_cuts(h->seg, nullptr, 0, &nc) != LSG_OK) fail(LSG_ERUNTIME, lsg_last_error());
       if (nc > (int64_t)cuts.size()) cuts.resize((size_t)nc);
@@ -300,16 +330,21 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
       std::vector<int> ready;
       std::vector<int> still;
       for (int id : pending)
-        (final || segs[(size_t)id].c.end + C.gather_margin_ms <= media_now ? ready : still).push_back(id);
+        (final || finished[segs[(size_t)id].c.stream] || segs[(size_t)id].c.end + C.gather_margin_ms <= media_now
+             ? ready
+             : still)
+            .push_back(id);
       pending.swap(still);
       for (size_t r0 = 0; r0 < ready.size(); r0 += 4096) {
         const size_t r1 = std::min(ready.size(), r0 + 4096);
         std::vector<int64_t> off, len, row0;
         int np = 0;
-        if (h->pad_pending) {
-          LSG_CUDA(cudaEventSynchronize(h->pad_ev));
-          h->pad_pending = false;
+        const int pr = h->pad_next;
+        if (h->pad_pending[pr]) {
+          LSG_CUDA(cudaEventSynchronize(h->pad_ev[pr]));
+          h->pad_pending[pr] = false;
         }
+        int64_t* ptab = h->h_pad_tab[pr].p;
         for (size_t r = r0; r < r1; ++r) {
           Seg& sg = segs[(size_t)ready[r]];
           const int64_t F = sg.c.sample_len < N ? 0 : 1 + (sg.c.sample_len - N) / hop;
@@ -327,9 +362,9 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
           len.push_back(sg.c.sample_len);
           row0.push_back(pos);
           if (F < 16) {
-            h->h_pad_tab.p[3 * np] = pos;
-            h->h_pad_tab.p[3 * np + 1] = F;
-            h->h_pad_tab.p[3 * np + 2] = R;
+            ptab[3 * np] = pos;
+            ptab[3 * np + 1] = F;
+            ptab[3 * np + 2] = R;
             ++np;
           }
           // frames of [begin - margin, end + margin] (FrameRing::window, inclusive)
@@ -353,9 +388,10 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
             LSG_OK)
           fail(LSG_ERUNTIME, std::string("lsg_paced_run: mel: ") + lsg_last_error());
         if (np) {
-          LSG_CUDA(cudaMemcpyAsync(h->pad_tab.p, h->h_pad_tab.p, 3 * np * 8, cudaMemcpyHostToDevice, rs));
-          LSG_CUDA(cudaEventRecord(h->pad_ev, rs));
-          h->pad_pending = true;
+          LSG_CUDA(cudaMemcpyAsync(h->pad_tab.p, ptab, 3 * np * 8, cudaMemcpyHostToDevice, rs));
+          LSG_CUDA(cudaEventRecord(h->pad_ev[pr], rs));
+          h->pad_pending[pr] = true;
+          h->pad_next = (pr + 1) % lsg_paced_s::kPadRing;
           paced_pad<<<np, 256, 0, rs>>>(h->pad_tab.p, np, h->rows.p, 80, floor_v);
           LSG_LAUNCHED(h->rctx);
         }
@@ -366,8 +402,12 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
         launch(h->B);
         h->slots[(h->next_slot + kSlots - 1) % kSlots].row_hi = row_end;
       }
+      // a partial batch when the GPU has nothing queued (continuous batching:
+      // batches grow only while the GPU is busy), or once the oldest queued
+      // frame has waited deadline_ms
       const size_t left = q.size() - q_head;
-      if (left && (final || ms_since(h->t0) - q[q_head].queued >= C.deadline_ms)) {
+      if (left && (final || h->inflight.load(std::memory_order_acquire) == 0 ||
+                   ms_since(h->t0) - q[q_head].queued >= C.deadline_ms)) {
         const int64_t row_end = h->ring_pos;
         launch((int)left);
         h->slots[(h->next_slot + kSlots - 1) % kSlots].row_hi = row_end;

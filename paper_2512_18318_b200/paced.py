@@ -219,7 +219,7 @@ class LibPacedRunner:
         lat = np.array([s["rendered_ms"] - s["end"] for s in out])
         dec = np.array([s["decided_ms"] - s["end"] for s in out])
         ren = np.array([s["rendered_ms"] - s["decided_ms"] for s in out])
-        total_ms = int(min(n_samples) * 1000 // 16000) if seconds <= 0 else int(seconds * 1000)
+        total_ms = int(max(n_samples) * 1000 // 16000) if seconds <= 0 else int(seconds * 1000)
         res = PacedResult(lat, dec, ren, int(n_fr.value), k, total_ms // 40 + 1, int(late.value))
         rec = None
         if recs is not None:
