@@ -432,8 +432,9 @@ def main():
                                  "timed": "the pipeline's generator stage inside the step (device events), rank 0"},
                      "ms_per_launch_sequence": gen_ms, "flops_per_frame": FLOPS_PER_FRAME,
                      "traffic": generator_traffic(B),
-                     "traffic_source": "profiles/r01_gen512_launches.csv: sum of dram__bytes_read+write over the "
-                                       "forward's launches (ncu), bytes per launch sequence of 512 frames"},
+                     "traffic_source": "profiles/r02_gen512_launches.csv (r01 if absent): sum of "
+                                       "dram__bytes_read+write over the forward's launches (ncu), bytes per launch "
+                                       "sequence of 512 frames"},
         "generator_b128": ({"ms": gen_b128_ms, "frames_per_s": 128 / (gen_b128_ms / 1000.0),
                             "tflops": FLOPS_PER_FRAME * 128 / (gen_b128_ms / 1000.0) / 1e12}
                            if gen_b128_ms else None),
@@ -471,7 +472,9 @@ def generator_traffic(B):
     """DRAM bytes of one generator forward from the committed ncu launch list
     (profiles/r01_gen512_launches.csv, B=512), or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_gen512_launches.csv")
+    path = os.path.join(ROOT, "profiles", "r02_gen512_launches.csv")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01_gen512_launches.csv")
     if B != 512 or not os.path.exists(path):
         return None
     rows = list(csv.reader(open(path)))

@@ -28,7 +28,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include <cuda_bf16.h>
@@ -449,6 +451,11 @@ struct lsg_gen_s {
   DevBuf<float> splitk_ws2;
   DevBuf<float> ae0w;  // ae0 weights [32][9] as quantized for the MMA (audio_stem)
   ~lsg_gen_s() {
+    for (auto& g : fwd_graphs) {
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+      if (g.second.graph) cudaGraphDestroy(g.second.graph);
+    }
+    if (cap) cudaStreamDestroy(cap);
     delete head;
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -457,6 +464,19 @@ struct lsg_gen_s {
   View x_face, x_mel, cat[7], S0, S1, A0, A1;
   View X16;  // dense copy of fe0's output (fe1.0's input; cat[6] keeps the concat copy)
   std::vector<LayerRun> plan;
+  // The forward at B = max_batch as a CUDA graph (one cudaGraphLaunch instead
+  // of ~55 launches; the round-1 tools/graph_test.py measured -40 us), one per
+  // (output mode, gathered targets); the three kernels that take caller
+  // pointers -- input prep and the fused output conv -- are re-pointed per
+  // call (cudaGraphExecKernelNodeSetParams).
+  struct FwdGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t n_face = nullptr, n_mel = nullptr, n_out = nullptr;
+    int kernels = 0;
+  };
+  std::map<std::tuple<int, int, int>, FwdGraph> fwd_graphs;
+  cudaStream_t cap = nullptr;  // capture stream (the caller's may be the legacy stream, which cannot capture)
   // LSG_PREC_FP8_TAIL: this fp8 engine runs plan layers [tail0, end); the
   // 16-bit engine `head` runs [0, tail0) and its tensors that the tail reads
   // (cat[5] whole, cat[6]'s encoder slice) are requantised into this
@@ -1854,6 +1874,96 @@ static void requant_cat(lsg_gen h, int k, int c0, int C, int B, cudaStream_t st)
   LSG_LAUNCHED(h->ctx);
 }
 
+// the node the last operation captured on st created
+static cudaGraphNode_t last_captured(cudaStream_t st) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  LSG_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+  if (cs != cudaStreamCaptureStatusActive || nd != 1) fail(LSG_ERUNTIME, "generator graph: unexpected capture state");
+  return deps[0];
+}
+
+// re-point a captured kernel node at new arguments (same kernel, grid, smem)
+static void set_node_args(cudaGraphExec_t exec, cudaGraphNode_t node, void** args) {
+  cudaKernelNodeParams kp{};
+  LSG_CUDA(cudaGraphKernelNodeGetParams(node, &kp));
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  LSG_CUDA(cudaGraphExecKernelNodeSetParams(exec, node, &kp));
+}
+
+static void forward_graph(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target,
+                          const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, void* out,
+                          int mode, int B, cudaStream_t launch_st) {
+  Ctx* ctx = h->ctx;
+  if (!h->cap) LSG_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+  cudaStream_t st = h->cap;  // recording only: nothing runs on it
+  const int n = (int)h->plan.size();
+  LayerRun& last = h->plan[n - 1];
+  float inv_face = h->prec == PR_FP8 ? h->inv_face : 1.f, inv_mel = h->prec == PR_FP8 ? h->inv_mel : 1.f;
+  auto& g = h->fwd_graphs[std::make_tuple(B, mode, target_idx ? 1 : 0)];
+  if (!g.exec) {
+    const int64_t l0 = ctx->launches.load();
+    LSG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    struct EndOnError {  // a failure inside the capture must not leave st capturing
+      cudaStream_t st;
+      bool armed = true;
+      ~EndOnError() {
+        if (!armed) return;
+        cudaGraph_t gr = nullptr;
+        cudaStreamEndCapture(st, &gr);
+        if (gr) cudaGraphDestroy(gr);
+        cudaGetLastError();
+      }
+    } guard_capture{st};
+    const unsigned gf = (unsigned)ceil_div((int64_t)B * 96 * 96, 256), gm = (unsigned)ceil_div((int64_t)B * 80 * 16, 256);
+    if (h->prec == PR_FP8) prep_faces<PR_FP8><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, inv_face);
+    else if (h->prec == PR_FP16) prep_faces<PR_FP16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
+    else prep_faces<PR_BF16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
+    g.n_face = last_captured(st);
+    if (h->prec == PR_FP8) prep_mel<PR_FP8><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, inv_mel);
+    else if (h->prec == PR_FP16) prep_mel<PR_FP16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
+    else prep_mel<PR_BF16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
+    g.n_mel = last_captured(st);
+    LSG_LAUNCHED(ctx);
+    LSG_LAUNCHED(ctx);
+    run_plan(h, 0, n, mode, out, B, st);
+    g.n_out = last_captured(st);  // the fused output conv: the plan's last launch
+    guard_capture.armed = false;
+    LSG_CUDA(cudaStreamEndCapture(st, &g.graph));
+    LSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+    g.kernels = (int)(ctx->launches.load() - l0);
+  } else {
+    void* fa[] = {(void*)&target, (void*)&target_idx, (void*)&refs, (void*)&ref_index, (void*)&h->x_face.p,
+                  (void*)&B, (void*)&inv_face};
+    set_node_args(g.exec, g.n_face, fa);
+    void* ma[] = {(void*)&mel_rows, (void*)&chunk_row, (void*)&h->x_mel.p, (void*)&B, (void*)&inv_mel};
+    set_node_args(g.exec, g.n_mel, ma);
+    // the output conv's parameter block as captured (launch_* derive grid
+    // fields from B there), with only the caller's pointer replaced
+    cudaKernelNodeParams kp{};
+    LSG_CUDA(cudaGraphKernelNodeGetParams(g.n_out, &kp));
+    if (last.halo) {
+      HaloParams hp;
+      std::memcpy(&hp, kp.kernelParams[0], sizeof(hp));
+      hp.out_mode = mode;
+      hp.final_out = out;
+      void* oa[] = {(void*)&hp};
+      set_node_args(g.exec, g.n_out, oa);
+    } else {
+      ConvParams cp;
+      std::memcpy(&cp, kp.kernelParams[0], sizeof(cp));
+      cp.out_mode = mode;
+      cp.final_out = out;
+      void* oa[] = {(void*)&cp};
+      set_node_args(g.exec, g.n_out, oa);
+    }
+    ctx->launches.fetch_add(g.kernels, std::memory_order_relaxed);
+  }
+  LSG_CUDA(cudaGraphLaunch(g.exec, launch_st));
+}
+
 void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, const uint8_t* target_base,
                     const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, void* out,
                     int32_t out_format, int32_t B) {
@@ -1876,6 +1986,10 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
     requant_cat(h, 5, 0, 160, B, st);
     requant_cat(h, 6, 64, 16, B, st);
     run_plan(h, h->tail0, n, mode, out, B, st);
+    return;
+  }
+  if (B == h->max_batch && !(gen_knobs() & (1 << 17))) {
+    forward_graph(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, out, mode, B, st);
     return;
   }
   prep_inputs(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
