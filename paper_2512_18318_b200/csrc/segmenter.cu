@@ -872,6 +872,8 @@ struct lsg_seg_s {
     int kernels = 0;
   };
   std::map<std::pair<int, int>, Graph> graphs;
+  cudaStream_t cap = nullptr;  // capture stream
+  int prio_hi = 0;             // greatest stream / launch priority of the device
   bool slicing = true;  // lsgdbg_seg_slicing
   void tables_free() {
     if (tab_pending) {
@@ -919,6 +921,7 @@ struct lsg_seg_s {
     if (tab_ev) cudaEventDestroy(tab_ev);
     for (auto& g : graphs)
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    if (cap) cudaStreamDestroy(cap);
     if (sB) cudaStreamDestroy(sB);
     if (sC) cudaStreamDestroy(sC);
     if (k1a) cudaEventDestroy(k1a);
@@ -994,6 +997,23 @@ static void collect(lsg_seg h, bool finishing) {
 // A slot is reused only after the machine of the slice that last used it
 // (the slot's last reader) has completed.  Bit-identical to one launch: the
 // peak and machine state carry through DevState exactly as across pushes.
+// cudaLaunchKernelEx with a priority attribute (kept by stream capture)
+template <typename... KArgs, typename... Args>
+static void launch_hi(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int prio,
+                      Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = prio;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  LSG_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
 static void launch_sliced(lsg_seg h, int nc, int64_t max_frames) {
   Ctx* ctx = h->ctx;
   const Params& P = h->P;
@@ -1027,9 +1047,23 @@ static void launch_sliced(lsg_seg h, int nc, int64_t max_frames) {
   }
   auto& g = h->graphs[std::make_pair(nc, K)];
   if (!g.exec) {
-    // capture: sB / sC fork from the context stream and join back into it
-    LSG_CUDA(cudaStreamBeginCapture(sA, cudaStreamCaptureModeThreadLocal));
-    LSG_CUDA(cudaEventRecord(h->eJoin, sA));
+    // capture on a private stream (the context stream may be the legacy
+    // stream, which cannot capture): sB / sC fork from it and join back
+    if (!h->cap) LSG_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    cudaStream_t cs = h->cap;
+    LSG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    struct EndOnError {  // a failure inside the capture must not leave the stream capturing
+      cudaStream_t st;
+      bool armed = true;
+      ~EndOnError() {
+        if (!armed) return;
+        cudaGraph_t gr = nullptr;
+        cudaStreamEndCapture(st, &gr);
+        if (gr) cudaGraphDestroy(gr);
+        cudaGetLastError();
+      }
+    } guard_capture{cs};
+    LSG_CUDA(cudaEventRecord(h->eJoin, cs));
     LSG_CUDA(cudaStreamWaitEvent(h->sB, h->eJoin, 0));
     LSG_CUDA(cudaStreamWaitEvent(h->sC, h->eJoin, 0));
     const unsigned g2 = (unsigned)ceil_div(nc, K2_LANES);
@@ -1038,28 +1072,34 @@ static void launch_sliced(lsg_seg h, int nc, int64_t max_frames) {
     for (int k = 0; k < K; ++k) {
       const int j = k % kSlots;
       const Chunk* tab = h->chunks_sl.p + (size_t)k * nc;
-      if (k >= kSlots) LSG_CUDA(cudaStreamWaitEvent(sA, h->eM[j], 0));  // slot free
+      if (k >= kSlots) LSG_CUDA(cudaStreamWaitEvent(cs, h->eM[j], 0));  // slot free
       dim3 grid((unsigned)ceil_div(kSlice, K1_WARPS * K1_FPW), (unsigned)nc);
-      seg_frame_stats<<<grid, K1_WARPS * 32, 0, sA>>>(tab, h->carry.p, P.fs, h->stats.p);
-      LSG_CUDA(cudaEventRecord(h->eK1[j], sA));
+      seg_frame_stats<<<grid, K1_WARPS * 32, 0, cs>>>(tab, h->carry.p, P.fs, h->stats.p);
+      LSG_CUDA(cudaEventRecord(h->eK1[j], cs));
       LSG_CUDA(cudaStreamWaitEvent(h->sB, h->eK1[j], 0));
-      seg_peaks<<<g2, K2_LANES, PK_SMEM, h->sB>>>(tab, nc, h->stats.p, h->st.p, h->peaks.p, P, j * kSlice);
+      // the K2 kernels carry the highest priority as a launch attribute, so it
+      // survives into the graph's nodes (stream priorities do not)
+      launch_hi(seg_peaks, dim3(g2), dim3(K2_LANES), PK_SMEM, h->sB, h->prio_hi, tab, nc,
+                (const FrameStat*)h->stats.p, h->st.p, h->peaks.p, P, j * kSlice);
       LSG_CUDA(cudaEventRecord(h->ePk[j], h->sB));
       LSG_CUDA(cudaStreamWaitEvent(h->sC, h->ePk[j], 0));
-      seg_decide<<<dim3((unsigned)(kSlice / 256), (unsigned)nc), 256, 0, h->sC>>>(
-          tab, h->stats.p, h->peaks.p, h->st.p, h->flags.p, P, j * kSlice, j * kSlice / 32);
-      seg_machine<<<(unsigned)ceil_div(nc, MC_WARPS), MC_WARPS * 32, (size_t)MC_WARPS * row_words * 4, h->sC>>>(
-          tab, nc, h->st.p, h->cuts.p, h->flags.p, P, row_words, j * kSlice / 32);
+      launch_hi(seg_decide, dim3((unsigned)(kSlice / 256), (unsigned)nc), dim3(256), 0, h->sC, h->prio_hi, tab,
+                (const FrameStat*)h->stats.p, (const double*)h->peaks.p, h->st.p, h->flags.p, P, j * kSlice,
+                j * kSlice / 32);
+      launch_hi(seg_machine, dim3((unsigned)ceil_div(nc, MC_WARPS)), dim3(MC_WARPS * 32),
+                (size_t)MC_WARPS * row_words * 4, h->sC, h->prio_hi, tab, nc, h->st.p, h->cuts.p,
+                (const uint32_t*)h->flags.p, P, row_words, j * kSlice / 32);
       LSG_CUDA(cudaEventRecord(h->eM[j], h->sC));
       kernels += 4;
     }
     // join: the context stream continues after the last machine
-    LSG_CUDA(cudaStreamWaitEvent(sA, h->eM[(K - 1) % kSlots], 0));
-    LSG_CUDA(cudaStreamWaitEvent(sA, h->ePk[(K - 1) % kSlots], 0));
-    seg_carry<<<nc, 256, 0, sA>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
+    LSG_CUDA(cudaStreamWaitEvent(cs, h->eM[(K - 1) % kSlots], 0));
+    LSG_CUDA(cudaStreamWaitEvent(cs, h->ePk[(K - 1) % kSlots], 0));
+    seg_carry<<<nc, 256, 0, cs>>>(h->chunks_dev.p, h->carry.p, h->st.p, P.fs);
     kernels += 1;
     cudaGraph_t graph = nullptr;
-    LSG_CUDA(cudaStreamEndCapture(sA, &graph));
+    guard_capture.armed = false;
+    LSG_CUDA(cudaStreamEndCapture(cs, &graph));
     const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     LSG_CUDA(e);
@@ -1166,6 +1206,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
         // (short) K1 CTA retires instead of after the whole K1 grid
         int lo = 0, hi = 0;
         LSG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        h->prio_hi = hi;
         LSG_CUDA(cudaStreamCreateWithPriority(&h->sB, cudaStreamNonBlocking, hi));
         LSG_CUDA(cudaStreamCreateWithPriority(&h->sC, cudaStreamNonBlocking, hi));
         for (int j = 0; j < kSlots; ++j) {
