@@ -590,9 +590,20 @@ def scaled_leg(args, local, torch, ctx, stream, api):
             cuts = seg.take_all_cuts()
             if rep:
                 seg_ms.append(e0.elapsed_time(e1))
+        # K1 alone (HBM roofline): the same push without time slicing, whose K1
+        # is one launch between the debug events (sliced, K1 overlaps K2)
+        ctx.lib.check(ctx.lib.dll.lsgdbg_seg_slicing(seg.h, 0))
+        for rep in range(3):
+            lib.call("lsg_seg_reset", seg.h)
+            flush.zero_()
+            seg.push_finish_prepared(seg_args)
+            stream.synchronize()
+            seg.take_all_cuts()
+            if rep:
                 k1 = Cc.c_float()
                 ctx.lib.check(ctx.lib.dll.lsgdbg_seg_k1_ms(seg.h, Cc.byref(k1)))
                 k1_ms.append(k1.value)
+        ctx.lib.check(ctx.lib.dll.lsgdbg_seg_slicing(seg.h, 1))
         N, hop = 1024, 256
         offs = [c.stream * n + c.sample_off for c in cuts]
         lens = [c.sample_len for c in cuts]
@@ -698,7 +709,8 @@ def scaled_leg(args, local, torch, ctx, stream, api):
                                               "achieved": (nbytes + nbytes // 640 * 16) / (float(np.median(k1_ms)) / 1e3) / 1e9,
                                               "frac": (nbytes + nbytes // 640 * 16) / (float(np.median(k1_ms)) / 1e3) / 1e9
                                               / peaks.get("hbm_gbs", 6650.0),
-                                              "timed": "CUDA events around the K1 launch inside lsg_seg_push"}
+                                              "timed": "CUDA events around the K1 launch inside lsg_seg_push "
+                                                       "(the same push with time slicing off: K1 is one launch)"}
                                              if k1_ms else None)},
         "align": {"energy_envelope": {"bound": "hbm", "ms": float(np.median(en_ms)),
                                       "bytes": nbytes + S * secs * 1000 * 8,

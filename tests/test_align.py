@@ -125,3 +125,20 @@ def test_gpu_align_batch_bit_exact(restated, reference):
     from paper_2512_18318_b200._lib import InvalidArgument
     with pytest.raises(InvalidArgument):
         api.align_envelopes(energy, energy, -1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rate", [44100, 48000, 8000])
+def test_gpu_energy_other_rates_bit_exact(reference, rate):
+    """Hops of 441 (hop % 8 != 0), 480 and 80 samples: the energy kernel's
+    staging for non-16 kHz rates, bit-identical to the reference build; a
+    rate whose staging would exceed shared memory is rejected with EINVAL."""
+    from paper_2512_18318_b200 import api
+    rng = np.random.default_rng(rate)
+    pcms = [(rng.normal(0, 3000, n)).astype(np.int16) for n in (rate * 3 + 123, rate // 2, 1000)]
+    got = api.energy_envelopes([api.AudioBuffer(samples=p, sample_rate=rate) for p in pcms])
+    for g, p in zip(got, pcms):
+        np.testing.assert_array_equal(g, reference.energy_envelope(p, rate))
+    from paper_2512_18318_b200._lib import InvalidArgument
+    with pytest.raises(InvalidArgument, match="rate too high"):
+        api.energy_envelopes([api.AudioBuffer(samples=pcms[0], sample_rate=192000)])
