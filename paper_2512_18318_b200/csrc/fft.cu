@@ -82,20 +82,27 @@ extern "C" lsg_status lsg_fft_radix2(lsg_ctx ctx, double* data, int64_t n, int32
     if (count == 0 || n == 1) return;  // a 1-point transform is the identity
     DeviceGuard g(ctx);
     const std::vector<double2> tw = fft::twiddles(log2n);
-    const size_t bytes = size_t(n) * count * sizeof(double2);
     const bool dev = is_device_ptr(data);
+    // host data goes through the context scratch in batches of <= 32 MiB
+    const int64_t per = dev ? count : std::max<int64_t>(1, (int64_t(32) << 20) / (n * (int64_t)sizeof(double2)));
+    const size_t bytes = size_t(n) * std::min<int64_t>(per, count) * sizeof(double2);
     ScratchLease sc(ctx, tw.size() * sizeof(double2) + (dev ? 0 : bytes));
     double2* dtw = static_cast<double2*>(sc.p);
-    double2* buf = dev ? reinterpret_cast<double2*>(data) : dtw + tw.size();
     LSG_CUDA(cudaMemcpyAsync(dtw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
-    if (!dev) LSG_CUDA(cudaMemcpyAsync(buf, data, bytes, cudaMemcpyHostToDevice, ctx->stream));
     const size_t smem = size_t(n) * sizeof(double2) * 3 / 2;
     if (smem > 48 * 1024)
       LSG_CUDA(cudaFuncSetAttribute(fft::radix2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fft::radix2_kernel<<<(unsigned)count, (unsigned)std::min<int64_t>(512, std::max<int64_t>(32, n / 2)), smem,
-                         ctx->stream>>>(buf, dtw, log2n);
-    LSG_LAUNCHED(ctx);
-    if (!dev) LSG_CUDA(cudaMemcpyAsync(data, buf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    for (int64_t c0 = 0; c0 < count; c0 += per) {
+      const int64_t cn = std::min<int64_t>(per, count - c0);
+      double2* host = reinterpret_cast<double2*>(data) + c0 * n;
+      double2* buf = dev ? host : dtw + tw.size();
+      if (!dev) LSG_CUDA(cudaMemcpyAsync(buf, host, size_t(n) * cn * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+      fft::radix2_kernel<<<(unsigned)cn, (unsigned)std::min<int64_t>(512, std::max<int64_t>(32, n / 2)), smem,
+                           ctx->stream>>>(buf, dtw, log2n);
+      LSG_LAUNCHED(ctx);
+      if (!dev)
+        LSG_CUDA(cudaMemcpyAsync(host, buf, size_t(n) * cn * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    }
     ctx->sync();  // the twiddle table lives in the context scratch
   });
 }

@@ -229,10 +229,13 @@ lsg_status lsg_paced_run(lsg_paced h, const int16_t* pcm, const int64_t* n_sampl
     std::vector<Seg> segs;
     std::vector<int> pending;  // segment ids waiting for their frame window
     std::vector<int> per_stream(S, 0);
-    // completion stamps, written by the host callbacks: sized up front (a
-    // segment holds at least one frame of speech and a pause of min_silence,
-    // or ends the stream), never reallocated while callbacks may run
-    const int64_t max_segs = (int64_t)S * (total_ms / std::max<int64_t>(h->seg_cfg.min_silence_ms, 1) + 2);
+    // completion stamps, written by the host callbacks: sized up front, never
+    // reallocated while callbacks may run
+    // (pause cuts need min_silence of silence, forced cuts max_segment of
+    // speech, plus the EOS flush)
+    const int64_t max_segs =
+        (int64_t)S * (total_ms / std::max<int64_t>(h->seg_cfg.min_silence_ms, 1) +
+                      total_ms / std::max<int64_t>(h->seg_cfg.max_segment_ms, 1) + 3);
     h->rendered.assign((size_t)max_segs, -1.0);
     struct Job {
       int32_t seg, row;

@@ -18,12 +18,27 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 REL = 1e-4
 
 
+def ulps(got, want):
+    """|got - want| in float32 ulps (ordered-integer distance)."""
+    def key(x):
+        i = np.ascontiguousarray(x, np.float32).view(np.int32).astype(np.int64)
+        return np.where(i < 0, -(i & 0x7FFFFFFF), i)
+    return np.abs(key(got) - key(want))
+
+
 def close(got, want):
     assert got.shape == want.shape
     err = np.abs(got.astype(np.float64) - want.astype(np.float64))
     bound = REL * np.maximum(np.abs(want.astype(np.float64)), 1.0)
     bad = err > bound
     assert not bad.any(), f"{bad.sum()} cells over 1e-4 rel; max err {err.max():.3g}"
+    # the strict figures too (the floor of 1 only matters where ln(acc) ~ 0)
+    nz = np.abs(want) > 0
+    strict = float((err[nz] / np.abs(want.astype(np.float64))[nz]).max()) if nz.any() else 0.0
+    u = ulps(got, want)
+    print(f"mel parity: max strict rel {strict:.3g}, max {int(u.max())} ulp, "
+          f"{100 * np.mean(u == 0):.1f}% bit-identical, {100 * np.mean(u <= 1):.2f}% within 1 ulp")
+    assert strict < 1e-4, strict  # no cell needs the floor of 1 on these inputs
     return float(np.mean(got == want))
 
 
