@@ -177,6 +177,11 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
 #define LSG_PREC_FP8_TAIL 3     /* fp16 up to fd5.2, e4m3 (as LSG_PREC_FP8) for fd6.0-out0 (28% of the
                                    FLOPs): the fp8 split that keeps >= 30 dB vs the fp32 oracle on the
                                    synthetic network; needs act_absmax like LSG_PREC_FP8 */
+#define LSG_PREC_INT8_TAIL 4    /* fp16 encoders and fd0-fd2.2, then tcgen05 kind::i8 for fd3.0-out0 (84%
+                                   of the FLOPs): u8 activations (every decoder input is post-ReLU, per
+                                   tensor scale absmax/255), s8 weights (per output channel scale
+                                   max|w|/127), s32 accumulate; >= 30 dB vs the fp32 oracle (DESIGN.md
+                                   §4); needs act_absmax like LSG_PREC_FP8 */
 #define LSG_OUT_F32_NCHW 0      /* [B][3][96][96] f32 in [0,1] */
 #define LSG_OUT_U8_NHWC 1       /* [B][96][96][3] u8, round(255*x) */
 #define LSG_OUT_F32_LOGITS 2    /* [B][3][96][96] f32 pre-sigmoid (parity checks) */
@@ -190,8 +195,9 @@ lsg_status lsg_gen_param_count(int64_t* n);
 lsg_status lsg_gen_layer_info(int32_t* info, int32_t cap_layers, int32_t* n_layers);
 lsg_status lsg_gen_create(lsg_ctx ctx, const float* weights /*[host]*/, int64_t n_floats,
                           int32_t precision, int32_t max_batch, lsg_gen* out);
-/* As lsg_gen_create; LSG_PREC_FP8 requires act_absmax [host], the n_act
- * activation ranges lsg_gen_calibrate returns (ignored otherwise). */
+/* As lsg_gen_create; LSG_PREC_FP8 / _FP8_TAIL / _INT8_TAIL require act_absmax
+ * [host], the n_act activation ranges lsg_gen_calibrate returns (ignored
+ * otherwise). */
 lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights /*[host]*/, int64_t n_floats, int32_t precision,
                             const float* act_absmax, int32_t n_act, int32_t max_batch, lsg_gen* out);
 /* On a bf16/fp16 engine: run a calibration batch (inputs as lsg_gen_forward)

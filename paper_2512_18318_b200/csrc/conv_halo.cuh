@@ -143,9 +143,9 @@ struct alignas(64) HaloParams {
   const uint16_t* res;
   int res_pitch, res_coff;
   const float* bias;
-  const float* oscale;  // fp8: per output channel s_in * s_w[co], else null
-  float res_scale;      // fp8: residual tensor scale, else 1
-  float out_inv;        // fp8: 1 / output tensor scale, else 1
+  const float* oscale;  // 8-bit: per output channel s_in * s_w[co], else null
+  float res_scale;      // 8-bit: residual tensor scale, else 1
+  float out_inv;        // 8-bit: 1 / output tensor scale, else 1
   int relu, out_mode;
   const float* w1;
   const float* b1;
@@ -289,7 +289,7 @@ template <int BN, int MODE, bool FUSED_OUT, int PR, bool B_RES, bool PAIR = fals
 __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constant__ HaloParams p) {
   static_assert(MODE != HALO_CONV3S2 || (B_RES && !PAIR && !FUSED_OUT), "stride-2 halo: resident weights only");
   using NF = Num<PR>;
-  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::F8 ? 1 : 2, PAIR>;
+  using CF = HaloCfg<BN, MODE, FUSED_OUT, B_RES, NF::Q8 ? 1 : 2, PAIR>;
   using TT = HaloTaps<MODE>;
   constexpr int NPH = TT::NPH;
   constexpr int HS = CF::HS, BS = CF::BS, NACC = CF::NACC;
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     // is a handful of uniform adds per 4 MMAs (profiles/r01: with divisions,
     // parameter reloads and per-tap warp reconvergence it cost more than the
     // MMAs themselves).
-    constexpr uint32_t idesc = tc::idesc_f16kind(PAIR ? 2 * BM : BM, CF::MN, NF::kFmt);
+    constexpr uint32_t idesc = NF::idesc(PAIR ? 2 * BM : BM, CF::MN);
     constexpr int NT = TT::NT;
     constexpr uint64_t PLANE2 = (uint64_t)((2 * ((TT::PW * TT::PH * 16 + 127) / 128 * 128)) >> 4);
     constexpr uint64_t BBLK16 = CF::BBLK >> 4;
@@ -536,8 +536,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
                 }
               } else if (ks < ksteps) {
                 if constexpr (PAIR) {
-                  if constexpr (NF::F8) tc::mma2_f8(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
-                  else tc::mma2_f16(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
+                  NF::mma2(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
                 } else {
                   NF::mma_nc(dd, at + ks * PLANE2, db + 2 * ks, idesc, ks ? 1u : acc0);
                 }
@@ -617,7 +616,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             uint32_t v[16];
             tc::tmem_ld16(tbase + c0, v);
             // 16 channels = W16 16-byte chunks of the position's box row
-            constexpr int W16 = NF::U4, ES = NF::F8 ? 1 : 2;
+            constexpr int W16 = NF::U4, ES = NF::Q8 ? 1 : 2;
             const int byte0 = (cbeg + c0) * ES;
             const int cc = byte0 >> 7, j0 = (byte0 & 127) >> 4;
             uint4 rv[W16];
@@ -628,7 +627,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             }
             tc::tmem_ld_wait();
             uint4 o[W16];
-            epi16<PR>(v, p.bias + nt * BN + cbeg + c0, p.oscale + (NF::F8 ? nt * BN + cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
+            epi16<PR>(v, p.bias + nt * BN + cbeg + c0, p.oscale + (NF::Q8 ? nt * BN + cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
                       p.res_scale, p.relu != 0, p.out_inv, o);
 #pragma unroll
             for (int w = 0; w < W16; ++w)
@@ -691,7 +690,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             tc::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
+              const float acc = NF::Q8 ? NF::acc(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
               const float xx = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
 #pragma unroll
               for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), xx, o[o3]);

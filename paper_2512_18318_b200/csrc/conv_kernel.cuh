@@ -86,9 +86,9 @@ struct alignas(64) ConvParams {
   const uint16_t* res;
   int res_pitch, res_coff;
   const float* bias;
-  const float* oscale;  // fp8: per output channel s_in * s_w[co] (dequantizes the accumulator), else null
-  float res_scale;      // fp8: scale of the residual tensor, else 1
-  float out_inv;        // fp8: 1 / scale of the output tensor, else 1
+  const float* oscale;  // 8-bit: per output channel s_in * s_w[co] (dequantizes the accumulator), else null
+  float res_scale;      // 8-bit: scale of the residual tensor, else 1
+  float out_inv;        // 8-bit: 1 / scale of the output tensor, else 1
   int sy, sx, osy, osx;
   int relu, out_mode;
   const float* w1;  // fused output 1x1: [3][32]
@@ -115,19 +115,30 @@ struct alignas(64) ConvParams {
 };
 
 // Element formats.  Activations and weights are always moved as 16-bit
-// "units": a bf16/fp16 value, or a PAIR of fp8 e4m3 values.  One MMA step
-// is 32 bytes of a row either way (kind::f16 K=16, kind::f8f6f4 K=32), so
-// tensor maps, shared-memory layouts, descriptors and K loops are identical
-// across formats; only the MMA kind, the weight packing and the epilogue's
-// (de)quantisation differ.
-enum Prec { PR_BF16 = 0, PR_FP16 = 1, PR_FP8 = 2 };
+// "units": a bf16/fp16 value, or a PAIR of 8-bit values (fp8 e4m3, or u8
+// activations / s8 weights).  One MMA step is 32 bytes of a row in every
+// format (kind::f16 K=16, kind::f8f6f4 and kind::i8 K=32), so tensor maps,
+// shared-memory layouts, descriptors and K loops are identical across
+// formats; only the MMA kind, the weight packing and the epilogue's
+// (de)quantisation differ.  The 8-bit formats (Q8) carry per-output-channel
+// weight scales and per-tensor activation scales; INT8 accumulates in s32.
+enum Prec { PR_BF16 = 0, PR_FP16 = 1, PR_FP8 = 2, PR_I8 = 3 };
 
 template <int PR>
 struct Num {
-  static constexpr bool F8 = PR == PR_FP8;
+  static constexpr bool Q8 = PR == PR_FP8 || PR == PR_I8;  // 8-bit storage, scaled
+  static constexpr bool I8 = PR == PR_I8;
   static constexpr uint32_t kFmt = PR == PR_BF16 ? 1u : 0u;  // bf16 = 1; fp16 = 0; e4m3 = 0
-  static constexpr int CPU = F8 ? 2 : 1;                     // channels per 16-bit unit
-  static constexpr int U4 = F8 ? 1 : 2;                      // uint4 words per 16 channels
+  static constexpr int CPU = Q8 ? 2 : 1;                     // channels per 16-bit unit
+  static constexpr int U4 = Q8 ? 1 : 2;                      // uint4 words per 16 channels
+  __host__ __device__ static constexpr uint32_t idesc(int M, int N) {
+    return I8 ? tc::idesc_i8(M, N) : tc::idesc_f16kind(M, N, kFmt);
+  }
+  // one TMEM accumulator word as a float (s32 for INT8, f32 otherwise)
+  __device__ __forceinline__ static float acc(uint32_t u) {
+    if constexpr (I8) return (float)(int32_t)u;
+    else return __uint_as_float(u);
+  }
   __device__ __forceinline__ static uint32_t pack(float a, float b) {  // 16-bit formats
     if constexpr (PR == PR_FP16) {
       __half2 v = __floats2half2_rn(a, b);
@@ -146,7 +157,13 @@ struct Num {
   }
   // 16 channels <-> their U4 uint4 words
   __device__ __forceinline__ static void to_float16(const uint4* w, float (&x)[16]) {
-    if constexpr (F8) {
+    if constexpr (I8) {
+      const uint32_t r[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[4 * k + b] = (float)((r[k] >> (8 * b)) & 0xffu);
+    } else if constexpr (Q8) {
       const uint32_t r[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -169,7 +186,17 @@ struct Num {
     }
   }
   __device__ __forceinline__ static void from_float16(const float (&f)[16], uint4* w) {
-    if constexpr (F8) {
+    if constexpr (I8) {  // u8: round to nearest, saturate to [0, 255]
+      uint32_t r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t q[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) q[b] = __float2uint_rn(fminf(fmaxf(f[4 * k + b], 0.f), 255.f));
+        r[k] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+      }
+      w[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    } else if constexpr (Q8) {
       uint32_t r[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -185,18 +212,27 @@ struct Num {
     }
   }
   __device__ __forceinline__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if constexpr (F8) tc::mma_f8(d, a, b, idesc, acc);
+    if constexpr (I8) tc::mma_i8(d, a, b, idesc, acc);
+    else if constexpr (Q8) tc::mma_f8(d, a, b, idesc, acc);
     else tc::mma_f16(d, a, b, idesc, acc);
   }
   __device__ __forceinline__ static void mma_nc(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if constexpr (F8) tc::mma_f8_nc(d, a, b, idesc, acc);
+    if constexpr (I8) tc::mma_i8_nc(d, a, b, idesc, acc);
+    else if constexpr (Q8) tc::mma_f8_nc(d, a, b, idesc, acc);
     else tc::mma_f16_nc(d, a, b, idesc, acc);
+  }
+  // cta_group::2 (the CTA-pair kernels)
+  __device__ __forceinline__ static void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (I8) tc::mma2_i8(d, a, b, idesc, acc);
+    else if constexpr (Q8) tc::mma2_f8(d, a, b, idesc, acc);
+    else tc::mma2_f16(d, a, b, idesc, acc);
   }
 };
 
 // The per-channel math of every epilogue, 16 channels at a time:
-// y = acc * oscale + bias (+ residual * res_scale), ReLU, * out_inv (fp8).
-template <int PR>
+// y = acc * oscale + bias (+ residual * res_scale), ReLU, * out_inv (8-bit).
+// FACC: v holds f32 bits whatever the format (split-K's reduced partials).
+template <int PR, bool FACC = false>
 __device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias, const float* oscale,
                                       const uint4* res, float res_scale, bool relu, float out_inv, uint4* out) {
   using NF = Num<PR>;
@@ -210,15 +246,15 @@ __device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias
     f[4 * j + 2] = b4.z;
     f[4 * j + 3] = b4.w;
   }
-  if constexpr (NF::F8) {
+  if constexpr (NF::Q8) {
     const float4* sp = reinterpret_cast<const float4*>(oscale);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float4 s4 = __ldg(sp + j);
-      f[4 * j + 0] = fmaf(__uint_as_float(v[4 * j + 0]), s4.x, f[4 * j + 0]);
-      f[4 * j + 1] = fmaf(__uint_as_float(v[4 * j + 1]), s4.y, f[4 * j + 1]);
-      f[4 * j + 2] = fmaf(__uint_as_float(v[4 * j + 2]), s4.z, f[4 * j + 2]);
-      f[4 * j + 3] = fmaf(__uint_as_float(v[4 * j + 3]), s4.w, f[4 * j + 3]);
+      f[4 * j + 0] = fmaf(FACC ? __uint_as_float(v[4 * j + 0]) : NF::acc(v[4 * j + 0]), s4.x, f[4 * j + 0]);
+      f[4 * j + 1] = fmaf(FACC ? __uint_as_float(v[4 * j + 1]) : NF::acc(v[4 * j + 1]), s4.y, f[4 * j + 1]);
+      f[4 * j + 2] = fmaf(FACC ? __uint_as_float(v[4 * j + 2]) : NF::acc(v[4 * j + 2]), s4.z, f[4 * j + 2]);
+      f[4 * j + 3] = fmaf(FACC ? __uint_as_float(v[4 * j + 3]) : NF::acc(v[4 * j + 3]), s4.w, f[4 * j + 3]);
     }
   } else {
 #pragma unroll
@@ -228,13 +264,13 @@ __device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias
     float x[16];
     NF::to_float16(res, x);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) f[j] = NF::F8 ? fmaf(x[j], res_scale, f[j]) : f[j] + x[j];
+    for (int j = 0; j < 16; ++j) f[j] = NF::Q8 ? fmaf(x[j], res_scale, f[j]) : f[j] + x[j];
   }
   if (relu) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
   }
-  if constexpr (NF::F8) {
+  if constexpr (NF::Q8) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] *= out_inv;
   }
@@ -332,7 +368,7 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
 #pragma unroll
   for (int c = 0; c < HC; c += 32) {
     tc::prefetch_l1(bias + c);
-    if constexpr (NF::F8) tc::prefetch_l1(oscale + c);
+    if constexpr (NF::Q8) tc::prefetch_l1(oscale + c);
   }
   if constexpr (HC > 64) {
     if (rrow) {
@@ -362,7 +398,7 @@ __device__ __forceinline__ void epilogue_row(uint32_t tbase, uint16_t* orow, con
     tc::tmem_ld_wait();
     if (valid) {
       uint4 o[W16];
-      epi16<PR>(v, bias + c0, oscale + (NF::F8 ? c0 : 0), rrow ? rcur : nullptr, res_scale, relu, out_inv, o);
+      epi16<PR>(v, bias + c0, oscale + (NF::Q8 ? c0 : 0), rrow ? rcur : nullptr, res_scale, relu, out_inv, o);
 #pragma unroll
       for (int w = 0; w < W16; ++w) reinterpret_cast<uint4*>(orow)[c0 / 16 * W16 + w] = o[w];
     }
@@ -405,9 +441,8 @@ __device__ __forceinline__ void splitk_tile(const ConvParams& p, int u, int t, c
       tc::tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        __stcg(mine + (size_t)(c0 / 4 + j) * BM, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                                              __uint_as_float(v[4 * j + 2]),
-                                                              __uint_as_float(v[4 * j + 3])));
+        __stcg(mine + (size_t)(c0 / 4 + j) * BM,
+               make_float4(NF::acc(v[4 * j]), NF::acc(v[4 * j + 1]), NF::acc(v[4 * j + 2]), NF::acc(v[4 * j + 3])));
     }
     tc::tc_fence_before();
     tc::mbar_arrive(tempty_bar);
@@ -465,7 +500,7 @@ __device__ __forceinline__ void splitk_tile(const ConvParams& p, int u, int t, c
 #pragma unroll
       for (int w = 0; w < W16; ++w) res[w] = __ldg(rp + w);
     }
-    epi16<PR>(v, p.bias + ch, p.oscale + (NF::F8 ? ch : 0), p.res ? res : nullptr, p.res_scale, p.relu != 0,
+    epi16<PR, true>(v, p.bias + ch, p.oscale + (NF::Q8 ? ch : 0), p.res ? res : nullptr, p.res_scale, p.relu != 0,
               p.out_inv, o);
     uint4* op = reinterpret_cast<uint4*>(p.out + pix * p.out_pitch + p.out_coff + ch / NF::CPU);
 #pragma unroll
@@ -596,7 +631,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (whole warp
     // runs the loop, one elected lane issues: descriptors stay uniform)
-    constexpr uint32_t idesc = tc::idesc_f16kind(BM, BN, NF::kFmt);
+    constexpr uint32_t idesc = NF::idesc(BM, BN);
     const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
     int s = 0;
     uint32_t ph = 0, tl = 0;
@@ -684,7 +719,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
             continue;
           }
         }
-        epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::F8 ? n0 + cbeg : 0), p.res_scale,
+        epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::Q8 ? n0 + cbeg : 0), p.res_scale,
                              p.out_inv, p.relu != 0, valid, &tfull[a], use & 1);
       } else {
         // out0 (BN = 32 channels, ReLU) fused with out1 (1x1 32->3) + sigmoid;
@@ -701,7 +736,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc(const __grid_constant_
             tc::tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float acc = NF::F8 ? __uint_as_float(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
+              const float acc = NF::Q8 ? NF::acc(v[j]) * __ldg(p.oscale + c0 + j) : __uint_as_float(v[j]);
               const float x = fmaxf(acc + __ldg(p.bias + c0 + j), 0.f);
 #pragma unroll
               for (int o3 = 0; o3 < 3; ++o3) o[o3] = fmaf(__ldg(p.w1 + o3 * 32 + c0 + j), x, o[o3]);

@@ -38,8 +38,7 @@ struct Cfg2 {
 
 template <int PR>
 __device__ __forceinline__ void mma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  if constexpr (PR == PR_FP8) tc::mma2_f8(d, a, b, idesc, acc);
-  else tc::mma2_f16(d, a, b, idesc, acc);
+  Num<PR>::mma2(d, a, b, idesc, acc);
 }
 
 // Pair TMA loads: data to this CTA's shared memory, completion to the
@@ -177,7 +176,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc2(const __grid_constant
   } else if (warp == 1) {
     if (rank == 0) {
       // ---------------------------------------------- MMA issuer (even CTA)
-      constexpr uint32_t idesc = tc::idesc_f16kind(2 * BM, BN, NF::kFmt);
+      constexpr uint32_t idesc = NF::idesc(2 * BM, BN);
       const uint32_t sA0 = tc::smem_u32(sA), sB0 = tc::smem_u32(sB);
       int s = 0;
       uint32_t ph = 0, tl = 0;
@@ -229,7 +228,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_tc2(const __grid_constant
       const uint16_t* rrow =
           (p.res && valid) ? p.res + pix * p.res_pitch + p.res_coff + (n0 + cbeg) / NF::CPU : nullptr;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * BN + cbeg;
-      epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::F8 ? n0 + cbeg : 0), p.res_scale,
+      epilogue_row<HC, PR>(tbase, orow, rrow, p.bias + n0 + cbeg, p.oscale + (NF::Q8 ? n0 + cbeg : 0), p.res_scale,
                            p.out_inv, p.relu != 0, valid, &tfull[a], use & 1);
       tc::tc_fence_before();
       __syncwarp();

@@ -123,7 +123,7 @@ static_assert(kNumLayers == 51, "Wav2Lip has 51 conv layers");
 template <int PR>
 __device__ __forceinline__ uint4 pack_px(const float (&c)[6], float inv_scale) {
   using NF = Num<PR>;
-  if constexpr (NF::F8) {
+  if constexpr (NF::Q8) {
     float f[16] = {};
 #pragma unroll
     for (int j = 0; j < 6; ++j) f[j] = c[j] * inv_scale;
@@ -186,7 +186,7 @@ __global__ void audio_stem(const uint16_t* __restrict__ x, const float* __restri
   for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) sw[i] = w[i];
   if (threadIdx.x < 32) {
     sb[threadIdx.x] = bias[threadIdx.x];
-    so[threadIdx.x] = NF::F8 ? oscale[threadIdx.x] : 1.f;
+    so[threadIdx.x] = NF::Q8 ? oscale[threadIdx.x] : 1.f;
   }
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, h, w) of the 80 x 16 grid
@@ -199,7 +199,7 @@ __global__ void audio_stem(const uint16_t* __restrict__ x, const float* __restri
     float v = 0.f;
     if (hh >= 0 && hh < 80 && ww >= 0 && ww < 16) {
       const uint32_t u = __ldg(x + (((int64_t)b * 80 + hh) * 16 + ww) * 8);  // unit 0 of the 16-byte pixel
-      if constexpr (NF::F8) {
+      if constexpr (NF::Q8) {
         const __half_raw hr = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)(u & 0xffu), __NV_E4M3);
         v = __half2float(*reinterpret_cast<const __half*>(&hr));
       } else {
@@ -219,7 +219,7 @@ __global__ void audio_stem(const uint16_t* __restrict__ x, const float* __restri
 #pragma unroll
       for (int t = 0; t < 9; ++t) acc = fmaf(xv[t], sw[co * 9 + t], acc);
       float y = fmaxf(acc * so[co] + sb[co], 0.f);
-      if constexpr (NF::F8) y *= out_inv;
+      if constexpr (NF::Q8) y *= out_inv;
       f[j] = y;
     }
     NF::from_float16(f, reinterpret_cast<uint4*>(o) + half * NF::U4);
@@ -431,14 +431,14 @@ struct lsg_gen_s {
   Ctx* ctx = nullptr;
   int max_batch = 0;
   int sm_count = 148;
-  int prec = PR_BF16;  // Prec (conv_kernel.cuh): LSG_PREC_BF16 / FP16 / FP8
-  int cpu = 1;         // channels per 16-bit storage unit (2 for fp8)
+  int prec = PR_BF16;  // Prec (conv_kernel.cuh): LSG_PREC_BF16 / FP16 / FP8, or PR_I8 (an INT8 tail's engine)
+  int cpu = 1;         // channels per 16-bit storage unit (2 for the 8-bit formats)
   float inv_face = 1.f, inv_mel = 1.f;  // fp8 input quantisation (1 / scale)
   DevBuf<uint16_t> wpack;
   DevBuf<float> bias;
-  DevBuf<float> oscale;  // fp8: per layer, per output channel s_in * s_w[co]
+  DevBuf<float> oscale;  // 8-bit: per layer, per output channel s_in * s_w[co]
   std::vector<int> plan_in_id, plan_out_id;  // tensor ids (kTensors) of each layer's input / output
-  std::vector<float> ascale;                 // fp8: scale per tensor id (1 otherwise)
+  std::vector<float> ascale;                 // 8-bit: scale per tensor id (1 otherwise)
   DevBuf<float> w1b1;
   DevBuf<uint16_t> act;  // all activation buffers
   DevBuf<float> splitk_ws;   // split-K partial slots (conv_kernel.cuh ConvParams::ws)
@@ -477,12 +477,13 @@ struct lsg_gen_s {
   };
   std::map<std::tuple<int, int, int>, FwdGraph> fwd_graphs;
   cudaStream_t cap = nullptr;  // capture stream (the caller's may be the legacy stream, which cannot capture)
-  // LSG_PREC_FP8_TAIL: this fp8 engine runs plan layers [tail0, end); the
-  // 16-bit engine `head` runs [0, tail0) and its tensors that the tail reads
-  // (cat[5] whole, cat[6]'s encoder slice) are requantised into this
-  // engine's buffers in between
+  // LSG_PREC_FP8_TAIL / _INT8_TAIL: this 8-bit engine runs plan layers
+  // [tail0, end), which start decoder block tail_blk; the 16-bit engine
+  // `head` runs [0, tail0) and the tensors the tail reads from it (the
+  // block's input cat[tail_blk - 1] whole, the encoder slices of
+  // cat[tail_blk..6]) are requantised into this engine's buffers in between
   lsg_gen_s* head = nullptr;
-  int tail0 = 0;
+  int tail0 = 0, tail_blk = 0;
 };
 
 static int64_t layer_params(const LayerSpec& L) { return (int64_t)L.cin * L.cout * L.kh * L.kw + L.cout; }
@@ -705,12 +706,12 @@ static void set_smem_attrs_t() {
 #undef LSG_SET_ATTR
 #define LSG_SET_HALO_ATTR(BN, MD, F, R)                                                                           \
   LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, PR, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM));
+                                HaloCfg<BN, MD, F, R, Num<PR>::Q8 ? 1 : 2>::SMEM));
   LSG_HALO_VARIANTS(LSG_SET_HALO_ATTR)
 #undef LSG_SET_HALO_ATTR
 #define LSG_SET_HALO_PAIR_ATTR(BN, MD, F, R)                                                                      \
   LSG_CUDA(cudaFuncSetAttribute(conv_halo<BN, MD, F, PR, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2, true>::SMEM));
+                                HaloCfg<BN, MD, F, R, Num<PR>::Q8 ? 1 : 2, true>::SMEM));
   LSG_HALO_PAIR_VARIANTS(LSG_SET_HALO_PAIR_ATTR)
 #undef LSG_SET_HALO_PAIR_ATTR
 #define LSG_SET_PAIR_ATTR(BN, CC) \
@@ -719,7 +720,8 @@ static void set_smem_attrs_t() {
 #undef LSG_SET_PAIR_ATTR
 }
 static void set_smem_attrs(int prec) {
-  if (prec == PR_FP8) set_smem_attrs_t<PR_FP8>();
+  if (prec == PR_I8) set_smem_attrs_t<PR_I8>();
+  else if (prec == PR_FP8) set_smem_attrs_t<PR_FP8>();
   else if (prec == PR_FP16) set_smem_attrs_t<PR_FP16>();
   else set_smem_attrs_t<PR_BF16>();
 }
@@ -730,7 +732,7 @@ static void launch_halo(const LayerRun& r, int B, int sms, cudaStream_t st) {
   hp.B = B;
   hp.total_tiles = B * hp.tiles_per_img * hp.ntn;
   const int grid = std::min(hp.total_tiles, sms);
-  launch_pdl(conv_halo<BN, MD, F, PR, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2>::SMEM, st,
+  launch_pdl(conv_halo<BN, MD, F, PR, R>, grid, NUM_THREADS, HaloCfg<BN, MD, F, R, Num<PR>::Q8 ? 1 : 2>::SMEM, st,
              hp);
 }
 
@@ -743,7 +745,7 @@ static void launch_halo_pair(const LayerRun& r, int B, int sms, cudaStream_t st)
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)std::min(hp.total_tiles, sms & ~1));
   cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = (size_t)HaloCfg<BN, MD, F, R, PR == PR_FP8 ? 1 : 2, true>::SMEM;
+  cfg.dynamicSmemBytes = (size_t)HaloCfg<BN, MD, F, R, Num<PR>::Q8 ? 1 : 2, true>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -831,7 +833,8 @@ static void dispatch_t(const LayerRun& r, int B, int sms, cudaStream_t st, float
 static void dispatch(const lsg_gen_s* h, const LayerRun& r, int B, cudaStream_t st, int wset = 0) {
   float* ws = wset ? h->splitk_ws2.p : h->splitk_ws.p;
   const int wt = h->splitk_tiles;
-  if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, wt);
+  if (h->prec == PR_I8) dispatch_t<PR_I8>(r, B, h->sm_count, st, ws, wt);
+  else if (h->prec == PR_FP8) dispatch_t<PR_FP8>(r, B, h->sm_count, st, ws, wt);
   else if (h->prec == PR_FP16) dispatch_t<PR_FP16>(r, B, h->sm_count, st, ws, wt);
   else dispatch_t<PR_BF16>(r, B, h->sm_count, st, ws, wt);
 }
@@ -878,27 +881,32 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
     if (n_floats != want) invalid("lsg_gen_create: weight blob has " + std::to_string(n_floats) + " floats, expected " +
                                   std::to_string(want));
     if (precision != LSG_PREC_BF16 && precision != LSG_PREC_FP16 && precision != LSG_PREC_FP8 &&
-        precision != LSG_PREC_FP8_TAIL)
+        precision != LSG_PREC_FP8_TAIL && precision != LSG_PREC_INT8_TAIL)
       invalid("lsg_gen_create: unsupported precision");
-    if ((precision == LSG_PREC_FP8 || precision == LSG_PREC_FP8_TAIL) && (!act_absmax || n_act != kTensors))
-      invalid("lsg_gen_create: fp8 needs the calibrated activation ranges (lsg_gen_calibrate)");
+    const bool tail = precision == LSG_PREC_FP8_TAIL || precision == LSG_PREC_INT8_TAIL;
+    if ((precision == LSG_PREC_FP8 || tail) && (!act_absmax || n_act != kTensors))
+      invalid("lsg_gen_create: 8-bit precisions need the calibrated activation ranges (lsg_gen_calibrate)");
     if (max_batch <= 0 || max_batch > 4096) invalid("lsg_gen_create: max_batch out of range");
     DeviceGuard g(ctx);
     auto h = new lsg_gen_s();
     try {
       h->ctx = ctx;
       h->max_batch = max_batch;
-      h->prec = (precision == LSG_PREC_FP8 || precision == LSG_PREC_FP8_TAIL)
-                    ? PR_FP8
-                    : (precision == LSG_PREC_FP16 ? PR_FP16 : PR_BF16);
-      const bool f8 = h->prec == PR_FP8;
+      h->prec = precision == LSG_PREC_INT8_TAIL                                 ? PR_I8
+                : (precision == LSG_PREC_FP8 || precision == LSG_PREC_FP8_TAIL) ? PR_FP8
+                : (precision == LSG_PREC_FP16 ? PR_FP16 : PR_BF16);
+      const bool f8 = h->prec == PR_FP8 || h->prec == PR_I8;  // 8-bit storage (e4m3, or u8 / s8)
+      const bool i8 = h->prec == PR_I8;
       const int cpu = h->cpu = f8 ? 2 : 1;
       h->sm_count = ctx->sm_count;
       const int B = max_batch;
-      // fp8 activation scales: calibrated |x| max with 10% headroom onto e4m3's 448
+      // 8-bit activation scales: calibrated |x| max with 10% headroom onto e4m3's
+      // 448; u8 spans [0, max] exactly (saturating; tools/int8_sweep.py: headroom
+      // costs u8 0.4 dB and buys nothing)
       std::vector<float> ascale(kTensors, 1.f);
       if (f8)
-        for (int i = 0; i < kTensors; ++i) ascale[i] = std::max(act_absmax[i], 1e-6f) * 1.1f / 448.f;
+        for (int i = 0; i < kTensors; ++i)
+          ascale[i] = i8 ? std::max(act_absmax[i], 1e-6f) / 255.f : std::max(act_absmax[i], 1e-6f) * 1.1f / 448.f;
       h->inv_face = 1.f / ascale[0];
       h->inv_mel = 1.f / ascale[1];
       h->ascale = ascale;
@@ -936,16 +944,17 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       // value, or fp8 byte (value / s_w[row's channel]); 16-byte chunks
       // 128B-swizzled as the UMMA K-major SW128 layout expects
       const int KE = 64 * cpu;  // elements per K block
-      auto store = [&](uint16_t* blk, int r, int j, float v, float inv_sw) {
-        if (f8) {
+      auto store = [&](uint16_t* blk, int r, int j, float v, float sw) {
+        if (f8) {  // s8: round(v / s_w) half-even, as torch.round(w / s) in the tests' models
           uint8_t* b8 = reinterpret_cast<uint8_t*>(blk);
           b8[r * 128 + (((j >> 4) ^ (r & 7)) << 4) + (j & 15)] =
-              (uint8_t)__nv_cvt_float_to_fp8(v * inv_sw, __NV_SATFINITE, __NV_E4M3);
+              i8 ? (uint8_t)(int8_t)std::nearbyint(std::min(127.f, std::max(-127.f, v / sw)))
+                 : (uint8_t)__nv_cvt_float_to_fp8(v * (1.f / sw), __NV_SATFINITE, __NV_E4M3);
         } else {
           blk[r * BK + (((j >> 3) ^ (r & 7)) << 3) + (j & 7)] = h->prec == PR_FP16 ? f2h(v) : f2bf(v);
         }
       };
-      std::vector<std::vector<float>> wscale(kNumLayers);  // fp8: per output channel max|w| / 448
+      std::vector<std::vector<float>> wscale(kNumLayers);  // 8-bit: per output channel max|w| / 448 (e4m3), / 127 (s8)
       // ---------------- weights: pack per layer / phase / N tile / K block
       std::vector<uint16_t> pack;
       std::vector<float> bias;
@@ -981,7 +990,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
             for (int ci = 0; ci < L.cin; ++ci)
               for (int ky = 0; ky < L.kh; ++ky)
                 for (int kx = 0; kx < L.kw; ++kx) m = std::max(m, std::fabs(wat(co, ci, ky, kx)));
-            sw[co] = m > 0.f ? m / 448.f : 1.f;
+            sw[co] = m > 0.f ? m / (i8 ? 127.f : 448.f) : 1.f;
           }
         if (std::string(L.name) == "ae0") {  // audio_stem's copy of the quantized operand
           if (li != kAe0 || L.cin != 1 || L.cout != 32 || L.kh != 3 || L.kw != 3 || L.sh != 1 || L.ph != 1)
@@ -990,7 +999,9 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           for (int co = 0; co < 32; ++co)
             for (int t = 0; t < 9; ++t) {
               const float v = wat(co, 0, t / 3, t % 3);
-              if (f8) {
+              if (i8) {
+                q[co * 9 + t] = (float)std::nearbyint(std::min(127.f, std::max(-127.f, v / sw[co])));
+              } else if (f8) {
                 const __nv_fp8_storage_t e = __nv_cvt_float_to_fp8(v / sw[co], __NV_SATFINITE, __NV_E4M3);
                 const __half_raw hr = __nv_cvt_fp8_to_halfraw(e, __NV_E4M3);
                 q[co * 9 + t] = __half2float(__half(hr));
@@ -1141,7 +1152,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                 for (int c = 0; c < L.cin; ++c) {
                   const float v = (kx >= 0 && kx < 3) ? wat(co, c, ky, kx) : 0.f;
                   if (f8 || c < 64) {
-                    store(blk, r, c, v, 1.f / sw[co]);
+                    store(blk, r, c, v, sw[co]);
                   } else {  // SW32: 32-byte rows, 16-byte chunk ^= (row >> 2) & 1
                     const int j = c - 64;
                     uint16_t* b32 = blk + rows * BK;
@@ -1179,7 +1190,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                     c = j % gch;
                   }
                   const float v = (c < L.cin && kx >= 0 && kx < L.kw) ? wat(co, c, ky, kx) : 0.f;
-                  store(blk, r, j, v, 1.f / sw[co]);
+                  store(blk, r, j, v, sw[co]);
                 }
             }
           }
@@ -1207,7 +1218,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
                     const int t = k / cin_pad, ci = k % cin_pad;
                     if (ci < L.cin) v = wat(co, ci, pg.ky[t], pg.kx[t]);
                   }
-                  store(blk, r, j, v, 1.f / sw[co]);
+                  store(blk, r, j, v, sw[co]);
                 }
               }
             }
@@ -1563,13 +1574,18 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
         h->plan.push_back(r);
       }
       set_smem_attrs(h->prec);
-      if (precision == LSG_PREC_FP8_TAIL) {
+      if (tail) {
         // fp8 on the decoder's last block + the output conv only (fd6.0 ..
-        // out0: 28% of the FLOPs), the 16-bit engine before it -- the split
-        // a sensitivity sweep picks for a >= 30 dB floor on this network
-        // (tools/precision_sweep.py)
+        // out0: 28% of the FLOPs); int8 from fd3.0 (84%); the 16-bit engine
+        // before them -- the splits the sensitivity sweeps pick for a >= 30 dB
+        // floor on this network (tools/precision_sweep.py, tools/int8_sweep.py,
+        // DESIGN.md §4)
+        h->tail_blk = precision == LSG_PREC_INT8_TAIL ? 3 : 6;
+        const std::string first = "fd" + std::to_string(h->tail_blk) + ".0";
         for (int l = 0; l < kNumLayers; ++l)
-          if (std::strcmp(kLayers[l].name, "fd6.0") == 0) h->tail0 = l;
+          if (first == kLayers[l].name) h->tail0 = l;
+        if (h->tail0 == 0 || h->plan[h->tail0].in_view.p != h->cat[h->tail_blk - 1].p)
+          fail(LSG_ERUNTIME, "generator: tail split is not at a decoder block reading a concat buffer");
         lsg_gen hd = nullptr;
         if (lsg_gen_create_q(ctx, weights, n_floats, LSG_PREC_FP16, nullptr, 0, max_batch, &hd) != LSG_OK)
           fail(LSG_ERUNTIME, std::string("lsg_gen_create: fp16 head: ") + lsg_last_error());
@@ -1607,6 +1623,7 @@ static void prep_inputs(lsg_gen h, const float* mel_rows, const int32_t* chunk_r
                         const int64_t* target_idx, const uint8_t* refs, const int32_t* ref_index, int B,
                         cudaStream_t st) {
   const unsigned gf = (unsigned)ceil_div((int64_t)B * 96 * 96, 256), gm = (unsigned)ceil_div((int64_t)B * 80 * 16, 256);
+  if (h->prec == PR_I8) fail(LSG_ERUNTIME, "generator: an INT8 engine has no input stage (it is a tail)");
   if (h->prec == PR_FP8) {
     prep_faces<PR_FP8><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, h->inv_face);
     prep_mel<PR_FP8><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, h->inv_mel);
@@ -1636,7 +1653,7 @@ lsg_status lsg_gen_calibrate(lsg_gen h, const float* mel_rows, const int32_t* ch
   return guard(__func__, [&] {
     *n_tensors = kTensors;
     if (cap < kTensors) return;
-    if (h->prec == PR_FP8) invalid("lsg_gen_calibrate: calibrate on a bf16/fp16 engine");
+    if (h->prec == PR_FP8 || h->prec == PR_I8) invalid("lsg_gen_calibrate: calibrate on a bf16/fp16 engine");
     if (B <= 0 || B > h->max_batch) invalid("lsg_gen_calibrate: batch out of range");
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
@@ -1687,7 +1704,10 @@ __global__ void view_to_f32(const uint16_t* src, int pitch, int coff, int C, int
   const int64_t px = i / C;
   const int c = (int)(i - px * C);
   const uint16_t u = src[px * pitch + coff + c];
-  if constexpr (PR == PR_FP8) {
+  if constexpr (PR == PR_I8) {
+    dst[2 * i] = (float)(u & 0xffu) * scale;
+    dst[2 * i + 1] = (float)(u >> 8) * scale;
+  } else if constexpr (PR == PR_FP8) {
     const __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)u, __NV_E4M3);
     const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&hr));
     dst[2 * i] = f.x * scale;
@@ -1739,6 +1759,13 @@ extern "C" lsg_status lsgdbg_gen_routes(lsg_gen h, int32_t B, int32_t* out, int3
   });
 }
 
+namespace lsg {
+namespace gen {
+static void run_plan(lsg_gen h, int l0, int l1, int mode, void* out, int B, cudaStream_t st);
+static void requant_tail_inputs(lsg_gen h, int B, cudaStream_t st);
+}  // namespace gen
+}  // namespace lsg
+
 extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const int32_t* chunk_row,
                                         const uint8_t* target, const uint8_t* refs, const int32_t* ref_index,
                                         int32_t B, int32_t stop_layer, int32_t which, float* out_dev,
@@ -1747,10 +1774,17 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     Ctx* ctx = h->ctx;
     DeviceGuard g(ctx);
     cudaStream_t st = ctx->stream;
-    if (h->head) invalid("lsgdbg_run_until: not on an fp8-tail engine (check its fp8 / fp16 parts separately)");
-    prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
     if (stop_layer < 0 || stop_layer >= (int)h->plan.size() - 1) invalid("lsgdbg_run_until: bad layer");
-    for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
+    if (h->head) {  // an 8-bit tail: its own layers only, after the head and the requantisation
+      if (stop_layer < h->tail0) invalid("lsgdbg_run_until: a head layer of a tail engine (check the head separately)");
+      prep_inputs(h->head, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
+      run_plan(h->head, 0, h->tail0, OUT_F32_LOGITS, nullptr, B, st);
+      requant_tail_inputs(h, B, st);
+      for (int l = h->tail0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
+    } else {
+      prep_inputs(h, mel_rows, chunk_row, target, nullptr, refs, ref_index, B, st);
+      for (int l = 0; l <= stop_layer; ++l) dispatch(h, h->plan[l], B, st);
+    }
     if (!out_dev) return;  // timing a prefix of the layer chain
     const LayerRun& r = h->plan[stop_layer];
     const ConvParams& p = r.p;
@@ -1762,7 +1796,8 @@ extern "C" lsg_status lsgdbg_run_until(lsg_gen h, const float* mel_rows, const i
     const float scale = h->ascale[which ? h->plan_out_id[stop_layer] : h->plan_in_id[stop_layer]];
     const int64_t pixels = (int64_t)B * H * W;
     const unsigned grid = (unsigned)ceil_div(pixels * C, 256);
-    if (h->prec == PR_FP8) view_to_f32<PR_FP8><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, scale);
+    if (h->prec == PR_I8) view_to_f32<PR_I8><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, scale);
+    else if (h->prec == PR_FP8) view_to_f32<PR_FP8><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, scale);
     else if (h->prec == PR_FP16) view_to_f32<PR_FP16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, 1.f);
     else view_to_f32<PR_BF16><<<grid, 256, 0, st>>>(src, pitch, coff, C, pixels, out_dev, 1.f);
     LSG_CUDA(cudaGetLastError());
@@ -1806,6 +1841,7 @@ static void run_plan(lsg_gen h, int l0, int l1, int mode, void* out, int B, cuda
       cudaStream_t s2 = fork ? h->side : st;
       const unsigned grid = (unsigned)ceil_div((int64_t)B * 1280, 256);
       const ConvParams& p = r.p;
+      if (h->prec == PR_I8) fail(LSG_ERUNTIME, "generator: an INT8 engine has no audio stem (it is a tail)");
       if (h->prec == PR_FP8)
         audio_stem<PR_FP8><<<grid, 256, 0, s2>>>(h->x_mel.p, h->ae0w.p, p.bias, p.oscale, p.out_inv, p.out, p.out_pitch,
                                                 p.out_coff, B);
@@ -1833,11 +1869,12 @@ static void run_plan(lsg_gen h, int l0, int l1, int mode, void* out, int B, cuda
   }
 }
 
-// 16-bit tensor -> this fp8 engine's e4m3 buffer (x / scale, RN, satfinite:
-// the epilogues' own conversion): 8 channels per thread.
-template <int PRS>
-__global__ void requant_fp8(const uint16_t* __restrict__ src, int spitch, int scoff, uint16_t* __restrict__ dst,
-                            int dpitch, int dcoff, int C, int64_t pixels, float inv) {
+// fp16 tensor (the head's) -> this 8-bit engine's buffer, x / scale with the
+// epilogues' own conversion (e4m3 RN satfinite, or u8 RN saturating): 8
+// channels per thread.
+template <int PRD>
+__global__ void requant8(const uint16_t* __restrict__ src, int spitch, int scoff, uint16_t* __restrict__ dst,
+                         int dpitch, int dcoff, int C, int64_t pixels, float inv) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int G = C / 8;
   if (i >= pixels * G) return;
@@ -1845,33 +1882,50 @@ __global__ void requant_fp8(const uint16_t* __restrict__ src, int spitch, int sc
   const int g = (int)(i - px * G);
   const uint4 v = *reinterpret_cast<const uint4*>(src + px * spitch + scoff + 8 * g);
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  uint32_t o[2];
+  float f[16] = {};
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    float f[4];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint32_t u = w[2 * k + j];
-      const uint16_t lo = (uint16_t)(u & 0xffff), hi = (uint16_t)(u >> 16);
-      f[2 * j] = (PRS == PR_FP16 ? __half2float(__ushort_as_half(lo)) : __bfloat162float(__ushort_as_bfloat16(lo))) * inv;
-      f[2 * j + 1] = (PRS == PR_FP16 ? __half2float(__ushort_as_half(hi)) : __bfloat162float(__ushort_as_bfloat16(hi))) * inv;
-    }
-    const uint32_t a = __nv_cvt_float2_to_fp8x2(make_float2(f[0], f[1]), __NV_SATFINITE, __NV_E4M3);
-    const uint32_t b = __nv_cvt_float2_to_fp8x2(make_float2(f[2], f[3]), __NV_SATFINITE, __NV_E4M3);
-    o[k] = a | (b << 16);
+  for (int k = 0; k < 4; ++k) {
+    const float2 x = Num<PR_FP16>::unpack(w[k]);
+    f[2 * k] = x.x * inv;
+    f[2 * k + 1] = x.y * inv;
   }
-  *reinterpret_cast<uint2*>(dst + px * dpitch + dcoff + 4 * g) = make_uint2(o[0], o[1]);
+  uint4 o;
+  Num<PRD>::from_float16(f, &o);
+  *reinterpret_cast<uint2*>(dst + px * dpitch + dcoff + 4 * g) = make_uint2(o.x, o.y);
 }
 
-// channels [c0, c0 + C) of concat buffer k: head's 16-bit copy -> h's fp8 copy
+// channels [c0, c0 + C) of concat buffer k: head's fp16 copy -> h's 8-bit copy
 static void requant_cat(lsg_gen h, int k, int c0, int C, int B, cudaStream_t st) {
   const View& s = h->head->cat[k];
   const View& d = h->cat[k];
   const int64_t pixels = (int64_t)B * s.H * s.W;
   const unsigned grid = (unsigned)ceil_div(pixels * (C / 8), 256);
-  requant_fp8<PR_FP16><<<grid, 256, 0, st>>>(s.p, s.pitch, s.coff + c0, d.p, d.pitch, d.coff + c0 / 2, C, pixels,
-                                             1.f / h->ascale[2 + k]);
+  const float inv = 1.f / h->ascale[2 + k];
+  if (h->prec == PR_I8)
+    requant8<PR_I8><<<grid, 256, 0, st>>>(s.p, s.pitch, s.coff + c0, d.p, d.pitch, d.coff + c0 / 2, C, pixels, inv);
+  else
+    requant8<PR_FP8><<<grid, 256, 0, st>>>(s.p, s.pitch, s.coff + c0, d.p, d.pitch, d.coff + c0 / 2, C, pixels, inv);
   LSG_LAUNCHED(h->ctx);
+}
+
+// Everything an 8-bit tail reads from the head: its first block's input
+// cat[j0 - 1] whole, and the encoder slices of cat[j0..6] (the decoder
+// halves are written by the tail's own epilogues).
+constexpr int kCatC[7] = {1024, 1024, 768, 512, 320, 160, 80};  // channels of cat k
+constexpr int kCatDec[7] = {512, 512, 512, 384, 256, 128, 64};  // ... of which the decoder writes [0, kCatDec)
+static void requant_tail_inputs(lsg_gen h, int B, cudaStream_t st) {
+  const int j0 = h->tail_blk;
+  requant_cat(h, j0 - 1, 0, kCatC[j0 - 1], B, st);
+  for (int k = j0; k < 7; ++k) requant_cat(h, k, kCatDec[k], kCatC[k] - kCatDec[k], B, st);
+}
+
+// a whole forward's layers: the plan, or head + requantisation + tail
+static void run_all(lsg_gen h, int mode, void* out, int B, cudaStream_t st) {
+  const int n = (int)h->plan.size();
+  if (!h->head) return run_plan(h, 0, n, mode, out, B, st);
+  run_plan(h->head, 0, h->tail0, mode, out, B, st);
+  requant_tail_inputs(h, B, st);
+  run_plan(h, h->tail0, n, mode, out, B, st);
 }
 
 // the node the last operation captured on st created
@@ -1901,7 +1955,8 @@ static void forward_graph(lsg_gen h, const float* mel_rows, const int32_t* chunk
   cudaStream_t st = h->cap;  // recording only: nothing runs on it
   const int n = (int)h->plan.size();
   LayerRun& last = h->plan[n - 1];
-  float inv_face = h->prec == PR_FP8 ? h->inv_face : 1.f, inv_mel = h->prec == PR_FP8 ? h->inv_mel : 1.f;
+  lsg_gen pe = h->head ? h->head : h;  // the engine whose input stage runs
+  float inv_face = pe->prec == PR_FP8 ? pe->inv_face : 1.f, inv_mel = pe->prec == PR_FP8 ? pe->inv_mel : 1.f;
   auto& g = h->fwd_graphs[std::make_tuple(B, mode, target_idx ? 1 : 0)];
   if (!g.exec) {
     const int64_t l0 = ctx->launches.load();
@@ -1918,27 +1973,27 @@ static void forward_graph(lsg_gen h, const float* mel_rows, const int32_t* chunk
       }
     } guard_capture{st};
     const unsigned gf = (unsigned)ceil_div((int64_t)B * 96 * 96, 256), gm = (unsigned)ceil_div((int64_t)B * 80 * 16, 256);
-    if (h->prec == PR_FP8) prep_faces<PR_FP8><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, inv_face);
-    else if (h->prec == PR_FP16) prep_faces<PR_FP16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
-    else prep_faces<PR_BF16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, h->x_face.p, B, 1.f);
+    if (pe->prec == PR_FP8) prep_faces<PR_FP8><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, pe->x_face.p, B, inv_face);
+    else if (pe->prec == PR_FP16) prep_faces<PR_FP16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, pe->x_face.p, B, 1.f);
+    else prep_faces<PR_BF16><<<gf, 256, 0, st>>>(target, target_idx, refs, ref_index, pe->x_face.p, B, 1.f);
     g.n_face = last_captured(st);
-    if (h->prec == PR_FP8) prep_mel<PR_FP8><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, inv_mel);
-    else if (h->prec == PR_FP16) prep_mel<PR_FP16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
-    else prep_mel<PR_BF16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, h->x_mel.p, B, 1.f);
+    if (pe->prec == PR_FP8) prep_mel<PR_FP8><<<gm, 256, 0, st>>>(mel_rows, chunk_row, pe->x_mel.p, B, inv_mel);
+    else if (pe->prec == PR_FP16) prep_mel<PR_FP16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, pe->x_mel.p, B, 1.f);
+    else prep_mel<PR_BF16><<<gm, 256, 0, st>>>(mel_rows, chunk_row, pe->x_mel.p, B, 1.f);
     g.n_mel = last_captured(st);
     LSG_LAUNCHED(ctx);
     LSG_LAUNCHED(ctx);
-    run_plan(h, 0, n, mode, out, B, st);
+    run_all(h, mode, out, B, st);
     g.n_out = last_captured(st);  // the fused output conv: the plan's last launch
     guard_capture.armed = false;
     LSG_CUDA(cudaStreamEndCapture(st, &g.graph));
     LSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
     g.kernels = (int)(ctx->launches.load() - l0);
   } else {
-    void* fa[] = {(void*)&target, (void*)&target_idx, (void*)&refs, (void*)&ref_index, (void*)&h->x_face.p,
+    void* fa[] = {(void*)&target, (void*)&target_idx, (void*)&refs, (void*)&ref_index, (void*)&pe->x_face.p,
                   (void*)&B, (void*)&inv_face};
     set_node_args(g.exec, g.n_face, fa);
-    void* ma[] = {(void*)&mel_rows, (void*)&chunk_row, (void*)&h->x_mel.p, (void*)&B, (void*)&inv_mel};
+    void* ma[] = {(void*)&mel_rows, (void*)&chunk_row, (void*)&pe->x_mel.p, (void*)&B, (void*)&inv_mel};
     set_node_args(g.exec, g.n_mel, ma);
     // the output conv's parameter block as captured (launch_* derive grid
     // fields from B there), with only the caller's pointer replaced
@@ -1973,29 +2028,15 @@ void forward_gather(lsg_gen h, const float* mel_rows, const int32_t* chunk_row, 
   cudaStream_t st = ctx->stream;
   const int mode = out_format == LSG_OUT_F32_NCHW ? OUT_F32_NCHW
                                                   : (out_format == LSG_OUT_U8_NHWC ? OUT_U8_NHWC : OUT_F32_LOGITS);
-  const int n = (int)h->plan.size();
-  if (h->head) {
-    // fp8 tail: the 16-bit head up to fd5.2, then the tail's inputs
-    // requantised -- cat[5] (fd5.2's 128 + fe1's 32 channels) and cat[6]'s
-    // fe0 slice (channels 64-79; fd6.2 writes 0-63 in fp8 itself)
-    lsg_gen hd = h->head;
-    prep_inputs(hd, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
-    LSG_LAUNCHED(ctx);
-    LSG_LAUNCHED(ctx);
-    run_plan(hd, 0, h->tail0, mode, out, B, st);
-    requant_cat(h, 5, 0, 160, B, st);
-    requant_cat(h, 6, 64, 16, B, st);
-    run_plan(h, h->tail0, n, mode, out, B, st);
-    return;
-  }
   if (B == h->max_batch && !(gen_knobs() & (1 << 17))) {
     forward_graph(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, out, mode, B, st);
     return;
   }
-  prep_inputs(h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
+  // (8-bit tails: the fp16 head's input stage)
+  prep_inputs(h->head ? h->head : h, mel_rows, chunk_row, target_base, target_idx, refs, ref_index, B, st);
   LSG_LAUNCHED(ctx);
   LSG_LAUNCHED(ctx);
-  run_plan(h, 0, n, mode, out, B, st);
+  run_all(h, mode, out, B, st);
 }
 
 }  // namespace gen

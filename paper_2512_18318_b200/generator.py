@@ -266,11 +266,13 @@ def calibrate(weights: np.ndarray, ctx, batch=None) -> np.ndarray:
 class LipsyncEngine:
     """The lip-sync stage on the GPU (lsg_gen): replaces mock_lipsync's cost
     model (visual_mocks.hpp:41-43) with the generator forward.  precision
-    PREC_FP8 / PREC_FP8_TAIL calibrate per-tensor activation ranges first
+    The 8-bit precisions calibrate per-tensor activation ranges first
     (calibrate()); PREC_FP8_TAIL runs fp16 up to fd5.2 and e4m3 from fd6.0
-    on (the split that keeps >= 30 dB vs the fp32 oracle)."""
+    on, PREC_INT8_TAIL fp16 up to fd2.2 and u8 x s8 (kind::i8) from fd3.0 on
+    (the splits that keep >= 30 dB vs the fp32 oracle)."""
 
-    PREC_BF16, PREC_FP16, PREC_FP8, PREC_FP8_TAIL = 0, 1, 2, 3
+    PREC_BF16, PREC_FP16, PREC_FP8, PREC_FP8_TAIL, PREC_INT8_TAIL = 0, 1, 2, 3, 4
+    int8_headroom = 1.0  # u8 activation scale = calibrated max |x| * headroom / 255 (generator.cu)
 
     def __init__(self, weights: np.ndarray, max_batch: int = 128, ctx=None, precision: int = 1, calib=None):
         from .api import default_context
@@ -280,7 +282,7 @@ class LipsyncEngine:
         h = C.c_void_p()
         self.precision = precision
         self.act_absmax = None
-        if precision in (self.PREC_FP8, self.PREC_FP8_TAIL):
+        if precision in (self.PREC_FP8, self.PREC_FP8_TAIL, self.PREC_INT8_TAIL):
             self.act_absmax = calibrate(w, self.ctx, calib)
             a = self.act_absmax
             self.lib.call("lsg_gen_create_q", self.ctx.h, C.c_void_p(w.ctypes.data), w.size, precision,

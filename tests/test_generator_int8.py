@@ -1,0 +1,301 @@
+"""INT8 generator tail, SURVEY.md §8 config 4 (LSG_PREC_INT8_TAIL): the fp16
+engine runs the encoders and fd0..fd2.2, the rest of the decoder (fd3.0 ..
+out0, 84% of the FLOPs) runs tcgen05 kind::i8 -- u8 activations (every decoder input is
+post-ReLU) x s8 weights with one scale per output channel, int32
+accumulators in TMEM, dequantised once in the epilogue -- with per-tensor
+activation scales from lsg_gen_calibrate.
+
+Per-tensor u8 ranges only work when the calibration batch comes from the
+distribution the engine then sees: the synthetic network's BatchNorm was
+folded on N(-5, 2.5) mel rows (generator.synthetic_weights), speech log-mel
+(silence at the ln(1e-10) floor) drives its activations ~30x higher.  So the
+floor is stated -- as for any post-training quantisation -- for held-out
+inputs of the calibration distribution; on speech mel (outside the weights'
+BN range) the test only checks that the GPU tracks its rounding model.
+
+Checks: every int8 layer in isolation; the whole forward against the fp32
+oracle (the stated INT8 floor, >= 30 dB) and against a CPU int8 rounding
+model built from the engine's own scales (the GPU's int32 accumulation is
+exact, so it must land within 1.5 dB of the model)."""
+import numpy as np
+import pytest
+
+from test_generator import _inputs, _oracle  # noqa: F401
+
+TAIL0 = 37  # fd3.0: first layer of the int8 tail
+
+
+def _calib():
+    """Held-out calibration batch from the evaluation inputs' distribution
+    (test_generator._inputs: N(-5, 2.5) mel rows, jittered faces)."""
+    return _inputs(64, 900)
+
+
+@pytest.fixture(scope="module")
+def gref():
+    return _oracle()
+
+
+@pytest.fixture(scope="module")
+def weights(lsg):
+    from paper_2512_18318_b200 import generator
+    return generator.synthetic_weights(seed=0)
+
+
+def _wq(torch, w, kind):
+    """s8 with one scale per output channel (dim 0 for conv, 1 for convT),
+    as lsg_gen_create_q packs them for LSG_PREC_INT8_TAIL."""
+    t = torch.from_numpy(np.ascontiguousarray(w)).float()
+    co_dim = 0 if kind == 0 else 1
+    red = [d for d in range(4) if d != co_dim]
+    m = t.abs().amax(dim=red, keepdim=True)
+    s = torch.where(m > 0, m / 127.0, torch.ones_like(m))
+    return torch.round(t / s).clamp(-127, 127) * s
+
+
+def _walk(gref, blob, mel, faces, conv_q, store):
+    """The oracle's forward with hooks: conv_q(li) -> quantise weights?,
+    store(t, tid, li_next) rounds a stored tensor (tid: 0 faces, 1 mel,
+    2..8 cat0..cat6, 9 + l layer l's output) consumed next by layer li_next."""
+    import torch
+    import torch.nn.functional as F
+    layers = list(zip(gref.layer_table(), gref.split_blob(blob)))
+    li = [0]
+
+    def conv(x):
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        wt = conv_q(li[0], w, kind)
+        b = torch.from_numpy(np.ascontiguousarray(b))
+        y = F.conv2d(x, wt, b, s_, p) if kind == 0 else F.conv_transpose2d(x, wt, b, s_, p, op)
+        if res:
+            y = y + x
+        li[0] += 1
+        return torch.relu(y)
+    with torch.no_grad():
+        x = store(torch.from_numpy(faces), 0, 0)
+        feats = []
+        for j, blk in enumerate(gref.FACE):
+            for n, _ in enumerate(blk):
+                last = n == len(blk) - 1
+                x = store(conv(x), 2 + (6 - j) if last else 9 + li[0] - 1, li[0])
+            feats.append(x)  # and again below, as part of its concat buffer
+        a = store(torch.from_numpy(mel), 1, 18)
+        for _ in gref.AUDIO:
+            a = store(conv(a), 9 + li[0] - 1, li[0])
+        x = a
+        for j, blk in enumerate(gref.DECODER):
+            for n, _ in enumerate(blk):
+                last = n == len(blk) - 1
+                y = conv(x)
+                x = y if last else store(y, 9 + li[0] - 1, li[0])
+            x = store(torch.cat([x, feats.pop()], 1), 2 + j, li[0])
+        x = conv(x)  # out0: kept in f32 by the fused epilogue
+        (kind, cin, cout, k, s_, p, op, res), (w, b) = layers[li[0]]
+        y = F.conv2d(x, torch.from_numpy(np.ascontiguousarray(w)), torch.from_numpy(np.ascontiguousarray(b)))
+        return torch.sigmoid(y).numpy()
+
+
+def oracle_absmax(gref, blob, mel, faces):
+    """max |x| per scale group of the fp32 oracle (lsg_gen_calibrate's
+    grouping), for the CPU sweep (tools/int8_sweep.py)."""
+    a = np.zeros(9 + 51, np.float32)
+
+    def store(t, tid, _):
+        a[tid] = max(a[tid], float(t.abs().max()))
+        return t
+    import torch
+    _walk(gref, blob, mel, faces, lambda i, w, k: torch.from_numpy(np.ascontiguousarray(w)), store)
+    return a
+
+
+def int8_tail_rounding_model(gref, blob, mel, faces, absmax, tail0=TAIL0, headroom=1.0):
+    """LSG_PREC_INT8_TAIL's quantisation points: fp16 weights and stored
+    tensors for layers < tail0; every tensor a tail layer reads (the
+    concat buffers with their requantised encoder slices, the tail's own
+    outputs) rounded to u8 with its calibrated per-tensor scale
+    absmax * headroom / 255; s8 weights for the tail; out0 + out1 in f32."""
+    import torch
+    scale = np.maximum(absmax, 1e-6) * headroom / 255.0
+    h16 = lambda t: t.to(torch.float16).float()  # noqa: E731
+
+    def conv_q(li, w, kind):
+        return _wq(torch, w, kind) if li >= tail0 else h16(torch.from_numpy(np.ascontiguousarray(w)))
+
+    def store(t, tid, consumer):
+        if consumer >= tail0:
+            s = float(scale[tid])
+            return torch.round(t / s).clamp(0, 255) * s
+        return h16(t)
+    return _walk(gref, blob, mel, faces, conv_q, store)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B", [5, 16, 128])
+def test_int8_tail_meets_30db_floor(weights, gref, B):
+    """LSG_PREC_INT8_TAIL: PSNR >= 30 dB vs the fp32 oracle on the [0,1]
+    frames and on the u8 frames -- the stated INT8 floor -- and within 1.5 dB
+    of its CPU rounding model; at B=128 on a seeded subset of one launch."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_INT8_TAIL,
+                                     calib=_calib())
+    rows, chunk_row, target, refs, ref_index = _inputs(B, 400 + B)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    out = torch.empty(B, 3, 96, 96, dtype=torch.float32, device="cuda")
+    u8 = torch.empty(B, 96, 96, 3, dtype=torch.uint8, device="cuda")
+    eng.forward_device(*[t.data_ptr() for t in d], out.data_ptr(), 0, B)
+    eng.forward_device(*[t.data_ptr() for t in d], u8.data_ptr(), 1, B)
+    torch.cuda.synchronize()
+    idx = list(range(B)) if B <= 16 else sorted({0, 1, 63, 64, 126, 127, 17, 90})
+    mel = np.stack([gref.mel_chunk(rows, int(chunk_row[b]))[None] for b in idx])
+    faces = np.stack([gref.face_input(target[b], refs[ref_index[b]]) for b in idx])
+    want = gref.forward(weights, mel, faces)
+    got = out.cpu().numpy()[idx]
+    assert np.isfinite(got).all()
+    p = gref.psnr(got, want)
+    pu8 = gref.psnr(u8.cpu().numpy()[idx].astype(np.float64) / 255.0, want.transpose(0, 2, 3, 1))
+    pm = gref.psnr(int8_tail_rounding_model(gref, weights, mel, faces, eng.act_absmax, TAIL0,
+                                            eng.int8_headroom), want)
+    print(f"int8-tail B={B}: GPU {p:.2f} dB (u8 {pu8:.2f}), CPU rounding model {pm:.2f} dB")
+    assert p >= 30.0 and pu8 >= 30.0, (p, pu8)
+    assert p >= pm - 1.5, (p, pm)
+    eng.close()
+    ctx.set_stream(None)
+
+
+@pytest.mark.gpu
+def test_int8_tail_batch_size_independence(weights):
+    """The CUDA-graph forward (B = max_batch) and the eager launches agree
+    exactly at the same batch size (same routes: int32 accumulation, the
+    same split-K order).  Across batch sizes the split-K factor changes, so
+    the f32 sum of the int32 partials can flip a u8 rounding; a flipped code
+    is a whole step, which perturbs the next layer's roundings, and the
+    cascade decorrelates the quantisation noise by the output (each batch
+    size still tracks the rounding model to 0.05 dB, test above): frames of
+    different batch sizes agree to the INT8 floor, not bit for bit."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    E = generator.LipsyncEngine
+    cal = _calib()
+    eng = E(weights, max_batch=64, ctx=ctx, precision=E.PREC_INT8_TAIL, calib=cal)
+    eng65 = E(weights, max_batch=65, ctx=ctx, precision=E.PREC_INT8_TAIL, calib=cal)  # B = 64 runs eagerly
+    rows, chunk_row, target, refs, ref_index = _inputs(65, 77)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+
+    def run(e, B):
+        o = torch.empty(B, 96, 96, 3, dtype=torch.uint8, device="cuda")
+        e.forward_device(*[t.data_ptr() for t in d], o.data_ptr(), 1, B)
+        torch.cuda.synchronize()
+        return o.cpu().numpy().astype(np.float64)
+    graph, eager = run(eng, 64), run(eng65, 64)
+    assert np.array_equal(graph, eager)
+    eng65.close()
+    small = run(eng, 5)
+    mse = np.mean((graph[:5] - small) ** 2) / 255.0 ** 2
+    p = 10 * np.log10(1 / max(mse, 1e-30))
+    print(f"int8-tail B=5 vs B=64 frames: {p:.2f} dB")
+    assert p >= 30.0
+    eng.close()
+    ctx.set_stream(None)
+
+
+@pytest.mark.gpu
+def test_int8_every_tail_layer_in_isolation(weights, gref):
+    """Each kind::i8 layer (fd3.0 .. fd6.2) against an fp32 conv of the GPU's
+    own dequantised u8 input with the same s8 weights: the int32
+    accumulation is exact, so the only error left is the output's u8
+    rounding (half a step of the tensor's scale) and its saturation at the
+    calibrated maximum."""
+    torch = pytest.importorskip("torch")
+    import ctypes as C
+    import torch.nn.functional as F
+    from paper_2512_18318_b200 import generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    B = 3
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_INT8_TAIL,
+                                     calib=_calib())
+    rows, chunk_row, target, refs, ref_index = _inputs(B, 78)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    buf = torch.empty(B * 96 * 96 * 1024, dtype=torch.float32, device="cuda")
+    shape = (C.c_int32 * 4)()
+    fn = eng.lib.dll.lsgdbg_run_until
+    params = gref.split_blob(weights)
+    Ls = generator.layers()
+
+    def dump(layer, which):
+        rc = fn(eng.h, *[C.c_void_p(t.data_ptr()) for t in d], B, layer, which, C.c_void_p(buf.data_ptr()), shape)
+        assert rc == 0, eng.lib.dll.lsg_last_error()
+        torch.cuda.synchronize()
+        n = shape[0] * shape[1] * shape[2] * shape[3]
+        return buf[:n].reshape(*shape).permute(0, 3, 1, 2).cpu()
+    worst, errs = 0.0, {}
+    for i in range(TAIL0, len(Ls) - 2):
+        L = Ls[i]
+        x, y = dump(i, 0)[:, :L.cin], dump(i, 1)
+        u = torch.unique(y)
+        step = float((u[1:] - u[:-1]).min())  # the output's u8 step (its scale)
+        w = _wq(torch, params[i][0], L.kind).double()  # f64: the check's own rounding stays negligible
+        b = torch.from_numpy(np.ascontiguousarray(params[i][1])).double()
+        x, y = x.double(), y.double()
+        ref = F.conv2d(x, w, b, (L.sh, L.sw), (L.ph, L.pw)) if L.kind == 0 else \
+            F.conv_transpose2d(x, w, b, (L.sh, L.sw), (L.ph, L.pw), (L.oph, L.opw))
+        ref = torch.relu(ref + x if L.res else ref).clamp(max=float(y.max()))
+        err = (y - ref).abs().max().item() / step
+        worst = max(worst, err)
+        errs[i] = round(err, 4)
+    print(f"int8 per-layer max error (u8 steps): {errs}")
+    assert worst <= 0.505, errs
+    eng.close()
+    ctx.set_stream(None)
+
+
+@pytest.mark.gpu
+def test_int8_tail_tracks_model_on_speech_mel(weights, gref):
+    """Speech log-mel through the library's mel stage (the bench workload's
+    distribution), calibrated on the default speech calibration batch: no
+    floor is claimed here (the weights' BN range excludes the log floor; fp8
+    and int8 both lose there), but the GPU must still track its
+    CPU rounding model."""
+    torch = pytest.importorskip("torch")
+    from paper_2512_18318_b200 import api, generator
+    from paper_2512_18318_b200.api import Context
+    ctx = Context(0)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    B = 16
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_INT8_TAIL)
+    pcm = api.synth_pattern(500, [(700, 900), (1500, 400), (600, 800)], 180.0, 0.25, 6000)
+    rows = api.compute_mel(api.AudioBuffer(samples=pcm)).data.reshape(-1, 80).astype(np.float32)
+    _, _, target, refs, ref_index = _inputs(B, 31)
+    chunk_row = np.random.default_rng(31).integers(0, rows.shape[0] - 16, B).astype(np.int32)
+    d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (rows, chunk_row, target, refs, ref_index)]
+    out = torch.empty(B, 3, 96, 96, dtype=torch.float32, device="cuda")
+    eng.forward_device(*[t.data_ptr() for t in d], out.data_ptr(), 0, B)
+    torch.cuda.synchronize()
+    mel = np.stack([gref.mel_chunk(rows, int(r))[None] for r in chunk_row])
+    faces = np.stack([gref.face_input(target[b], refs[ref_index[b]]) for b in range(B)])
+    want = gref.forward(weights, mel, faces)
+    p = gref.psnr(out.cpu().numpy(), want)
+    pm = gref.psnr(int8_tail_rounding_model(gref, weights, mel, faces, eng.act_absmax, TAIL0,
+                                            eng.int8_headroom), want)
+    print(f"int8-tail on speech mel: GPU {p:.2f} dB, CPU rounding model {pm:.2f} dB")
+    assert abs(p - pm) <= 1.5, (p, pm)
+    eng.close()
+    # the fp8 tail on the same frames, for DESIGN.md §4's comparison
+    from test_generator_fp8 import fp8_tail_rounding_model
+    eng = generator.LipsyncEngine(weights, max_batch=B, ctx=ctx, precision=generator.LipsyncEngine.PREC_FP8_TAIL)
+    eng.forward_device(*[t.data_ptr() for t in d], out.data_ptr(), 0, B)
+    torch.cuda.synchronize()
+    p8 = gref.psnr(out.cpu().numpy(), want)
+    pm8 = gref.psnr(fp8_tail_rounding_model(gref, weights, mel, faces, eng.act_absmax), want)
+    print(f"fp8-tail on speech mel: GPU {p8:.2f} dB, CPU rounding model {pm8:.2f} dB")
+    assert abs(p8 - pm8) <= 1.5, (p8, pm8)
+    eng.close()
+    ctx.set_stream(None)
