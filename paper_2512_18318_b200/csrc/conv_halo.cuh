@@ -126,6 +126,7 @@ struct alignas(64) HaloParams {
   int shift_planes;  // planes are x-shifted copies of channels 0..7 (fe0)
   int xmul;          // input columns per grid column (4 for the macro-pixel stem)
   int out2;          // also store every output box through tmap_out2
+  int trace_slot;    // layer index (LSG_TRACE builds: wait accounting)
   int ntaps;
   int aoff[MAX_HTAPS];   // tap start offset in the patch, 16-byte units (= pixels)
   int tphase[MAX_HTAPS]; // output phase the tap accumulates into
@@ -357,9 +358,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   const uint32_t tmem = *tmem_slot;
   const uint32_t box_bytes = (uint32_t)(p.pw * p.ph * 16);
   tc::griddep_launch();
+  // LSG_TRACE: cycles per role -- 0 producer hempty, 1 (unused),
+  // 2 producer total, 3 MMA tempty, 4 MMA hfull, 5 MMA total, 6 epilogue
+  // staging drain + group barrier, 7 epilogue rfull, 8 epilogue tfull,
+  // 9 epilogue math + staging, 10 epilogue total (summed over the two groups)
+  long long hw[11] = {};
+  (void)hw;
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
+#ifdef LSG_TRACE
+    const long long tr0 = clock64();
+#endif
     const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
     if constexpr (B_RES) {
       if (lane == 0) {  // every weight block of this layer, once per CTA
@@ -382,8 +392,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     tc::griddep_wait();  // weights are constant; activations come from the previous layer
     // plane g of channel block cb: channels (cb*8 + g)*8 at x0, or channels 0..7 at x0 + g
     const int cstep = p.shift_planes ? 0 : 8, xstep = p.shift_planes ? 1 : 0;
-    int hs = 0, bs = 0, rs = 0;
-    uint32_t hph = 0, bph = 0, rph = 0;
+    int hs = 0, bs = 0;
+    uint32_t hph = 0, bph = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       int ts, nt;
       halo_tile(p, t, ts, nt);
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
 
       for (int cb = 0; cb < p.ncb; ++cb) {
         const int g0 = cb * 8, ng = min(8, p.ngran - g0);
-        tc::mbar_wait(&hempty[hs], hph ^ 1);
+        LSG_HW(hw, 0, tc::mbar_wait(&hempty[hs], hph ^ 1));
         if (lane == 0 && rank == 0)
           tc::mbar_arrive_expect_tx(&hfull[hs], (PAIR ? 2 : 1) *
                                                     (MODE == HALO_CONV3S2   ? 8
@@ -449,22 +459,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
           }
         }
       }
-      if constexpr (CF::HAS_RES) {
-        tc::mbar_wait(&rempty[rs], rph ^ 1);
-        if (lane == 0) {
-          tc::mbar_arrive_expect_tx(&rfull[rs], CF::RES_BYTES);
-          const uint32_t dst = tc::smem_u32(smem + CF::OFF_RES + rs * CF::RES_BYTES);
-#pragma unroll
-          for (int cc = 0; cc < CF::NCH; ++cc)
-            tma_tile_4d(dst + cc * CF::BOX, &p.tmap_res, &rfull[rs], nt * (BN / NF::CPU) + cc * 64, tx * HTW, ty * HTH, n);
-        }
-        __syncwarp();
-        if (++rs == CF::NRES) {
-          rs = 0;
-          rph ^= 1;
-        }
-      }
     }
+#ifdef LSG_TRACE
+    hw[2] = clock64() - tr0;
+    if (lane == 0) LSG_HW_FLUSH(p.trace_slot, hw, 0, 3);
+#endif
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     // One elected lane issues everything.  Descriptors are linear in the
@@ -480,6 +479,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     constexpr uint64_t BBLK16 = CF::BBLK >> 4;
     constexpr uint64_t HST16 = CF::HSTAGE >> 4;
     if ((!PAIR || rank == 0) && elect_one()) {
+#ifdef LSG_TRACE
+      const long long tr0 = clock64();
+#endif
       const uint32_t sH0 = tc::smem_u32(sH), sB0 = tc::smem_u32(sB);
       if constexpr (B_RES) tc::mbar_wait_nc(&bfull[0], 0);
       const uint64_t a_desc0 = halo_desc(sH0, (uint32_t)(PLANE2 << 3), (uint32_t)(TT::PW * 16));
@@ -489,15 +491,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       uint32_t hph = 0, bph = 0, tl = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-        if constexpr (PAIR) tc::mbar_wait_cluster(&tempty[a], (use & 1) ^ 1);  // both CTAs' epilogues
-        else tc::mbar_wait_fast(&tempty[a], (use & 1) ^ 1);
+        if constexpr (PAIR) LSG_HW(hw, 3, tc::mbar_wait_cluster(&tempty[a], (use & 1) ^ 1));  // both CTAs' epilogues
+        else LSG_HW(hw, 3, tc::mbar_wait_fast(&tempty[a], (use & 1) ^ 1));
         tc::tc_fence_after_nc();  // TMEM reuse after the epilogue's reads
         const uint32_t d = tmem + a * CF::ACC_COLS;
         for (int cb = 0; cb < ncb; ++cb) {
           const int ksteps = MODE == HALO_CONV3S2   ? 1
                              : MODE == HALO_CONV3X2 ? min(4, ngran - cb * 4) >> 1
                                                     : min(8, ngran - cb * 8) >> 1;
-          tc::mbar_wait_fast(&hfull[hs], hph);  // TMA data: the mbarrier alone orders it
+          LSG_HW(hw, 4, tc::mbar_wait_fast(&hfull[hs], hph));  // TMA data: the mbarrier alone orders it
           const uint64_t ah = a_desc0 + (uint64_t)hs * HST16;
           const uint64_t bcb = b_desc0 + (uint64_t)(cb * NT) * BBLK16;
 #pragma unroll
@@ -562,6 +564,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         if constexpr (PAIR) tc::mma_commit2(&tfull[a]);
         else tc::mma_commit_nc(&tfull[a]);
       }
+#ifdef LSG_TRACE
+      hw[5] = clock64() - tr0;
+      LSG_HW_FLUSH(p.trace_slot, hw, 3, 6);
+#endif
     }
     __syncwarp();
   } else {
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     constexpr int HC = SPLIT ? BN / 2 : BN;
     const int cbeg = SPLIT ? half * HC : 0;
     const int r = q * 32 + lane;  // tile position: row r / 8, column r % 8
-    const int step = EPI_ALT ? 2 : 1;
+    constexpr int step = EPI_ALT ? 2 : 1;
     uint32_t tl = EPI_ALT ? (uint32_t)half : 0u;
     // grid position of tile t for this thread
     auto gpos = [&](int t, int& n, int& gy, int& gx) {
@@ -591,9 +597,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
       const int grp = EPI_ALT ? half : 0;
       const bool leader = (warp == 2 + 4 * grp) && lane == 0;  // issues the group's stores
       int sb = 0;
+      // Residual boxes: the group's leader loads them (not the producer, whose
+      // patch prefetch would otherwise stall behind the epilogue on the ring),
+      // the next tile's as soon as every thread of the group holds this
+      // tile's in registers -- its latency hides under this tile's math.  One
+      // slot per group (NRES == step): tile tl's slot is tl % NRES.
+      static_assert(!CF::HAS_RES || (CF::NRES == step && NPH == 1), "residual ring: one slot per epilogue group");
+      auto issue_res = [&](int tt, int slot) {
+        int ts2, nt2;
+        halo_tile(p, tt, ts2, nt2);
+        const int n2 = ts2 / p.tiles_per_img, r2 = ts2 - n2 * p.tiles_per_img;
+        const int ty2 = r2 / p.tiles_x, tx2 = r2 - ty2 * p.tiles_x;
+        tc::mbar_arrive_expect_tx(&rfull[slot], CF::RES_BYTES);
+        const uint32_t dst = tc::smem_u32(smem + CF::OFF_RES + slot * CF::RES_BYTES);
+#pragma unroll
+        for (int cc = 0; cc < CF::NCH; ++cc)
+          tma_tile_4d(dst + cc * CF::BOX, &p.tmap_res, &rfull[slot], nt2 * (BN / NF::CPU) + cc * 64, tx2 * HTW,
+                      ty2 * HTH, n2);
+      };
+      if constexpr (CF::HAS_RES) {
+        const int t0 = blockIdx.x + (int)tl * gridDim.x;
+        if (leader && t0 < p.total_tiles) issue_res(t0, (int)(tl % (uint32_t)step));
+      }
+#ifdef LSG_TRACE
+      const long long tr0 = clock64();
+#endif
       for (int t = blockIdx.x + (int)tl * gridDim.x; t < p.total_tiles; t += step * gridDim.x, tl += step) {
         const uint32_t a = NACC == 2 ? (tl & 1) : 0, use = NACC == 2 ? (tl >> 1) : tl;
-        // residual ring slot of this tile (the producer fills slots in tile order)
+        // residual ring slot of this tile
         const int rs = CF::NRES ? (int)(tl % (uint32_t)(CF::NRES ? CF::NRES : 1)) : 0;
         const uint32_t rph = CF::NRES ? (tl / (uint32_t)(CF::NRES ? CF::NRES : 1)) & 1u : 0u;
         int ts, nt;
@@ -602,48 +633,89 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         const int ty = rr / p.tiles_x, tx = rr - ty * p.tiles_x;
         uint8_t* stg = smem + CF::OFF_STG + (EPI_ALT ? grp : sb) * CF::STG_BYTES;
         // the store that last read this staging buffer must have drained
-        if (leader) bulk_wait_read<EPI_ALT ? 0 : CF::NSTG - 1>();
-        named_bar(1 + grp, EPI_THREADS);
-        const uint8_t* res = smem + CF::OFF_RES + rs * CF::RES_BYTES;
-        if constexpr (CF::HAS_RES) tc::mbar_wait(&rfull[rs], rph);
-        tc::mbar_wait(&tfull[a], use & 1);
+        LSG_HW(hw, 6, if (leader) bulk_wait_read<EPI_ALT ? 0 : CF::NSTG - 1>(); named_bar(1 + grp, EPI_THREADS));
+        constexpr int W16 = NF::U4, ES = NF::Q8 ? 1 : 2;
+        uint4 rvall[CF::HAS_RES ? HC / 16 : 1][W16];
+        if constexpr (CF::HAS_RES) {
+          const uint8_t* res = smem + CF::OFF_RES + rs * CF::RES_BYTES;
+          LSG_HW(hw, 7, tc::mbar_wait(&rfull[rs], rph));
+#pragma unroll
+          for (int c0 = 0; c0 < HC; c0 += 16) {
+            const int byte0 = (cbeg + c0) * ES;
+            const int cc = byte0 >> 7, j0 = (byte0 & 127) >> 4;
+#pragma unroll
+            for (int w = 0; w < W16; ++w)
+              rvall[c0 / 16][w] = *reinterpret_cast<const uint4*>(res + cc * CF::BOX + swz<IB>(r, j0 + w));
+          }
+          tc::mbar_arrive(&rempty[rs]);
+          if (leader && t + step * (int)gridDim.x < p.total_tiles) {
+            tc::mbar_wait(&rempty[rs], rph);  // the whole group holds this box
+            issue_res(t + step * (int)gridDim.x, rs);
+          }
+        }
+        LSG_HW(hw, 8, tc::mbar_wait(&tfull[a], use & 1));
         tc::tc_fence_after();
+#ifdef LSG_TRACE
+        const long long tm0 = clock64();
+#endif
+        // EARLY: this thread's whole share of the accumulator (<= 64 columns)
+        // goes to registers in one TMEM round trip and the accumulator is
+        // released before the math, so the next-but-one tile's MMAs overlap
+        // this epilogue instead of waiting for it (2 accumulators)
+        constexpr bool EARLY = NPH * HC <= 64;
+        uint32_t vall[EARLY ? NPH * HC / 16 : 1][16];
+        if constexpr (EARLY) {
+#pragma unroll
+          for (int z = 0; z < NPH; ++z)
+#pragma unroll
+            for (int c0 = 0; c0 < HC; c0 += 16)
+              tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS + z * BN + cbeg + c0,
+                            vall[(z * HC + c0) / 16]);
+          tc::tmem_ld_wait();
+          tc::tc_fence_before();
+          if constexpr (PAIR) {
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote(&tempty[a], 0);
+          } else {
+            tc::mbar_arrive(&tempty[a]);
+          }
+        }
 #pragma unroll
         for (int z = 0; z < NPH; ++z) {
           const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + a * CF::ACC_COLS + z * BN + cbeg;
 #pragma unroll
           for (int c0 = 0; c0 < HC; c0 += 16) {
             uint32_t v[16];
-            tc::tmem_ld16(tbase + c0, v);
+            if constexpr (EARLY) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = vall[(z * HC + c0) / 16][j];
+            } else {
+              tc::tmem_ld16(tbase + c0, v);
+            }
             // 16 channels = W16 16-byte chunks of the position's box row
-            constexpr int W16 = NF::U4, ES = NF::Q8 ? 1 : 2;
             const int byte0 = (cbeg + c0) * ES;
             const int cc = byte0 >> 7, j0 = (byte0 & 127) >> 4;
-            uint4 rv[W16];
-            if constexpr (CF::HAS_RES) {
-#pragma unroll
-              for (int w = 0; w < W16; ++w)
-                rv[w] = *reinterpret_cast<const uint4*>(res + cc * CF::BOX + swz<IB>(r, j0 + w));
-            }
-            tc::tmem_ld_wait();
+            if constexpr (!EARLY) tc::tmem_ld_wait();
             uint4 o[W16];
-            epi16<PR>(v, p.bias + nt * BN + cbeg + c0, p.oscale + (NF::Q8 ? nt * BN + cbeg + c0 : 0), CF::HAS_RES ? rv : nullptr,
-                      p.res_scale, p.relu != 0, p.out_inv, o);
+            epi16<PR>(v, p.bias + nt * BN + cbeg + c0, p.oscale + (NF::Q8 ? nt * BN + cbeg + c0 : 0),
+                      CF::HAS_RES ? rvall[c0 / 16] : nullptr, p.res_scale, p.relu != 0, p.out_inv, o);
 #pragma unroll
             for (int w = 0; w < W16; ++w)
               *reinterpret_cast<uint4*>(stg + (z * CF::NCH + cc) * CF::BOX + swz<IB>(r, j0 + w)) = o[w];
           }
         }
-        tc::tc_fence_before();
-        if constexpr (PAIR) {
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive_remote(&tempty[a], 0);
-        } else {
-          tc::mbar_arrive(&tempty[a]);
+        if constexpr (!EARLY) {
+          tc::tc_fence_before();
+          if constexpr (PAIR) {
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_remote(&tempty[a], 0);
+          } else {
+            tc::mbar_arrive(&tempty[a]);
+          }
         }
-        if constexpr (CF::HAS_RES) {
-          tc::mbar_arrive(&rempty[rs]);
-        }
+#ifdef LSG_TRACE
+        hw[9] += clock64() - tm0;
+#endif
         tc::fence_proxy_async();  // staging writes -> visible to the TMA (async proxy)
         named_bar(1 + grp, EPI_THREADS);
         if (leader) {
@@ -667,6 +739,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
         if (++sb == CF::NSTG) sb = 0;
       }
       if (leader) bulk_wait_all();
+#ifdef LSG_TRACE
+      hw[10] = clock64() - tr0;
+      if ((warp & 3) == 2 && lane == 0) LSG_HW_FLUSH(p.trace_slot, hw, 6, 11);
+#endif
     } else {
       for (int t = blockIdx.x + (int)tl * gridDim.x; t < p.total_tiles; t += step * gridDim.x, tl += step) {
         const uint32_t a = tl & 1, use = tl >> 1;

@@ -47,9 +47,32 @@ __device__ unsigned long long g_lsg_trace[TRACE_LAYERS * TRACE_CTAS * TRACE_EV];
     if ((slot) >= 0 && blockIdx.x < TRACE_CTAS)                                                         \
       g_lsg_trace[((size_t)(slot) * TRACE_CTAS + blockIdx.x) * TRACE_EV + (i)] = t_;                    \
   } while (0)
+// conv_halo's role accounting: clock64 cycles spent in each wait, summed per
+// CTA (tools/halo_waits.py): LSG_HW(acc, i, stmt) times stmt into acc[i],
+// LSG_HW_FLUSH adds acc[i0, i1) into the layer's per-CTA slots.
+#define LSG_HW(acc, i, ...)                        \
+  do {                                             \
+    const long long t0_ = clock64();               \
+    __VA_ARGS__;                                   \
+    (acc)[i] += clock64() - t0_;                   \
+  } while (0)
+#define LSG_HW_FLUSH(slot, acc, i0, i1)                                                                    \
+  do {                                                                                                  \
+    if ((slot) >= 0 && blockIdx.x < TRACE_CTAS)                                                         \
+      for (int i_ = (i0); i_ < (i1); ++i_)                                                              \
+        atomicAdd(&g_lsg_trace[((size_t)(slot) * TRACE_CTAS + blockIdx.x) * TRACE_EV + i_],             \
+                  (unsigned long long)(acc)[i_]);                                                       \
+  } while (0)
 #else
 #define LSG_TR(slot, i) \
   do {                  \
+  } while (0)
+#define LSG_HW(acc, i, ...) \
+  do {                      \
+    __VA_ARGS__;            \
+  } while (0)
+#define LSG_HW_FLUSH(slot, acc, i0, i1) \
+  do {                                  \
   } while (0)
 #endif
 
@@ -158,11 +181,14 @@ struct Num {
   // 16 channels <-> their U4 uint4 words
   __device__ __forceinline__ static void to_float16(const uint4* w, float (&x)[16]) {
     if constexpr (I8) {
+      // byte b -> the float 2^23 + b (PRMT into 0x4B0000bb) - 2^23: full-rate
+      // ALU/FMA work instead of the quarter-rate I2F conversion
       const uint32_t r[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) x[4 * k + b] = (float)((r[k] >> (8 * b)) & 0xffu);
+        for (int b = 0; b < 4; ++b)
+          x[4 * k + b] = __uint_as_float(__byte_perm(r[k], 0x4B000000u, 0x7540u + b)) - 8388608.f;
     } else if constexpr (Q8) {
       const uint32_t r[4] = {w[0].x, w[0].y, w[0].z, w[0].w};
 #pragma unroll
@@ -186,14 +212,17 @@ struct Num {
     }
   }
   __device__ __forceinline__ static void from_float16(const float (&f)[16], uint4* w) {
-    if constexpr (I8) {  // u8: round to nearest, saturate to [0, 255]
+    if constexpr (I8) {
+      // u8: saturate to [0, 255], round to nearest even by adding 2^23 (the
+      // code lands in the low mantissa byte), pack the four low bytes with
+      // PRMTs -- no quarter-rate F2I
       uint32_t r[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         uint32_t q[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) q[b] = __float2uint_rn(fminf(fmaxf(f[4 * k + b], 0.f), 255.f));
-        r[k] = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+        for (int b = 0; b < 4; ++b) q[b] = __float_as_uint(fminf(fmaxf(f[4 * k + b], 0.f), 255.f) + 8388608.f);
+        r[k] = __byte_perm(__byte_perm(q[0], q[1], 0x0040u), __byte_perm(q[2], q[3], 0x0040u), 0x5410u);
       }
       w[0] = make_uint4(r[0], r[1], r[2], r[3]);
     } else if constexpr (Q8) {
@@ -230,7 +259,11 @@ struct Num {
 };
 
 // The per-channel math of every epilogue, 16 channels at a time:
-// y = acc * oscale + bias (+ residual * res_scale), ReLU, * out_inv (8-bit).
+// y = acc * oscale + bias (+ residual * res_scale), ReLU, * out_inv (fp8).
+// INT8 works in output-code units: the plan folds 1 / (output scale) into
+// oscale, bias and res_scale, and the u8 conversion's saturation at 0 is the
+// ReLU (8.75 instructions per value instead of 12: these epilogues bound
+// the int8 halo layers).
 // FACC: v holds f32 bits whatever the format (split-K's reduced partials).
 template <int PR, bool FACC = false>
 __device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias, const float* oscale,
@@ -266,11 +299,11 @@ __device__ __forceinline__ void epi16(const uint32_t (&v)[16], const float* bias
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] = NF::Q8 ? fmaf(x[j], res_scale, f[j]) : f[j] + x[j];
   }
-  if (relu) {
+  if (!NF::I8 && relu) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.f);
   }
-  if constexpr (NF::Q8) {
+  if constexpr (NF::Q8 && !NF::I8) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) f[j] *= out_inv;
   }

@@ -1351,11 +1351,16 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       std::vector<int64_t> osc_off(kNumLayers, 0);
       if (f8) {
         for (int l = 0; l < kNumLayers - 1; ++l) {
+          // int8 epilogues work in output-code units (epi16): 1 / s_out folded
+          // into this layer's oscale and bias here, into res_scale below
+          const float fold = i8 && l != kNumLayers - 2 ? 1.f / ascale[out_id[l]] : 1.f;
           osc_off[l] = (int64_t)osc.size();
-          for (int co = 0; co < kLayers[l].cout; ++co) osc.push_back(ascale[in_id[l]] * wscale[l][co]);
+          for (int co = 0; co < kLayers[l].cout; ++co) osc.push_back(ascale[in_id[l]] * wscale[l][co] * fold);
+          for (int co = 0; co < kLayers[l].cout; ++co) bias[bias_off[l] + co] *= fold;
         }
         h->oscale.alloc(osc.size());
         LSG_CUDA(cudaMemcpy(h->oscale.p, osc.data(), osc.size() * 4, cudaMemcpyHostToDevice));
+        if (i8) LSG_CUDA(cudaMemcpy(h->bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
       }
       for (int l = 0; l < kNumLayers - 1; ++l) {
         const LayerSpec& L = kLayers[l];
@@ -1395,8 +1400,8 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
         p.res_coff = in.coff;
         p.bias = h->bias.p + bias_off[l];
         p.oscale = f8 ? h->oscale.p + osc_off[l] : nullptr;
-        p.res_scale = f8 ? ascale[in_id[l]] : 1.f;
-        p.out_inv = f8 && !fused ? 1.f / ascale[out_id[l]] : 1.f;
+        p.res_scale = f8 ? ascale[in_id[l]] / (i8 && !fused ? ascale[out_id[l]] : 1.f) : 1.f;
+        p.out_inv = f8 && !i8 && !fused ? 1.f / ascale[out_id[l]] : 1.f;  // int8: folded (epi16)
         p.relu = 1;
         p.out_mode = OUT_16;
         if (L.kind == CONV) {
@@ -1571,6 +1576,7 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
           }
         }
         r.p.trace_slot = (int)h->plan.size();
+        r.hp.trace_slot = r.p.trace_slot;
         h->plan.push_back(r);
       }
       set_smem_attrs(h->prec);

@@ -20,9 +20,9 @@ def main():
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
         if r["Metric Name"] == "gpu__time_duration.sum":
-            k["us"] = v / 1000.0 if unit == "nsecond" else (v if unit == "usecond" else v * 1000.0)
+            k["us"] = v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[unit]
         elif r["Metric Name"].startswith("dram__bytes"):
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}[unit]
             k["dram"] = k.get("dram", 0.0) + v * scale
     last = list(rows.values())[-n:]
     tot_us = tot_mb = 0.0

@@ -39,6 +39,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("--cuda", action="store_true", help="also: hottest CUDA source lines (needs -lineinfo)")
     a = ap.parse_args()
     rows = ncu_csv(a.rep, "raw")
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -63,6 +64,39 @@ def main():
     print(f"  stall samples total {tot:.0f}; hottest SASS lines:")
     for r in sorted(data, key=lambda r: -float(r[iss] or 0))[:a.top]:
         print(f"    {float(r[iss] or 0) / tot * 100:5.1f}%  exec {int(r[iex] or 0):>10d}  {r[isrc].strip()[:90]}")
+    if a.cuda:
+        for sec in ("WarpStateStats", "SchedulerStats"):
+            out = subprocess.run(["ncu", "-i", a.rep, "--page", "details", "--section", sec, "--csv"],
+                                 capture_output=True, text=True).stdout
+            rows = list(csv.reader(io.StringIO(out)))
+            if rows:
+                h = rows[0]
+                im, iu, iv = h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+                print(f"  [{sec}]")
+                for r in rows[1:]:
+                    if len(r) == len(h):
+                        print(f"    {r[im]:50s} {r[iv]:>12s} {r[iu]}")
+        out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda"],
+                             capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        files, cur, lines = [], None, []
+        for r in rows:
+            if len(r) == 1 and r[0].startswith("File"):
+                cur = r[0]
+                continue
+            if r and r[0] == "Line":
+                h = r
+                continue
+            if cur is not None and len(r) > 3 and r[0].isdigit():
+                try:
+                    lines.append((float(r[h.index("Warp Stall Sampling (All Samples)")] or 0), cur.split("/")[-1],
+                                  r[0], r[h.index("Source")].strip()[:80]))
+                except (ValueError, NameError):
+                    pass
+        tot2 = sum(x[0] for x in lines) or 1.0
+        print(f"  hottest CUDA lines ({tot2:.0f} samples):")
+        for smp, f, ln, src in sorted(lines, key=lambda x: -x[0])[:a.top]:
+            print(f"    {smp / tot2 * 100:5.1f}%  {f}:{ln}  {src}")
 
 
 if __name__ == "__main__":
