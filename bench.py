@@ -452,7 +452,7 @@ def main():
     if scaled:
         out["stage_rooflines"] = scaled
     if cfg4:
-        out["config4_fp8"] = cfg4
+        out["config4_int8"] = cfg4
     if world == 1 and not args.no_cpu_baseline:
         out.update(config12_leg(args, local, torch, ctx, torch_stream, api, eng, weights))
     if not args.no_cpu_baseline and world == 1:
