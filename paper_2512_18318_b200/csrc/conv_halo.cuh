@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
   const uint32_t tmem = *tmem_slot;
   const uint32_t box_bytes = (uint32_t)(p.pw * p.ph * 16);
   tc::griddep_launch();
-  // LSG_TRACE: cycles per role -- 0 producer hempty, 1 (unused),
+  // LSG_TRACE: cycles per role -- 0 producer hempty, 1 MMA bfull (streamed weights),
   // 2 producer total, 3 MMA tempty, 4 MMA hfull, 5 MMA total, 6 epilogue
   // staging drain + group barrier, 7 epilogue rfull, 8 epilogue tfull,
   // 9 epilogue math + staging, 10 epilogue total (summed over the two groups)
@@ -462,7 +462,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
     }
 #ifdef LSG_TRACE
     hw[2] = clock64() - tr0;
-    if (lane == 0) LSG_HW_FLUSH(p.trace_slot, hw, 0, 3);
+    if (lane == 0) {
+      LSG_HW_FLUSH(p.trace_slot, hw, 0, 1);
+      LSG_HW_FLUSH(p.trace_slot, hw, 2, 3);
+    }
 #endif
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
             } else if constexpr (B_RES) {
               db = bcb + (uint64_t)tap * BBLK16;
             } else {
-              if (tap % CF::WG == 0) tc::mbar_wait_fast(&bfull[bs], bph);
+              if (tap % CF::WG == 0) LSG_HW(hw, 1, tc::mbar_wait_fast(&bfull[bs], bph));
               db = b_desc0 + (uint64_t)bs * (CF::GBLK >> 4) + (uint64_t)(tap % CF::WG) * BBLK16;
             }
             const uint64_t at = ah + (uint64_t)TT::aoff(tap);
@@ -567,6 +570,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) conv_halo(const __grid_constan
 #ifdef LSG_TRACE
       hw[5] = clock64() - tr0;
       LSG_HW_FLUSH(p.trace_slot, hw, 3, 6);
+      LSG_HW_FLUSH(p.trace_slot, hw, 1, 2);
 #endif
     }
     __syncwarp();

@@ -7,7 +7,7 @@ barrier, from an instrumented library (-DLSG_TRACE: conv_halo.cuh LSG_HW).
     LSG_LIB=abtest/trace/liblsg.so python tools/halo_waits.py [B] [precision]
 
 Per layer (CTA average, % of that role's own loop time): producer waits on
-hempty / rempty; MMA waits on tempty / hfull; epilogue waits on the staging
+hempty; MMA waits on tempty / hfull / bfull (streamed weights); epilogue waits on the staging
 drain + group barrier, rfull, tfull, and its math + staging share."""
 import ctypes as C
 import os
@@ -45,7 +45,7 @@ def main():
     lib.lsgdbg_trace_read(C.c_void_p(buf.ctypes.data), C.c_int64(buf.size))
     t = buf.reshape(LAYERS, CTAS, EV).astype(np.float64)
     print(f"B={B} precision={prec}: per-CTA averages, % of the role's loop time")
-    print("layer     | producer: loop us  hempty rempty | MMA: loop us  tempty hfull | "
+    print("layer     | producer: loop us  hempty | MMA: loop us  tempty hfull bfull | "
           "epilogue: loop us  drain  rfull  tfull  math")
     for l in range(LAYERS):
         x = t[l]
@@ -59,8 +59,8 @@ def main():
         def pc(v, tot):
             return 100.0 * v / tot if tot else 0.0
         name = NAMES[l] if l < len(NAMES) else str(l)
-        print(f"{l:2d} {name:6s} | {pr / ghz:8.1f} {pc(m[0], pr):7.1f} {pc(m[1], pr):6.1f} | "
-              f"{mm / ghz:8.1f} {pc(m[3], mm):7.1f} {pc(m[4], mm):5.1f} | "
+        print(f"{l:2d} {name:6s} | {pr / ghz:8.1f} {pc(m[0], pr):7.1f} | "
+              f"{mm / ghz:8.1f} {pc(m[3], mm):7.1f} {pc(m[4], mm):5.1f} {pc(m[1], mm):5.1f} | "
               f"{ep / ghz:8.1f} {pc(m[6] / 2, ep):6.1f} {pc(m[7] / 2, ep):6.1f} {pc(m[8] / 2, ep):6.1f} "
               f"{pc(m[9] / 2, ep):5.1f}")
 

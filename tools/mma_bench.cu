@@ -6,6 +6,9 @@
 //        3 = 1 + bulk-copy fill traffic from L2 into a separate region
 //        4 no-swizzle, SBO 160 (halo patch rows), start +16 B (shifted tap)
 //        5 no-swizzle, SBO 160, 128-aligned start | 6 no-swizzle, SBO 128, start +16 B
+// bench_coll: groups of 4 MMAs sharing one A (halo-patch descriptor) with 4
+// different B blocks -- the ConvT phases of one input shift -- without and
+// with the A collector (.collector::a::fill / use / lastuse).
 #include <cstdio>
 #include <cstdint>
 
@@ -108,6 +111,83 @@ __global__ void bench(long long* out, int iters, const uint8_t* src, unsigned lo
   }
 }
 
+__device__ __forceinline__ void mma_coll(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, int c) {
+  if (c == 0)
+    asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a), "l"(b),
+                 "r"(idesc));
+  else if (c == 1)
+    asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::use [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a), "l"(b),
+                 "r"(idesc));
+  else
+    asm volatile("tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, 1;" ::"r"(d), "l"(a),
+                 "l"(b), "r"(idesc));
+}
+
+template <int N, int G, bool COLL>
+__global__ void bench_coll(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 128 * 1024; i += blockDim.x) smem[i] = (uint8_t)(i * 7);
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc<256>(&slot);
+  tc::fence_proxy_async();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t base = tc::smem_u32(smem);
+  if (threadIdx.x == 0) {
+    const uint64_t db0 = tc::sdesc_sw128(base + 65536);
+    constexpr uint32_t idesc = tc::idesc_f16kind(128, N, 0);
+    const uint64_t da0 = desc_noswz(base + 16, 2944, 160);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const uint64_t da = da0 + (uint64_t)((i & 3) * (5888 >> 4));
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint64_t db = db0 + (uint64_t)(g * (N * 128 >> 4));  // B block g (N rows x 128 B)
+        if constexpr (COLL) mma_coll(tmem + (g & 3) * 64 % 256, da, db, idesc, g == 0 ? 0 : (g == G - 1 ? 2 : 1));
+        else tc::mma_f16(tmem + (g & 3) * 64 % 256, da, db, idesc, 1);
+      }
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<256>(tmem);
+  }
+}
+
+template <int N, int G, bool COLL>
+void run_coll(int blocks) {
+  long long* d;
+  cudaMalloc(&d, sizeof(long long) * blocks);
+  cudaFuncSetAttribute(bench_coll<N, G, COLL>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  const int iters = 4000;
+  bench_coll<N, G, COLL><<<blocks, 128, SMEM>>>(d, 10);
+  bench_coll<N, G, COLL><<<blocks, 128, SMEM>>>(d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < blocks; ++i) avg += h[i];
+  avg /= blocks;
+  printf("A shared by %d MMAs, N=%3d, collector %d: %7.1f cyc/MMA (ideal %5.1f)  %s\n", G, N, (int)COLL,
+         avg / (iters * (double)G), 128 * N / 256.0, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 static uint8_t* g_src;
 static unsigned long long* g_fill;
 
@@ -155,5 +235,11 @@ int main() {
   RUN(4)
   RUN(5)
   RUN(6)
+  run_coll<64, 4, false>(148);
+  run_coll<64, 4, true>(148);
+  run_coll<64, 2, false>(148);
+  run_coll<64, 2, true>(148);
+  run_coll<128, 4, false>(148);
+  run_coll<128, 4, true>(148);
   return 0;
 }
