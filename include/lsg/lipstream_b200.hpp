@@ -423,7 +423,25 @@ inline void validate_lipsync(DurationMs audio_span_ms, DurationMs frame_span_ms,
   check(lsg_lipsync_validate(audio_span_ms, frame_span_ms, n_frames));
 }
 
-enum class Precision { BF16 = LSG_PREC_BF16, FP16 = LSG_PREC_FP16 };
+enum class Precision {
+  BF16 = LSG_PREC_BF16,
+  FP16 = LSG_PREC_FP16,
+  FP8_TAIL = LSG_PREC_FP8_TAIL,    // 8-bit: need a CalibrationBatch
+  INT8_TAIL = LSG_PREC_INT8_TAIL,  //
+};
+
+// Device-resident inputs of a calibration forward (the 8-bit precisions'
+// per-tensor activation ranges come from an fp16 forward over them; pick
+// frames from the distribution the stage will render).  Same layouts as
+// LipsyncStage::render / lsg_gen_forward.
+struct CalibrationBatch {
+  const float* mel_rows = nullptr;
+  const std::int32_t* chunk_row = nullptr;
+  const std::uint8_t* target = nullptr;
+  const std::uint8_t* refs = nullptr;
+  const std::int32_t* ref_index = nullptr;
+  std::int32_t frames = 0;
+};
 
 // The lip-sync stage with mock_lipsync's contract (visual_mocks.hpp:32-43):
 // validate the pair exactly as mock_lipsync does, render every frame through
@@ -438,9 +456,32 @@ enum class Precision { BF16 = LSG_PREC_BF16, FP16 = LSG_PREC_FP16 };
 class LipsyncStage {
  public:
   LipsyncStage(const std::vector<float>& weights, int max_batch = 128, Precision prec = Precision::FP16,
-               Context& ctx = Context::default_context())
+               Context& ctx = Context::default_context(), const CalibrationBatch* calib = nullptr)
       : ctx_(ctx), max_batch_(max_batch) {
-    check(lsg_gen_create(ctx.handle(), weights.data(), std::int64_t(weights.size()), int32_t(prec), max_batch, &g_));
+    if (prec != Precision::FP8_TAIL && prec != Precision::INT8_TAIL) {
+      check(lsg_gen_create(ctx.handle(), weights.data(), std::int64_t(weights.size()), int32_t(prec), max_batch, &g_));
+      return;
+    }
+    if (!calib || calib->frames <= 0) throw std::invalid_argument("LipsyncStage: 8-bit precisions need a calibration batch");
+    // ranges from an fp16 forward over the calibration frames (lsg_gen_calibrate)
+    lsg_gen c = nullptr;
+    check(lsg_gen_create(ctx.handle(), weights.data(), std::int64_t(weights.size()), LSG_PREC_FP16, calib->frames, &c));
+    std::int32_t n = 0;
+    lsg_status st = lsg_gen_calibrate(c, calib->mel_rows, calib->chunk_row, calib->target, calib->refs,
+                                      calib->ref_index, calib->frames, nullptr, 0, &n);
+    std::vector<float> absmax(std::size_t(n > 0 ? n : 0));
+    if (st == LSG_OK)
+      st = lsg_gen_calibrate(c, calib->mel_rows, calib->chunk_row, calib->target, calib->refs, calib->ref_index,
+                             calib->frames, absmax.data(), n, &n);
+    if (st != LSG_OK) {  // the error text before the destroy can touch it
+      const std::string m = lsg_last_error();
+      lsg_gen_destroy(c);
+      if (st == LSG_EINVAL) throw std::invalid_argument(m);
+      throw std::runtime_error(m);
+    }
+    lsg_gen_destroy(c);
+    check(lsg_gen_create_q(ctx.handle(), weights.data(), std::int64_t(weights.size()), int32_t(prec), absmax.data(),
+                           n, max_batch, &g_));
   }
   ~LipsyncStage() {
     for (void* p : bufs_) lsg_dev_free(ctx_.handle(), p);

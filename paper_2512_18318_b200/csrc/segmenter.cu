@@ -20,8 +20,9 @@
 //                       exactly like process_frame (segmenter.cpp:51-99).
 //   K3 seg_carry        keeps each stream's sub-frame tail (stage_,
 //                       segmenter.cpp:40-48) on the device.
-//   K4 seg_collect      compacts cuts/flags/state into mapped pinned memory,
-//                       so a push costs one stream synchronisation.
+//   K4 seg_collect_scan + seg_collect_copy: cut offsets, then a warp per
+//                       stream compacts cuts/flags/state into mapped pinned
+//                       memory, so a collection costs one synchronisation.
 //
 // Bit-exactness: sqrt, division and the peak multiply are
 // IEEE round-to-nearest on both sides (__dsqrt_rn/__ddiv_rn/__dmul_rn, no
@@ -758,16 +759,17 @@ __global__ void seg_finish(const int32_t* __restrict__ streams, const int64_t* _
 }
 
 // Compacts the touched streams' cuts + state (+flags) into mapped host
-// memory: block-wide scan of the per-stream cut counts, then one warp per
-// stream copying its cuts as coalesced 16-byte words (lsg_cut is 48 B).
+// memory in two launches: seg_collect_scan (one block) turns the per-stream
+// cut counts into offsets; seg_collect_copy then runs a warp per stream over
+// the whole GPU, copying its state, its cuts as coalesced 16-byte words
+// (lsg_cut is 48 B) and its flags -- many SMs' worth of outstanding writes to
+// the mapped buffers instead of one block's.
 constexpr int COLLECT_THREADS = 1024;
 constexpr int COLLECT_MAX = 4096;  // streams per push / finish
+constexpr int COPY_WARPS = 8;
 __global__ void __launch_bounds__(COLLECT_THREADS)
-seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
-            const lsg_cut* __restrict__ cuts_all, const uint32_t* __restrict__ flags_all, Params P,
-            DevState* h_state, int32_t* h_offsets, lsg_cut* h_cuts, uint32_t* h_flags, int cut_cap_total,
-            DevState* st_mut) {
-  __shared__ int s_off[COLLECT_MAX + 1];
+seg_collect_scan(const int32_t* __restrict__ streams, int n, const DevState* __restrict__ st,
+                 int32_t* __restrict__ d_offsets, int32_t* h_offsets) {
   __shared__ int s_warp[COLLECT_THREADS / 32];
   __shared__ int s_carry;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -795,28 +797,41 @@ seg_collect(const int32_t* __restrict__ streams, int n, const DevState* __restri
     }
     __syncthreads();
     const int excl = s_carry + (warp ? s_warp[warp - 1] : 0) + x - v;
-    if (i < n) s_off[i] = excl;
+    if (i < n) {
+      d_offsets[i] = excl;
+      h_offsets[i] = excl;
+    }
     __syncthreads();
     if (tid == 0) s_carry += s_warp[31];
     __syncthreads();
   }
-  if (tid == 0) s_off[n] = s_carry;
-  __syncthreads();
-  for (int i = tid; i <= n; i += COLLECT_THREADS) h_offsets[i] = s_off[i];
-  for (int i = tid; i < n; i += COLLECT_THREADS) h_state[i] = st[streams[i]];
-  for (int i = warp; i < n; i += COLLECT_THREADS / 32) {
-    const int s = streams[i];
-    const int k = min(st[s].n_cuts, max(0, cut_cap_total - s_off[i]));
-    const uint4* src = reinterpret_cast<const uint4*>(cuts_all + (int64_t)s * P.cut_cap);
-    uint4* dst = reinterpret_cast<uint4*>(h_cuts + s_off[i]);
-    for (int u = lane; u < k * 3; u += 32) dst[u] = src[u];
-    if (P.flags_only) {
-      const int nw = (st[s].n_flag_frames + 31) >> 5;
-      for (int j = lane; j < nw; j += 32) h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
-    }
+  if (tid == 0) {
+    d_offsets[n] = s_carry;
+    h_offsets[n] = s_carry;
   }
-  __syncthreads();  // every copy above read st[] first
-  for (int i = tid; i < n; i += COLLECT_THREADS) st_mut[streams[i]].n_cuts = 0;
+}
+
+__global__ void __launch_bounds__(COPY_WARPS * 32)
+seg_collect_copy(const int32_t* __restrict__ streams, int n, DevState* st, const lsg_cut* __restrict__ cuts_all,
+                 const uint32_t* __restrict__ flags_all, Params P, const int32_t* __restrict__ d_offsets,
+                 DevState* h_state, lsg_cut* h_cuts, uint32_t* h_flags, int cut_cap_total) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * COPY_WARPS + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int s = streams[i];
+  const DevState d = st[s];
+  if (lane == 0) h_state[i] = d;
+  const int off = d_offsets[i];
+  const int k = min(d.n_cuts, max(0, cut_cap_total - off));
+  const uint4* src = reinterpret_cast<const uint4*>(cuts_all + (int64_t)s * P.cut_cap);
+  uint4* dst = reinterpret_cast<uint4*>(h_cuts + off);
+  for (int u = lane; u < k * 3; u += 32) dst[u] = src[u];
+  if (P.flags_only) {
+    const int nw = (d.n_flag_frames + 31) >> 5;
+    for (int j = lane; j < nw; j += 32) h_flags[(int64_t)i * P.flag_words + j] = flags_all[(int64_t)s * P.flag_words + j];
+  }
+  __syncwarp();
+  if (lane == 0) st[s].n_cuts = 0;  // after every lane read d
 }
 
 }  // namespace seg
@@ -889,6 +904,7 @@ struct lsg_seg_s {
   DevBuf<int16_t> staging;
   DevBuf<int32_t> streams_dev;
   DevBuf<int32_t> collect_dev;  // streams whose results are still on the device
+  DevBuf<int32_t> collect_off;  // their cut offsets (seg_collect_scan)
   DevBuf<int64_t> totals_dev;
   PinnedBuf<Chunk> chunks_host;
   PinnedBuf<int32_t> streams_host;
@@ -958,9 +974,11 @@ static void collect(lsg_seg h, bool finishing) {
   std::memcpy(h->collect_host.p, h->dirty_list.data(), sizeof(int32_t) * n);
   LSG_CUDA(cudaMemcpyAsync(h->collect_dev.p, h->collect_host.p, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
                            ctx->stream));
-  seg_collect<<<1, COLLECT_THREADS, 0, ctx->stream>>>(h->collect_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P,
-                                          h->h_state, h->h_off, h->h_cuts, h->h_flags,
-                                          (int)h->h_cut_cap, h->st.p);
+  seg_collect_scan<<<1, COLLECT_THREADS, 0, ctx->stream>>>(h->collect_dev.p, n, h->st.p, h->collect_off.p, h->h_off);
+  LSG_LAUNCHED(ctx);
+  seg_collect_copy<<<(unsigned)ceil_div(n, COPY_WARPS), COPY_WARPS * 32, 0, ctx->stream>>>(
+      h->collect_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P, h->collect_off.p, h->h_state, h->h_cuts, h->h_flags,
+      (int)h->h_cut_cap);
   LSG_LAUNCHED(ctx);
   ctx->sync();
   for (int s : h->dirty_list) {
@@ -1189,6 +1207,7 @@ lsg_status lsg_seg_create(lsg_ctx ctx, const lsg_seg_cfg* cfg, int32_t n_streams
       h->staging.alloc((size_t)n_streams * (size_t)((max_push_samples + 63) & ~int64_t(63)) + 64);
       h->streams_dev.alloc(n_streams);
       h->collect_dev.alloc(n_streams);
+      h->collect_off.alloc(n_streams + 1);
       h->totals_dev.alloc(n_streams);
       h->chunks_host.alloc(n_streams);
       h->streams_host.alloc(n_streams);

@@ -233,6 +233,60 @@ int main(int argc, char** argv) {
       reg.alloc(u, LSG_BUF_MEL, 2 << 20, &p);  // exhausted
     }));
   }
+  // the lip-sync stage at 16 and 8 bits (weights: argv[2], a raw f32 blob
+  // written by tests/test_cpp_dropin.py): an INT8 stage needs a calibration
+  // batch, and calibrated on the frames it renders it lands within the
+  // INT8 floor of the fp16 render
+  if (argc > 2) {
+    std::ifstream wf(argv[2], std::ios::binary | std::ios::ate);
+    const std::streamsize nb = wf.tellg();
+    std::vector<float> w(std::size_t(nb / 4));
+    wf.seekg(0);
+    wf.read(reinterpret_cast<char*>(w.data()), nb);
+    CHECK(wf.good() && !w.empty());
+    constexpr int B = 16, R = B + 16;
+    std::vector<float> mel(std::size_t(R) * 80);
+    for (std::size_t i = 0; i < mel.size(); ++i) mel[i] = float(-5.0 + 2.5 * std::sin(0.37 * double(i)));
+    std::vector<std::int32_t> chunk(B), ridx(B, 0);
+    for (int b = 0; b < B; ++b) chunk[b] = b;
+    const std::size_t crop = 96 * 96 * 3;
+    std::vector<std::uint8_t> faces(B * crop);
+    for (std::size_t i = 0; i < faces.size(); ++i)
+      faces[i] = std::uint8_t((i % crop) / (96 * 3) * 2 + (i / crop) * 3 + (i % 3) * 40);
+    Context& ctx = Context::default_context();
+    auto up = [&](const void* src, std::size_t bytes) {
+      void* d = nullptr;
+      check(lsg_dev_alloc(ctx.handle(), bytes, &d));
+      check(lsg_copy(ctx.handle(), d, src, bytes));
+      return d;
+    };
+    auto* d_mel = static_cast<float*>(up(mel.data(), mel.size() * 4));
+    auto* d_chunk = static_cast<std::int32_t*>(up(chunk.data(), chunk.size() * 4));
+    auto* d_ridx = static_cast<std::int32_t*>(up(ridx.data(), ridx.size() * 4));
+    auto* d_faces = static_cast<std::uint8_t*>(up(faces.data(), faces.size()));
+    std::uint8_t* d_out[2];
+    for (auto& o : d_out) o = static_cast<std::uint8_t*>(up(faces.data(), faces.size()));
+    check(lsg_ctx_sync(ctx.handle()));
+    CHECK(throws<std::invalid_argument>([&] { LipsyncStage bad(w, B, Precision::INT8_TAIL); }));
+    const CalibrationBatch cal{d_mel, d_chunk, d_faces, d_faces, d_ridx, B};
+    {
+      LipsyncStage f16(w, B, Precision::FP16);
+      LipsyncStage i8(w, B, Precision::INT8_TAIL, ctx, &cal);
+      CHECK(f16.render(640, 640, B, d_mel, d_chunk, d_faces, d_faces, d_out[0]).frames == B);
+      CHECK(i8.render(640, 640, B, d_mel, d_chunk, d_faces, d_faces, d_out[1]).frames == B);
+    }
+    std::vector<std::uint8_t> o16(faces.size()), o8(faces.size());
+    check(lsg_copy(ctx.handle(), o16.data(), d_out[0], o16.size()));
+    check(lsg_copy(ctx.handle(), o8.data(), d_out[1], o8.size()));
+    check(lsg_ctx_sync(ctx.handle()));
+    double se = 0.0;
+    for (std::size_t i = 0; i < o16.size(); ++i) se += (double(o16[i]) - o8[i]) * (double(o16[i]) - o8[i]);
+    const double psnr = 10.0 * std::log10(255.0 * 255.0 / std::max(se / double(o16.size()), 1e-12));
+    std::printf("INT8-tail stage vs fp16 stage: %.2f dB\n", psnr);
+    CHECK(psnr >= 30.0);
+    for (void* p : {(void*)d_mel, (void*)d_chunk, (void*)d_ridx, (void*)d_faces, (void*)d_out[0], (void*)d_out[1]})
+      lsg_dev_free(ctx.handle(), p);
+  }
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "all drop-in checks passed", g_fail);
   return g_fail ? 1 : 0;
 }

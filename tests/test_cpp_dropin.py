@@ -19,8 +19,14 @@ def test_dropin_header_compiles(lsg):
 
 
 @pytest.mark.gpu
-def test_dropin_known_answers():
+def test_dropin_known_answers(tmp_path):
+    from paper_2512_18318_b200 import generator
     exe = _build()
-    r = subprocess.run([exe, os.path.join(ROOT, "tests", "golden")], capture_output=True, text=True, timeout=300)
+    wfile = tmp_path / "weights.f32"
+    generator.synthetic_weights(0).astype("<f4").tofile(wfile)  # the LipsyncStage checks' blob
+    r = subprocess.run([exe, os.path.join(ROOT, "tests", "golden"), str(wfile)], capture_output=True, text=True,
+                       timeout=300)
+    print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all drop-in checks passed" in r.stdout
+    assert "INT8-tail stage vs fp16 stage" in r.stdout
