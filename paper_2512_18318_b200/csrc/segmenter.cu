@@ -33,6 +33,7 @@
 // i.e. with the correctly rounded value, which agrees with glibc's log10 on
 // every decision tested (tests/test_segmenter_gpu.py exact-threshold frames).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -927,6 +928,7 @@ struct lsg_seg_s {
   // benchmark's per-kernel roofline (lsgdbg_seg_k1_ms)
   cudaEvent_t k1a = nullptr, k1b = nullptr;
   bool k1_recorded = false;
+  double collect_wait_ms = 0.0, collect_host_ms = 0.0;  // last collection: sync wait, host distribution
   ~lsg_seg_s() {
     for (int j = 0; j < 3; ++j) {
       if (eK1[j]) cudaEventDestroy(eK1[j]);
@@ -980,7 +982,15 @@ static void collect(lsg_seg h, bool finishing) {
       h->collect_dev.p, n, h->st.p, h->cuts.p, h->flags.p, h->P, h->collect_off.p, h->h_state, h->h_cuts, h->h_flags,
       (int)h->h_cut_cap);
   LSG_LAUNCHED(ctx);
+  const auto tw0 = std::chrono::steady_clock::now();
   ctx->sync();
+  const auto tw1 = std::chrono::steady_clock::now();
+  struct Stamp {  // host distribution time of this collection (lsgdbg_seg_collect_ms)
+    lsg_seg h;
+    std::chrono::steady_clock::time_point t0;
+    ~Stamp() { h->collect_host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+  } stamp{h, tw1};
+  h->collect_wait_ms = std::chrono::duration<double, std::milli>(tw1 - tw0).count();
   for (int s : h->dirty_list) {
     h->dirty[s] = 0;
     h->cut_bound[s] = 0;
@@ -1282,6 +1292,16 @@ lsg_status lsgdbg_seg_k1_ms(lsg_seg h, float* ms) {
     DeviceGuard g(h->ctx);
     LSG_CUDA(cudaEventSynchronize(h->k1b));
     LSG_CUDA(cudaEventElapsedTime(ms, h->k1a, h->k1b));
+  });
+}
+
+// Host-side split of the last collection (ms): waiting in its stream
+// synchronisation, distributing the cuts / state to the per-stream mirrors.
+lsg_status lsgdbg_seg_collect_ms(lsg_seg h, double* wait_ms, double* host_ms) {
+  return guard(__func__, [&] {
+    if (!h || !wait_ms || !host_ms) invalid("lsgdbg_seg_collect_ms: null argument");
+    *wait_ms = h->collect_wait_ms;
+    *host_ms = h->collect_host_ms;
   });
 }
 

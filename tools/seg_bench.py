@@ -50,9 +50,12 @@ def main():
         cuts = seg.take_all_cuts()
         k1 = C.c_float()
         ctx.lib.check(ctx.lib.dll.lsgdbg_seg_k1_ms(seg.h, C.byref(k1)))
+        cw, chh = C.c_double(), C.c_double()
+        ctx.lib.check(ctx.lib.dll.lsgdbg_seg_collect_ms(seg.h, C.byref(cw), C.byref(chh)))
         ms = e0.elapsed_time(e1)
         print(f"segmenter {S} x {secs} s: host push {1e3 * (thp - th0):.3f} ms (+finish {1e3 * (th1 - thp):.3f}); call {ms:.3f} ms = {S * n * 2 / ms / 1e6:.0f} GB/s, "
-              f"K1 {k1.value:.3f} ms = {S * n * 2 / k1.value / 1e6:.0f} GB/s, {len(cuts)} cuts")
+              f"K1 {k1.value:.3f} ms = {S * n * 2 / k1.value / 1e6:.0f} GB/s, {len(cuts)} cuts; "
+              f"finish: sync wait {cw.value:.3f} ms, host distribution {chh.value:.3f} ms")
 
 
 if __name__ == "__main__":
