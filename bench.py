@@ -235,7 +235,7 @@ def main():
     ap.add_argument("--paced-streams", type=int, default=256, help="config-5 paced streams over all GPUs")
     ap.add_argument("--scaled-streams", type=int, default=512, help="segmenter/mel roofline set: streams x 60 s")
     ap.add_argument("--config4-streams", type=int, default=64,
-                    help="fp8 leg (config 4): streams of the whole job, s mod N (0: skip)")
+                    help="8-bit leg (config 4, INT8 tail): streams of the whole job, s mod N (0: skip)")
     ap.add_argument("--ref-streams", type=int, default=0, help="reference arm sample: streams (0: host threads)")
     ap.add_argument("--ref-seconds", type=int, default=20, help="reference arm sample: seconds per stream")
     ap.add_argument("--ref-gen-frames", type=int, default=64, help="reference arm sample: generator frames")
@@ -387,7 +387,7 @@ def main():
         ctx.set_stream(torch_stream.cuda_stream)
     # ------------------------------- segmenter / mel rooflines (scaled set)
     scaled = scaled_leg(args, local, torch, ctx, torch_stream, api) if args.scaled_streams > 0 else None
-    # ---------------------------------- config 4: fp8 generator, batches of 128
+    # ---------------------------------- config 4: INT8-tail generator, batches of 128
     cfg4 = config4_leg(args, rank, world, local, dist, torch, ctx, torch_stream, api, generator, weights, fps) \
         if args.config4_streams > 0 else None
     # -------------------------------------------- generator kernel roofline

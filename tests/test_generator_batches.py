@@ -1,5 +1,6 @@
 """Generator parity at the batch sizes the benchmark runs (config 3: B=128;
-config 5's pipeline: B=512; config 4: fp8 at B=128), against the fp32 oracle
+config 5's pipeline: B=512; config 4: the fp8 and INT8 tails at B=128, tests/test_generator_fp8.py and
+test_generator_int8.py), against the fp32 oracle
 (oracle/generator_ref.py) on a seeded subset of frames of ONE full-size
 launch -- so the CTA-pair (conv_tc2, halo pairs), split-K / narrow-tile and
 persistent multi-wave paths that only large batches take are compared with

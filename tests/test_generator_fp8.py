@@ -233,7 +233,7 @@ def fp8_tail_rounding_model(gref, blob, mel, faces, absmax, tail0=TAIL0):
 @pytest.mark.gpu
 @pytest.mark.parametrize("B", [16, 128])
 def test_fp8_tail_meets_30db_floor(weights, gref, B):
-    """LSG_PREC_FP8_TAIL (config 4's fp8 generator): PSNR >= 30 dB vs the fp32
+    """LSG_PREC_FP8_TAIL (config 4's fp8 variant): PSNR >= 30 dB vs the fp32
     oracle on the [0,1] frames and on the u8 frames -- the stated fp8 floor
     -- and within 1.5 dB of its CPU rounding model; at B=128 on a seeded
     subset of one full launch."""
