@@ -14,7 +14,7 @@ timeout 300 python tools/mel_bench.py 4096 8 > $O/mel_bench.txt 2>&1
 # launch lists (ncu serialises kernels: per-launch times are cold-cache; shares are what to compare)
 # one forward each (the graph's first launch; bench.py reads the B=1024 list for roofline.traffic)
 for b in 1024 512; do timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/gen${b}_launches.csv python tools/gen_forward.py $b 1 1 > /dev/null 2>&1; done
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --launch-skip 60 --launch-count 60 --log-file $O/gen128_bf16_launches.csv python tools/gen_forward.py 128 2 0 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/gen128_bf16_launches.csv python tools/gen_forward.py 128 1 0 > /dev/null 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -c 600 --log-file $O/gen128_int8_launches.csv python tools/gen_forward.py 128 2 4 > /dev/null 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/seg_launches.csv python tools/seg_bench.py 512 1 0 > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/bench_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --paced-seconds 0 --scaled-streams 0 --config4-streams 0 > $O/bench_under_ncu.log 2>&1
