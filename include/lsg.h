@@ -177,7 +177,7 @@ lsg_status lsg_mel_compute_batch(lsg_mel h, int32_t n_seg, const int16_t* pcm_ba
 #define LSG_PREC_FP8_TAIL 3     /* fp16 up to fd5.2, e4m3 (as LSG_PREC_FP8) for fd6.0-out0 (28% of the
                                    FLOPs): the fp8 split that keeps >= 30 dB vs the fp32 oracle on the
                                    synthetic network; needs act_absmax like LSG_PREC_FP8 */
-#define LSG_PREC_INT8_TAIL 4    /* fp16 encoders and fd0-fd2.2, then tcgen05 kind::i8 for fd3.0-out0 (84%
+#define LSG_PREC_INT8_TAIL 4    /* fp16 encoders and fd0, then tcgen05 kind::i8 for fd1.0-out0 (90%
                                    of the FLOPs): u8 activations (every decoder input is post-ReLU, per
                                    tensor scale absmax/255), s8 weights (per output channel scale
                                    max|w|/127), s32 accumulate; >= 30 dB vs the fp32 oracle (DESIGN.md

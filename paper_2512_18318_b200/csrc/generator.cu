@@ -1582,11 +1582,11 @@ lsg_status lsg_gen_create_q(lsg_ctx ctx, const float* weights, int64_t n_floats,
       set_smem_attrs(h->prec);
       if (tail) {
         // fp8 on the decoder's last block + the output conv only (fd6.0 ..
-        // out0: 28% of the FLOPs); int8 from fd3.0 (84%); the 16-bit engine
+        // out0: 28% of the FLOPs); int8 from fd1.0 (90%); the 16-bit engine
         // before them -- the splits the sensitivity sweeps pick for a >= 30 dB
         // floor on this network (tools/precision_sweep.py, tools/int8_sweep.py,
         // DESIGN.md §4)
-        h->tail_blk = precision == LSG_PREC_INT8_TAIL ? 3 : 6;
+        h->tail_blk = precision == LSG_PREC_INT8_TAIL ? 1 : 6;
         const std::string first = "fd" + std::to_string(h->tail_blk) + ".0";
         for (int l = 0; l < kNumLayers; ++l)
           if (first == kLayers[l].name) h->tail0 = l;

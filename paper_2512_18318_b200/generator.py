@@ -268,7 +268,7 @@ class LipsyncEngine:
     model (visual_mocks.hpp:41-43) with the generator forward.  precision
     The 8-bit precisions calibrate per-tensor activation ranges first
     (calibrate()); PREC_FP8_TAIL runs fp16 up to fd5.2 and e4m3 from fd6.0
-    on, PREC_INT8_TAIL fp16 up to fd2.2 and u8 x s8 (kind::i8) from fd3.0 on
+    on, PREC_INT8_TAIL fp16 up to fd0 and u8 x s8 (kind::i8) from fd1.0 on
     (the splits that keep >= 30 dB vs the fp32 oracle)."""
 
     PREC_BF16, PREC_FP16, PREC_FP8, PREC_FP8_TAIL, PREC_INT8_TAIL = 0, 1, 2, 3, 4
