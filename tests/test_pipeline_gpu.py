@@ -3,7 +3,8 @@ Segmenter's, frame gathering follows the FrameRing window rule
 (frame_ring.cpp:36-55, +-50 ms, orchestrator.cpp:90-91), the frame -> mel
 chunk index rule is exact, and every rendered frame is
 bit-identical to the standalone stages (compute_mel of the segment audio +
-generator forward of that frame)."""
+generator forward of that frame) -- with the fp16 engine and with the INT8
+tail."""
 import numpy as np
 import pytest
 
@@ -12,7 +13,8 @@ from streams import random_scenario_pattern
 pytestmark = pytest.mark.gpu
 
 
-def test_pipeline_matches_standalone_stages(reference):
+@pytest.mark.parametrize("precision", [1, 4])  # fp16; the INT8 tail (config 4's engine)
+def test_pipeline_matches_standalone_stages(reference, precision):
     torch = pytest.importorskip("torch")
     from paper_2512_18318_b200 import api, generator
     from paper_2512_18318_b200.pipeline import Pipeline, PipelineConfig
@@ -28,7 +30,7 @@ def test_pipeline_matches_standalone_stages(reference):
     w = generator.synthetic_weights(0)
     ctx = api.Context(0)
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-    eng = generator.LipsyncEngine(w, max_batch=64, ctx=ctx, precision=1)
+    eng = generator.LipsyncEngine(w, max_batch=64, ctx=ctx, precision=precision)
     pipe = Pipeline(PipelineConfig(S, 12000, fps, 50, 64, True), eng, ctx=ctx)
     recs, frames, st = pipe.run(pcm, video, refs)
     assert st["frames_rendered"] == len(recs) == len(frames)
